@@ -1,0 +1,220 @@
+/*
+ * hfz.h -- C-ABI of the B200-native coverage-feedback core ("hetfuzz on B200").
+ *
+ * This is the drop-in boundary: plain pointers and sizes, int status codes, no
+ * exceptions, no torch/C++ types.  The reference has no FFI of its own -- its
+ * hot path sits behind the C++ headers proj/include/hetfuzz/{coverage,rng,
+ * engine}.hpp (statically linked, proj/CMakeLists.txt:14-23) and the pybind11
+ * module proj/python/bindings.cpp:310-350.  Each entry point below names the
+ * reference interface it replaces; include/hetfuzz_b200/*.hpp re-creates the
+ * reference's C++ API on top of these calls and INTEGRATION.md shows the
+ * binding a maintainer of the reference would add.
+ *
+ * Conventions
+ *   - every function returns 0 (HFZ_OK) or an HFZ_E* code; hfz_last_error()
+ *     gives a thread-local message.  Nothing throws across the ABI.
+ *   - all *device* pointers are caller-owned CUDA device memory on the
+ *     context's device; the library never frees or reallocates them.  Scratch
+ *     (first-occurrence table, candidate list, novelty delta) is owned by the
+ *     context.
+ *   - work is enqueued on the context's stream and is asynchronous unless the
+ *     function name ends in _host (those take HOST buffers and synchronise).
+ *   - there is NO CPU fallback: without a CUDA device every call fails with
+ *     HFZ_ECUDA.
+ *
+ * Raw map record ("trace_bits" of one execution), S logical slots, H = S/2:
+ *     [ H x u8  host counters   (CoverageMap::host_,   coverage.hpp:19) ]
+ *     [ H x u32 device counters (CoverageMap::device_, coverage.hpp:20) ]
+ *   = 5*H bytes (163,840 B for the reference's S = 65,536).  Records of a batch
+ *   are contiguous; the base pointer must be 16-byte aligned.
+ * Virgin map: S bytes, REFERENCE polarity (0 = never seen, class bits are OR-ed
+ * in; VirginMap, coverage.hpp:155-180).  AFL's AND-merge == bitwise OR here.
+ */
+#ifndef HFZ_H_
+#define HFZ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(_WIN32)
+#define HFZ_API
+#else
+#define HFZ_API __attribute__((visibility("default")))
+#endif
+
+#define HFZ_VERSION 100 /* 0.1.0 */
+
+enum {
+  HFZ_OK = 0,
+  HFZ_EINVAL = 1,   /* bad argument (null pointer, unsupported map size, ...) */
+  HFZ_ECUDA = 2,    /* CUDA runtime error; see hfz_last_error() */
+  HFZ_ENOMEM = 3,   /* scratch allocation failed */
+  HFZ_ECAP = 4,     /* batch exceeds a capacity fixed at context creation */
+  HFZ_ENCCL = 5     /* NCCL not loadable / collective failed */
+};
+
+/* Admit codes: enum class Admit, coverage.hpp:182-186 */
+enum { HFZ_ADMIT_NONE = 0, HFZ_ADMIT_NEW_COUNTS = 1, HFZ_ADMIT_NEW_EDGES = 2 };
+
+#define HFZ_MAX_INPUT_BYTES (1u << 20) /* kMaxInputBytes, engine.hpp:17 */
+
+typedef struct hfz_ctx hfz_ctx;
+
+HFZ_API int hfz_version(void);
+HFZ_API const char* hfz_last_error(void);
+
+/*
+ * Context: one per (host thread, GPU).  map_slots = S (power of two,
+ * 1024 <= S <= 2^24; the reference's kMapSize is 65536, coverage.hpp:13).
+ * stream is a cudaStream_t (NULL = the legacy default stream).
+ * Threading contract of SPEC.md:124-125 is kept: one writer per virgin map.
+ */
+HFZ_API int hfz_ctx_create(hfz_ctx** out, int device, uint32_t map_slots, void* stream);
+HFZ_API int hfz_ctx_destroy(hfz_ctx* ctx);
+HFZ_API int hfz_ctx_set_stream(hfz_ctx* ctx, void* stream);
+HFZ_API int hfz_ctx_sync(hfz_ctx* ctx);
+HFZ_API uint32_t hfz_ctx_map_slots(const hfz_ctx* ctx);
+HFZ_API uint64_t hfz_record_bytes(uint32_t map_slots);
+/* Tuning knobs, mostly for bench/profiling: key in {"scan_warps","scan_variant"} */
+HFZ_API int hfz_ctx_set_option(hfz_ctx* ctx, const char* key, int64_t value);
+/* Kernels launched by this context since creation (for bench.py's gpu_launches). */
+HFZ_API uint64_t hfz_ctx_launch_count(const hfz_ctx* ctx);
+
+/* ------------------------------------------------------------------------- */
+/* Fused feedback (K2): replaces, for a whole batch folded IN EXEC ORDER,
+ *   classify_trace   coverage.hpp:152, src/coverage.cpp:58-72
+ *   trace_signature  coverage.hpp:199, src/coverage.cpp:89-97 (Full and Simple)
+ *   has_new_bits     coverage.hpp:191, src/coverage.cpp:74-87 (+VirginMap::observe)
+ * i.e. lines 471-478 of Campaign::run_one (src/engine.cpp).
+ *
+ *   raw_maps          device, n_exec records
+ *   virgin_inout      device, S bytes; on return = virgin after the last exec
+ *   edge_counts_inout device, 2 x u64 {host_edges, device_edges}
+ *                     (VirginMap::host_edges/device_edges, coverage.hpp:163-164)
+ *   classed_out       device, n_exec x S bytes or NULL (ClassedTrace::classed)
+ *   admit_out         device, n_exec x u8 Admit codes, exactly the sequential ones
+ *   sig_full_out / sig_simple_out   device, n_exec x u64
+ *   nnz_out           device, n_exec x u32 (ClassedTrace::nonzero.size()) or NULL
+ */
+HFZ_API int hfz_feedback_batch(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec,
+                               uint8_t* virgin_inout, uint64_t* edge_counts_inout,
+                               uint8_t* classed_out, uint8_t* admit_out,
+                               uint64_t* sig_full_out, uint64_t* sig_simple_out,
+                               uint32_t* nnz_out);
+
+/* Same call with HOST buffers (pageable or pinned): copies in chunks through
+ * context-owned staging, overlapping H2D with the kernels; synchronous. */
+HFZ_API int hfz_feedback_batch_host(hfz_ctx* ctx, const uint8_t* raw_maps_host, uint64_t n_exec,
+                                    uint8_t* virgin_inout_host, uint64_t* edge_counts_inout_host,
+                                    uint8_t* classed_out_host, uint8_t* admit_out_host,
+                                    uint64_t* sig_full_out_host, uint64_t* sig_simple_out_host,
+                                    uint32_t* nnz_out_host);
+
+/* The two halves of hfz_feedback_batch, exposed for multi-GPU sharding
+ * (SURVEY.md 8e).  Rank r owns a contiguous exec range of the global batch.
+ *
+ * scan:    one HBM pass over the rank's maps against the batch-start virgin V0:
+ *          classed maps, signatures, nnz, and this rank's novelty delta
+ *          D_r = OR of class bits not in V0 (S bytes, written to delta_out).
+ * resolve: given all ranks' deltas (n_ranks x S bytes, rank-major, e.g. the
+ *          output of an NCCL allgather of delta_out), computes the exact
+ *          sequential Admit codes of this rank's execs against
+ *          P_r = V0 | OR_{q<r} D_q, then folds virgin_inout = V0 | OR_q D_q in
+ *          fixed rank order and bumps the edge counters.  Identical on every
+ *          rank and identical to the single-rank sequential oracle.
+ * With n_ranks == 1 and deltas == delta_out the pair equals hfz_feedback_batch.
+ */
+HFZ_API int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec,
+                              const uint8_t* virgin_v0, uint8_t* classed_out,
+                              uint64_t* sig_full_out, uint64_t* sig_simple_out,
+                              uint32_t* nnz_out, uint8_t* delta_out);
+HFZ_API int hfz_feedback_resolve(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec,
+                                 uint8_t* virgin_inout, uint64_t* edge_counts_inout,
+                                 const uint8_t* deltas, uint32_t n_ranks, uint32_t rank,
+                                 uint8_t* admit_out);
+
+/* K4 alone: virgin_inout |= OR_q deltas[q] in rank order, edge counters updated
+ * (bitwise OR in reference polarity == AFL's virgin AND-merge). */
+HFZ_API int hfz_virgin_merge(hfz_ctx* ctx, uint8_t* virgin_inout, uint64_t* edge_counts_inout,
+                             const uint8_t* deltas, uint32_t n_ranks);
+
+/* allgather + resolve in one call for C/C++ hosts: nccl_comm is an ncclComm_t
+ * (libnccl is dlopen()ed on first use; HFZ_ENCCL if unavailable). */
+HFZ_API int hfz_feedback_resolve_allgather(hfz_ctx* ctx, void* nccl_comm, const uint8_t* raw_maps,
+                                           uint64_t n_exec, uint8_t* virgin_inout,
+                                           uint64_t* edge_counts_inout, const uint8_t* delta_local,
+                                           uint8_t* deltas_scratch, uint32_t n_ranks,
+                                           uint32_t rank, uint8_t* admit_out);
+
+/* ------------------------------------------------------------------------- */
+/* Edge record (K1): replaces DeviceThreadCtx::Impl::edge + Runtime::bump_counter
+ * (src/hdvm.cpp:415-431, 362-366), the thread/warp enumeration of
+ * Runtime::do_launch (src/hdvm.cpp:556-603) and merge_device_into_map
+ * (coverage.hpp:204-205) for a batch of executions.
+ *
+ *   launch_off  device, (n_exec+1) x u64: exec e owns launches [launch_off[e], launch_off[e+1])
+ *   dims        device, n_launch x 6 x u32: grid.x,y,z, block.x,y,z  (LaunchConfig, hdvm.hpp:31-45)
+ *   thread_off  device, (n_launch+1) x u64: first simulated thread of each launch; threads are
+ *               numbered block-linear outer, linear-in-block inner (hdvm.cpp:562,583)
+ *   ev_off      device, (n_threads+1) x u64: thread t's sites are sites[ev_off[t], ev_off[t+1])
+ *   sites       device, u32 basic-block ids in execution order
+ *   raw_maps    device, n_exec records; the DEVICE HALF of each is overwritten with the
+ *               saturating warp counters (host half untouched)
+ *   warp_events_out device, n_exec x u64 (ExecutionReport::warp_edge_events) or NULL
+ */
+HFZ_API int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, const uint32_t* dims,
+                                  const uint64_t* thread_off, const uint64_t* ev_off,
+                                  const uint32_t* sites, uint64_t n_exec, uint64_t n_launch,
+                                  uint8_t* raw_maps, uint64_t* warp_events_out);
+
+/* Host edge record: host_edge_update + CoverageMap::host_increment
+ * (coverage.hpp:24-32,79-84) for batched u16 host site traces.
+ *   site_off device (n_exec+1) x u64; sites device u16; fills the HOST HALF. */
+HFZ_API int hfz_host_edge_record_batch(hfz_ctx* ctx, const uint64_t* site_off,
+                                       const uint16_t* sites, uint64_t n_exec, uint8_t* raw_maps);
+
+/* ------------------------------------------------------------------------- */
+/* Batched havoc (K3): replaces havoc_mutant(input, Rng&) (engine.hpp:29-30,
+ * src/engine.cpp:119-193), one independent Rng per slot (rng.hpp:11-46).
+ *   in_bytes / in_off   device, inputs back to back, (n+1) x u64 offsets
+ *   rng_state_inout     device, n x u64 splitmix64 states (Rng(seed) has state == seed);
+ *                       on return the state after the slot's draws
+ *   out_bytes           device, slot j's output starts at out_off[j]; it must hold
+ *                       hfz_havoc_max_out(len_j) bytes
+ *   out_off             device, (n+1) x u64 (capacity layout, caller-computed)
+ *   out_len             device, n x u64 actual mutant lengths
+ *   draws_out           device, n x u32 draws consumed, or NULL
+ */
+HFZ_API uint64_t hfz_havoc_max_out(uint64_t in_len);
+HFZ_API int hfz_havoc_batch(hfz_ctx* ctx, const uint8_t* in_bytes, const uint64_t* in_off,
+                            uint64_t n, uint64_t* rng_state_inout, uint8_t* out_bytes,
+                            const uint64_t* out_off, uint64_t* out_len, uint32_t* draws_out);
+
+/* splice_mutant (engine.hpp:33-35, src/engine.cpp:195-204): slot j splices
+ * a = input a_idx[j], b = input b_idx[j] of the same packed input set. */
+HFZ_API int hfz_splice_batch(hfz_ctx* ctx, const uint8_t* in_bytes, const uint64_t* in_off,
+                             const uint32_t* a_idx, const uint32_t* b_idx, uint64_t n,
+                             uint64_t* rng_state_inout, uint8_t* out_bytes,
+                             const uint64_t* out_off, uint64_t* out_len);
+
+/* deterministic_mutants (engine.hpp:25-26, src/engine.cpp:53-117) of ONE input:
+ * count first (host arithmetic), then materialise count x in_len bytes. */
+HFZ_API uint64_t hfz_deterministic_count(const uint8_t* in_host, uint64_t in_len);
+HFZ_API int hfz_deterministic_batch(hfz_ctx* ctx, const uint8_t* in_dev, uint64_t in_len,
+                                    const uint8_t* in_host, uint8_t* out_dev, uint64_t count);
+
+/* Rng helpers (host side, O(1)): rng.hpp:15-21,39-42.  State after k draws =
+ * state + k*gamma; split() child seed of the tag-th split from a parent state. */
+HFZ_API uint64_t hfz_rng_jump(uint64_t state, uint64_t k);
+HFZ_API uint64_t hfz_rng_next(uint64_t* state);
+HFZ_API uint64_t hfz_rng_below(uint64_t* state, uint64_t n);
+HFZ_API uint64_t hfz_rng_split(uint64_t* state, uint64_t tag);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HFZ_H_ */

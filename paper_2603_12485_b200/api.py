@@ -1,0 +1,271 @@
+"""Host-side wrapper of the C-ABI (include/hfz.h) over torch device tensors.
+
+PyTorch is plumbing only (device memory, streams, torch.distributed); every
+computation below is a call into libhfz.so.  Method names follow the reference's
+vocabulary (classify_trace / has_new_bits / trace_signature ->
+``feedback_batch``; ``havoc_mutant`` -> ``havoc_batch``; DeviceThreadCtx::edge ->
+``edge_record_batch``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib
+
+MAP_SIZE = 65536          # kMapSize, include/hetfuzz/coverage.hpp:13
+HOST_SLOTS = MAP_SIZE // 2  # kHostSlots, coverage.hpp:14
+MAX_INPUT_BYTES = 1 << 20   # kMaxInputBytes, engine.hpp:17
+GAMMA = 0x9E3779B97F4A7C15
+MASK64 = (1 << 64) - 1
+
+
+def record_bytes(S: int = MAP_SIZE) -> int:
+    return int(lib.hfz_record_bytes(S))
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    assert t.is_contiguous()
+    return C.c_void_p(t.data_ptr())
+
+
+def _dev(t: torch.Tensor, device, dtype=None):
+    assert t.is_cuda and t.device == device, f"tensor must live on {device}"
+    if dtype is not None:
+        assert t.dtype == dtype, f"expected {dtype}, got {t.dtype}"
+    return t
+
+
+class Context:
+    """One hfz_ctx: one host thread driving one GPU (SPEC.md:124-125 threading contract)."""
+
+    def __init__(self, device: int | torch.device = 0, map_slots: int = MAP_SIZE):
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2603_12485_b200 needs a CUDA device; there is no CPU fallback")
+        self.device = torch.device("cuda", device if isinstance(device, int) else device.index or 0)
+        self.S = int(map_slots)
+        self.H = self.S // 2
+        self.rec = record_bytes(self.S)
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+            check(lib.hfz_ctx_create(C.byref(h), self.device.index, self.S, C.c_void_p(stream)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.hfz_ctx_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def _sync_stream(self):
+        check(lib.hfz_ctx_set_stream(self._h, C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
+
+    def set_option(self, key: str, value: int):
+        check(lib.hfz_ctx_set_option(self._h, key.encode(), int(value)))
+
+    @property
+    def launch_count(self) -> int:
+        return int(lib.hfz_ctx_launch_count(self._h))
+
+    def synchronize(self):
+        self._sync_stream()
+        check(lib.hfz_ctx_sync(self._h))
+
+    # ---- allocation helpers -------------------------------------------------
+    def new_virgin(self) -> torch.Tensor:
+        return torch.zeros(self.S, dtype=torch.uint8, device=self.device)
+
+    def new_edge_counts(self) -> torch.Tensor:
+        return torch.zeros(2, dtype=torch.int64, device=self.device)
+
+    # ---- K2 -----------------------------------------------------------------
+    def feedback_batch(self, raw: torch.Tensor, virgin: torch.Tensor, edge_counts: torch.Tensor,
+                       want_classed: bool = False, want_nnz: bool = True, out: dict | None = None):
+        """Fold `raw` (n_exec records) into `virgin` in exec order.  Returns a dict of device
+        tensors: admit (u8), sig_full / sig_simple (int64 bit patterns of the u64
+        signatures), nnz (int32), optionally classed (n_exec x S u8)."""
+        _dev(raw, self.device, torch.uint8)
+        _dev(virgin, self.device, torch.uint8)
+        _dev(edge_counts, self.device, torch.int64)
+        n = raw.numel() // self.rec
+        assert raw.numel() == n * self.rec and virgin.numel() == self.S and edge_counts.numel() == 2
+        o = out or {}
+        if "admit" not in o:
+            o["admit"] = torch.empty(n, dtype=torch.uint8, device=self.device)
+            o["sig_full"] = torch.empty(n, dtype=torch.int64, device=self.device)
+            o["sig_simple"] = torch.empty(n, dtype=torch.int64, device=self.device)
+        if want_nnz and "nnz" not in o:
+            o["nnz"] = torch.empty(n, dtype=torch.int32, device=self.device)
+        if want_classed and "classed" not in o:
+            o["classed"] = torch.empty((n, self.S), dtype=torch.uint8, device=self.device)
+        self._sync_stream()
+        check(lib.hfz_feedback_batch(self._h, _ptr(raw), n, _ptr(virgin), _ptr(edge_counts),
+                                     _ptr(o.get("classed")) if want_classed else None,
+                                     _ptr(o["admit"]), _ptr(o["sig_full"]), _ptr(o["sig_simple"]),
+                                     _ptr(o.get("nnz")) if want_nnz else None))
+        return o
+
+    def feedback_scan(self, raw, virgin_v0, want_classed=False, out: dict | None = None):
+        """Rank-local half of the sharded step: signatures, nnz and this rank's novelty delta."""
+        _dev(raw, self.device, torch.uint8)
+        n = raw.numel() // self.rec
+        o = out or {}
+        if "sig_full" not in o:
+            o["sig_full"] = torch.empty(n, dtype=torch.int64, device=self.device)
+            o["sig_simple"] = torch.empty(n, dtype=torch.int64, device=self.device)
+            o["nnz"] = torch.empty(n, dtype=torch.int32, device=self.device)
+        if "delta" not in o:
+            o["delta"] = torch.empty(self.S, dtype=torch.uint8, device=self.device)
+        if want_classed and "classed" not in o:
+            o["classed"] = torch.empty((n, self.S), dtype=torch.uint8, device=self.device)
+        self._sync_stream()
+        check(lib.hfz_feedback_scan(self._h, _ptr(raw), n, _ptr(virgin_v0),
+                                    _ptr(o.get("classed")) if want_classed else None,
+                                    _ptr(o["sig_full"]), _ptr(o["sig_simple"]), _ptr(o["nnz"]),
+                                    _ptr(o["delta"])))
+        return o
+
+    def feedback_resolve(self, raw, virgin, edge_counts, deltas, n_ranks, rank, admit=None):
+        """Second half: exact Admit codes against P_rank and the ordered virgin merge."""
+        n = raw.numel() // self.rec
+        if admit is None:
+            admit = torch.empty(n, dtype=torch.uint8, device=self.device)
+        assert deltas.numel() == n_ranks * self.S
+        self._sync_stream()
+        check(lib.hfz_feedback_resolve(self._h, _ptr(raw), n, _ptr(virgin), _ptr(edge_counts),
+                                       _ptr(deltas), n_ranks, rank, _ptr(admit)))
+        return admit
+
+    def virgin_merge(self, virgin, edge_counts, deltas, n_ranks):
+        self._sync_stream()
+        check(lib.hfz_virgin_merge(self._h, _ptr(virgin), _ptr(edge_counts), _ptr(deltas), n_ranks))
+
+    def feedback_batch_host(self, raw: np.ndarray, virgin: np.ndarray, edge_counts: np.ndarray,
+                            want_classed: bool = False):
+        """Same fold through HOST buffers (numpy, ideally pinned): the e2e path of bench.py."""
+        n = raw.size // self.rec
+        assert raw.dtype == np.uint8 and raw.size == n * self.rec
+        assert virgin.dtype == np.uint8 and virgin.size == self.S
+        assert edge_counts.dtype == np.uint64 and edge_counts.size == 2
+        admit = np.empty(n, np.uint8)
+        sf = np.empty(n, np.uint64)
+        ss = np.empty(n, np.uint64)
+        nnz = np.empty(n, np.uint32)
+        classed = np.empty((n, self.S), np.uint8) if want_classed else None
+        vp = lambda a: None if a is None else C.c_void_p(a.ctypes.data)
+        self._sync_stream()
+        check(lib.hfz_feedback_batch_host(self._h, vp(raw), n, vp(virgin), vp(edge_counts), vp(classed),
+                                          vp(admit), vp(sf), vp(ss), vp(nnz)))
+        o = dict(admit=admit, sig_full=sf, sig_simple=ss, nnz=nnz)
+        if want_classed:
+            o["classed"] = classed
+        return o
+
+    # ---- K1 -----------------------------------------------------------------
+    def edge_record_batch(self, launch_off, dims, thread_off, ev_off, sites, n_exec, raw=None,
+                          want_events=True):
+        """Device basic-block traces -> device half of each raw record (+ warp_edge_events)."""
+        for t in (launch_off, thread_off, ev_off):
+            _dev(t, self.device, torch.int64)
+        _dev(dims, self.device, torch.int32)
+        _dev(sites, self.device, torch.int32)
+        if raw is None:
+            raw = torch.zeros(n_exec * self.rec, dtype=torch.uint8, device=self.device)
+        ev = torch.empty(n_exec, dtype=torch.int64, device=self.device) if want_events else None
+        n_launch = thread_off.numel() - 1
+        self._sync_stream()
+        check(lib.hfz_edge_record_batch(self._h, _ptr(launch_off), _ptr(dims), _ptr(thread_off),
+                                        _ptr(ev_off), _ptr(sites), n_exec, n_launch, _ptr(raw),
+                                        _ptr(ev)))
+        return raw, ev
+
+    def host_edge_record_batch(self, site_off, sites, n_exec, raw=None):
+        _dev(site_off, self.device, torch.int64)
+        _dev(sites, self.device, torch.int16)
+        if raw is None:
+            raw = torch.zeros(n_exec * self.rec, dtype=torch.uint8, device=self.device)
+        self._sync_stream()
+        check(lib.hfz_host_edge_record_batch(self._h, _ptr(site_off), _ptr(sites), n_exec, _ptr(raw)))
+        return raw
+
+    # ---- K3 -----------------------------------------------------------------
+    def havoc_batch(self, in_bytes, in_off, rng_state, want_draws=True):
+        """Batched havoc_mutant.  in_off / rng_state are int64 device tensors (u64 bit
+        patterns); rng_state is advanced in place.  Returns (out_bytes, out_off, out_len, draws):
+        slot j's mutant is out_bytes[out_off[j] : out_off[j] + out_len[j]]."""
+        _dev(in_bytes, self.device, torch.uint8)
+        _dev(in_off, self.device, torch.int64)
+        _dev(rng_state, self.device, torch.int64)
+        n = in_off.numel() - 1
+        lens = in_off[1:] - in_off[:-1]
+        caps = torch.clamp(lens + 1024, max=MAX_INPUT_BYTES)
+        caps = (caps + 15) // 16 * 16  # keep every slot 16-byte aligned
+        out_off = torch.zeros(n + 1, dtype=torch.int64, device=self.device)
+        torch.cumsum(caps, 0, out=out_off[1:])
+        total = int(out_off[-1].item()) if n else 0
+        out_bytes = torch.empty(max(total, 16), dtype=torch.uint8, device=self.device)
+        out_len = torch.empty(n, dtype=torch.int64, device=self.device)
+        draws = torch.empty(n, dtype=torch.int32, device=self.device) if want_draws else None
+        self._sync_stream()
+        check(lib.hfz_havoc_batch(self._h, _ptr(in_bytes), _ptr(in_off), n, _ptr(rng_state),
+                                  _ptr(out_bytes), _ptr(out_off), _ptr(out_len), _ptr(draws)))
+        return out_bytes, out_off, out_len, draws
+
+    def splice_batch(self, in_bytes, in_off, a_idx, b_idx, rng_state):
+        _dev(in_bytes, self.device, torch.uint8)
+        n = a_idx.numel()
+        lens = in_off[1:] - in_off[:-1]
+        caps = torch.clamp(lens[a_idx.long()] + lens[b_idx.long()], max=MAX_INPUT_BYTES)
+        caps = (caps + 15) // 16 * 16
+        out_off = torch.zeros(n + 1, dtype=torch.int64, device=self.device)
+        torch.cumsum(caps, 0, out=out_off[1:])
+        total = int(out_off[-1].item()) if n else 0
+        out_bytes = torch.empty(max(total, 16), dtype=torch.uint8, device=self.device)
+        out_len = torch.empty(n, dtype=torch.int64, device=self.device)
+        self._sync_stream()
+        check(lib.hfz_splice_batch(self._h, _ptr(in_bytes), _ptr(in_off), _ptr(a_idx), _ptr(b_idx), n,
+                                   _ptr(rng_state), _ptr(out_bytes), _ptr(out_off), _ptr(out_len)))
+        return out_bytes, out_off, out_len
+
+    def deterministic_mutants(self, data: bytes):
+        """deterministic_mutants of one input, materialised on the device; returns (count, tensor
+        of shape (count, len))."""
+        L = len(data)
+        host = np.frombuffer(data, np.uint8).copy() if L else np.zeros(1, np.uint8)
+        cnt = int(lib.hfz_deterministic_count(C.c_void_p(host.ctypes.data), L))
+        if cnt == 0 or L == 0:
+            return cnt, torch.empty((cnt, L), dtype=torch.uint8, device=self.device)
+        dev_in = torch.from_numpy(host).to(self.device)
+        out = torch.empty((cnt, L), dtype=torch.uint8, device=self.device)
+        self._sync_stream()
+        check(lib.hfz_deterministic_batch(self._h, _ptr(dev_in), L, C.c_void_p(host.ctypes.data),
+                                          _ptr(out), cnt))
+        return cnt, out
+
+
+# ---- scalar Rng helpers (host arithmetic, rng.hpp) ------------------------------------
+
+def rng_jump(state: int, k: int) -> int:
+    return int(lib.hfz_rng_jump(state & MASK64, k & MASK64))
+
+
+def rng_split(state: int, tag: int):
+    s = C.c_uint64(state & MASK64)
+    child = int(lib.hfz_rng_split(C.byref(s), tag & MASK64))
+    return child, int(s.value)
+
+
+def u64_to_i64(a: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.uint64).view(np.int64)
+
+
+def i64_to_u64(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy().view(np.uint64)

@@ -1,0 +1,90 @@
+"""Drop-in for the stateless entry points of the reference's pybind11 module
+``hetfuzz._core`` (proj/python/bindings.cpp): same names, argument meaning and
+error behaviour, computed on the GPU.
+
+    havoc_mutant(data: bytes, seed: int) -> bytes          bindings.cpp:220-223, :336-337
+    splice_mutant(a: bytes, b: bytes, seed: int) -> bytes  bindings.cpp:225-229, :338-339
+    deterministic_mutants(data: bytes) -> list[bytes]      bindings.cpp:213-218, :334-335
+
+Each call creates a fresh ``Rng(seed)`` exactly like the reference.  The batched
+variants are what a fuzzer should call; the single-item ones are batch-of-one
+device calls (latency-bound, kept for API parity).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import api
+
+_default = {}
+
+
+class TargetError(ValueError):
+    """bindings.cpp:314 maps hetfuzz::TargetError to ValueError."""
+
+
+def default_context(device: int = 0, map_slots: int = api.MAP_SIZE) -> api.Context:
+    key = (device, map_slots)
+    if key not in _default:
+        _default[key] = api.Context(device, map_slots)
+    return _default[key]
+
+
+def _check_seed(seed: int) -> int:
+    if not isinstance(seed, int) or seed < 0 or seed > api.MASK64:
+        raise TypeError("seed must be an unsigned 64-bit integer")  # pybind11 raises TypeError too
+    return seed
+
+
+def havoc_batch(inputs, seeds, device: int = 0):
+    """inputs: list[bytes]; seeds: list[int] (slot j uses a fresh Rng(seeds[j])).
+    Returns (list[bytes], end_states list[int], draws list[int])."""
+    ctx = default_context(device)
+    n = len(inputs)
+    lens = np.array([len(b) for b in inputs], np.int64)
+    off = np.zeros(n + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    blob = np.frombuffer(b"".join(inputs), np.uint8) if off[-1] else np.zeros(0, np.uint8)
+    d_in = torch.from_numpy(np.concatenate([blob, np.zeros(16, np.uint8)])).to(ctx.device)
+    d_off = torch.from_numpy(off).to(ctx.device)
+    d_state = torch.from_numpy(api.u64_to_i64(np.array(seeds, np.uint64))).to(ctx.device)
+    out_bytes, out_off, out_len, draws = ctx.havoc_batch(d_in, d_off, d_state)
+    ob = out_bytes.cpu().numpy()
+    oo = out_off.cpu().numpy()
+    ol = out_len.cpu().numpy()
+    res = [ob[oo[j]:oo[j] + ol[j]].tobytes() for j in range(n)]
+    return res, [int(x) for x in api.i64_to_u64(d_state)], [int(x) for x in draws.cpu().numpy()]
+
+
+def havoc_mutant(data: bytes, seed: int) -> bytes:
+    return havoc_batch([bytes(data)], [_check_seed(seed)])[0][0]
+
+
+def splice_mutant(a: bytes, b: bytes, seed: int) -> bytes:
+    ctx = default_context()
+    a, b = bytes(a), bytes(b)
+    off = np.array([0, len(a), len(a) + len(b)], np.int64)
+    blob = np.frombuffer(a + b + bytes(16), np.uint8)
+    d_in = torch.from_numpy(blob.copy()).to(ctx.device)
+    d_off = torch.from_numpy(off).to(ctx.device)
+    ai = torch.zeros(1, dtype=torch.int32, device=ctx.device)
+    bi = torch.ones(1, dtype=torch.int32, device=ctx.device)
+    st = torch.from_numpy(api.u64_to_i64(np.array([_check_seed(seed)], np.uint64))).to(ctx.device)
+    ob, oo, ol = ctx.splice_batch(d_in, d_off, ai, bi, st)
+    n = int(ol[0].item())
+    return ob[:n].cpu().numpy().tobytes()
+
+
+def deterministic_mutants(data: bytes):
+    ctx = default_context()
+    cnt, out = ctx.deterministic_mutants(bytes(data))
+    host = out.cpu().numpy()
+    return [host[i].tobytes() for i in range(cnt)]
+
+
+def feedback_batch(raw: np.ndarray, virgin: np.ndarray, edge_counts: np.ndarray, device: int = 0,
+                   want_classed: bool = False, map_slots: int = api.MAP_SIZE):
+    """Host-buffer feedback fold (classify_trace + trace_signature x2 + has_new_bits per exec,
+    src/engine.cpp:471-478).  Mutates virgin / edge_counts like has_new_bits mutates VirginMap."""
+    return default_context(device, map_slots).feedback_batch_host(raw, virgin, edge_counts, want_classed)

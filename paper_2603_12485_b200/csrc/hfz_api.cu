@@ -1,0 +1,247 @@
+// hfz_api.cu -- context management, error reporting, host-buffer front-end, Rng helpers.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "hfz_common.cuh"
+
+static thread_local char g_err[512] = "";
+
+void hfz_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int hfz_cuda_fail(cudaError_t e, const char* what) {
+  hfz_set_error("CUDA error %d (%s) in %s", (int)e, cudaGetErrorString(e), what);
+  return HFZ_ECUDA;
+}
+
+extern "C" int hfz_version(void) { return HFZ_VERSION; }
+extern "C" const char* hfz_last_error(void) { return g_err; }
+extern "C" uint64_t hfz_record_bytes(uint32_t map_slots) { return (uint64_t)(map_slots / 2) * 5; }
+
+extern "C" int hfz_ctx_create(hfz_ctx** out, int device, uint32_t map_slots, void* stream) {
+  if (!out) {
+    hfz_set_error("hfz_ctx_create: null out");
+    return HFZ_EINVAL;
+  }
+  *out = nullptr;
+  if (map_slots < 1024u || map_slots > (1u << 24) || (map_slots & (map_slots - 1u))) {
+    hfz_set_error("hfz_ctx_create: map_slots must be a power of two in [1024, 2^24], got %u",
+                  map_slots);
+    return HFZ_EINVAL;
+  }
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    hfz_set_error("no CUDA device available (%s); this library has no CPU fallback",
+                  e != cudaSuccess ? cudaGetErrorString(e) : "device count 0");
+    return HFZ_ECUDA;
+  }
+  if (device < 0 || device >= ndev) {
+    hfz_set_error("hfz_ctx_create: device %d out of range (%d devices)", device, ndev);
+    return HFZ_EINVAL;
+  }
+  HFZ_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  HFZ_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10) {
+    hfz_set_error("device %d is sm_%d%d; the kernels are built for sm_100a only", device,
+                  prop.major, prop.minor);
+    return HFZ_ECUDA;
+  }
+  hfz_ctx* c = new hfz_ctx;
+  c->device = device;
+  c->S = map_slots;
+  c->H = map_slots / 2;
+  c->rec_bytes = (uint64_t)c->H * 5;
+  c->stream = (cudaStream_t)stream;
+  c->num_sms = prop.multiProcessorCount;
+  c->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
+  cudaError_t a = cudaMalloc(&c->first, (size_t)map_slots * 8 * sizeof(uint32_t));
+  if (a == cudaSuccess) a = cudaMalloc(&c->cand_count, sizeof(uint32_t));
+  if (a == cudaSuccess) a = cudaMalloc(&c->prior, map_slots);
+  if (a == cudaSuccess) a = cudaMalloc(&c->delta, map_slots);
+  if (a == cudaSuccess) a = cudaMalloc(&c->v0, map_slots);
+  if (a != cudaSuccess) {
+    hfz_ctx_destroy(c);
+    hfz_set_error("hfz_ctx_create: scratch allocation failed (%s)", cudaGetErrorString(a));
+    return HFZ_ENOMEM;
+  }
+  *out = c;
+  return HFZ_OK;
+}
+
+extern "C" int hfz_ctx_destroy(hfz_ctx* c) {
+  if (!c) return HFZ_OK;
+  cudaSetDevice(c->device);
+  cudaFree(c->first);
+  cudaFree(c->cand_list);
+  cudaFree(c->cand_count);
+  cudaFree(c->prior);
+  cudaFree(c->delta);
+  cudaFree(c->v0);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(c->stage_raw[i]);
+    if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
+    if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
+  }
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  cudaFree(c->d_virgin);
+  cudaFree(c->d_counts);
+  cudaFree(c->d_admit);
+  cudaFree(c->d_sigf);
+  cudaFree(c->d_sigs);
+  cudaFree(c->d_nnz);
+  cudaFree(c->d_classed);
+  delete c;
+  return HFZ_OK;
+}
+
+extern "C" int hfz_ctx_set_stream(hfz_ctx* c, void* stream) {
+  if (!c) return HFZ_EINVAL;
+  c->stream = (cudaStream_t)stream;
+  return HFZ_OK;
+}
+
+extern "C" int hfz_ctx_sync(hfz_ctx* c) {
+  if (!c) return HFZ_EINVAL;
+  HFZ_CUDA(cudaSetDevice(c->device));
+  HFZ_CUDA(cudaStreamSynchronize(c->stream));
+  return HFZ_OK;
+}
+
+extern "C" uint32_t hfz_ctx_map_slots(const hfz_ctx* c) { return c ? c->S : 0; }
+extern "C" uint64_t hfz_ctx_launch_count(const hfz_ctx* c) { return c ? c->launches : 0; }
+
+extern "C" int hfz_ctx_set_option(hfz_ctx* c, const char* key, int64_t value) {
+  if (!c || !key) return HFZ_EINVAL;
+  if (!strcmp(key, "scan_warps")) {
+    if (value < 0 || value > 32) return HFZ_EINVAL;
+    c->scan_warps = (int)value;
+  } else if (!strcmp(key, "scan_variant")) {
+    if (value < 0 || value > 5) return HFZ_EINVAL;
+    c->scan_variant = (int)value;
+  } else if (!strcmp(key, "stage_execs")) {
+    if (value < 32 || c->stage_raw[0]) return HFZ_EINVAL;
+    c->stage_execs = (uint64_t)value;
+  } else {
+    hfz_set_error("hfz_ctx_set_option: unknown key %s", key);
+    return HFZ_EINVAL;
+  }
+  return HFZ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Host-buffer front-end: chunked, double-buffered H2D overlapped with the kernels.
+
+static int ensure_host_path(hfz_ctx* c, uint64_t n_exec, bool want_classed) {
+  if (!c->stage_raw[0]) {
+    if (c->stage_execs == 0) {
+      // ~256 MB per staging buffer
+      uint64_t se = (256ull << 20) / c->rec_bytes;
+      se = se < 32 ? 32 : (se / 32) * 32;
+      c->stage_execs = se;
+    }
+    for (int i = 0; i < 2; ++i) {
+      HFZ_CUDA(cudaMalloc(&c->stage_raw[i], c->stage_execs * c->rec_bytes));
+      HFZ_CUDA(cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming));
+      HFZ_CUDA(cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming));
+    }
+    HFZ_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    HFZ_CUDA(cudaMalloc(&c->d_virgin, c->S));
+    HFZ_CUDA(cudaMalloc(&c->d_counts, 2 * sizeof(uint64_t)));
+  }
+  if (c->d_out_cap < n_exec) {
+    cudaFree(c->d_admit);
+    cudaFree(c->d_sigf);
+    cudaFree(c->d_sigs);
+    cudaFree(c->d_nnz);
+    c->d_admit = nullptr;
+    c->d_sigf = c->d_sigs = nullptr;
+    c->d_nnz = nullptr;
+    c->d_out_cap = 0;
+    const uint64_t cap = n_exec < 1024 ? 1024 : n_exec;
+    HFZ_CUDA(cudaMalloc(&c->d_admit, cap));
+    HFZ_CUDA(cudaMalloc(&c->d_sigf, cap * 8));
+    HFZ_CUDA(cudaMalloc(&c->d_sigs, cap * 8));
+    HFZ_CUDA(cudaMalloc(&c->d_nnz, cap * 4));
+    c->d_out_cap = cap;
+  }
+  if (want_classed && !c->d_classed) {
+    HFZ_CUDA(cudaMalloc(&c->d_classed, c->stage_execs * (uint64_t)c->S));
+    c->d_classed_cap = c->stage_execs;
+  }
+  return HFZ_OK;
+}
+
+extern "C" int hfz_feedback_batch_host(hfz_ctx* c, const uint8_t* raw, uint64_t n_exec,
+                                       uint8_t* virgin, uint64_t* counts, uint8_t* classed,
+                                       uint8_t* admit, uint64_t* sigf, uint64_t* sigs,
+                                       uint32_t* nnz) {
+  if (!c || !virgin || !counts || (n_exec && (!raw || !admit || !sigf || !sigs))) {
+    hfz_set_error("hfz_feedback_batch_host: null argument");
+    return HFZ_EINVAL;
+  }
+  HFZ_CUDA(cudaSetDevice(c->device));
+  int rc = ensure_host_path(c, n_exec, classed != nullptr);
+  if (rc) return rc;
+  cudaStream_t st = c->stream;
+  HFZ_CUDA(cudaMemcpyAsync(c->d_virgin, virgin, c->S, cudaMemcpyHostToDevice, st));
+  HFZ_CUDA(cudaMemcpyAsync(c->d_counts, counts, 16, cudaMemcpyHostToDevice, st));
+  uint64_t done = 0;
+  int buf = 0;
+  bool used[2] = {false, false};
+  while (done < n_exec) {
+    const uint64_t n = n_exec - done < c->stage_execs ? n_exec - done : c->stage_execs;
+    if (used[buf]) HFZ_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev_done[buf], 0));
+    HFZ_CUDA(cudaMemcpyAsync(c->stage_raw[buf], raw + done * c->rec_bytes, n * c->rec_bytes,
+                             cudaMemcpyHostToDevice, c->copy_stream));
+    HFZ_CUDA(cudaEventRecord(c->ev_copied[buf], c->copy_stream));
+    HFZ_CUDA(cudaStreamWaitEvent(st, c->ev_copied[buf], 0));
+    rc = hfz_feedback_batch(c, c->stage_raw[buf], n, c->d_virgin, c->d_counts,
+                            classed ? c->d_classed : nullptr, c->d_admit + done, c->d_sigf + done,
+                            c->d_sigs + done, c->d_nnz + done);
+    if (rc) return rc;
+    if (classed)
+      HFZ_CUDA(cudaMemcpyAsync(classed + done * (uint64_t)c->S, c->d_classed, n * (uint64_t)c->S,
+                               cudaMemcpyDeviceToHost, st));
+    HFZ_CUDA(cudaEventRecord(c->ev_done[buf], st));
+    used[buf] = true;
+    buf ^= 1;
+    done += n;
+  }
+  if (n_exec) {
+    HFZ_CUDA(cudaMemcpyAsync(admit, c->d_admit, n_exec, cudaMemcpyDeviceToHost, st));
+    HFZ_CUDA(cudaMemcpyAsync(sigf, c->d_sigf, n_exec * 8, cudaMemcpyDeviceToHost, st));
+    HFZ_CUDA(cudaMemcpyAsync(sigs, c->d_sigs, n_exec * 8, cudaMemcpyDeviceToHost, st));
+    if (nnz) HFZ_CUDA(cudaMemcpyAsync(nnz, c->d_nnz, n_exec * 4, cudaMemcpyDeviceToHost, st));
+  }
+  HFZ_CUDA(cudaMemcpyAsync(virgin, c->d_virgin, c->S, cudaMemcpyDeviceToHost, st));
+  HFZ_CUDA(cudaMemcpyAsync(counts, c->d_counts, 16, cudaMemcpyDeviceToHost, st));
+  HFZ_CUDA(cudaStreamSynchronize(st));
+  return HFZ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Rng helpers (host arithmetic on a scalar state; include/hetfuzz/rng.hpp:11-46)
+
+extern "C" uint64_t hfz_rng_jump(uint64_t state, uint64_t k) { return state + k * HFZ_GAMMA; }
+
+extern "C" uint64_t hfz_rng_next(uint64_t* state) {
+  *state += HFZ_GAMMA;
+  return hfz_sm64_mix(*state);
+}
+
+extern "C" uint64_t hfz_rng_below(uint64_t* state, uint64_t n) {
+  if (n <= 1) return 0;
+  return (uint64_t)(((unsigned __int128)hfz_rng_next(state) * n) >> 64);
+}
+
+extern "C" uint64_t hfz_rng_split(uint64_t* state, uint64_t tag) {
+  const uint64_t s = hfz_rng_next(state);
+  return s ^ (tag * HFZ_GAMMA) ^ 0xd1b54a32d192ed03ULL;
+}

@@ -1,0 +1,170 @@
+// hfz_common.cuh -- shared device helpers and the context struct (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hfz.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "hfz kernels are written for sm_100a (B200) only"
+#endif
+
+// ---------------------------------------------------------------------------
+// Context
+
+struct hfz_ctx {
+  int device = 0;
+  uint32_t S = 0;          // logical slots
+  uint32_t H = 0;          // S / 2
+  uint64_t rec_bytes = 0;  // 5 * H
+  cudaStream_t stream = nullptr;
+  int num_sms = 0;
+  int max_smem_optin = 0;
+  uint64_t launches = 0;
+
+  // K2 scratch (owned)
+  uint32_t* first = nullptr;      // [S * 8] first local exec index showing (slot, class bit); ~0u = none
+  uint32_t* cand_list = nullptr;  // candidate exec indices (unordered)
+  uint64_t cand_cap = 0;
+  uint32_t* cand_count = nullptr;  // [1]
+  uint8_t* prior = nullptr;        // [S] P_r = V0 | OR_{q<r} D_q
+  uint8_t* delta = nullptr;        // [S] this rank's delta (hfz_feedback_batch)
+  uint8_t* v0 = nullptr;           // [S] batch-start snapshot
+
+  // host-buffer path staging (owned, lazily allocated)
+  uint8_t* stage_raw[2] = {nullptr, nullptr};
+  uint64_t stage_execs = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+  cudaEvent_t ev_done[2] = {nullptr, nullptr};
+  uint8_t* d_virgin = nullptr;
+  uint64_t* d_counts = nullptr;
+  uint8_t* d_admit = nullptr;
+  uint64_t* d_sigf = nullptr;
+  uint64_t* d_sigs = nullptr;
+  uint32_t* d_nnz = nullptr;
+  uint8_t* d_classed = nullptr;
+  uint64_t d_out_cap = 0;
+  uint64_t d_classed_cap = 0;
+
+  // tuning
+  int scan_warps = 0;    // 0 = auto
+  int scan_variant = 0;  // 0 = auto
+};
+
+void hfz_set_error(const char* fmt, ...);
+int hfz_cuda_fail(cudaError_t e, const char* what);
+
+#define HFZ_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t _e = (call);                             \
+    if (_e != cudaSuccess) return hfz_cuda_fail(_e, #call); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Arithmetic of the path
+
+// Host ladder (src/coverage.cpp:7-19): {1}->1 {2}->2 {3}->4 {4-7}->8 {8-15}->16
+// {16-31}->32 {32-127}->64 {128+}->128.  c in 1..255.
+__device__ __forceinline__ uint32_t hfz_class_host(uint32_t c) {
+  // rung = 0,1,2 for c = 1,2,3; else 1 + floor(log2 c) for 4..31 (3,4,5); 6 for 32..127; 7 above
+  uint32_t lg = 31u - __clz(c);                   // floor(log2 c), c >= 1
+  uint32_t r = c <= 3u ? c - 1u : (lg + 1u);      // 4-7 ->3, 8-15 ->4, 16-31 ->5, 32-63 ->6, 64-127 ->7, 128+ ->8
+  r = c >= 32u ? (c >= 128u ? 7u : 6u) : r;
+  return 1u << r;
+}
+
+// Device ladder (src/coverage.cpp:21-32): {1}->1 {2}->2 {3-511}->4 {512-4095}->8
+// {4096-16383}->16 {16384-65535}->32 {65536+}->64.  c >= 1, full u32 range.
+__device__ __forceinline__ uint32_t hfz_class_device(uint32_t c) {
+  uint32_t r = (c >= 2u) + (c >= 3u) + (c >= 512u) + (c >= 4096u) + (c >= 16384u) + (c >= 65536u);
+  return 1u << r;
+}
+
+// FNV-1a step (include/hetfuzz/coverage.hpp:208-213), P = 2^40 + 0x1b3.
+__device__ __forceinline__ uint64_t hfz_fnv(uint64_t h, uint32_t byte) {
+  return (h ^ (uint64_t)byte) * 1099511628211ULL;
+}
+#define HFZ_FNV_OFFSET 14695981039346656037ULL
+
+// splitmix64 (include/hetfuzz/rng.hpp:15-21)
+#define HFZ_GAMMA 0x9e3779b97f4a7c15ULL
+__host__ __device__ __forceinline__ uint64_t hfz_sm64_mix(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// ---------------------------------------------------------------------------
+// PTX wrappers: mbarrier + bulk async copy (TMA, 1-D) + proxy fence
+
+__device__ __forceinline__ uint32_t hfz_smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void hfz_mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(hfz_smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void hfz_fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void hfz_fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void hfz_mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(hfz_smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool hfz_mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(hfz_smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void hfz_mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!hfz_mbar_try_wait(bar, parity)) {
+  }
+}
+// global -> shared::cta bulk copy, completion on an mbarrier (SASS: UBLKCP)
+__device__ __forceinline__ void hfz_bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          hfz_smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(hfz_smem_u32(bar))
+      : "memory");
+}
+// same with an L2 evict-first policy for streamed-once data
+__device__ __forceinline__ void hfz_bulk_g2s_stream(void* smem_dst, const void* gsrc,
+                                                    uint32_t bytes, uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(hfz_smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(hfz_smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t hfz_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t hfz_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ uint4 hfz_ldg_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}

@@ -1,0 +1,206 @@
+"""K2/K2b/K4 parity: the CUDA feedback path vs the CPU oracle, bit-exact, through the C-ABI.
+
+Compared per exec: classed map bytes, Admit code, Full and Simple signatures, nnz; after the
+batch: every virgin byte and both distinct-edge counters.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2603_12485_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+S = 65536
+
+
+def run_gpu(ctx, raw, virgin0=None, counts0=None, want_classed=True):
+    d_raw = torch.from_numpy(raw).to(ctx.device)
+    virgin = ctx.new_virgin() if virgin0 is None else torch.from_numpy(virgin0).to(ctx.device)
+    counts = ctx.new_edge_counts() if counts0 is None else torch.from_numpy(counts0.view(np.int64)).to(ctx.device)
+    o = ctx.feedback_batch(d_raw, virgin, counts, want_classed=want_classed)
+    ctx.synchronize()
+    res = dict(admit=o["admit"].cpu().numpy(), sig_full=o["sig_full"].cpu().numpy().view(np.uint64),
+               sig_simple=o["sig_simple"].cpu().numpy().view(np.uint64),
+               nnz=o["nnz"].cpu().numpy().view(np.uint32))
+    if want_classed:
+        res["classed"] = o["classed"].cpu().numpy()
+    return res, virgin.cpu().numpy(), counts.cpu().numpy().view(np.uint64)
+
+
+def run_cpu(checker, raw, n, S_=S, virgin0=None, counts0=None, want_classed=True):
+    v = np.zeros(S_, np.uint8) if virgin0 is None else virgin0.copy()
+    c = np.zeros(2, np.uint64) if counts0 is None else counts0.copy()
+    o = checker.feedback_batch(raw, n, S_, v, c, want_classed=want_classed)
+    return o, v, c
+
+
+def assert_same(g, c):
+    (go, gv, gc), (co, cv, cc) = g, c
+    for k in co:
+        assert np.array_equal(go[k], co[k]), f"{k} differs at {np.nonzero(go[k] != co[k])[0][:8]}"
+    assert np.array_equal(gv, cv), "virgin differs"
+    assert np.array_equal(gc, cc), f"edge counts differ {gc} vs {cc}"
+
+
+@pytest.mark.parametrize("mode", ["iid", "campaign"])
+def test_config1_cold_start_1024(ctx, checker, mode):
+    """BASELINE.json configs[0]: 1,024 maps, ~2 % density, virgin starts empty so all three
+    Admit codes occur; the whole ordered sequence is compared."""
+    raw = synth.maps_iid(1024, S) if mode == "iid" else synth.maps_campaign(1024, S)
+    g = run_gpu(ctx, raw)
+    c = run_cpu(checker, raw, 1024)
+    assert_same(g, c)
+    assert len(set(c[0]["admit"].tolist())) >= 2
+
+
+def test_edge_vectors(ctx, checker):
+    raw, n = synth.maps_edge_cases(S)
+    assert_same(run_gpu(ctx, raw), run_cpu(checker, raw, n))
+    # and again in reverse order (full-density map last)
+    rec = synth.record_bytes(S)
+    rev = raw.reshape(n, rec)[::-1].copy().reshape(-1)
+    assert_same(run_gpu(ctx, rev), run_cpu(checker, rev, n))
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 32, 33, 63, 65, 257])
+def test_ragged_batch_sizes(ctx, checker, n):
+    raw = synth.maps_campaign(n, S, seed=1000 + n)
+    assert_same(run_gpu(ctx, raw), run_cpu(checker, raw, n))
+
+
+def test_empty_batch(ctx):
+    virgin = ctx.new_virgin()
+    counts = ctx.new_edge_counts()
+    raw = torch.zeros(0, dtype=torch.uint8, device=ctx.device)
+    o = ctx.feedback_batch(raw, virgin, counts)
+    ctx.synchronize()
+    assert o["admit"].numel() == 0 and int(virgin.sum()) == 0 and int(counts.sum()) == 0
+
+
+def test_virgin_carried_across_batches(ctx, checker):
+    """Warm virgin: fold 512 maps, then 512 more in a second call; equals one 1,024 fold."""
+    raw = synth.maps_campaign(1024, S, seed=77)
+    rec = synth.record_bytes(S)
+    a, b = raw[: 512 * rec], raw[512 * rec:]
+    d_v, d_c = ctx.new_virgin(), ctx.new_edge_counts()
+    o1 = ctx.feedback_batch(torch.from_numpy(a).to(ctx.device), d_v, d_c)
+    adm1 = o1["admit"].cpu().numpy()
+    o2 = ctx.feedback_batch(torch.from_numpy(b).to(ctx.device), d_v, d_c)
+    adm2 = o2["admit"].cpu().numpy()
+    co, cv, cc = run_cpu(checker, raw, 1024, want_classed=False)
+    assert np.array_equal(np.concatenate([adm1, adm2]), co["admit"])
+    assert np.array_equal(d_v.cpu().numpy(), cv)
+    assert np.array_equal(d_c.cpu().numpy().view(np.uint64), cc)
+
+
+def test_reference_known_answers(ctx):
+    """tests/test_coverage.cpp:157-259 restated: classify example, Admit sequence on slot
+    42/43/dev+9, OR-folding, byte-level FNV values."""
+    rec = synth.record_bytes(S)
+    H = S // 2
+
+    def mk(host=(), dev=()):
+        r = np.zeros(rec, np.uint8)
+        for i, v in host:
+            r[i] = v
+        d = r[H:].view(np.uint32)
+        for i, v in dev:
+            d[i - H] = v
+        return r
+
+    # signatures: {5: 3 hits -> class 4, 40000: 700 -> class 8}
+    m = mk(host=[(5, 3)], dev=[(40000, 700)])
+    (o, _, _) = run_gpu(ctx, m)
+    assert int(o["sig_simple"][0]) == 0x2E1A3655EF7B3874
+    assert int(o["sig_full"][0]) == 0x31CF681E15834C40
+    assert o["classed"][0][5] == 4 and o["classed"][0][40000] == 8 and o["nnz"][0] == 2
+    (o, _, _) = run_gpu(ctx, mk())
+    assert int(o["sig_simple"][0]) == 0xCBF29CE484222325 == int(o["sig_full"][0])
+    # classify example (test_coverage.cpp:157-175)
+    (o, _, _) = run_gpu(ctx, mk(host=[(10, 1), (500, 5)], dev=[(H + 3, 700), (S - 1, 2)]))
+    assert np.nonzero(o["classed"][0])[0].tolist() == [10, 500, H + 3, S - 1]
+    assert o["classed"][0][[10, 500, H + 3, S - 1]].tolist() == [1, 8, 8, 2]
+    # Admit sequence (test_coverage.cpp:177-221)
+    seq = [mk(host=[(42, 1)]), mk(host=[(42, 1)]), mk(host=[(42, 2)]), mk(host=[(42, 4)]),
+           mk(host=[(42, 5)]), mk(host=[(42, 3), (43, 1)]), mk(dev=[(H + 9, 1)])]
+    (o, v, c) = run_gpu(ctx, np.concatenate(seq))
+    assert o["admit"].tolist() == [2, 0, 1, 1, 0, 2, 2]
+    assert c.tolist() == [2, 1]
+    # OR-folding (test_coverage.cpp:223-237)
+    (o, v, c) = run_gpu(ctx, np.concatenate([mk(host=[(100, 9)], dev=[(H + 5, 600)]), mk(host=[(100, 1)])]))
+    assert v[100] == (16 | 1) and v[H + 5] == 8
+
+
+def test_host_buffer_path(ctx, checker):
+    """hfz_feedback_batch_host: chunked H2D staging gives the same fold."""
+    raw = synth.maps_campaign(300, S, seed=5)
+    v = np.zeros(S, np.uint8)
+    c = np.zeros(2, np.uint64)
+    o = ctx.feedback_batch_host(raw, v, c, want_classed=True)
+    co, cv, cc = run_cpu(checker, raw, 300)
+    for k in co:
+        assert np.array_equal(o[k], co[k]), k
+    assert np.array_equal(v, cv) and np.array_equal(c, cc)
+
+
+def test_sharded_scan_resolve_equals_sequential(ctx, checker):
+    """R simulated ranks on one GPU -- per-rank scan against V0, 'allgather' of
+    the deltas by concatenation, resolve in rank order -- must reproduce the single-rank
+    sequential Admit codes, virgin and counters."""
+    R, per = 4, 96
+    rec = synth.record_bytes(S)
+    warm = synth.maps_campaign(64, S, seed=9)
+    raw = synth.maps_campaign(R * per, S, seed=9, first=64, p_extra=8, p_rare=8)
+    v0 = np.zeros(S, np.uint8)
+    c0 = np.zeros(2, np.uint64)
+    checker.feedback_batch(warm, 64, S, v0, c0)
+    co, cv, cc = run_cpu(checker, raw, R * per, virgin0=v0, counts0=c0, want_classed=False)
+    shards = [torch.from_numpy(raw[r * per * rec:(r + 1) * per * rec]).to(ctx.device) for r in range(R)]
+    d_v0 = torch.from_numpy(v0).to(ctx.device)
+    import paper_2603_12485_b200 as hfz
+    ctxs = [hfz.Context(0) for _ in range(R)]
+    try:
+        scans = [ctxs[r].feedback_scan(shards[r], d_v0) for r in range(R)]
+        deltas = torch.cat([s["delta"] for s in scans])
+        admits, virgins, counts = [], [], []
+        for r in range(R):
+            v = d_v0.clone()
+            c = torch.from_numpy(c0.view(np.int64).copy()).to(ctx.device)
+            admits.append(ctxs[r].feedback_resolve(shards[r], v, c, deltas, R, r).cpu().numpy())
+            virgins.append(v.cpu().numpy())
+            counts.append(c.cpu().numpy().view(np.uint64))
+        assert np.array_equal(np.concatenate(admits), co["admit"])
+        for r in range(R):
+            assert np.array_equal(virgins[r], cv) and np.array_equal(counts[r], cc)
+        sf = np.concatenate([s["sig_full"].cpu().numpy().view(np.uint64) for s in scans])
+        assert np.array_equal(sf, co["sig_full"])
+    finally:
+        for c in ctxs:
+            c.close()
+
+
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5])
+def test_scan_variants_agree(ctx, checker, variant):
+    raw = synth.maps_campaign(200, S, seed=31)
+    ctx.set_option("scan_variant", variant)
+    try:
+        assert_same(run_gpu(ctx, raw), run_cpu(checker, raw, 200))
+    finally:
+        ctx.set_option("scan_variant", 0)
+
+
+def test_large_map_262144(checker):
+    """BASELINE.json configs[2] map size: 262,144 slots (virgin no longer fits shared memory)."""
+    import paper_2603_12485_b200 as hfz
+    from oracle import pyoracle
+    S2 = 262144
+    ck = pyoracle.Ref(S2) if pyoracle.Ref.available(S2) else pyoracle.Port()
+    c2 = hfz.Context(0, S2)
+    try:
+        raw = synth.maps_iid(48, S2, density=0.01, seed=3)
+        g = run_gpu(c2, raw)
+        c = run_cpu(ck, raw, 48, S_=S2)
+        assert_same(g, c)
+    finally:
+        c2.close()
