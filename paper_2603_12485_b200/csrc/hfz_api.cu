@@ -122,9 +122,13 @@ extern "C" int hfz_ctx_set_option(hfz_ctx* c, const char* key, int64_t value) {
   if (!strcmp(key, "scan_warps")) {
     if (value < 0 || value > 32) return HFZ_EINVAL;
     c->scan_warps = (int)value;
-  } else if (!strcmp(key, "scan_variant")) {
-    if (value < 0 || value > 5) return HFZ_EINVAL;
-    c->scan_variant = (int)value;
+  } else if (!strcmp(key, "scan_row")) {
+    if (value != 256 && value != 512) return HFZ_EINVAL;
+    c->scan_row = (int)value;
+  } else if (!strcmp(key, "scan_prefetch")) {
+    c->scan_prefetch = value != 0;
+  } else if (!strcmp(key, "virgin_smem")) {
+    c->virgin_smem = value != 0;
   } else if (!strcmp(key, "stage_execs")) {
     if (value < 32 || c->stage_raw[0]) return HFZ_EINVAL;
     c->stage_execs = (uint64_t)value;

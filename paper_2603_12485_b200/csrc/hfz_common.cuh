@@ -49,8 +49,10 @@ struct hfz_ctx {
   uint64_t d_classed_cap = 0;
 
   // tuning
-  int scan_warps = 0;    // 0 = auto
-  int scan_variant = 0;  // 0 = auto
+  int scan_warps = 0;     // 0 = as many as fit
+  int scan_row = 512;     // bytes per map per row (512 or 256)
+  int scan_prefetch = 1;  // L2 prefetch of the row after next
+  int virgin_smem = 1;    // stage V0 in shared memory when it fits
 };
 
 void hfz_set_error(const char* fmt, ...);

@@ -6,19 +6,15 @@
 //   per-exec order  src/engine.cpp:471-478
 //
 // Design (DESIGN.md has the long form):
-//  * scan: ONE pass over the raw maps.  A warp owns 32 maps, one per lane ("lane-per-map"):
-//    the FNV-1a signature is a strictly serial 64-bit chain per map, so the only way to keep
-//    all 32 lanes of a warp busy on it is to run 32 independent chains.  Every lane pulls its
-//    own map chunk by chunk into a padded shared-memory slot with a 1-D TMA bulk copy
-//    (cp.async.bulk + mbarrier, STAGES deep), builds a non-zero bitmask of the chunk with
-//    128-bit shared loads, and then only visits the ~2% non-zero slots: classify, look the
-//    virgin byte up in the shared-memory copy of V0 (TMA-staged once per CTA), advance both
-//    hash chains.  Nothing is written back except 21 bytes per map.
+//  * scan: ONE coalesced pass over the raw maps (see hfz_k_scan below).  Nothing is written
+//    back except 21 bytes per map.
 //  * exact sequential has_new_bits without a sequential pass: for every (slot, class bit) not
 //    in V0 the scan records the FIRST exec that shows it (atomicMin into `first`).  An exec's
 //    Admit code then only depends on whether it is that first exec (resolve kernel, runs on
 //    the few candidate maps only).  Final virgin = V0 | OR of the novelty deltas (merge).
 #include <stdio.h>
+
+#include <type_traits>
 
 #include "hfz_common.cuh"
 
@@ -41,6 +37,7 @@ struct ScanParams {
   uint32_t* nnz;
   uint8_t* classed;
   uint32_t n_groups;
+  int prefetch;
 };
 
 // non-zero-byte bitmask (4 bits) of a 32-bit word
@@ -68,107 +65,119 @@ struct Lane {
   }
 };
 
-// Process one staged chunk of CHUNK bytes belonging to this lane's map.
-template <int CHUNK, bool HOST, bool VSMEM, bool CLASSED>
-__device__ __forceinline__ void scan_chunk(const uint8_t* chunk, uint32_t slot_base,
-                                           Lane<VSMEM, CLASSED>& st, const uint8_t* virgin,
-                                           uint32_t* first, uint32_t e, uint8_t* classed_row) {
-  constexpr int NV = CHUNK / 16;  // uint4 per chunk
-  constexpr int NQ = CHUNK / 256; // 64-word mask registers
-  static_assert(NQ == 1 || NQ == 2, "CHUNK must be 256 or 512");
-  const uint4* c4 = reinterpret_cast<const uint4*>(chunk);
-  const uint32_t* c1 = reinterpret_cast<const uint32_t*>(chunk);
-  uint64_t mk[NQ];
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    uint32_t lo = 0, hi = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint4 v = c4[q * 16 + i];
-      lo |= ((v.x != 0u) | ((v.y != 0u) << 1) | ((v.z != 0u) << 2) | ((v.w != 0u) << 3)) << (4 * i);
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint4 v = c4[q * 16 + 8 + i];
-      hi |= ((v.x != 0u) | ((v.y != 0u) << 1) | ((v.z != 0u) << 2) | ((v.w != 0u) << 3)) << (4 * i);
-    }
-    mk[q] = ((uint64_t)hi << 32) | lo;
-  }
-  (void)NV;
-  uint64_t A = mk[0], B = NQ == 2 ? mk[NQ - 1] : 0ull;
-  uint32_t base = 0;
-  uint32_t w = 0, bm = 0, wpos = 0;
+// ---------------------------------------------------------------------------
+// K2 scan.
+//   phase A (per row of ROW bytes per map, per map m of the warp's group): the whole warp
+//           loads map m's chunk with ONE coalesced 128-bit load per lane (registers,
+//           L1::no_allocate, two register buffers of 16 loads); one ballot gives the chunk's
+//           non-zero-vector mask (handed to lane m through shared memory) and only the
+//           non-zero 16-byte vectors are scattered into lane m's padded shared-memory slot;
+//   phase B (per row): lane m walks ITS map's non-zero vectors: classify, virgin lookup in
+//           the TMA-staged shared copy of V0, both FNV chains -- 32 serial chains per warp.
+// The FNV-1a signature is a strictly serial 64-bit chain per map, so the only way to keep all
+// 32 lanes busy on it is to run 32 independent chains ("lane-per-map").
+// Work split: maps are dealt evenly to all warps (groups of <= 32 lanes), so the last wave is
+// never a mostly-empty one.  REC_CT is the compile-time record size (0 = run-time): it turns
+// the 32 per-map addresses of a row into immediates of one base register.
+template <int ROW>
+struct RowCfg {
+  static constexpr int kSlot = ROW + kPad;      // per-lane shared slot
+  static constexpr int kMapsPerLoad = 512 / ROW;  // maps covered by one warp-wide 128-bit load
+  static constexpr int kLanesPerMap = ROW / 16;
+  static constexpr int kLoads = 32 / kMapsPerLoad;  // loads per row
+};
+
+template <bool HOST, int ROW, bool VSMEM, bool CLASSED>
+__device__ __forceinline__ void phase_b(uint32_t slot_addr, uint32_t vm, uint32_t slot_base,
+                                        Lane<VSMEM, CLASSED>& st, const uint8_t* virgin,
+                                        uint32_t* first, uint32_t e, uint8_t* classed_row) {
+  uint32_t em = 0, vaddr = 0, vslot = 0;  // remaining non-zero elements of the current vector
   for (;;) {
-    if (bm == 0) {
-      if (NQ == 2 && A == 0) {
-        A = B;
-        B = 0;
-        base = 64;
+    if (em == 0) {
+      if (vm == 0) break;
+      const uint32_t vpos = __ffs(vm) - 1;
+      vm &= vm - 1;
+      vaddr = slot_addr + vpos * 16;
+      uint4 v;
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                   : "r"(vaddr));
+      if (HOST) {
+        em = nz_bytes(v.x) | (nz_bytes(v.y) << 4) | (nz_bytes(v.z) << 8) | (nz_bytes(v.w) << 12);
+        vslot = slot_base + vpos * 16;
+      } else {
+        em = min(v.x, 1u) | (min(v.y, 1u) << 1) | (min(v.z, 1u) << 2) | (min(v.w, 1u) << 3);
+        vslot = slot_base + vpos * 4;
       }
-      if (A == 0) break;
-      const uint32_t p = __ffsll((long long)A) - 1;
-      A &= A - 1;
-      wpos = base + p;
-      w = c1[wpos];
-      bm = HOST ? nz_bytes(w) : 1u;
     }
+    const uint32_t k = __ffs(em) - 1;
+    em &= em - 1;
+    uint32_t c;
     if (HOST) {
-      const uint32_t j = __ffs(bm) - 1;
-      bm &= bm - 1;
-      const uint32_t c = (w >> (8 * j)) & 0xffu;
-      st.visit(slot_base + wpos * 4 + j, hfz_class_host(c), virgin, first, e, classed_row);
+      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(c) : "r"(vaddr + k));
+      st.visit(vslot + k, hfz_class_host(c), virgin, first, e, classed_row);
     } else {
-      bm = 0;
-      st.visit(slot_base + wpos, hfz_class_device(w), virgin, first, e, classed_row);
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(c) : "r"(vaddr + k * 4));
+      st.visit(vslot + k, hfz_class_device(c), virgin, first, e, classed_row);
     }
   }
 }
 
-template <int CHUNK, int STAGES, bool VSMEM, bool CLASSED>
-__global__ void __launch_bounds__(1024, 1) hfz_k_scan(const ScanParams p) {
+template <int REC_CT, int ROW, bool VSMEM, bool CLASSED>
+__global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const ScanParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int SLOT = CHUNK + kPad;
-  constexpr int STAGE_BYTES = 32 * SLOT;
+  using C = RowCfg<ROW>;
+  constexpr int LB = C::kLoads / 2;  // loads per register buffer
+  constexpr int WARP_SMEM = 32 * C::kSlot + 128;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-
+  const uint64_t rec = REC_CT ? (uint64_t)REC_CT : p.rec_bytes;
   uint8_t* s_virgin = smem;
-  uint8_t* s_stage = smem + (VSMEM ? p.S : 0) + (size_t)warp * STAGES * STAGE_BYTES;
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + (VSMEM ? p.S : 0) +
-                                                (size_t)nwarps * STAGES * STAGE_BYTES);
-  uint64_t* bar_virgin = s_bar;                     // [1]
-  uint64_t* bar = s_bar + 1 + warp * STAGES;        // [STAGES] per warp
+  uint8_t* s_buf = smem + (VSMEM ? p.S : 0) + (size_t)warp * WARP_SMEM;
+  uint64_t* bar_virgin =
+      reinterpret_cast<uint64_t*>(smem + (VSMEM ? p.S : 0) + (size_t)nwarps * WARP_SMEM);
+  const uint32_t buf_addr = hfz_smem_u32(s_buf);
+  const uint32_t mask_addr = buf_addr + 32 * C::kSlot;  // [32] u32 per warp
 
-  if (threadIdx.x == 0) hfz_mbar_init(bar_virgin, 1);
-  if (lane == 0)
-    for (int s = 0; s < STAGES; ++s) hfz_mbar_init(bar + s, 1);
-  hfz_fence_barrier_init();
-  __syncthreads();
-
-  if (VSMEM && threadIdx.x == 0) {
-    // stage V0 in shared memory: one TMA bulk copy per 16 KB, kept in L2 for the other CTAs
-    const uint64_t pol = hfz_policy_evict_last();
-    hfz_mbar_expect_tx(bar_virgin, p.S);
-    for (uint32_t off = 0; off < p.S; off += 16384u) {
-      const uint32_t n = p.S - off < 16384u ? p.S - off : 16384u;
-      hfz_bulk_g2s_stream(s_virgin + off, p.v0 + off, n, bar_virgin, pol);
+  if (VSMEM) {
+    if (threadIdx.x == 0) {
+      hfz_mbar_init(bar_virgin, 1);
+      hfz_fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // V0 -> shared memory with TMA bulk copies (SASS: UBLKCP), kept in L2 for the other CTAs
+      const uint64_t pol = hfz_policy_evict_last();
+      hfz_mbar_expect_tx(bar_virgin, p.S);
+      for (uint32_t off = 0; off < p.S; off += 16384u) {
+        const uint32_t n = p.S - off < 16384u ? p.S - off : 16384u;
+        hfz_bulk_g2s_stream(s_virgin + off, p.v0 + off, n, bar_virgin, pol);
+      }
     }
   }
-
-  const uint64_t stream_pol = hfz_policy_evict_first();
-  const uint32_t rows_host = p.H / CHUNK;
-  const uint32_t rows = (uint32_t)(p.rec_bytes / CHUNK);
-  const uint32_t total_warps = gridDim.x * nwarps;
-  uint32_t it_issue = 0, it_wait = 0;  // running stage counters over the warp's lifetime
   const uint8_t* virgin = VSMEM ? s_virgin : p.v0;
   bool virgin_ready = !VSMEM;
 
-  for (uint32_t g = blockIdx.x + gridDim.x * warp; g < p.n_groups; g += total_warps) {
-    const uint64_t e64 = (uint64_t)g * 32 + lane;
-    const bool valid = e64 < p.n_exec;
+  // even split of the batch over all warps of the grid
+  const uint64_t W = (uint64_t)gridDim.x * nwarps;
+  const uint64_t wg = (uint64_t)warp * gridDim.x + blockIdx.x;
+  const uint64_t per = p.n_exec / W, rem = p.n_exec % W;
+  const uint64_t start = wg * per + (wg < rem ? wg : rem);
+  const uint64_t cnt = per + (wg < rem ? 1 : 0);
+  const uint32_t rows_host = p.H / ROW;
+  const uint32_t rows = (uint32_t)(rec / ROW);
+  const uint32_t my_slot = buf_addr + lane * C::kSlot;
+  // lane -> (map within load, 16-byte unit within the map's chunk)
+  const uint32_t sub = lane / C::kLanesPerMap, unit = lane % C::kLanesPerMap;
+  const uint32_t scat_addr = buf_addr + sub * C::kSlot + unit * 16;
+
+  for (uint64_t base = start; base < start + cnt; base += 32) {
+    const uint32_t nm = (uint32_t)min((uint64_t)32, start + cnt - base);
+    const bool valid = (uint32_t)lane < nm;
+    const uint64_t e64 = base + lane;
     const uint32_t e = (uint32_t)e64;
-    const uint8_t* src = p.raw + (valid ? e64 : 0) * p.rec_bytes;
-    const uint32_t n_valid = (uint32_t)min((uint64_t)32, p.n_exec - (uint64_t)g * 32);
     uint8_t* classed_row = CLASSED ? p.classed + e64 * p.S : nullptr;
+    // lane's source for load i: map (i*kMapsPerLoad + sub), unit `unit`
+    const uint8_t* gsrc = p.raw + (base + sub) * rec + unit * 16;
 
     Lane<VSMEM, CLASSED> st;
     st.hf = HFZ_FNV_OFFSET;
@@ -176,49 +185,94 @@ __global__ void __launch_bounds__(1024, 1) hfz_k_scan(const ScanParams p) {
     st.nnz = 0;
     st.novel = 0;
 
-    auto issue = [&](uint32_t row) {
-      const uint32_t s = it_issue % STAGES;
-      if (lane == 0) hfz_mbar_expect_tx(bar + s, n_valid * CHUNK);
-      __syncwarp();
-      if (valid)
-        hfz_bulk_g2s_stream(s_stage + s * STAGE_BYTES + lane * SLOT, src + (size_t)row * CHUNK,
-                            CHUNK, bar + s, stream_pol);
-      ++it_issue;
-    };
+    // maps >= nm of a partial group alias the group's last map: always in bounds, their
+    // votes are masked off below and their lanes never run phase B.
+    const uint32_t last = nm - 1;
+    auto run = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
+      uint4 A[LB], B[LB];
+      auto load = [&](uint4* X, uint32_t row, int half) {
+        const uint8_t* src = gsrc + (size_t)row * ROW;
+#pragma unroll
+        for (int i = 0; i < LB; ++i) {
+          const uint32_t m0 = (half * LB + i) * C::kMapsPerLoad;  // first map of this load
+          if (FULL) {
+            X[i] = hfz_ldg_stream(reinterpret_cast<const uint4*>(src + (size_t)m0 * rec));
+          } else {
+            const uint32_t m = min(m0 + sub, last) - sub;  // clamp to the last map of the group
+            X[i] = hfz_ldg_stream(reinterpret_cast<const uint4*>(src + (int64_t)(int32_t)m * (int64_t)rec));
+          }
+        }
+      };
+      auto scatter = [&](const uint4* X, int half) {
+#pragma unroll
+        for (int i = 0; i < LB; ++i) {
+          const uint32_t m0 = (half * LB + i) * C::kMapsPerLoad;
+          bool nz = (X[i].x | X[i].y | X[i].z | X[i].w) != 0u;
+          if (!FULL) nz = nz && (m0 + sub < nm);
+          const uint32_t b = __ballot_sync(0xffffffffu, nz);
+          if (lane == 0) {
+            if (C::kMapsPerLoad == 1) {
+              asm volatile("st.shared.u32 [%0], %1;" ::"r"(mask_addr + m0 * 4), "r"(b));
+            } else {
+              asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(mask_addr + m0 * 4),
+                           "r"(b & 0xffffu), "r"(b >> 16));
+            }
+          }
+          if (nz)
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(scat_addr + m0 * C::kSlot),
+                         "r"(X[i].x), "r"(X[i].y), "r"(X[i].z), "r"(X[i].w));
+        }
+      };
+      // L2 prefetch of the row after next (32 maps x ROW bytes, one 128-byte line per lane-step)
+      constexpr int PF_LINES = 32 * ROW / 128;  // lines per row
+      const uint32_t pf_map = (uint32_t)lane / (ROW / 128), pf_off = ((uint32_t)lane % (ROW / 128)) * 128;
+      auto prefetch = [&](uint32_t row) {
+        if (p.prefetch && row < rows) {
+#pragma unroll
+          for (int j = 0; j < PF_LINES / 32; ++j) {
+            const uint32_t m = pf_map + j * (32 / (ROW / 128));
+            if (FULL || m < nm)
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(p.raw + (base + m) * rec + pf_off +
+                                                            (size_t)row * ROW));
+          }
+        }
+      };
 
-    const uint32_t pre = rows < (uint32_t)(STAGES - 1) ? rows : (uint32_t)(STAGES - 1);
-    for (uint32_t r = 0; r < pre; ++r) issue(r);
-
-    if (!virgin_ready) {
-      hfz_mbar_wait(bar_virgin, 0);
-      virgin_ready = true;
-    }
-
-    for (uint32_t r = 0; r < rows; ++r) {
-      // the stage refilled here was consumed in iteration r-1 (all lanes passed __syncwarp)
-      if (r + STAGES - 1 < rows) issue(r + STAGES - 1);
-      const uint32_t s = it_wait % STAGES;
-      hfz_mbar_wait(bar + s, (it_wait / STAGES) & 1u);
-      ++it_wait;
-      if (valid) {
-        const uint8_t* chunk = s_stage + s * STAGE_BYTES + lane * SLOT;
-        if (r < rows_host)
-          scan_chunk<CHUNK, true, VSMEM, CLASSED>(chunk, r * CHUNK, st, virgin, p.first, e,
-                                                  classed_row);
-        else
-          scan_chunk<CHUNK, false, VSMEM, CLASSED>(chunk, p.H + (r - rows_host) * (CHUNK / 4), st,
-                                                   virgin, p.first, e, classed_row);
+      prefetch(1);
+      load(A, 0, 0);
+      if (!virgin_ready) {
+        hfz_mbar_wait(bar_virgin, 0);
+        virgin_ready = true;
       }
-      __syncwarp();
-      hfz_fence_proxy_async();
-    }
+      for (uint32_t r = 0; r < rows; ++r) {
+        load(B, r, 1);
+        prefetch(r + 2);
+        scatter(A, 0);
+        if (r + 1 < rows) load(A, r + 1, 0);
+        scatter(B, 1);
+        __syncwarp();
+        uint32_t vm;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(vm) : "r"(mask_addr + lane * 4));
+        if (!FULL && !valid) vm = 0;  // no branch on `valid`: idle lanes just see an empty mask
+        if (r < rows_host)
+          phase_b<true, ROW, VSMEM, CLASSED>(my_slot, vm, r * ROW, st, virgin, p.first, e, classed_row);
+        else
+          phase_b<false, ROW, VSMEM, CLASSED>(my_slot, vm, p.H + (r - rows_host) * (ROW / 4), st,
+                                              virgin, p.first, e, classed_row);
+        __syncwarp();
+      }
+    };
+    if (nm == 32)
+      run(std::true_type{});
+    else
+      run(std::false_type{});
 
     if (valid) {
       p.sig_full[e64] = st.hf;
       p.sig_simple[e64] = st.hs;
       if (p.nnz) p.nnz[e64] = st.nnz;
     }
-    // warp-aggregated append of the candidate execs
     const uint32_t cm = __ballot_sync(0xffffffffu, valid && st.novel);
     if (cm) {
       uint32_t basei = 0;
@@ -227,7 +281,7 @@ __global__ void __launch_bounds__(1024, 1) hfz_k_scan(const ScanParams p) {
       if (valid && st.novel) p.cand_list[basei + __popc(cm & ((1u << lane) - 1u))] = e;
     }
   }
-  if (!virgin_ready) hfz_mbar_wait(bar_virgin, 0);  // never leave a bulk copy in flight
+  if (!virgin_ready) hfz_mbar_wait(bar_virgin, 0);  // never leave the bulk copy in flight
 }
 
 // ---------------------------------------------------------------------------
@@ -345,56 +399,44 @@ __global__ void __launch_bounds__(256) hfz_k_resolve(const ResolveParams p) {
 // ---------------------------------------------------------------------------
 // launch plumbing
 
-template <int CHUNK, int STAGES>
+template <int ROW>
 size_t scan_smem_bytes(uint32_t S, bool vsmem, int warps) {
-  return (vsmem ? S : 0) + (size_t)warps * STAGES * 32 * (CHUNK + kPad) + (1 + warps * STAGES) * 8;
+  return (vsmem ? S : 0) + (size_t)warps * (32 * RowCfg<ROW>::kSlot + 128) + 16;
 }
 
-template <int CHUNK, int STAGES, bool VSMEM, bool CLASSED>
-int launch_scan_t(hfz_ctx* ctx, const ScanParams& p, int warps) {
-  auto kern = hfz_k_scan<CHUNK, STAGES, VSMEM, CLASSED>;
-  const size_t smem = scan_smem_bytes<CHUNK, STAGES>(p.S, VSMEM, warps);
+template <int REC_CT, int ROW, bool VSMEM, bool CLASSED>
+int launch_scan_t(hfz_ctx* ctx, const ScanParams& p) {
+  auto kern = hfz_k_scan<REC_CT, ROW, VSMEM, CLASSED>;
+  int warps = ROW == 512 ? 10 : 20;  // __launch_bounds__ of the kernel
+  while (warps > 1 && scan_smem_bytes<ROW>(p.S, VSMEM, warps) > (size_t)ctx->max_smem_optin) --warps;
+  if (ctx->scan_warps > 0 && ctx->scan_warps < warps) warps = ctx->scan_warps;
+  const size_t smem = scan_smem_bytes<ROW>(p.S, VSMEM, warps);
   HFZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  uint32_t grid = (uint32_t)ctx->num_sms;
-  if (grid > p.n_groups) grid = p.n_groups;
-  kern<<<grid, warps * 32, smem, ctx->stream>>>(p);
+  uint64_t grid = (uint64_t)ctx->num_sms;
+  if (grid * warps > p.n_exec) grid = (p.n_exec + warps - 1) / warps;  // >= one map per warp
+  kern<<<(uint32_t)grid, warps * 32, smem, ctx->stream>>>(p);
   ++ctx->launches;
   HFZ_CUDA(cudaGetLastError());
   return HFZ_OK;
 }
 
-template <int CHUNK, int STAGES>
-int launch_scan_v(hfz_ctx* ctx, const ScanParams& p, bool vsmem, int warps) {
+template <int REC_CT, bool VSMEM>
+int launch_scan_r(hfz_ctx* ctx, const ScanParams& p, int row) {
   const bool classed = p.classed != nullptr;
-  if (vsmem)
-    return classed ? launch_scan_t<CHUNK, STAGES, true, true>(ctx, p, warps)
-                   : launch_scan_t<CHUNK, STAGES, true, false>(ctx, p, warps);
-  return classed ? launch_scan_t<CHUNK, STAGES, false, true>(ctx, p, warps)
-                 : launch_scan_t<CHUNK, STAGES, false, false>(ctx, p, warps);
+  if (row == 256)
+    return classed ? launch_scan_t<REC_CT, 256, VSMEM, true>(ctx, p)
+                   : launch_scan_t<REC_CT, 256, VSMEM, false>(ctx, p);
+  return classed ? launch_scan_t<REC_CT, 512, VSMEM, true>(ctx, p)
+                 : launch_scan_t<REC_CT, 512, VSMEM, false>(ctx, p);
 }
 
-template <int CHUNK, int STAGES>
-int max_warps(const hfz_ctx* ctx, uint32_t S, bool vsmem) {
-  int w = 32;
-  while (w > 0 && scan_smem_bytes<CHUNK, STAGES>(S, vsmem, w) > (size_t)ctx->max_smem_optin) --w;
-  return w;
-}
-
-// pick the warp count (<= cap) that wastes the least of the last wave
-int pick_warps(const hfz_ctx* ctx, uint32_t n_groups, int cap) {
-  if (ctx->scan_warps > 0) return ctx->scan_warps < cap ? ctx->scan_warps : cap;
-  int best = cap;
-  double best_eff = 0;
-  for (int w = cap; w >= (cap + 1) / 2 && w >= 1; --w) {
-    const double workers = (double)ctx->num_sms * w;
-    const double waves = n_groups / workers;
-    const double eff = waves / (double)(uint64_t)(waves + 0.999999);
-    if (eff > best_eff + 0.02) {
-      best_eff = eff;
-      best = w;
-    }
-  }
-  return best;
+int launch_scan(hfz_ctx* ctx, const ScanParams& p) {
+  // virgin copy in shared memory whenever it leaves room for the per-warp slots
+  const bool vsmem = ctx->virgin_smem && p.S <= 65536u;
+  const int row = ctx->scan_row == 256 ? 256 : 512;
+  if (p.S == 65536u && vsmem) return launch_scan_r<163840, true>(ctx, p, row);
+  if (p.S == 262144u && !vsmem) return launch_scan_r<655360, false>(ctx, p, row);
+  return vsmem ? launch_scan_r<0, true>(ctx, p, row) : launch_scan_r<0, false>(ctx, p, row);
 }
 
 int ensure_cand(hfz_ctx* ctx, uint64_t n_exec) {
@@ -452,33 +494,8 @@ extern "C" int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t
     p.nnz = nnz_out;
     p.classed = classed_out;
     p.n_groups = (uint32_t)((n_exec + 31) / 32);
-    // virgin copy in shared memory whenever it leaves room for the staging ring
-    const bool vsmem = ctx->S <= 65536u;
-    int variant = ctx->scan_variant;
-    if (variant == 0) variant = 1;
-    int cap;
-    switch (variant) {
-      case 1: cap = max_warps<256, 3>(ctx, p.S, vsmem); break;
-      case 2: cap = max_warps<256, 4>(ctx, p.S, vsmem); break;
-      case 3: cap = max_warps<512, 2>(ctx, p.S, vsmem); break;
-      case 4: cap = max_warps<512, 3>(ctx, p.S, vsmem); break;
-      case 5: cap = max_warps<256, 2>(ctx, p.S, vsmem); break;
-      default:
-        hfz_set_error("unknown scan_variant %d", variant);
-        return HFZ_EINVAL;
-    }
-    if (cap < 1) {
-      hfz_set_error("scan: shared memory too small for map size %u", p.S);
-      return HFZ_EINVAL;
-    }
-    const int warps = pick_warps(ctx, p.n_groups, cap);
-    switch (variant) {
-      case 1: rc = launch_scan_v<256, 3>(ctx, p, vsmem, warps); break;
-      case 2: rc = launch_scan_v<256, 4>(ctx, p, vsmem, warps); break;
-      case 3: rc = launch_scan_v<512, 2>(ctx, p, vsmem, warps); break;
-      case 4: rc = launch_scan_v<512, 3>(ctx, p, vsmem, warps); break;
-      case 5: rc = launch_scan_v<256, 2>(ctx, p, vsmem, warps); break;
-    }
+    p.prefetch = ctx->scan_prefetch;
+    rc = launch_scan(ctx, p);
     if (rc) return rc;
   }
   hfz_k_delta<<<(ctx->S + 255) / 256, 256, 0, ctx->stream>>>(ctx->first, delta_out, ctx->S);

@@ -180,14 +180,30 @@ def test_sharded_scan_resolve_equals_sequential(ctx, checker):
             c.close()
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5])
-def test_scan_variants_agree(ctx, checker, variant):
+@pytest.mark.parametrize("opts", [dict(scan_row=256), dict(scan_row=512, scan_prefetch=0),
+                                  dict(scan_row=512, virgin_smem=0), dict(scan_row=256, scan_warps=3)])
+def test_scan_tunings_agree(ctx, checker, opts):
+    """Every tuning of the scan kernel (row size, warps, L2 prefetch, virgin in smem or not)
+    is the same function."""
     raw = synth.maps_campaign(200, S, seed=31)
-    ctx.set_option("scan_variant", variant)
+    for k, v in opts.items():
+        ctx.set_option(k, v)
     try:
         assert_same(run_gpu(ctx, raw), run_cpu(checker, raw, 200))
     finally:
-        ctx.set_option("scan_variant", 0)
+        for k, v in dict(scan_row=512, scan_warps=0, scan_prefetch=1, virgin_smem=1).items():
+            ctx.set_option(k, v)
+
+
+def test_many_maps_per_warp(ctx, checker):
+    """More maps than one group per warp: 3 warps x 148 CTAs must walk 32+ maps each."""
+    n = 148 * 3 * 32 + 148 * 3 * 5 + 7
+    raw = synth.maps_campaign(n, S, seed=13)
+    ctx.set_option("scan_warps", 3)
+    try:
+        assert_same(run_gpu(ctx, raw, want_classed=False), run_cpu(checker, raw, n, want_classed=False))
+    finally:
+        ctx.set_option("scan_warps", 0)
 
 
 def test_large_map_262144(checker):
