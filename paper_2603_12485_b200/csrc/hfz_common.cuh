@@ -163,10 +163,5 @@ __device__ __forceinline__ uint64_t hfz_policy_evict_last() {
   return p;
 }
 
-__device__ __forceinline__ uint4 hfz_ldg_stream(const uint4* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
+// streaming 128-bit load (ld.global.cs: evict-first, read once)
+__device__ __forceinline__ uint4 hfz_ldg_stream(const uint4* p) { return __ldcs(p); }

@@ -32,6 +32,7 @@ struct ScanParams {
   uint32_t* first;
   uint32_t* cand_list;
   uint32_t* cand_count;
+  uint32_t* cand_flags;
   uint64_t* sig_full;
   uint64_t* sig_simple;
   uint32_t* nnz;
@@ -88,37 +89,32 @@ struct RowCfg {
 };
 
 template <bool HOST, int ROW, bool VSMEM, bool CLASSED>
-__device__ __forceinline__ void phase_b(uint32_t slot_addr, uint32_t vm, uint32_t slot_base,
+__device__ __forceinline__ void phase_b(const uint8_t* slot, uint32_t vm, uint32_t slot_base,
                                         Lane<VSMEM, CLASSED>& st, const uint8_t* virgin,
                                         uint32_t* first, uint32_t e, uint8_t* classed_row) {
-  uint32_t em = 0, vaddr = 0, vslot = 0;  // remaining non-zero elements of the current vector
-  for (;;) {
-    if (em == 0) {
-      if (vm == 0) break;
-      const uint32_t vpos = __ffs(vm) - 1;
+  // Warp-uniform loop (exit by vote) so the warp is provably converged around it; lanes that
+  // have run out of entries are predicated off inside.
+  uint32_t em = 0, vpos = 0;  // remaining non-zero elements of the current vector
+  while (__any_sync(0xffffffffu, (vm | em) != 0u)) {
+    if (em == 0 && vm != 0) {
+      vpos = __ffs(vm) - 1;
       vm &= vm - 1;
-      vaddr = slot_addr + vpos * 16;
-      uint4 v;
-      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                   : "r"(vaddr));
-      if (HOST) {
+      const uint4 v = *reinterpret_cast<const uint4*>(slot + vpos * 16);
+      if (HOST)
         em = nz_bytes(v.x) | (nz_bytes(v.y) << 4) | (nz_bytes(v.z) << 8) | (nz_bytes(v.w) << 12);
-        vslot = slot_base + vpos * 16;
-      } else {
+      else
         em = min(v.x, 1u) | (min(v.y, 1u) << 1) | (min(v.z, 1u) << 2) | (min(v.w, 1u) << 3);
-        vslot = slot_base + vpos * 4;
-      }
     }
-    const uint32_t k = __ffs(em) - 1;
-    em &= em - 1;
-    uint32_t c;
-    if (HOST) {
-      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(c) : "r"(vaddr + k));
-      st.visit(vslot + k, hfz_class_host(c), virgin, first, e, classed_row);
-    } else {
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(c) : "r"(vaddr + k * 4));
-      st.visit(vslot + k, hfz_class_device(c), virgin, first, e, classed_row);
+    if (em != 0) {
+      const uint32_t k = __ffs(em) - 1;
+      em &= em - 1;
+      if (HOST) {
+        const uint32_t c = slot[vpos * 16 + k];
+        st.visit(slot_base + vpos * 16 + k, hfz_class_host(c), virgin, first, e, classed_row);
+      } else {
+        const uint32_t c = *reinterpret_cast<const uint32_t*>(slot + vpos * 16 + k * 4);
+        st.visit(slot_base + vpos * 4 + k, hfz_class_device(c), virgin, first, e, classed_row);
+      }
     }
   }
 }
@@ -135,8 +131,7 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
   uint8_t* s_buf = smem + (VSMEM ? p.S : 0) + (size_t)warp * WARP_SMEM;
   uint64_t* bar_virgin =
       reinterpret_cast<uint64_t*>(smem + (VSMEM ? p.S : 0) + (size_t)nwarps * WARP_SMEM);
-  const uint32_t buf_addr = hfz_smem_u32(s_buf);
-  const uint32_t mask_addr = buf_addr + 32 * C::kSlot;  // [32] u32 per warp
+  uint32_t* s_mask = reinterpret_cast<uint32_t*>(s_buf + 32 * C::kSlot);  // [32] u32 per warp
 
   if (VSMEM) {
     if (threadIdx.x == 0) {
@@ -165,10 +160,10 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
   const uint64_t cnt = per + (wg < rem ? 1 : 0);
   const uint32_t rows_host = p.H / ROW;
   const uint32_t rows = (uint32_t)(rec / ROW);
-  const uint32_t my_slot = buf_addr + lane * C::kSlot;
+  const uint8_t* my_slot = s_buf + lane * C::kSlot;
   // lane -> (map within load, 16-byte unit within the map's chunk)
   const uint32_t sub = lane / C::kLanesPerMap, unit = lane % C::kLanesPerMap;
-  const uint32_t scat_addr = buf_addr + sub * C::kSlot + unit * 16;
+  uint8_t* scat = s_buf + sub * C::kSlot + unit * 16;
 
   for (uint64_t base = start; base < start + cnt; base += 32) {
     const uint32_t nm = (uint32_t)min((uint64_t)32, start + cnt - base);
@@ -213,15 +208,12 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
           const uint32_t b = __ballot_sync(0xffffffffu, nz);
           if (lane == 0) {
             if (C::kMapsPerLoad == 1) {
-              asm volatile("st.shared.u32 [%0], %1;" ::"r"(mask_addr + m0 * 4), "r"(b));
+              s_mask[m0] = b;
             } else {
-              asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(mask_addr + m0 * 4),
-                           "r"(b & 0xffffu), "r"(b >> 16));
+              *reinterpret_cast<uint2*>(s_mask + m0) = make_uint2(b & 0xffffu, b >> 16);
             }
           }
-          if (nz)
-            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(scat_addr + m0 * C::kSlot),
-                         "r"(X[i].x), "r"(X[i].y), "r"(X[i].z), "r"(X[i].w));
+          if (nz) *reinterpret_cast<uint4*>(scat + m0 * C::kSlot) = X[i];
         }
       };
       // L2 prefetch of the row after next (32 maps x ROW bytes, one 128-byte line per lane-step)
@@ -249,11 +241,10 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
         load(B, r, 1);
         prefetch(r + 2);
         scatter(A, 0);
-        if (r + 1 < rows) load(A, r + 1, 0);
+        load(A, r + 1 < rows ? r + 1 : r, 0);  // unconditional (last one reloads row r, unused)
         scatter(B, 1);
         __syncwarp();
-        uint32_t vm;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(vm) : "r"(mask_addr + lane * 4));
+        uint32_t vm = s_mask[lane];
         if (!FULL && !valid) vm = 0;  // no branch on `valid`: idle lanes just see an empty mask
         if (r < rows_host)
           phase_b<true, ROW, VSMEM, CLASSED>(my_slot, vm, r * ROW, st, virgin, p.first, e, classed_row);
@@ -278,7 +269,11 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
       uint32_t basei = 0;
       if (lane == 0) basei = atomicAdd(p.cand_count, __popc(cm));
       basei = __shfl_sync(0xffffffffu, basei, 0);
-      if (valid && st.novel) p.cand_list[basei + __popc(cm & ((1u << lane) - 1u))] = e;
+      if (valid && st.novel) {
+        const uint32_t ci = basei + __popc(cm & ((1u << lane) - 1u));
+        p.cand_list[ci] = e;
+        p.cand_flags[ci] = 0;
+      }
     }
   }
   if (!virgin_ready) hfz_mbar_wait(bar_virgin, 0);  // never leave the bulk copy in flight
@@ -331,7 +326,9 @@ __global__ void hfz_k_merge(uint8_t* __restrict__ virgin, const uint8_t* __restr
 }
 
 // ---------------------------------------------------------------------------
-// K2b: exact Admit codes of the candidate execs.  One warp per candidate map.
+// K2b: exact Admit codes of the candidate execs.  Work item = (candidate, 16 KB piece of its
+// raw record), dealt round-robin to all warps; a piece ORs {1: new class bit on a known slot,
+// 2: new slot} into cand_flags[i]; hfz_k_admit turns the flags into Admit codes.
 struct ResolveParams {
   const uint8_t* raw;
   uint64_t rec_bytes;
@@ -340,6 +337,7 @@ struct ResolveParams {
   const uint32_t* first;
   const uint32_t* cand_list;
   const uint32_t* cand_count;
+  uint32_t* cand_flags;
   uint8_t* admit;
 };
 
@@ -358,41 +356,62 @@ __device__ __forceinline__ uint32_t resolve_entry(const ResolveParams& p, uint32
   return 1;
 }
 
-__global__ void __launch_bounds__(256) hfz_k_resolve(const ResolveParams p) {
+constexpr uint32_t kPiece = 16384;  // bytes per work item (divides H and 4H for S >= 32768... checked on host)
+
+__global__ void __launch_bounds__(256) hfz_k_resolve(const ResolveParams p, uint32_t piece) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t total_warps = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t n = *p.cand_count;
-  for (uint32_t i = warp; i < n; i += total_warps) {
-    const uint32_t e = p.cand_list[i];
-    const uint8_t* src = p.raw + (uint64_t)e * p.rec_bytes;
+  const uint32_t pieces = (uint32_t)(p.rec_bytes / piece);
+  const uint32_t host_pieces = p.H / piece;
+  const uint64_t items = (uint64_t)(*p.cand_count) * pieces;
+  for (uint64_t it = warp; it < items; it += total_warps) {
+    const uint32_t ci = (uint32_t)(it / pieces), pc = (uint32_t)(it % pieces);
+    const uint32_t e = p.cand_list[ci];
+    const uint4* src = reinterpret_cast<const uint4*>(p.raw + (uint64_t)e * p.rec_bytes + (uint64_t)pc * piece);
     uint32_t flags = 0;
-    const uint4* h4 = reinterpret_cast<const uint4*>(src);
-    for (uint32_t v = lane; v < p.H / 16; v += 32) {
-      const uint4 x = hfz_ldg_stream(h4 + v);
-      if ((x.x | x.y | x.z | x.w) == 0u) continue;
-      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+    const bool host = pc < host_pieces;
+    const uint32_t slot0 = host ? pc * piece : p.H + (pc - host_pieces) * (piece / 4);
+    for (uint32_t v0 = 0; v0 < piece / 16; v0 += 32 * 8) {
+      uint4 x[8];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        uint32_t bm = nz_bytes(w[k]);
-        while (bm) {
-          const uint32_t j = __ffs(bm) - 1;
-          bm &= bm - 1;
-          flags |= resolve_entry(p, v * 16 + k * 4 + j, hfz_class_host((w[k] >> (8 * j)) & 0xffu), e);
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t v = v0 + j * 32 + lane;
+        x[j] = v < piece / 16 ? hfz_ldg_stream(src + v) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if ((x[j].x | x[j].y | x[j].z | x[j].w) == 0u) continue;
+        const uint32_t v = v0 + j * 32 + lane;
+        const uint32_t w[4] = {x[j].x, x[j].y, x[j].z, x[j].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (host) {
+            uint32_t bm = nz_bytes(w[k]);
+            while (bm) {
+              const uint32_t b = __ffs(bm) - 1;
+              bm &= bm - 1;
+              flags |= resolve_entry(p, slot0 + v * 16 + k * 4 + b,
+                                     hfz_class_host((w[k] >> (8 * b)) & 0xffu), e);
+            }
+          } else if (w[k]) {
+            flags |= resolve_entry(p, slot0 + v * 4 + k, hfz_class_device(w[k]), e);
+          }
         }
       }
     }
-    const uint4* d4 = reinterpret_cast<const uint4*>(src + p.H);
-    for (uint32_t v = lane; v < p.H / 4; v += 32) {
-      const uint4 x = hfz_ldg_stream(d4 + v);
-      if ((x.x | x.y | x.z | x.w) == 0u) continue;
-      const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (w[k]) flags |= resolve_entry(p, p.H + v * 4 + k, hfz_class_device(w[k]), e);
-    }
     flags = __reduce_or_sync(0xffffffffu, flags);
-    if (lane == 0) p.admit[e] = (flags & 2u) ? 2 : ((flags & 1u) ? 1 : 0);
+    if (lane == 0 && flags) atomicOr(p.cand_flags + ci, flags);
+  }
+}
+
+__global__ void hfz_k_admit(const uint32_t* __restrict__ cand_list,
+                            const uint32_t* __restrict__ cand_count,
+                            const uint32_t* __restrict__ cand_flags, uint8_t* __restrict__ admit) {
+  const uint32_t n = *cand_count;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t f = cand_flags[i];
+    admit[cand_list[i]] = (f & 2u) ? 2 : ((f & 1u) ? 1 : 0);
   }
 }
 
@@ -445,7 +464,7 @@ int ensure_cand(hfz_ctx* ctx, uint64_t n_exec) {
   ctx->cand_list = nullptr;
   ctx->cand_cap = 0;
   const uint64_t cap = n_exec < 1024 ? 1024 : n_exec;
-  if (cudaMalloc(&ctx->cand_list, cap * sizeof(uint32_t)) != cudaSuccess) {
+  if (cudaMalloc(&ctx->cand_list, 2 * cap * sizeof(uint32_t)) != cudaSuccess) {
     hfz_set_error("cudaMalloc(cand_list, %llu) failed", (unsigned long long)cap * 4);
     return HFZ_ENOMEM;
   }
@@ -489,6 +508,7 @@ extern "C" int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t
     p.first = ctx->first;
     p.cand_list = ctx->cand_list;
     p.cand_count = ctx->cand_count;
+    p.cand_flags = ctx->cand_list + ctx->cand_cap;
     p.sig_full = sig_full_out;
     p.sig_simple = sig_simple_out;
     p.nnz = nnz_out;
@@ -545,11 +565,15 @@ extern "C" int hfz_feedback_resolve(hfz_ctx* ctx, const uint8_t* raw_maps, uint6
     p.first = ctx->first;
     p.cand_list = ctx->cand_list;
     p.cand_count = ctx->cand_count;
+    p.cand_flags = ctx->cand_list + ctx->cand_cap;
     p.admit = admit_out;
-    uint64_t blocks = (n_exec + 7) / 8;  // 8 warps per block, at most one warp per exec
-    const uint64_t maxb = (uint64_t)ctx->num_sms * 8;
-    if (blocks > maxb) blocks = maxb;
-    hfz_k_resolve<<<(uint32_t)blocks, 256, 0, ctx->stream>>>(p);
+    uint32_t piece = kPiece;
+    while (ctx->H % piece) piece >>= 1;  // H is a power of two >= 512
+    hfz_k_resolve<<<(uint32_t)ctx->num_sms * 4, 256, 0, ctx->stream>>>(p, piece);
+    ++ctx->launches;
+    HFZ_CUDA(cudaGetLastError());
+    hfz_k_admit<<<(uint32_t)ctx->num_sms, 256, 0, ctx->stream>>>(ctx->cand_list, ctx->cand_count,
+                                                                  p.cand_flags, admit_out);
     ++ctx->launches;
     HFZ_CUDA(cudaGetLastError());
   }
