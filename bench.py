@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""Headline benchmark: coverage-map evals/sec of the fused feedback step (BASELINE.json).
+
+    python bench.py --gpus N --steps K --warmup W [--impl reference]
+
+A "step" is one pass of the hot path (classify + has_new_bits + 2 signatures + virgin fold)
+over one batch of synthetic raw maps: configs[1] of BASELINE.json, a 65,536-exec batch of
+64 KB (65,536-slot) maps per GPU, ~2 % density, campaign-like novelty, virgin pre-warmed with
+4,096 maps.  N > 1 (launched by torchrun, one rank per GPU) shards the campaign batch
+(N x 65,536 execs), allgathers the per-rank novelty deltas over NCCL and merges in rank order
+("scaling": "weak").  Prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+
+S = 65536
+REC = (S // 2) * 5
+METRIC = "coverage_map_evals_per_sec"
+UNIT = "evals/s"
+
+
+def make_maps(n, first, mode):
+    from paper_2603_12485_b200 import synth
+    gen = synth.maps_campaign if mode == "campaign" else synth.maps_iid
+    return gen(n, S, first=first)
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            f = [x.strip() for x in r.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------- CPU baseline
+def cpu_feedback_rate(raw_sample, n_sample, v0, threads, min_seconds, reps_cap=64):
+    """Reference CPU path (classify_trace + 2x trace_signature + has_new_bits, engine.cpp:471-478)
+    on `threads` host threads, each folding the whole sample as an independent replica with a
+    private pre-warmed virgin map.  Returns (evals/s, kind, reps, seconds)."""
+    from oracle import pyoracle
+    if pyoracle.Ref.available(S):
+        ck = pyoracle.Ref(S)
+        h = ck.maps_create(raw_sample, n_sample)  # CoverageMap objects, outside the timed region
+
+        def fold(v, c):
+            ck.feedback_run(h, 0, n_sample, v, c)
+    else:
+        ck = pyoracle.Port()
+        h = None
+        adm = [np.zeros(n_sample, np.uint8) for _ in range(threads)]
+        sf = [np.zeros(n_sample, np.uint64) for _ in range(threads)]
+        ss = [np.zeros(n_sample, np.uint64) for _ in range(threads)]
+        nz = [np.zeros(n_sample, np.uint32) for _ in range(threads)]
+        tl = threading.local()
+
+        def fold(v, c, _i=[0]):
+            i = getattr(tl, "i", None)
+            if i is None:
+                i = tl.i = _i[0]
+                _i[0] += 1
+            ck._feedback(raw_sample, n_sample, S, v, c, None, adm[i], sf[i], ss[i], nz[i])
+
+    done = [0] * threads
+    stop_at = [None]
+
+    def worker(i):
+        reps = 0
+        while True:
+            v = v0.copy()
+            c = np.zeros(2, np.uint64)
+            fold(v, c)
+            reps += 1
+            if reps >= reps_cap or time.perf_counter() >= stop_at[0]:
+                break
+        done[i] = reps
+
+    t0 = time.perf_counter()
+    stop_at[0] = t0 + min_seconds
+    ths = [threading.Thread(target=worker, args=(i,)) for i in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    dt = time.perf_counter() - t0
+    if h is not None:
+        ck.maps_free(h)
+    total = sum(done) * n_sample
+    return total / dt, ck.kind, sum(done), dt
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU implementation on this box's host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n_sample = args.cpu_sample
+    raw = make_maps(n_sample, 0, args.mode)
+    warm = make_maps(4096, 1 << 24, args.mode)
+    from oracle import pyoracle
+    port = pyoracle.Port()
+    v0 = np.zeros(S, np.uint8)
+    port.feedback_batch(warm, 4096, S, v0, np.zeros(2, np.uint64))
+    for _ in range(args.warmup):
+        cpu_feedback_rate(raw, n_sample, v0, threads, 0.0, reps_cap=1)
+    rates, secs = [], 0.0
+    kind = "port"
+    for _ in range(args.steps):
+        r, kind, reps, dt = cpu_feedback_rate(raw, n_sample, v0, threads, args.cpu_seconds / max(1, args.steps))
+        rates.append(r)
+        secs += dt
+    value = float(np.mean(rates))
+    sample = (f"{n_sample} maps of the workload per replica, {threads} independent replicas "
+              f"(private pre-warmed virgin), each step ~{args.cpu_seconds / max(1, args.steps):.1f} s")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / max(1, args.steps) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32->u64", "data": "synthetic",
+        "config": {"workload": workload_name(args), "map_slots": S, "bytes_per_eval": REC,
+                   "execs_per_gpu": args.execs, "density": 0.02, "mode": args.mode},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_name(args):
+    return (f"BASELINE.json configs[1]: {args.execs}-exec batch of 64 KB (65,536-slot) maps per GPU, "
+            f"fused classify+has_new_bits+signatures, {args.mode}-like novelty, virgin pre-warmed with 4,096 maps")
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_12485_b200 as hfz
+    from paper_2603_12485_b200.sharding import ShardedFeedback
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback); use --impl reference for the CPU arm")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    assert world == args.gpus or world == 1, f"WORLD_SIZE={world} but --gpus {args.gpus}"
+
+    n = args.execs
+    ctx = hfz.Context(local_rank, S)
+    ctx.set_option("time_scan", 1)
+    # --- synthetic data: this rank's shard of the campaign batch, generated on the host in chunks
+    t0 = time.time()
+    raw = torch.empty(n * REC, dtype=torch.uint8, device=dev)
+    chunk = 4096
+    host_keep = None
+    for i in range(0, n, chunk):
+        m = min(chunk, n - i)
+        a = make_maps(m, rank * n + i, args.mode)
+        raw[i * REC:(i + m) * REC] = torch.from_numpy(a).to(dev)
+        if i == 0:
+            host_keep = a  # first chunk stays on the host: parity check + cpu_baseline sample
+    gen_s = time.time() - t0
+    # --- campaign state: virgin warmed by folding 4,096 maps (same on every rank)
+    virgin = ctx.new_virgin()
+    counts = ctx.new_edge_counts()
+    warm_host = make_maps(4096, 1 << 24, args.mode)
+    ctx.feedback_batch(torch.from_numpy(warm_host).to(dev), virgin, counts)
+    v0 = virgin.clone()
+    c0 = counts.clone()
+    eng = ShardedFeedback(ctx)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    out = None
+
+    def one_step():
+        nonlocal out
+        virgin.copy_(v0)  # every step folds the same batch into the same warmed state
+        counts.copy_(c0)
+        out = eng.step(raw, virgin, counts, out=out)
+
+    for _ in range(max(3, args.warmup)):
+        one_step()
+    barrier()
+    # --- parity spot check against the oracle on the first 512 execs of rank 0's shard (untimed)
+    parity = None
+    if rank == 0 and not args.no_check:
+        from oracle import pyoracle
+        ck = pyoracle.best_checker(S)
+        vv = v0.cpu().numpy().copy()
+        cc = c0.cpu().numpy().view(np.uint64).copy()
+        want = ck.feedback_batch(host_keep[:512 * REC], 512, S, vv, cc)
+        got_f = out["sig_full"][:512].cpu().numpy().view(np.uint64)
+        got_s = out["sig_simple"][:512].cpu().numpy().view(np.uint64)
+        got_a = out["admit"][:512].cpu().numpy()
+        parity = bool(np.array_equal(got_f, want["sig_full"]) and np.array_equal(got_s, want["sig_simple"])
+                      and np.array_equal(got_a, want["admit"]))
+        if not parity:
+            raise SystemExit("bench.py: GPU results differ from the oracle -- refusing to report a number")
+
+    ctx.get_stat("scan_ms_total")  # reset kernel-time accumulators
+    launches0 = ctx.launch_count
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.25)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        one_step()
+    e1.record()
+    barrier()
+    ms_total = e0.elapsed_time(e1)
+    scan_launches = args.steps
+    scan_ms = ctx.get_stat("scan_ms_total")
+    launches = ctx.launch_count - launches0
+    clocks = None
+    if sampler:
+        extra = 0
+        if ms_total < 600:  # nvidia-smi samples every 100 ms: keep the same load running a little longer
+            t_end = time.time() + 0.7
+            while time.time() < t_end:
+                one_step()
+                extra += 1
+            torch.cuda.synchronize()
+            ctx.get_stat("scan_ms_total")
+        clocks = sampler.stop()
+        if clocks is not None:
+            clocks["note"] = (f"sampled over the timed region plus {extra} identical untimed steps"
+                              if extra else "sampled over the timed region")
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_per_step = ms_total / args.steps
+    value = world * n / (ms_per_step / 1e3)
+    admits = int((out["admit"] != 0).sum().item())
+
+    # --- end-to-end through the C-ABI with HOST buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        n_e2e = args.e2e_execs or n
+        pinned = torch.empty(n_e2e * REC, dtype=torch.uint8, pin_memory=True)
+        pinned.copy_(raw[: n_e2e * REC])
+        raw_host = pinned.numpy()
+        v0_host = v0.cpu().numpy()
+        c0_host = c0.cpu().numpy().view(np.uint64)
+        ts = []
+        for i in range(1 + args.e2e_steps):
+            vh, ch = v0_host.copy(), c0_host.copy()
+            barrier()
+            t1 = time.perf_counter()
+            res = ctx.feedback_batch_host(raw_host, vh, ch)
+            dt = time.perf_counter() - t1
+            if i:
+                ts.append(dt)
+        te = torch.tensor([float(np.mean(ts))], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * n_e2e / float(te.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(n_e2e * REC + S + 16),
+               "d2h_bytes_per_step": int(n_e2e * (1 + 8 + 8 + 4) + S + 16),
+               "execs_per_step": n_e2e, "api": "hfz_feedback_batch_host (pinned host buffers, chunked overlapped H2D)"}
+        del pinned
+
+    if rank == 0:
+        peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        if os.path.exists(peaks_path):
+            peak = float(json.load(open(peaks_path))["hbm_gbs"])
+            peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)"
+        else:
+            peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+        algo_bytes = n * REC  # 163,840 B read per eval x evals per launch
+        achieved = algo_bytes / (scan_ms / scan_launches / 1e3) / 1e9
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "r1_scan_summary.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        roofline = {"bound": "hbm", "kernel": "hfz_k_scan", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": algo_bytes,
+                    "kernel_ms_per_launch": scan_ms / scan_launches,
+                    "step_frac": (world * n * REC / (ms_per_step / 1e3) / 1e9) / (peak * world)}
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            threads = os.cpu_count() or 1
+            rate, kind, reps, dt = cpu_feedback_rate(host_keep[: args.cpu_sample * REC], args.cpu_sample,
+                                                     v0.cpu().numpy(), threads, args.cpu_seconds)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind,
+                   "sample": f"first {args.cpu_sample} maps of the batch per replica, {threads} independent "
+                             f"replicas with private pre-warmed virgin maps, {reps} replica folds in {dt:.1f} s"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32->u64", "data": "synthetic",
+            "config": {"workload": workload_name(args), "map_slots": S, "bytes_per_eval": REC,
+                       "execs_per_gpu": n, "global_execs_per_step": world * n, "density": 0.02, "mode": args.mode,
+                       "l2_policy": "inputs larger than L2 (10.7 GB per GPU per step)",
+                       "admits_per_step_rank0": admits, "parallelism": f"exec-sharded x{world}",
+                       "gen_seconds": round(gen_s, 1), "parity_checked": parity},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks,
+            "hbm_gbs_algorithmic": world * n * REC / (ms_per_step / 1e3) / 1e9,
+            "logical_map_gbs": world * n * S / (ms_per_step / 1e3) / 1e9,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--execs", type=int, default=65536, help="executions per GPU per step")
+    ap.add_argument("--mode", default="campaign", choices=["campaign", "iid"])
+    ap.add_argument("--cpu-sample", type=int, default=2048)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-execs", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-check", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -79,10 +79,15 @@ HFZ_API int hfz_ctx_set_stream(hfz_ctx* ctx, void* stream);
 HFZ_API int hfz_ctx_sync(hfz_ctx* ctx);
 HFZ_API uint32_t hfz_ctx_map_slots(const hfz_ctx* ctx);
 HFZ_API uint64_t hfz_record_bytes(uint32_t map_slots);
-/* Tuning knobs, mostly for bench/profiling: key in {"scan_warps","scan_variant"} */
+/* Tuning knobs, mostly for bench/profiling: key in {"scan_warps","scan_row","scan_prefetch","virgin_smem","time_scan","stage_execs"} */
 HFZ_API int hfz_ctx_set_option(hfz_ctx* ctx, const char* key, int64_t value);
 /* Kernels launched by this context since creation (for bench.py's gpu_launches). */
 HFZ_API uint64_t hfz_ctx_launch_count(const hfz_ctx* ctx);
+/* Live kernel timing for the roofline line of bench.py: with option "time_scan" = 1 every
+ * launch of the scan kernel (K2, the dominant kernel) is bracketed by CUDA events on the
+ * context's stream.  key in {"scan_ms_total", "scan_launches"}; reading synchronises the
+ * stream and resets the accumulators. */
+HFZ_API int hfz_ctx_get_stat(hfz_ctx* ctx, const char* key, double* out);
 
 /* ------------------------------------------------------------------------- */
 /* Fused feedback (K2): replaces, for a whole batch folded IN EXEC ORDER,

@@ -30,6 +30,7 @@ PROTOTYPES = {
     "hfz_record_bytes": (_u64, [_u32]),
     "hfz_ctx_set_option": (C.c_int, [_vp, C.c_char_p, C.c_int64]),
     "hfz_ctx_launch_count": (_u64, [_vp]),
+    "hfz_ctx_get_stat": (C.c_int, [_vp, C.c_char_p, C.POINTER(C.c_double)]),
     "hfz_feedback_batch": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hfz_feedback_batch_host": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hfz_feedback_scan": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -59,7 +59,7 @@ class Context:
         self._h = h
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:
             lib.hfz_ctx_destroy(self._h)
             self._h = None
 
@@ -70,6 +70,11 @@ class Context:
 
     def set_option(self, key: str, value: int):
         check(lib.hfz_ctx_set_option(self._h, key.encode(), int(value)))
+
+    def get_stat(self, key: str) -> float:
+        v = C.c_double(0)
+        check(lib.hfz_ctx_get_stat(self._h, key.encode(), C.byref(v)))
+        return float(v.value)
 
     @property
     def launch_count(self) -> int:

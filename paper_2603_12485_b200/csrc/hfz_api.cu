@@ -89,6 +89,10 @@ extern "C" int hfz_ctx_destroy(hfz_ctx* c) {
     if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
     if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
   }
+  for (auto& ev : c->scan_events) {
+    cudaEventDestroy(ev.first);
+    cudaEventDestroy(ev.second);
+  }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   cudaFree(c->d_virgin);
   cudaFree(c->d_counts);
@@ -129,6 +133,8 @@ extern "C" int hfz_ctx_set_option(hfz_ctx* c, const char* key, int64_t value) {
     c->scan_prefetch = value != 0;
   } else if (!strcmp(key, "virgin_smem")) {
     c->virgin_smem = value != 0;
+  } else if (!strcmp(key, "time_scan")) {
+    c->time_scan = value != 0;
   } else if (!strcmp(key, "stage_execs")) {
     if (value < 32 || c->stage_raw[0]) return HFZ_EINVAL;
     c->stage_execs = (uint64_t)value;
@@ -137,6 +143,31 @@ extern "C" int hfz_ctx_set_option(hfz_ctx* c, const char* key, int64_t value) {
     return HFZ_EINVAL;
   }
   return HFZ_OK;
+}
+
+extern "C" int hfz_ctx_get_stat(hfz_ctx* c, const char* key, double* out) {
+  if (!c || !key || !out) return HFZ_EINVAL;
+  HFZ_CUDA(cudaSetDevice(c->device));
+  if (!strcmp(key, "scan_launches")) {
+    *out = (double)c->scan_events.size();
+    return HFZ_OK;
+  }
+  if (!strcmp(key, "scan_ms_total")) {
+    HFZ_CUDA(cudaStreamSynchronize(c->stream));
+    double total = 0;
+    for (auto& ev : c->scan_events) {
+      float ms = 0;
+      HFZ_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second));
+      total += ms;
+      cudaEventDestroy(ev.first);
+      cudaEventDestroy(ev.second);
+    }
+    c->scan_events.clear();
+    *out = total;
+    return HFZ_OK;
+  }
+  hfz_set_error("hfz_ctx_get_stat: unknown key %s", key);
+  return HFZ_EINVAL;
 }
 
 // ---------------------------------------------------------------------------

@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+#include <vector>
+
 #include "../../include/hfz.h"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -53,6 +56,8 @@ struct hfz_ctx {
   int scan_row = 512;     // bytes per map per row (512 or 256)
   int scan_prefetch = 1;  // L2 prefetch of the row after next
   int virgin_smem = 1;    // stage V0 in shared memory when it fits
+  int time_scan = 0;      // bracket scan launches with events (bench roofline)
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> scan_events;
 };
 
 void hfz_set_error(const char* fmt, ...);

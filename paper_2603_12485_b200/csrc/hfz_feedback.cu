@@ -515,7 +515,17 @@ extern "C" int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t
     p.classed = classed_out;
     p.n_groups = (uint32_t)((n_exec + 31) / 32);
     p.prefetch = ctx->scan_prefetch;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (ctx->time_scan) {
+      HFZ_CUDA(cudaEventCreate(&ev0));
+      HFZ_CUDA(cudaEventCreate(&ev1));
+      HFZ_CUDA(cudaEventRecord(ev0, ctx->stream));
+    }
     rc = launch_scan(ctx, p);
+    if (ctx->time_scan) {
+      HFZ_CUDA(cudaEventRecord(ev1, ctx->stream));
+      ctx->scan_events.emplace_back(ev0, ev1);
+    }
     if (rc) return rc;
   }
   hfz_k_delta<<<(ctx->S + 255) / 256, 256, 0, ctx->stream>>>(ctx->first, delta_out, ctx->S);

@@ -1,0 +1,60 @@
+"""Multi-GPU sharding of the feedback step: one process per GPU,
+``torch.distributed`` for the plumbing.
+
+The batch is partitioned into contiguous exec ranges in rank order; the only
+exchange step is ONE allgather of the per-rank novelty deltas (S bytes per rank,
+NCCL over NVLink/NVSwitch on GPUs).  Everything else is rank-local:
+
+    scan   (rank-local)   signatures, nnz, delta D_r = class bits not in V0
+    allgather(D_r)        R x S bytes
+    resolve (rank-local)  exact Admit codes against P_r = V0 | OR_{q<r} D_q, then the
+                          ordered merge virgin = V0 | D_0 | ... | D_{R-1}
+                          (bitwise OR in the reference's polarity == AFL's AND-merge)
+
+Exactness: the sequential virgin before global exec i is V0 | OR_{j<i} classed_j;
+maps with no novelty versus V0 contribute nothing, so the state at rank r's first
+exec is exactly P_r, and the rank-local first-occurrence resolve reproduces the
+single-rank sequential Admit codes (checked against the oracle in
+tests/test_sharding_gloo.py on CPU and tests/test_feedback_gpu.py on the GPU).
+
+The module is backend-agnostic: ``engine`` is anything with ``feedback_scan`` /
+``feedback_resolve`` (``api.Context`` in production).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n_total: int, world: int, rank: int):
+    """Contiguous exec range [start, start+count) of `rank`; earlier ranks take the remainder."""
+    per, rem = divmod(n_total, world)
+    start = rank * per + min(rank, rem)
+    return start, per + (1 if rank < rem else 0)
+
+
+class ShardedFeedback:
+    def __init__(self, engine, group=None):
+        self.engine = engine
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self._deltas = None
+
+    def step(self, raw_local: torch.Tensor, virgin: torch.Tensor, edge_counts: torch.Tensor,
+             out: dict | None = None):
+        """One campaign iteration on this rank's shard.  `virgin`/`edge_counts` are the
+        replicated campaign state (identical on all ranks before and after)."""
+        o = self.engine.feedback_scan(raw_local, virgin, out=out)
+        delta = o["delta"]
+        if self.world == 1:
+            deltas = delta
+        else:
+            if self._deltas is None or self._deltas.numel() != self.world * delta.numel():
+                self._deltas = torch.empty(self.world * delta.numel(), dtype=delta.dtype,
+                                           device=delta.device)
+            deltas = self._deltas
+            dist.all_gather_into_tensor(deltas, delta, group=self.group)
+        o["admit"] = self.engine.feedback_resolve(raw_local, virgin, edge_counts, deltas, self.world,
+                                                  self.rank, admit=o.get("admit"))
+        return o
