@@ -1,0 +1,416 @@
+// hfz_mutate.cu -- K3 batched mutators: havoc, splice, deterministic stage.
+//
+// Reference semantics (paths under /root/reference/proj):
+//   havoc_mutant            src/engine.cpp:119-193   (tables :27-38, write_le :46-49)
+//   splice_mutant           src/engine.cpp:195-204
+//   for_each_deterministic  src/engine.cpp:53-105
+//   Rng                     include/hetfuzz/rng.hpp:11-46
+//
+// One warp owns one slot.  The splitmix64 stream is warp-uniform (every lane advances the
+// same state), single-byte edits are done by lane 0 and block moves (erase / insert / copy)
+// by the whole warp on a working buffer that lives in shared memory when the slot's maximum
+// output fits (inputs up to ~5 KB: BASELINE.json configs[3]) and directly in the slot's
+// output region in global memory otherwise (inputs up to kMaxInputBytes = 1 MiB).
+#include <string.h>
+
+#include <vector>
+
+#include "hfz_common.cuh"
+
+namespace {
+
+constexpr uint32_t kMaxInput = HFZ_MAX_INPUT_BYTES;
+constexpr int kHavocWarps = 8;
+constexpr uint32_t kSmemCap = 6144;  // working buffer bytes per warp (>= 4096 + 1024)
+
+__constant__ int16_t c_interesting16[10] = {-32768, -129, 128, 255, 256, 512, 1000, 1024, 4096, 32767};
+__constant__ int32_t c_interesting32[8] = {(-2147483647 - 1), -100663046, -32769, 32768,
+                                           65535,             65536,      100663045, 2147483647};
+
+struct WarpRng {
+  uint64_t s;
+  uint32_t draws;
+  __device__ __forceinline__ uint64_t next() {
+    s += HFZ_GAMMA;
+    ++draws;
+    return hfz_sm64_mix(s);
+  }
+  // below(n): n <= 1 returns 0 WITHOUT drawing (rng.hpp:24-28)
+  __device__ __forceinline__ uint64_t below(uint64_t n) {
+    if (n <= 1) return 0;
+    return __umul64hi(next(), n);
+  }
+};
+
+// non-overlapping copy by one warp
+__device__ __forceinline__ void warp_copy(uint8_t* dst, const uint8_t* src, uint64_t n, int lane) {
+  if ((((uintptr_t)dst ^ (uintptr_t)src) & 15) == 0 && n >= 64) {
+    uint64_t head = (16 - ((uintptr_t)dst & 15)) & 15;
+    if (head > n) head = n;
+    for (uint64_t i = lane; i < head; i += 32) dst[i] = src[i];
+    const uint64_t body = (n - head) / 16;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+    for (uint64_t i = lane; i < body; i += 32) d4[i] = s4[i];
+    for (uint64_t i = head + body * 16 + lane; i < n; i += 32) dst[i] = src[i];
+  } else {
+    for (uint64_t i = lane; i < n; i += 32) dst[i] = src[i];
+  }
+}
+
+// overlapping move towards lower addresses: buf[dst + i] = buf[src + i], i ascending (dst < src)
+__device__ __forceinline__ void warp_move_down(uint8_t* buf, uint64_t dst, uint64_t src, uint64_t n,
+                                               int lane) {
+  for (uint64_t base = 0; base < n; base += 128) {
+    uint8_t v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t i = base + k * 32 + lane;
+      v[k] = i < n ? buf[src + i] : 0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t i = base + k * 32 + lane;
+      if (i < n) buf[dst + i] = v[k];
+    }
+    __syncwarp();
+  }
+}
+
+// overlapping move towards higher addresses: buf[dst + i] = buf[src + i], i descending (dst > src)
+__device__ __forceinline__ void warp_move_up(uint8_t* buf, uint64_t dst, uint64_t src, uint64_t n,
+                                             int lane) {
+  uint64_t done = 0;
+  while (done < n) {
+    const uint64_t chunk = n - done < 128 ? n - done : 128;
+    const uint64_t base = n - done - chunk;  // process the highest remaining chunk first
+    uint8_t v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t i = k * 32 + lane;
+      v[k] = i < chunk ? buf[src + base + i] : 0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t i = k * 32 + lane;
+      if (i < chunk) buf[dst + base + i] = v[k];
+    }
+    __syncwarp();
+    done += chunk;
+  }
+}
+
+__device__ __forceinline__ uint64_t havoc_cap(uint64_t len) {
+  const uint64_t m = len + 64 * 16;
+  return m > kMaxInput ? kMaxInput : m;
+}
+
+__global__ void __launch_bounds__(kHavocWarps * 32) hfz_k_havoc(
+    const uint8_t* __restrict__ in_bytes, const uint64_t* __restrict__ in_off, uint64_t n,
+    uint64_t* __restrict__ state, uint8_t* __restrict__ out_bytes,
+    const uint64_t* __restrict__ out_off, uint64_t* __restrict__ out_len,
+    uint32_t* __restrict__ draws_out) {
+  __shared__ __align__(16) uint8_t s_buf[kHavocWarps][kSmemCap];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint64_t j = (uint64_t)blockIdx.x * kHavocWarps + warp; j < n;
+       j += (uint64_t)gridDim.x * kHavocWarps) {
+    const uint64_t i0 = in_off[j];
+    uint64_t len = in_off[j + 1] - i0;
+    uint8_t* out = out_bytes + out_off[j];
+    const bool in_smem = havoc_cap(len) <= kSmemCap;
+    uint8_t* v = in_smem ? s_buf[warp] : out;
+    warp_copy(v, in_bytes + i0, len, lane);
+    __syncwarp();
+
+    WarpRng rng;
+    rng.s = state[j];
+    rng.draws = 0;
+    const uint64_t ops = 1 + rng.below(64);
+    for (uint64_t op = 0; op < ops; ++op) {
+      if (len == 0) {  // engine.cpp:124-129 (no 1 MiB clamp on this branch)
+        const uint64_t cnt = 1 + rng.below(8);
+        for (uint64_t i = 0; i < cnt; ++i) {
+          const uint8_t b = (uint8_t)rng.below(256);
+          if (lane == 0) v[len] = b;
+          ++len;
+        }
+        __syncwarp();
+        continue;
+      }
+      switch ((uint32_t)rng.below(9)) {
+        case 0: {  // flip one bit, MSB-first numbering
+          const uint64_t pos = rng.below(len * 8);
+          if (lane == 0) v[pos / 8] ^= (uint8_t)(0x80u >> (pos % 8));
+          break;
+        }
+        case 1: {  // random byte: the VALUE is drawn before the index (C++17 sequencing of '=')
+          const uint8_t val = (uint8_t)rng.below(256);
+          const uint64_t i = rng.below(len);
+          if (lane == 0) v[i] = val;
+          break;
+        }
+        case 2: {  // byte +/- delta
+          const uint8_t d = (uint8_t)(1 + rng.below(35));
+          const uint64_t i = rng.below(len);
+          const bool add = rng.below(2) < 1;
+          if (lane == 0) v[i] = (uint8_t)(add ? v[i] + d : v[i] - d);
+          break;
+        }
+        case 3: {  // interesting 16-bit, little endian
+          if (len < 2) break;
+          const uint64_t off = rng.below(len - 1);
+          const uint16_t val = (uint16_t)c_interesting16[rng.below(10)];
+          if (lane < 2) v[off + lane] = (uint8_t)(val >> (8 * lane));
+          break;
+        }
+        case 4: {  // interesting 32-bit, little endian
+          if (len < 4) break;
+          const uint64_t off = rng.below(len - 3);
+          const uint32_t val = (uint32_t)c_interesting32[rng.below(8)];
+          if (lane < 4) v[off + lane] = (uint8_t)(val >> (8 * lane));
+          break;
+        }
+        case 5: {  // delete a block
+          if (len < 2) break;
+          const uint64_t off = rng.below(len);
+          const uint64_t q = len / 4 ? len / 4 : 1;
+          const uint64_t max_n = len - off < q ? len - off : q;
+          const uint64_t cnt = 1 + rng.below(max_n);
+          __syncwarp();
+          warp_move_down(v, off, off + cnt, len - off - cnt, lane);
+          len -= cnt;
+          break;
+        }
+        case 6: {  // duplicate a block elsewhere (copy first, then insert)
+          const uint64_t src = rng.below(len);
+          const uint64_t lim = len - src < 16 ? len - src : 16;
+          const uint64_t cnt = 1 + rng.below(lim);
+          const uint64_t dst = rng.below(len + 1);
+          __syncwarp();
+          const uint8_t blk = (uint64_t)lane < cnt ? v[src + lane] : 0;
+          // insert with the 1 MiB clamp folded in: bytes that would land past the cap are dropped
+          const uint64_t new_len = len + cnt > kMaxInput ? kMaxInput : len + cnt;
+          __syncwarp();
+          if (new_len > dst + cnt) warp_move_up(v, dst + cnt, dst, new_len - dst - cnt, lane);
+          if ((uint64_t)lane < cnt && dst + lane < new_len) v[dst + lane] = blk;
+          len = new_len;
+          break;
+        }
+        case 7: {  // constant fill
+          const uint64_t off = rng.below(len);
+          const uint64_t lim = len - off < 16 ? len - off : 16;
+          const uint64_t cnt = 1 + rng.below(lim);
+          const uint8_t b = (uint8_t)rng.below(256);
+          if ((uint64_t)lane < cnt) v[off + lane] = b;
+          break;
+        }
+        default: {  // 8: swap two bytes
+          const uint64_t i = rng.below(len);
+          const uint64_t k = rng.below(len);
+          if (lane == 0) {
+            const uint8_t t = v[i];
+            v[i] = v[k];
+            v[k] = t;
+          }
+          break;
+        }
+      }
+      __syncwarp();
+      if (len > kMaxInput) len = kMaxInput;
+    }
+    if (in_smem) {
+      warp_copy(out, v, len, lane);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      out_len[j] = len;
+      state[j] = rng.s;
+      if (draws_out) draws_out[j] = rng.draws;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) hfz_k_splice(
+    const uint8_t* __restrict__ in_bytes, const uint64_t* __restrict__ in_off,
+    const uint32_t* __restrict__ a_idx, const uint32_t* __restrict__ b_idx, uint64_t n,
+    uint64_t* __restrict__ state, uint8_t* __restrict__ out_bytes,
+    const uint64_t* __restrict__ out_off, uint64_t* __restrict__ out_len) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t j = warp; j < n; j += nw) {
+    const uint64_t a0 = in_off[a_idx[j]], alen = in_off[a_idx[j] + 1] - a0;
+    const uint64_t b0 = in_off[b_idx[j]], blen = in_off[b_idx[j] + 1] - b0;
+    WarpRng rng;
+    rng.s = state[j];
+    rng.draws = 0;
+    const uint64_t ca = rng.below(alen + 1);
+    const uint64_t cb = rng.below(blen + 1);
+    const uint64_t total = ca + (blen - cb);
+    const uint64_t keep = total > kMaxInput ? kMaxInput : total;
+    const uint64_t head = ca < keep ? ca : keep;
+    uint8_t* out = out_bytes + out_off[j];
+    warp_copy(out, in_bytes + a0, head, lane);
+    warp_copy(out + head, in_bytes + b0 + cb, keep - head, lane);
+    if (lane == 0) {
+      out_len[j] = keep;
+      state[j] = rng.s;
+    }
+  }
+}
+
+struct DetPatch {
+  uint32_t off, width, value;
+};
+
+__global__ void __launch_bounds__(128) hfz_k_deterministic(const uint8_t* __restrict__ in,
+                                                           uint64_t len,
+                                                           const DetPatch* __restrict__ patches,
+                                                           uint8_t* __restrict__ out, uint64_t count) {
+  for (uint64_t m = blockIdx.x; m < count; m += gridDim.x) {
+    const DetPatch p = patches[m];
+    uint8_t* o = out + m * len;
+    for (uint64_t i = threadIdx.x; i < len; i += blockDim.x) {
+      uint8_t b = in[i];
+      if (i >= p.off && i < (uint64_t)p.off + p.width) b = (uint8_t)(p.value >> (8 * (i - p.off)));
+      o[i] = b;
+    }
+  }
+}
+
+// host enumeration of the deterministic stage in the reference's order (engine.cpp:53-105)
+const int8_t kI8[9] = {-128, -1, 0, 1, 16, 32, 64, 100, 127};
+const int16_t kI16[10] = {-32768, -129, 128, 255, 256, 512, 1000, 1024, 4096, 32767};
+const int32_t kI32[8] = {(-2147483647 - 1), -100663046, -32769, 32768, 65535, 65536, 100663045, 2147483647};
+
+uint64_t read_le(const uint8_t* p, unsigned w) {
+  uint64_t v = 0;
+  for (unsigned i = 0; i < w; ++i) v |= (uint64_t)p[i] << (8 * i);
+  return v;
+}
+
+uint64_t enumerate_det(const uint8_t* in, uint64_t len, std::vector<DetPatch>* out) {
+  uint64_t count = 0;
+  auto emit = [&](uint64_t off, unsigned w, uint64_t v) {
+    if (out) out->push_back(DetPatch{(uint32_t)off, w, (uint32_t)v});
+    ++count;
+  };
+  const uint64_t cap = len < 32 ? len : 32;  // kDetOffsetCap
+  for (uint64_t i = 0; i < cap; ++i)
+    for (int b = 7; b >= 0; --b) emit(i, 1, in[i] ^ (1u << b));
+  const unsigned widths[3] = {1, 2, 4};
+  for (unsigned w : widths) {
+    if (len < w) continue;
+    const uint64_t end = len - w + 1 < cap ? len - w + 1 : cap;
+    const uint64_t mask = (1ull << (8 * w)) - 1;
+    for (uint64_t i = 0; i < end; ++i) {
+      const uint64_t orig = read_le(in + i, w);
+      for (uint64_t d = 1; d <= 35; ++d) {
+        emit(i, w, (orig + d) & mask);
+        emit(i, w, (orig - d) & mask);
+      }
+    }
+  }
+  for (int wi = 0; wi < 3; ++wi) {
+    const unsigned w = widths[wi];
+    if (len < w) continue;
+    const uint64_t end = len - w + 1 < cap ? len - w + 1 : cap;
+    const uint64_t mask = (1ull << (8 * w)) - 1;
+    const int nv = wi == 0 ? 9 : (wi == 1 ? 10 : 8);
+    for (uint64_t i = 0; i < end; ++i) {
+      const uint64_t orig = read_le(in + i, w);
+      for (int k = 0; k < nv; ++k) {
+        const int64_t vv = wi == 0 ? kI8[k] : (wi == 1 ? kI16[k] : kI32[k]);
+        const uint64_t v = (uint64_t)vv & mask;
+        if (v == orig) continue;  // no-op overwrites are skipped
+        emit(i, w, v);
+      }
+    }
+  }
+  return count;
+}
+
+}  // namespace
+
+extern "C" uint64_t hfz_havoc_max_out(uint64_t in_len) {
+  const uint64_t m = in_len + 64 * 16;
+  return m > kMaxInput ? kMaxInput : m;
+}
+
+extern "C" int hfz_havoc_batch(hfz_ctx* ctx, const uint8_t* in_bytes, const uint64_t* in_off,
+                               uint64_t n, uint64_t* rng_state_inout, uint8_t* out_bytes,
+                               const uint64_t* out_off, uint64_t* out_len, uint32_t* draws_out) {
+  if (!ctx || (n && (!in_bytes || !in_off || !rng_state_inout || !out_bytes || !out_off || !out_len))) {
+    hfz_set_error("hfz_havoc_batch: null argument");
+    return HFZ_EINVAL;
+  }
+  if (n == 0) return HFZ_OK;
+  HFZ_CUDA(cudaSetDevice(ctx->device));
+  uint64_t blocks = (n + kHavocWarps - 1) / kHavocWarps;
+  const uint64_t maxb = (uint64_t)ctx->num_sms * 8;
+  if (blocks > maxb) blocks = maxb;
+  hfz_k_havoc<<<(uint32_t)blocks, kHavocWarps * 32, 0, ctx->stream>>>(
+      in_bytes, in_off, n, rng_state_inout, out_bytes, out_off, out_len, draws_out);
+  ++ctx->launches;
+  HFZ_CUDA(cudaGetLastError());
+  return HFZ_OK;
+}
+
+extern "C" int hfz_splice_batch(hfz_ctx* ctx, const uint8_t* in_bytes, const uint64_t* in_off,
+                                const uint32_t* a_idx, const uint32_t* b_idx, uint64_t n,
+                                uint64_t* rng_state_inout, uint8_t* out_bytes,
+                                const uint64_t* out_off, uint64_t* out_len) {
+  if (!ctx || (n && (!in_bytes || !in_off || !a_idx || !b_idx || !rng_state_inout || !out_bytes ||
+                     !out_off || !out_len))) {
+    hfz_set_error("hfz_splice_batch: null argument");
+    return HFZ_EINVAL;
+  }
+  if (n == 0) return HFZ_OK;
+  HFZ_CUDA(cudaSetDevice(ctx->device));
+  uint64_t blocks = (n + 7) / 8;
+  const uint64_t maxb = (uint64_t)ctx->num_sms * 8;
+  if (blocks > maxb) blocks = maxb;
+  hfz_k_splice<<<(uint32_t)blocks, 256, 0, ctx->stream>>>(in_bytes, in_off, a_idx, b_idx, n,
+                                                           rng_state_inout, out_bytes, out_off, out_len);
+  ++ctx->launches;
+  HFZ_CUDA(cudaGetLastError());
+  return HFZ_OK;
+}
+
+extern "C" uint64_t hfz_deterministic_count(const uint8_t* in_host, uint64_t in_len) {
+  if (!in_host && in_len) return 0;
+  return enumerate_det(in_host, in_len, nullptr);
+}
+
+extern "C" int hfz_deterministic_batch(hfz_ctx* ctx, const uint8_t* in_dev, uint64_t in_len,
+                                       const uint8_t* in_host, uint8_t* out_dev, uint64_t count) {
+  if (!ctx || (in_len && (!in_dev || !in_host)) || (count && in_len && !out_dev)) {
+    hfz_set_error("hfz_deterministic_batch: null argument");
+    return HFZ_EINVAL;
+  }
+  std::vector<DetPatch> patches;
+  const uint64_t want = enumerate_det(in_host, in_len, &patches);
+  if (want != count) {
+    hfz_set_error("hfz_deterministic_batch: count %llu does not match the input (%llu)",
+                  (unsigned long long)count, (unsigned long long)want);
+    return HFZ_EINVAL;
+  }
+  if (count == 0 || in_len == 0) return HFZ_OK;
+  HFZ_CUDA(cudaSetDevice(ctx->device));
+  DetPatch* d_p = nullptr;
+  HFZ_CUDA(cudaMalloc(&d_p, count * sizeof(DetPatch)));
+  cudaError_t e = cudaMemcpyAsync(d_p, patches.data(), count * sizeof(DetPatch),
+                                  cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess) {
+    const uint32_t blocks = (uint32_t)(count < 65535 ? count : 65535);
+    hfz_k_deterministic<<<blocks, 128, 0, ctx->stream>>>(in_dev, in_len, d_p, out_dev, count);
+    ++ctx->launches;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);  // patches / d_p must outlive the kernel
+  cudaFree(d_p);
+  if (e != cudaSuccess) return hfz_cuda_fail(e, "hfz_deterministic_batch");
+  return HFZ_OK;
+}

@@ -1,0 +1,106 @@
+"""The C-ABI library loads and exports every symbol include/hfz.h declares (no GPU needed),
+the host-side helpers behave, and the product package never touches the oracle."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "hfz.h")).read()
+    return sorted(set(re.findall(r"HFZ_API\s+[^;(]*?\b(hfz_\w+)\s*\(", src)))
+
+
+def test_header_symbols_exported():
+    import paper_2603_12485_b200 as hfz
+    syms = declared_symbols()
+    assert len(syms) >= 25
+    lib = ctypes.CDLL(hfz.LIB_PATH)
+    for s in syms:
+        assert hasattr(lib, s), f"{s} declared in include/hfz.h but not exported by libhfz.so"
+    out = subprocess.run(["nm", "-D", "--defined-only", hfz.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (hfz_\w+)", out))
+    assert exported == set(syms), f"header/library mismatch: {exported ^ set(syms)}"
+
+
+def test_prototypes_cover_header():
+    from paper_2603_12485_b200 import _lib
+    assert set(_lib.PROTOTYPES) == set(declared_symbols())
+
+
+def test_library_is_sm100a_only():
+    import paper_2603_12485_b200 as hfz
+    out = subprocess.run(["cuobjdump", "-lelf", hfz.LIB_PATH], capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+def test_host_rng_helpers_match_oracle(port):
+    import paper_2603_12485_b200 as hfz
+    from paper_2603_12485_b200._lib import lib
+    st = ctypes.c_uint64(0)
+    assert lib.hfz_rng_next(ctypes.byref(st)) == 0xE220A8397B1DCDAF
+    assert hfz.rng_jump(99, 17) == (99 + 17 * 0x9E3779B97F4A7C15) & ((1 << 64) - 1)
+    s = 12345
+    for tag in range(20):
+        a = hfz.rng_split(s, tag)
+        b = port.rng_split(s, tag)
+        assert a == b
+        s = a[1]
+    for n in (0, 1, 2, 3, 9, 256, 1 << 40, (1 << 64) - 1):
+        st = ctypes.c_uint64(777)
+        v = lib.hfz_rng_below(ctypes.byref(st), n)
+        assert (v, st.value) == port.rng_below(777, n)
+    assert lib.hfz_havoc_max_out(0) == 1024 and lib.hfz_havoc_max_out(1 << 20) == 1 << 20
+    assert lib.hfz_record_bytes(65536) == 163840 and lib.hfz_record_bytes(262144) == 655360
+
+
+def test_deterministic_count_is_host_arithmetic(port):
+    from paper_2603_12485_b200._lib import lib
+    import numpy as np
+    for ln in (0, 1, 2, 3, 4, 8, 40):
+        d = np.arange(ln, dtype=np.uint8)
+        buf = d if ln else np.zeros(1, np.uint8)
+        assert lib.hfz_deterministic_count(ctypes.c_void_p(buf.ctypes.data), ln) == len(port.deterministic(d.tobytes()))
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_2603_12485_b200 as hfz
+    from paper_2603_12485_b200._lib import lib
+    h = ctypes.c_void_p()
+    rc = lib.hfz_ctx_create(ctypes.byref(h), 0, 65536, None)
+    assert rc == hfz._lib.HFZ_ECUDA and b"no CPU fallback" in lib.hfz_last_error()
+    with pytest.raises(RuntimeError):
+        hfz.Context(0)
+    with pytest.raises(RuntimeError):
+        hfz.havoc_mutant(b"abc", 1)
+
+
+def test_bad_arguments():
+    from paper_2603_12485_b200._lib import lib
+    h = ctypes.c_void_p()
+    assert lib.hfz_ctx_create(ctypes.byref(h), 0, 65537, None) == 1   # not a power of two
+    assert lib.hfz_ctx_create(ctypes.byref(h), 0, 512, None) == 1     # too small
+    assert lib.hfz_ctx_create(None, 0, 65536, None) == 1
+    assert lib.hfz_feedback_batch(None, None, 0, None, None, None, None, None, None, None) == 1
+
+
+def test_product_does_not_import_oracle():
+    """Only tests/, __graft_entry__.smoke() and bench.py's CPU legs may touch oracle/."""
+    pkg = os.path.join(ROOT, "paper_2603_12485_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".hpp", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in txt.lower() or f == "sharding.py", f"{f} mentions the oracle"
+    for f in os.listdir(os.path.join(ROOT, "include")):
+        p = os.path.join(ROOT, "include", f)
+        if os.path.isfile(p):
+            assert "hfz_oracle" not in open(p).read()

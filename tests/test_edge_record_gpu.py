@@ -1,0 +1,173 @@
+"""K1 parity: batched edge record on the GPU vs the CPU oracle (and the reference runtime for
+the cases it pins), counter for counter."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2603_12485_b200 as hfz
+from paper_2603_12485_b200 import synth
+
+pytestmark = pytest.mark.gpu
+S, H = 65536, 32768
+
+
+def to_dev(ctx, tr):
+    i64 = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.uint64).view(np.int64)).to(ctx.device)
+    sites = np.ascontiguousarray(tr["sites"], np.uint32)
+    if sites.size == 0:
+        sites = np.zeros(1, np.uint32)
+    return (i64(tr["launch_off"]), torch.from_numpy(np.ascontiguousarray(tr["dims"], np.uint32).view(np.int32)).to(ctx.device),
+            i64(tr["thread_off"]), i64(tr["ev_off"]), torch.from_numpy(sites.view(np.int32)).to(ctx.device))
+
+
+def run_gpu(ctx, tr, n_exec):
+    lo, dims, to, eo, sites = to_dev(ctx, tr)
+    raw, ev = ctx.edge_record_batch(lo, dims, to, eo, sites, n_exec)
+    ctx.synchronize()
+    return raw.cpu().numpy(), ev.cpu().numpy().view(np.uint64)
+
+
+def pack(execs):
+    """execs: list of (dims (L,6), ev_off (T+1), sites) per exec -> batch layout."""
+    launch_off, dims, thread_off, ev_off, sites = [0], [], [0], [0], []
+    for d, e, s in execs:
+        d = np.asarray(d, np.uint32).reshape(-1, 6)
+        base_ev = len(sites)
+        t = 0
+        for l in range(d.shape[0]):
+            threads = int(np.prod(d[l].astype(np.uint64)))
+            dims.append(d[l])
+            thread_off.append(thread_off[-1] + threads)
+        ev_off.extend((np.asarray(e, np.uint64)[1:] + base_ev).tolist())
+        sites.extend(np.asarray(s, np.uint32).tolist())
+        launch_off.append(launch_off[-1] + d.shape[0])
+    return dict(launch_off=np.array(launch_off, np.uint64), dims=np.array(dims, np.uint32).reshape(-1, 6),
+                thread_off=np.array(thread_off, np.uint64), ev_off=np.array(ev_off, np.uint64),
+                sites=np.array(sites, np.uint32))
+
+
+def check(ctx, port, tr, n_exec, S_=S):
+    raw, ev = run_gpu(ctx, tr, n_exec)
+    want_raw, want_ev = port.edge_record_batch(tr["launch_off"], tr["dims"], tr["thread_off"], tr["ev_off"],
+                                               tr["sites"], n_exec, S_)
+    assert np.array_equal(ev, want_ev), (ev[:8], want_ev[:8])
+    assert np.array_equal(raw, want_raw)
+    return raw
+
+
+def chain(block, launches, grid=(1, 1, 1)):
+    threads = int(np.prod(block)) * int(np.prod(grid))
+    dims, ev, sites = [], [0], []
+    for ch in launches:
+        dims.append([*grid, *block])
+        for _ in range(threads):
+            sites.extend(ch)
+            ev.append(len(sites))
+    return (np.array(dims, np.uint32), np.array(ev, np.uint64), np.array(sites, np.uint32))
+
+
+def test_reference_chains(ctx, port):
+    """tests/test_hdvm.cpp:89-127 + acceptance criterion 5 as one batch."""
+    execs = [chain((t, 1, 1), [[11, 29, 11, 500]]) for t in (1, 31, 32, 33, 64, 100, 1024)]
+    execs.append(chain((33, 1, 1), [[7]]))
+    execs.append(chain((40, 1, 1), [[3, 9]], grid=(2, 2, 1)))
+    execs.append(chain((8, 1, 1), [[5, 6], [6, 5, 6]]))
+    execs += [chain((t, 1, 1), [[7777]]) for t in (1, 31, 32, 33, 64, 100, 1024)]
+    raw = check(ctx, port, pack(execs), len(execs))
+    rec = synth.record_bytes(S)
+    dev = raw.reshape(len(execs), rec)[:, H:].view(np.uint32)
+    assert dev[7][7] == 2
+    for k, t in enumerate((1, 31, 32, 33, 64, 100, 1024)):
+        assert dev[10 + k][7777] == (t + 31) // 32
+
+
+def test_divergence_and_loops(ctx, port):
+    """tests/test_hdvm.cpp:129-187."""
+    dims = np.array([[1, 1, 1, 32, 1, 1]], np.uint32)
+    s1, e1 = [], [0]
+    for t in range(32):
+        s1 += [10, 999] if t == 5 else [10]
+        e1.append(len(s1))
+    s2, e2 = [], [0]
+    for t in range(32):
+        s2 += [77] * ((t % 31) + 1)
+        e2.append(len(s2))
+    raw = check(ctx, port, pack([(dims, e1, s1), (dims, e2, s2)]), 2)
+    dev = raw.reshape(2, synth.record_bytes(S))[:, H:].view(np.uint32)
+    assert dev[0][10] == 1 and dev[0][((10 >> 1) ^ 999) % 32768] == 1
+    assert dev[1][77] == 1 and dev[1][(77 >> 1) ^ 77] == 30
+
+
+def test_random_3d_multi_launch(ctx, port):
+    from tests.test_oracle_vs_ref import random_exec
+    rng = np.random.default_rng(11)
+    execs = [random_exec(rng, int(rng.integers(1, 4)), three_d=bool(i % 2)) for i in range(80)]
+    check(ctx, port, pack(execs), len(execs))
+
+
+def test_many_distinct_sites_forces_partitioning(ctx, port):
+    """Fully divergent warps with far more distinct sites than the per-warp table holds."""
+    rng = np.random.default_rng(12)
+    execs = []
+    for _ in range(3):
+        dims = np.array([[2, 1, 1, 64, 1, 1]], np.uint32)
+        ev, sites = [0], []
+        for t in range(128):
+            n = int(rng.integers(20, 60))
+            sites.extend(rng.integers(0, 2 ** 32, n, dtype=np.uint64).tolist())
+            # plus revisits of earlier sites so the k-th visit rule matters
+            sites.extend(int(sites[int(i)]) for i in rng.integers(max(0, len(sites) - 50), len(sites), 10))
+            ev.append(len(sites))
+        execs.append((dims, ev, sites))
+    check(ctx, port, pack(execs), 3)
+
+
+def test_empty_and_invalid_launches(ctx, port):
+    """Threads without events, an exec without launches; reference rejects oversized launches."""
+    d = np.array([[1, 1, 1, 40, 1, 1]], np.uint32)
+    ev = np.zeros(41, np.uint64)
+    execs = [(d, ev, []), (np.zeros((0, 6), np.uint32), [0], []), chain((16, 1, 1), [[1, 2, 3]])]
+    check(ctx, port, pack(execs), 3)
+
+
+def test_synthetic_config3_shape(ctx, port):
+    """BASELINE.json configs[2] trace recipe (4 launches x 16x256 threads) on a few execs, then the
+    fused feedback kernel on the produced maps."""
+    tr = synth.bb_traces(6, seed=44)
+    raw = check(ctx, port, tr, 6)
+    virgin, counts = ctx.new_virgin(), ctx.new_edge_counts()
+    o = ctx.feedback_batch(torch.from_numpy(raw).to(ctx.device), virgin, counts)
+    v = np.zeros(S, np.uint8)
+    c = np.zeros(2, np.uint64)
+    want = port.feedback_batch(raw, 6, S, v, c)
+    assert np.array_equal(o["admit"].cpu().numpy(), want["admit"])
+    assert np.array_equal(o["sig_full"].cpu().numpy().view(np.uint64), want["sig_full"])
+
+
+def test_large_map_262144_edges(port):
+    """262,144-slot map: 131,072 device slots do not fit shared memory -> global-atomic path."""
+    S2 = 262144
+    c2 = hfz.Context(0, S2)
+    try:
+        tr = synth.bb_traces(3, seed=5, grid=(4, 1, 1), block=(128, 1, 1), n_launch=2)
+        check(c2, port, tr, 3, S_=S2)
+    finally:
+        c2.close()
+
+
+def test_host_edge_record(ctx, port):
+    rng = np.random.default_rng(13)
+    seqs = [rng.integers(0, H, int(rng.integers(0, 4000)), dtype=np.uint64).astype(np.uint16) for _ in range(20)]
+    seqs.append(np.zeros(3000, np.uint16))          # one slot hit 3000 times: never-zero wrap
+    seqs.append(np.zeros(0, np.uint16))
+    off = np.zeros(len(seqs) + 1, np.uint64)
+    np.cumsum([len(s) for s in seqs], out=off[1:])
+    flat = np.concatenate(seqs + [np.zeros(1, np.uint16)])
+    raw = ctx.host_edge_record_batch(torch.from_numpy(off.view(np.int64)).to(ctx.device),
+                                     torch.from_numpy(flat.view(np.int16)).to(ctx.device), len(seqs))
+    ctx.synchronize()
+    raw = raw.cpu().numpy().reshape(len(seqs), synth.record_bytes(S))
+    for i, s in enumerate(seqs):
+        want, _ = port.host_edge_record(s)
+        assert np.array_equal(raw[i, :H], want), i
+    assert raw[-2, 0] == (3000 - 1) % 255 + 1
