@@ -1,0 +1,218 @@
+// hetfuzz/coverage.hpp -- source-compatible stand-in for the reference header of the same name
+// (proj/include/hetfuzz/coverage.hpp) whose data-parallel functions run on the B200:
+//   classify_trace / has_new_bits / trace_signature  -> K2 (hfz_feedback_batch_host)
+// The containers are plain host value types like the reference's; each single-item call is a
+// batch-of-one device call (latency-bound, kept for API parity) -- fuzzers should use
+// hetfuzz::b200::feedback_batch.  Header-only; link with libhfz.so.  No CPU implementation of
+// the classify / novelty / signature path exists here.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cstring>
+#include <unordered_map>
+#include <vector>
+
+#include "b200.hpp"
+
+namespace hetfuzz {
+
+inline constexpr std::uint32_t kMapSize = 65536;
+inline constexpr std::uint32_t kHostSlots = kMapSize / 2;
+inline constexpr std::uint32_t kDeviceIndexBase = kHostSlots;
+
+// One execution's raw map: u8 never-zero host counters + u32 device warp counters.
+class CoverageMap {
+ public:
+  CoverageMap() : host_(kHostSlots, 0), device_(kMapSize - kHostSlots, 0) {}
+
+  void host_increment(std::uint32_t idx) {
+    if (idx >= kHostSlots) {  // audited, then folded into the host half
+      ++host_violations_;
+      idx &= kHostSlots - 1;
+    }
+    const std::uint8_t next = static_cast<std::uint8_t>(host_[idx] + 1);
+    host_[idx] = next == 0 ? 1 : next;  // a wrap never reads as "unvisited"
+  }
+  void device_store(std::uint32_t logical_idx, std::uint32_t count) {
+    if (logical_idx < kDeviceIndexBase || logical_idx >= kMapSize) {
+      ++device_violations_;
+      logical_idx = kDeviceIndexBase + logical_idx % (kMapSize - kHostSlots);
+    }
+    device_[logical_idx - kDeviceIndexBase] = count;
+  }
+  std::uint8_t host_at(std::uint32_t idx) const { return host_[idx]; }
+  std::uint32_t device_at(std::uint32_t logical_idx) const { return device_[logical_idx - kDeviceIndexBase]; }
+  std::uint64_t count_at(std::uint32_t logical_idx) const {
+    return logical_idx < kHostSlots ? host_[logical_idx] : device_[logical_idx - kDeviceIndexBase];
+  }
+  const std::vector<std::uint8_t>& host_half() const { return host_; }
+  const std::vector<std::uint32_t>& device_half() const { return device_; }
+  std::uint64_t host_partition_violations() const { return host_violations_; }
+  std::uint64_t device_partition_violations() const { return device_violations_; }
+
+  // raw record in the library's layout: [host u8 x H][device u32 x H]
+  void pack(std::uint8_t* rec) const {
+    std::memcpy(rec, host_.data(), kHostSlots);
+    std::memcpy(rec + kHostSlots, device_.data(), std::size_t(kMapSize - kHostSlots) * 4);
+  }
+
+ private:
+  std::vector<std::uint8_t> host_;
+  std::vector<std::uint32_t> device_;
+  std::uint64_t host_violations_ = 0, device_violations_ = 0;
+};
+
+struct HostEdgeState {
+  std::uint16_t prev_loc = 0;
+};
+inline void host_edge_update(HostEdgeState& st, std::uint16_t cur_loc, CoverageMap& map) {
+  map.host_increment(static_cast<std::uint32_t>(st.prev_loc ^ cur_loc));
+  st.prev_loc = static_cast<std::uint16_t>(cur_loc >> 1);
+}
+inline std::uint32_t device_edge_index(std::uint32_t prev_loc, std::uint32_t cur_loc) {
+  return kDeviceIndexBase + ((prev_loc ^ cur_loc) % kHostSlots);
+}
+
+class DeviceEdgeState {
+ public:
+  std::uint32_t get(std::uint64_t tid) const {
+    auto it = prev_.find(tid);
+    return it == prev_.end() ? 0u : it->second;
+  }
+  void set(std::uint64_t tid, std::uint32_t v) { prev_[tid] = v; }
+  void clear() { prev_.clear(); }
+  std::size_t size() const { return prev_.size(); }
+
+ private:
+  std::unordered_map<std::uint64_t, std::uint32_t> prev_;
+};
+
+// Bucket ladders as data (rung lower bound -> one-hot class).  classify() on a single scalar is
+// table lookup for callers that need it; the batch path classifies on the device.
+class BucketLadder {
+ public:
+  struct Rung {
+    std::uint64_t lower;
+    std::uint8_t klass;
+  };
+  explicit BucketLadder(std::vector<Rung> rungs) : rungs_(std::move(rungs)) {}
+  std::uint8_t classify(std::uint64_t count) const {
+    std::uint8_t k = 0;
+    for (const Rung& r : rungs_)
+      if (count >= r.lower) k = r.klass;
+    return k;
+  }
+  const std::vector<Rung>& rungs() const { return rungs_; }
+  static const BucketLadder& host() {
+    static const BucketLadder l({{1, 1}, {2, 2}, {3, 4}, {4, 8}, {8, 16}, {16, 32}, {32, 64}, {128, 128}});
+    return l;
+  }
+  static const BucketLadder& device() {
+    static const BucketLadder l({{1, 1}, {2, 2}, {3, 4}, {512, 8}, {4096, 16}, {16384, 32}, {65536, 64}});
+    return l;
+  }
+
+ private:
+  std::vector<Rung> rungs_;
+};
+
+struct ClassedTrace {
+  std::vector<std::uint8_t> classed;   // kMapSize class bytes
+  std::vector<std::uint32_t> nonzero;  // ascending logical indices
+  ClassedTrace() : classed(kMapSize, 0) {}
+};
+
+class VirginMap {
+ public:
+  VirginMap() : bits_(kMapSize, 0) {}
+  std::uint8_t at(std::uint32_t idx) const { return bits_[idx]; }
+  bool edge_known(std::uint32_t idx) const { return bits_[idx] != 0; }
+  std::uint64_t host_edges() const { return edges_[0]; }
+  std::uint64_t device_edges() const { return edges_[1]; }
+  void observe(std::uint32_t idx, std::uint8_t klass) {
+    if (!bits_[idx]) ++edges_[idx < kHostSlots ? 0 : 1];
+    bits_[idx] = static_cast<std::uint8_t>(bits_[idx] | klass);
+  }
+  // direct access for the batched device calls
+  std::uint8_t* data() { return bits_.data(); }
+  std::uint64_t* edge_counts() { return edges_; }
+
+ private:
+  std::vector<std::uint8_t> bits_;
+  std::uint64_t edges_[2] = {0, 0};
+};
+
+enum class Admit : std::uint8_t { None = 0, NewCounts = 1, NewEdges = 2 };
+enum class SignatureMode : std::uint8_t { Full, Simple };
+
+namespace detail {
+// A raw record that classifies to exactly the given class bytes (lowest count of each rung):
+// has_new_bits / trace_signature take a ClassedTrace, the device path takes raw maps.
+inline void record_from_classed(const ClassedTrace& t, std::vector<std::uint8_t>& rec) {
+  static const std::uint32_t host_lo[8] = {1, 2, 3, 4, 8, 16, 32, 128};
+  static const std::uint32_t dev_lo[8] = {1, 2, 3, 512, 4096, 16384, 65536, 65536};
+  rec.assign(std::size_t(kHostSlots) * 5, 0);
+  for (std::uint32_t idx : t.nonzero) {
+    const std::uint8_t k = t.classed[idx];
+    int rung = 0;
+    while (rung < 7 && !(k >> rung & 1)) ++rung;
+    if (idx < kHostSlots) {
+      rec[idx] = static_cast<std::uint8_t>(host_lo[rung]);
+    } else {
+      const std::uint32_t c = dev_lo[rung];
+      std::memcpy(&rec[kHostSlots + std::size_t(idx - kHostSlots) * 4], &c, 4);
+    }
+  }
+}
+}  // namespace detail
+
+inline ClassedTrace classify_trace(const CoverageMap& map) {
+  std::vector<std::uint8_t> rec(std::size_t(kHostSlots) * 5);
+  map.pack(rec.data());
+  std::vector<std::uint8_t> scratch_virgin(kMapSize, 0);
+  std::uint64_t counts[2] = {0, 0};
+  b200::FeedbackResult r =
+      b200::feedback_batch(b200::default_context(), rec.data(), 1, scratch_virgin.data(), counts, true);
+  ClassedTrace out;
+  out.classed = std::move(r.classed);
+  out.nonzero.reserve(r.nnz[0]);
+  for (std::uint32_t i = 0; i < kMapSize; ++i)
+    if (out.classed[i]) out.nonzero.push_back(i);
+  return out;
+}
+
+inline Admit has_new_bits(const ClassedTrace& trace, VirginMap& virgin) {
+  std::vector<std::uint8_t> rec;
+  detail::record_from_classed(trace, rec);
+  b200::FeedbackResult r =
+      b200::feedback_batch(b200::default_context(), rec.data(), 1, virgin.data(), virgin.edge_counts());
+  return static_cast<Admit>(r.admit[0]);
+}
+
+inline std::uint64_t trace_signature(const ClassedTrace& trace, SignatureMode mode) {
+  std::vector<std::uint8_t> rec;
+  detail::record_from_classed(trace, rec);
+  std::vector<std::uint8_t> scratch_virgin(kMapSize, 0);
+  std::uint64_t counts[2] = {0, 0};
+  b200::FeedbackResult r =
+      b200::feedback_batch(b200::default_context(), rec.data(), 1, scratch_virgin.data(), counts);
+  return mode == SignatureMode::Full ? r.sig_full[0] : r.sig_simple[0];
+}
+
+inline void merge_device_into_map(const std::vector<std::uint32_t>& counters, CoverageMap& map) {
+  for (std::size_t i = 0; i < counters.size(); ++i)
+    if (counters[i]) map.device_store(kDeviceIndexBase + static_cast<std::uint32_t>(i), counters[i]);
+}
+
+// FNV-1a constants and helpers used by callers outside the hot path (dedup keys).
+inline constexpr std::uint64_t kFnvOffset = 14695981039346656037ULL;
+inline constexpr std::uint64_t kFnvPrime = 1099511628211ULL;
+inline std::uint64_t fnv1a_step(std::uint64_t h, std::uint8_t byte) { return (h ^ byte) * kFnvPrime; }
+inline std::uint64_t fnv1a_bytes(std::uint64_t h, const void* data, std::size_t len) {
+  const auto* p = static_cast<const std::uint8_t*>(data);
+  while (len--) h = fnv1a_step(h, *p++);
+  return h;
+}
+
+}  // namespace hetfuzz

@@ -212,6 +212,18 @@ HFZ_API uint64_t hfz_deterministic_count(const uint8_t* in_host, uint64_t in_len
 HFZ_API int hfz_deterministic_batch(hfz_ctx* ctx, const uint8_t* in_dev, uint64_t in_len,
                                     const uint8_t* in_host, uint8_t* out_dev, uint64_t count);
 
+/* HOST-buffer forms of the mutators (what include/hetfuzz/engine.hpp and the pybind-style
+ * single-item calls use): same semantics, all pointers are host memory, synchronous. */
+HFZ_API int hfz_havoc_batch_host(hfz_ctx* ctx, const uint8_t* in_bytes, const uint64_t* in_off,
+                                 uint64_t n, uint64_t* rng_state_inout, uint8_t* out_bytes,
+                                 const uint64_t* out_off, uint64_t* out_len, uint32_t* draws_out);
+HFZ_API int hfz_splice_batch_host(hfz_ctx* ctx, const uint8_t* in_bytes, const uint64_t* in_off,
+                                  uint64_t n_inputs, const uint32_t* a_idx, const uint32_t* b_idx,
+                                  uint64_t n, uint64_t* rng_state_inout, uint8_t* out_bytes,
+                                  const uint64_t* out_off, uint64_t* out_len);
+HFZ_API int hfz_deterministic_host(hfz_ctx* ctx, const uint8_t* in, uint64_t in_len, uint8_t* out,
+                                   uint64_t count);
+
 /* Rng helpers (host side, O(1)): rng.hpp:15-21,39-42.  State after k draws =
  * state + k*gamma; split() child seed of the tag-th split from a parent state. */
 HFZ_API uint64_t hfz_rng_jump(uint64_t state, uint64_t k);

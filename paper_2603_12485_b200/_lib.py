@@ -44,6 +44,9 @@ PROTOTYPES = {
     "hfz_splice_batch": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
     "hfz_deterministic_count": (_u64, [_vp, _u64]),
     "hfz_deterministic_batch": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _u64]),
+    "hfz_havoc_batch_host": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp]),
+    "hfz_splice_batch_host": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
+    "hfz_deterministic_host": (C.c_int, [_vp, _vp, _u64, _vp, _u64]),
     "hfz_rng_jump": (_u64, [_u64, _u64]),
     "hfz_rng_next": (_u64, [C.POINTER(_u64)]),
     "hfz_rng_below": (_u64, [C.POINTER(_u64), _u64]),

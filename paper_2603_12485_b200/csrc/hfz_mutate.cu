@@ -414,3 +414,123 @@ extern "C" int hfz_deterministic_batch(hfz_ctx* ctx, const uint8_t* in_dev, uint
   if (e != cudaSuccess) return hfz_cuda_fail(e, "hfz_deterministic_batch");
   return HFZ_OK;
 }
+
+// ---------------------------------------------------------------------------
+// host-buffer forms: stage through temporary device buffers, synchronous
+
+namespace {
+struct DevBuf {
+  void* p = nullptr;
+  ~DevBuf() { if (p) cudaFree(p); }
+  cudaError_t alloc(size_t n) { return cudaMalloc(&p, n ? n : 16); }
+  template <typename T> T* as() { return static_cast<T*>(p); }
+};
+#define HFZ_TRY(call)                                          \
+  do {                                                         \
+    cudaError_t _e = (call);                                   \
+    if (_e != cudaSuccess) return hfz_cuda_fail(_e, #call);    \
+  } while (0)
+}  // namespace
+
+extern "C" int hfz_havoc_batch_host(hfz_ctx* ctx, const uint8_t* in_bytes, const uint64_t* in_off,
+                                    uint64_t n, uint64_t* rng_state_inout, uint8_t* out_bytes,
+                                    const uint64_t* out_off, uint64_t* out_len, uint32_t* draws_out) {
+  if (!ctx || (n && (!in_off || !rng_state_inout || !out_bytes || !out_off || !out_len))) {
+    hfz_set_error("hfz_havoc_batch_host: null argument");
+    return HFZ_EINVAL;
+  }
+  if (n == 0) return HFZ_OK;
+  HFZ_TRY(cudaSetDevice(ctx->device));
+  const uint64_t in_total = in_off[n], out_total = out_off[n];
+  DevBuf d_in, d_ioff, d_state, d_out, d_ooff, d_olen, d_draws;
+  HFZ_TRY(d_in.alloc(in_total + 16));
+  HFZ_TRY(d_ioff.alloc((n + 1) * 8));
+  HFZ_TRY(d_state.alloc(n * 8));
+  HFZ_TRY(d_out.alloc(out_total + 16));
+  HFZ_TRY(d_ooff.alloc((n + 1) * 8));
+  HFZ_TRY(d_olen.alloc(n * 8));
+  HFZ_TRY(d_draws.alloc(n * 4));
+  cudaStream_t st = ctx->stream;
+  if (in_total) HFZ_TRY(cudaMemcpyAsync(d_in.p, in_bytes, in_total, cudaMemcpyHostToDevice, st));
+  HFZ_TRY(cudaMemcpyAsync(d_ioff.p, in_off, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+  HFZ_TRY(cudaMemcpyAsync(d_state.p, rng_state_inout, n * 8, cudaMemcpyHostToDevice, st));
+  HFZ_TRY(cudaMemcpyAsync(d_ooff.p, out_off, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+  int rc = hfz_havoc_batch(ctx, d_in.as<uint8_t>(), d_ioff.as<uint64_t>(), n, d_state.as<uint64_t>(),
+                           d_out.as<uint8_t>(), d_ooff.as<uint64_t>(), d_olen.as<uint64_t>(),
+                           d_draws.as<uint32_t>());
+  if (rc) return rc;
+  if (out_total) HFZ_TRY(cudaMemcpyAsync(out_bytes, d_out.p, out_total, cudaMemcpyDeviceToHost, st));
+  HFZ_TRY(cudaMemcpyAsync(out_len, d_olen.p, n * 8, cudaMemcpyDeviceToHost, st));
+  HFZ_TRY(cudaMemcpyAsync(rng_state_inout, d_state.p, n * 8, cudaMemcpyDeviceToHost, st));
+  if (draws_out) HFZ_TRY(cudaMemcpyAsync(draws_out, d_draws.p, n * 4, cudaMemcpyDeviceToHost, st));
+  HFZ_TRY(cudaStreamSynchronize(st));
+  return HFZ_OK;
+}
+
+extern "C" int hfz_splice_batch_host(hfz_ctx* ctx, const uint8_t* in_bytes, const uint64_t* in_off,
+                                     uint64_t n_inputs, const uint32_t* a_idx, const uint32_t* b_idx,
+                                     uint64_t n, uint64_t* rng_state_inout, uint8_t* out_bytes,
+                                     const uint64_t* out_off, uint64_t* out_len) {
+  if (!ctx || (n && (!in_off || !a_idx || !b_idx || !rng_state_inout || !out_bytes || !out_off || !out_len))) {
+    hfz_set_error("hfz_splice_batch_host: null argument");
+    return HFZ_EINVAL;
+  }
+  if (n == 0) return HFZ_OK;
+  for (uint64_t j = 0; j < n; ++j)
+    if (a_idx[j] >= n_inputs || b_idx[j] >= n_inputs) {
+      hfz_set_error("hfz_splice_batch_host: input index out of range");
+      return HFZ_EINVAL;
+    }
+  HFZ_TRY(cudaSetDevice(ctx->device));
+  const uint64_t in_total = in_off[n_inputs], out_total = out_off[n];
+  DevBuf d_in, d_ioff, d_a, d_b, d_state, d_out, d_ooff, d_olen;
+  HFZ_TRY(d_in.alloc(in_total + 16));
+  HFZ_TRY(d_ioff.alloc((n_inputs + 1) * 8));
+  HFZ_TRY(d_a.alloc(n * 4));
+  HFZ_TRY(d_b.alloc(n * 4));
+  HFZ_TRY(d_state.alloc(n * 8));
+  HFZ_TRY(d_out.alloc(out_total + 16));
+  HFZ_TRY(d_ooff.alloc((n + 1) * 8));
+  HFZ_TRY(d_olen.alloc(n * 8));
+  cudaStream_t st = ctx->stream;
+  if (in_total) HFZ_TRY(cudaMemcpyAsync(d_in.p, in_bytes, in_total, cudaMemcpyHostToDevice, st));
+  HFZ_TRY(cudaMemcpyAsync(d_ioff.p, in_off, (n_inputs + 1) * 8, cudaMemcpyHostToDevice, st));
+  HFZ_TRY(cudaMemcpyAsync(d_a.p, a_idx, n * 4, cudaMemcpyHostToDevice, st));
+  HFZ_TRY(cudaMemcpyAsync(d_b.p, b_idx, n * 4, cudaMemcpyHostToDevice, st));
+  HFZ_TRY(cudaMemcpyAsync(d_state.p, rng_state_inout, n * 8, cudaMemcpyHostToDevice, st));
+  HFZ_TRY(cudaMemcpyAsync(d_ooff.p, out_off, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+  int rc = hfz_splice_batch(ctx, d_in.as<uint8_t>(), d_ioff.as<uint64_t>(), d_a.as<uint32_t>(),
+                            d_b.as<uint32_t>(), n, d_state.as<uint64_t>(), d_out.as<uint8_t>(),
+                            d_ooff.as<uint64_t>(), d_olen.as<uint64_t>());
+  if (rc) return rc;
+  if (out_total) HFZ_TRY(cudaMemcpyAsync(out_bytes, d_out.p, out_total, cudaMemcpyDeviceToHost, st));
+  HFZ_TRY(cudaMemcpyAsync(out_len, d_olen.p, n * 8, cudaMemcpyDeviceToHost, st));
+  HFZ_TRY(cudaMemcpyAsync(rng_state_inout, d_state.p, n * 8, cudaMemcpyDeviceToHost, st));
+  HFZ_TRY(cudaStreamSynchronize(st));
+  return HFZ_OK;
+}
+
+extern "C" int hfz_deterministic_host(hfz_ctx* ctx, const uint8_t* in, uint64_t in_len, uint8_t* out,
+                                      uint64_t count) {
+  if (!ctx || (in_len && !in) || (count && in_len && !out)) {
+    hfz_set_error("hfz_deterministic_host: null argument");
+    return HFZ_EINVAL;
+  }
+  if (count == 0 || in_len == 0) {
+    if (hfz_deterministic_count(in, in_len) != count) {
+      hfz_set_error("hfz_deterministic_host: count mismatch");
+      return HFZ_EINVAL;
+    }
+    return HFZ_OK;
+  }
+  HFZ_TRY(cudaSetDevice(ctx->device));
+  DevBuf d_in, d_out;
+  HFZ_TRY(d_in.alloc(in_len));
+  HFZ_TRY(d_out.alloc(count * in_len));
+  HFZ_TRY(cudaMemcpyAsync(d_in.p, in, in_len, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = hfz_deterministic_batch(ctx, d_in.as<uint8_t>(), in_len, in, d_out.as<uint8_t>(), count);
+  if (rc) return rc;
+  HFZ_TRY(cudaMemcpyAsync(out, d_out.p, count * in_len, cudaMemcpyDeviceToHost, ctx->stream));
+  HFZ_TRY(cudaStreamSynchronize(ctx->stream));
+  return HFZ_OK;
+}
