@@ -66,6 +66,7 @@ extern "C" int hfz_ctx_create(hfz_ctx** out, int device, uint32_t map_slots, voi
   if (a == cudaSuccess) a = cudaMalloc(&c->prior, map_slots);
   if (a == cudaSuccess) a = cudaMalloc(&c->delta, map_slots);
   if (a == cudaSuccess) a = cudaMalloc(&c->v0, map_slots);
+  if (a == cudaSuccess) a = cudaMalloc(&c->d_small, 8 * sizeof(unsigned long long));
   if (a != cudaSuccess) {
     hfz_ctx_destroy(c);
     hfz_set_error("hfz_ctx_create: scratch allocation failed (%s)", cudaGetErrorString(a));
@@ -84,6 +85,8 @@ extern "C" int hfz_ctx_destroy(hfz_ctx* c) {
   cudaFree(c->prior);
   cudaFree(c->delta);
   cudaFree(c->v0);
+  cudaFree(c->d_small);
+  cudaFree(c->edge_prev);
   for (int i = 0; i < 2; ++i) {
     cudaFree(c->stage_raw[i]);
     if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);

@@ -35,6 +35,11 @@ struct hfz_ctx {
   uint8_t* delta = nullptr;        // [S] this rank's delta (hfz_feedback_batch)
   uint8_t* v0 = nullptr;           // [S] batch-start snapshot
 
+  // K1 scratch (owned, grow-only)
+  uint32_t* edge_prev = nullptr;
+  uint64_t edge_prev_words = 0;
+  unsigned long long* d_small = nullptr;  // [8] small device scalars
+
   // host-buffer path staging (owned, lazily allocated)
   uint8_t* stage_raw[2] = {nullptr, nullptr};
   uint64_t stage_execs = 0;

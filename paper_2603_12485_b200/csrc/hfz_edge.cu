@@ -19,19 +19,22 @@
 //   * a real warp replays one simulated warp, real lane L <-> simulated lane L:
 //       fast path   all active lanes walk the same site sequence (the SIMT common case):
 //                   only the lowest lane can ever bump, every event of it does;
-//       general     pass 1 counts visits per (site, lane) in a per-warp shared-memory table
-//                   (site -> row by hashing, one column per lane), an exclusive prefix-max
-//                   over lanes turns each row into M_L(s) = max_{L'<L} count_{L'}(s), pass 2
-//                   replays the events and bumps the visits with k > M_L(s).  If a warp has
-//                   more distinct sites than the table holds, the sites are partitioned by
-//                   hash prefix and the passes repeat per partition (splitting on overflow).
+//       general     the simulated lanes are replayed in order (that is the rule), but each
+//                   lane's events are spread over the 32 real lanes (coalesced loads):
+//                   __match_any gives the visit number within the chunk, a per-warp
+//                   shared-memory table site -> (max count of lower lanes, count of the current
+//                   lane) gives M_L(s); visits with k > M_L(s) bump in parallel.  If a warp has
+//                   more distinct sites than the table holds, the site space is partitioned by
+//                   hash prefix (the rule is separable per site) and the replay repeats per
+//                   partition, splitting on overflow.
 #include "hfz_common.cuh"
 
 namespace {
 
-constexpr int kEdgeWarps = 4;
-constexpr uint32_t kTC = 128;          // table rows per warp
-constexpr uint32_t kTCFill = 96;       // split the partition when more rows than this are in use
+constexpr int kEdgeWarps = 16;
+constexpr uint32_t kRows = 256;        // per-warp site table rows
+constexpr uint32_t kFill = 192;        // rows in use before a partition is split
+constexpr uint32_t kWarpTab = kRows * (8 + 4 + 4 + 4) + 64;  // keys u64, m u32, c u32, stamp u32, used
 constexpr uint32_t kSmemSlots = 32768; // device slots whose counters fit in shared memory
 constexpr uint32_t kMaxBlockThreads = 1024;         // hdvm.hpp:167
 constexpr uint64_t kMaxLaunchThreads = 1ull << 22;  // hdvm.hpp:168
@@ -76,35 +79,121 @@ __device__ __forceinline__ void bump(uint32_t* c) {
 }
 
 struct WarpTable {
-  unsigned long long* keys;  // [kTC]  0 = empty, else (1<<32 | site)
-  uint32_t* cnt;             // [kTC][32]
+  unsigned long long* keys;  // [kRows]  0 = empty, else (1<<32 | site)
+  uint32_t* m;               // [kRows]  max visit count of this site among LOWER simulated lanes
+  uint32_t* c;               // [kRows]  visits by the simulated lane `stamp` so far
+  uint32_t* stamp;           // [kRows]  simulated lane that owns c (lazy merge into m)
+  uint32_t* used;            // [1]
 };
 
-// find-or-insert; returns row or kTC when the table is over its fill limit
-__device__ __forceinline__ uint32_t table_insert(WarpTable& t, uint32_t site, uint32_t h, uint32_t* used) {
+// find-or-insert; returns the row or kRows when the table is full
+__device__ __forceinline__ uint32_t table_insert(WarpTable& t, uint32_t site, uint32_t h) {
   const unsigned long long want = (1ull << 32) | site;
-  uint32_t r = h & (kTC - 1);
-  for (uint32_t probe = 0; probe < kTC; ++probe) {
-    unsigned long long cur = t.keys[r];
+  uint32_t r = h & (kRows - 1);
+  for (uint32_t probe = 0; probe < kRows; ++probe) {
+    const unsigned long long cur = t.keys[r];
     if (cur == want) return r;
     if (cur == 0) {
       const unsigned long long old = atomicCAS(&t.keys[r], 0ull, want);
       if (old == 0) {
-        atomicAdd(used, 1u);
+        atomicAdd(t.used, 1u);
         return r;
       }
       if (old == want) return r;
     }
-    r = (r + 1) & (kTC - 1);
+    r = (r + 1) & (kRows - 1);
   }
-  return kTC;
+  return kRows;
 }
 
-__device__ __forceinline__ uint32_t table_find(const WarpTable& t, uint32_t site, uint32_t h) {
-  const unsigned long long want = (1ull << 32) | site;
-  uint32_t r = h & (kTC - 1);
-  while (t.keys[r] != want) r = (r + 1) & (kTC - 1);  // present by construction
-  return r;
+// General path for one simulated warp.  e0/n_ev/prev0 are per real lane = per simulated lane.
+// Returns this real lane's share of the bumps.
+__device__ __forceinline__ uint64_t general_path(WarpTable& tab, const uint32_t* sites, uint64_t e0,
+                                                 uint32_t n_ev, uint32_t prev0, uint32_t* counters,
+                                                 uint32_t hmask, int lane) {
+  uint64_t bumps = 0;
+  const uint32_t lane_le = 0xffffffffu >> (31 - lane);
+  const uint32_t ev_total = __reduce_add_sync(0xffffffffu, n_ev);
+  const bool may_overflow = ev_total > kFill;  // distinct sites <= events
+  uint32_t d0 = 0;
+  while (d0 < 26 && (ev_total >> d0) > kFill * 2) ++d0;  // assume some repetition; splits fix the rest
+  uint32_t stk_prefix[36], stk_depth[36];
+  for (uint32_t root = 0; root < (1u << d0); ++root) {
+    int sp = 1;
+    stk_prefix[0] = root;
+    stk_depth[0] = d0;
+    while (sp > 0) {
+      --sp;
+      const uint32_t prefix = stk_prefix[sp], depth = stk_depth[sp];
+      for (uint32_t i = lane; i < kRows; i += 32) {
+        tab.keys[i] = 0;
+        tab.stamp[i] = 0xffffffffu;  // row never touched in this partition: m = c = 0
+      }
+      if (lane == 0) *tab.used = 0;
+      __syncwarp();
+      if (may_overflow) {
+        // dry run: insert this partition's sites only, to know that the table holds them
+        bool full = false;
+        for (uint32_t i = 0; i < n_ev && !full; ++i) {
+          const uint32_t s = sites[e0 + i];
+          const uint32_t h = mix32(s);
+          if (depth && (h >> (32 - depth)) != prefix) continue;
+          full = table_insert(tab, s, h) == kRows;
+        }
+        __syncwarp();
+        if (__any_sync(0xffffffffu, full) || (*tab.used > kFill && depth < 32)) {
+          stk_prefix[sp] = prefix * 2 + 1;
+          stk_depth[sp] = depth + 1;
+          stk_prefix[sp + 1] = prefix * 2;
+          stk_depth[sp + 1] = depth + 1;
+          sp += 2;
+          continue;
+        }
+      }
+      // replay the simulated lanes in order; lane L's events are spread over the real lanes
+      for (int L = 0; L < 32; ++L) {
+        const uint32_t nL = __shfl_sync(0xffffffffu, n_ev, L);
+        if (nL == 0) continue;
+        const uint64_t eL = __shfl_sync(0xffffffffu, e0, L);
+        uint32_t carry = __shfl_sync(0xffffffffu, prev0, L);  // prev of the chunk's first event
+        for (uint32_t c0 = 0; c0 < nL; c0 += 32) {
+          const bool act = c0 + lane < nL;
+          const uint32_t s = act ? sites[eL + c0 + lane] : 0u;
+          const uint32_t h = mix32(s);
+          const bool mine = act && (!depth || (h >> (32 - depth)) == prefix);
+          uint32_t up = __shfl_up_sync(0xffffffffu, s, 1);
+          const uint32_t pv = lane ? (up >> 1) : carry;
+          carry = __shfl_sync(0xffffffffu, s, 31) >> 1;  // only used when the chunk is full
+          const unsigned long long key = mine ? ((1ull << 32) | s) : (unsigned long long)lane;
+          const uint32_t grp = __match_any_sync(0xffffffffu, key);
+          uint32_t row = 0, mm = 0, cc = 0;
+          if (mine) {
+            row = table_insert(tab, s, h);  // cannot fail: checked by the dry run / event bound
+            const uint32_t owner = tab.stamp[row];
+            if (owner == (uint32_t)L) {
+              mm = tab.m[row];
+              cc = tab.c[row];
+            } else if (owner != 0xffffffffu) {  // counts of an earlier lane: fold into the max
+              mm = max(tab.m[row], tab.c[row]);
+            }
+            const uint32_t k = cc + __popc(grp & lane_le);
+            if (k > mm) {
+              bump(&counters[(pv ^ s) & hmask]);
+              ++bumps;
+            }
+          }
+          __syncwarp();
+          if (mine && (grp & (0u - grp)) == (1u << lane)) {  // one writer per site
+            tab.m[row] = mm;
+            tab.c[row] = cc + __popc(grp);
+            tab.stamp[row] = (uint32_t)L;
+          }
+          __syncwarp();
+        }
+      }
+    }
+  }
+  return bumps;
 }
 
 template <bool SMEM_HIST>
@@ -114,10 +203,13 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
   uint8_t* wbase = smem + (SMEM_HIST ? (size_t)p.H * 4 : 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpTable tab;
-  tab.keys = reinterpret_cast<unsigned long long*>(wbase + (size_t)warp * (kTC * 8 + kTC * 32 * 4 + 64));
-  tab.cnt = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(tab.keys) + kTC * 8);
-  uint32_t* used = tab.cnt + kTC * 32;  // [1] rows in use (+ padding)
+  tab.keys = reinterpret_cast<unsigned long long*>(wbase + (size_t)warp * kWarpTab);
+  tab.m = reinterpret_cast<uint32_t*>(tab.keys + kRows);
+  tab.c = tab.m + kRows;
+  tab.stamp = tab.c + kRows;
+  tab.used = tab.stamp + kRows;
   __shared__ unsigned long long s_events;
+  __shared__ uint32_t s_next;
   uint32_t* prev_tab = p.prev_scratch + (size_t)blockIdx.x * p.prev_stride;
   const uint32_t hmask = p.H - 1;
 
@@ -146,131 +238,71 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
     uint64_t my_events = 0;
     for (uint64_t l = l0; l < l1; ++l) {
       const uint32_t* d = p.dims + l * 6;
+      if (threadIdx.x == 0) s_next = 0;
+      __syncthreads();
       if (launch_valid(d)) {
-        const uint64_t gx = d[0], gy = d[1], bdx = d[3], bdy = d[4], bdz = d[5];
-        const uint64_t tpb = bdx * bdy * bdz, blocks = gx * gy * (uint64_t)d[2];
-        const uint64_t wpb = (tpb + 31) / 32;
+        // all of these fit 32 bits: blocks * tpb <= 2^22, tpb <= 1024 (launch_valid)
+        const uint32_t gx = d[0], gy = d[1], bdx = d[3], bdy = d[4], bdz = d[5];
+        const uint32_t tpb = bdx * bdy * bdz, blocks = gx * gy * d[2];
+        const uint32_t wpb = (tpb + 31) / 32;
+        const uint32_t n_sw = blocks * wpb;
         const uint64_t t0 = p.thread_off[l];
-        for (uint64_t sw = warp; sw < blocks * wpb; sw += kEdgeWarps) {
-          const uint64_t bl = sw / wpb, tl = (sw % wpb) * 32 + lane;
+        // simulated warps are handed out dynamically: divergent ones take far longer
+        for (;;) {
+          uint32_t sw = 0;
+          if (lane == 0) sw = atomicAdd(&s_next, 1u);
+          sw = __shfl_sync(0xffffffffu, sw, 0);
+          if (sw >= n_sw) break;
+          const uint32_t bl = sw / wpb, tl = (sw - bl * wpb) * 32 + lane;
           const bool active = tl < tpb;
           uint64_t e0 = 0, e1 = 0, gtid = 0;
           if (active) {
-            const uint64_t t = t0 + bl * tpb + tl;
+            const uint64_t t = t0 + (uint64_t)bl * tpb + tl;
             e0 = p.ev_off[t];
             e1 = p.ev_off[t + 1];
-            const uint64_t bx = bl % gx, by = (bl / gx) % gy, bz = bl / (gx * gy);
-            const uint64_t tx = tl % bdx, ty = (tl / bdx) % bdy, tz = tl / (bdx * bdy);
-            gtid = tx + bx * bdx + ty * (bdx * gx) + by * (bdx * bdy * gx) + tz * (bdx * bdy * gx * gy) +
-                   bz * (bdx * bdy * bdz * gx * gy);
+            if (multi) {
+              const uint32_t bxy = bl / gx, bx = bl - bxy * gx, bz = bxy / gy, by = bxy - bz * gy;
+              const uint32_t txy = tl / bdx, tx = tl - txy * bdx, tz = txy / bdy, ty = txy - tz * bdy;
+              const uint64_t rowx = (uint64_t)bdx * gx;  // threads per grid row
+              gtid = tx + (uint64_t)bx * bdx + (ty + (uint64_t)by * bdy) * rowx +
+                     (tz + (uint64_t)bz * bdz) * rowx * bdy * gy;
+            }
           }
           const uint32_t n_ev = (uint32_t)(e1 - e0);
           uint32_t prev0 = (multi && active) ? prev_tab[gtid] : 0;
           const uint32_t amask = __ballot_sync(0xffffffffu, active);
           const int lead = __ffs(amask) - 1;  // lowest active lane (always lane 0 of the sim warp)
 
-          // ---- fast path: every active lane walks the same sequence
+          // ---- fast path: every active lane walks the same sequence as the lead lane.
+          // No votes inside the loop: each lane compares against the lead's sites read
+          // straight from global memory (a broadcast load), one vote at the end.
           const uint32_t n_lead = __shfl_sync(0xffffffffu, n_ev, lead);
-          bool same = __all_sync(0xffffffffu, !active || n_ev == n_lead);
-          if (same) {
-            for (uint32_t i = 0; i < n_lead; ++i) {
-              const uint32_t s = active ? p.sites[e0 + i] : 0;
-              const uint32_t sl = __shfl_sync(0xffffffffu, s, lead);
-              if (!__all_sync(0xffffffffu, !active || s == sl)) {
-                same = false;
-                break;
-              }
-            }
+          const uint64_t e0_lead = __shfl_sync(0xffffffffu, e0, lead);
+          const uint32_t* sl = p.sites + e0_lead;
+          const uint32_t* sm = p.sites + e0;
+          bool same_l = !active || n_ev == n_lead;
+          if (same_l && active) {
+            uint32_t diff = 0;
+#pragma unroll 4
+            for (uint32_t i = 0; i < n_lead; ++i) diff |= sl[i] ^ sm[i];
+            same_l = diff == 0;
           }
-          if (same) {
-            if (lane == lead) {
-              uint32_t pv = prev0;
-              for (uint32_t i = 0; i < n_lead; ++i) {
-                const uint32_t s = p.sites[e0 + i];
-                bump(&counters[(pv ^ s) & hmask]);
-                pv = s >> 1;
-              }
-              my_events += n_lead;
+          if (__all_sync(0xffffffffu, same_l)) {
+            // only the lead lane can bump, on every event; event i is independent of the
+            // others (prev_i = site_{i-1} >> 1), so the lanes share the bumps
+            const uint32_t prev_lead = __shfl_sync(0xffffffffu, prev0, lead);
+            for (uint32_t i = lane; i < n_lead; i += 32) {
+              const uint32_t s = sl[i];
+              const uint32_t pv = i ? (sl[i - 1] >> 1) : prev_lead;
+              bump(&counters[(pv ^ s) & hmask]);
             }
-            if (multi && active && n_ev) prev_tab[gtid] = p.sites[e1 - 1] >> 1;
+            if (lane == 0) my_events += n_lead;
+            if (multi && active && n_ev) prev_tab[gtid] = sm[n_ev - 1] >> 1;
             continue;
           }
 
-          // ---- general path: partitions of the site space by hash prefix, explicit stack
-          uint32_t stk_prefix[34], stk_depth[34];
-          int sp = 0;
-          stk_prefix[0] = 0;
-          stk_depth[0] = 0;
-          sp = 1;
-          while (sp > 0) {
-            --sp;
-            const uint32_t prefix = stk_prefix[sp], depth = stk_depth[sp];
-            // reset table
-            for (uint32_t i = lane; i < kTC; i += 32) tab.keys[i] = 0;
-            for (uint32_t i = lane; i < kTC * 32 / 4; i += 32)
-              reinterpret_cast<uint4*>(tab.cnt)[i] = make_uint4(0, 0, 0, 0);
-            if (lane == 0) *used = 0;
-            __syncwarp();
-            // pass 1: count visits per (site row, lane column)
-            bool overflow = false;
-            for (uint32_t i = 0; i < n_ev; ++i) {
-              const uint32_t s = p.sites[e0 + i];
-              const uint32_t h = mix32(s);
-              if (depth && (h >> (32 - depth)) != prefix) continue;
-              const uint32_t r = table_insert(tab, s, h, used);
-              if (r == kTC) {
-                overflow = true;
-                break;
-              }
-              tab.cnt[r * 32 + lane] += 1;
-            }
-            __syncwarp();
-            overflow = __any_sync(0xffffffffu, overflow) || (*used > kTCFill && depth < 32);
-            if (overflow) {  // split this partition in two and retry (depth 32 = a single site)
-              stk_prefix[sp] = prefix * 2 + 1;
-              stk_depth[sp] = depth + 1;
-              stk_prefix[sp + 1] = prefix * 2;
-              stk_depth[sp + 1] = depth + 1;
-              sp += 2;
-              __syncwarp();
-              continue;
-            }
-            // rows in use -> exclusive prefix-max over lanes: cnt[r][L] := max_{L'<L} cnt[r][L']
-            for (uint32_t r0 = 0; r0 < kTC; r0 += 32) {
-              uint32_t occ = __ballot_sync(0xffffffffu, tab.keys[r0 + lane] != 0);
-              while (occ) {
-                const uint32_t r = r0 + __ffs(occ) - 1;
-                occ &= occ - 1;
-                uint32_t c = tab.cnt[r * 32 + lane];
-#pragma unroll
-                for (int d2 = 1; d2 < 32; d2 <<= 1) {
-                  const uint32_t o = __shfl_up_sync(0xffffffffu, c, d2);
-                  if (lane >= d2) c = max(c, o);
-                }
-                const uint32_t excl = __shfl_up_sync(0xffffffffu, c, 1);
-                tab.cnt[r * 32 + lane] = lane ? excl : 0;
-              }
-            }
-            __syncwarp();
-            // pass 2: replay; the first M visits of a site by this lane do not bump
-            uint32_t pv = prev0;
-            for (uint32_t i = 0; i < n_ev; ++i) {
-              const uint32_t s = p.sites[e0 + i];
-              const uint32_t h = mix32(s);
-              if (!depth || (h >> (32 - depth)) == prefix) {
-                const uint32_t r = table_find(tab, s, h);
-                const uint32_t m = tab.cnt[r * 32 + lane];
-                if (m) {
-                  tab.cnt[r * 32 + lane] = m - 1;
-                } else {
-                  bump(&counters[(pv ^ s) & hmask]);
-                  ++my_events;
-                }
-              }
-              pv = s >> 1;
-            }
-            __syncwarp();
-          }
+          // ---- general path
+          my_events += general_path(tab, p.sites, e0, n_ev, prev0, counters, hmask, lane);
           if (multi && active && n_ev) prev_tab[gtid] = p.sites[e1 - 1] >> 1;
         }
       }
@@ -351,30 +383,32 @@ extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, c
   }
   if (n_exec == 0) return HFZ_OK;
   HFZ_CUDA(cudaSetDevice(ctx->device));
-  // size the per-CTA prev table from the launch geometry (one small D2H read)
-  unsigned long long* d_mx = nullptr;
+  // size the per-CTA prev table from the launch geometry (one 8-byte D2H read)
   unsigned long long mx = 0;
-  HFZ_CUDA(cudaMalloc(&d_mx, sizeof(unsigned long long)));
-  cudaError_t e = cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long), ctx->stream);
-  if (e == cudaSuccess && n_launch) {
-    hfz_k_edge_max_threads<<<64, 256, 0, ctx->stream>>>(dims, n_launch, d_mx);
+  HFZ_CUDA(cudaMemsetAsync(ctx->d_small, 0, sizeof(unsigned long long), ctx->stream));
+  if (n_launch) {
+    hfz_k_edge_max_threads<<<64, 256, 0, ctx->stream>>>(dims, n_launch, ctx->d_small);
     ++ctx->launches;
-    e = cudaGetLastError();
+    HFZ_CUDA(cudaGetLastError());
   }
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(&mx, d_mx, sizeof(mx), cudaMemcpyDeviceToHost, ctx->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  cudaFree(d_mx);
-  if (e != cudaSuccess) return hfz_cuda_fail(e, "hfz_edge_record_batch(prepare)");
+  HFZ_CUDA(cudaMemcpyAsync(&mx, ctx->d_small, sizeof(mx), cudaMemcpyDeviceToHost, ctx->stream));
+  HFZ_CUDA(cudaStreamSynchronize(ctx->stream));
 
   uint32_t grid = (uint32_t)(n_exec < (uint64_t)ctx->num_sms ? n_exec : (uint64_t)ctx->num_sms);
   const uint64_t stride = mx ? mx : 1;
-  uint32_t* d_prev = nullptr;
-  if (cudaMalloc(&d_prev, (size_t)grid * stride * sizeof(uint32_t)) != cudaSuccess) {
-    hfz_set_error("hfz_edge_record_batch: prev table allocation failed (%llu bytes)",
-                  (unsigned long long)grid * stride * 4);
-    return HFZ_ENOMEM;
+  if (ctx->edge_prev_words < (uint64_t)grid * stride) {
+    cudaFree(ctx->edge_prev);
+    ctx->edge_prev = nullptr;
+    ctx->edge_prev_words = 0;
+    if (cudaMalloc(&ctx->edge_prev, (size_t)grid * stride * sizeof(uint32_t)) != cudaSuccess) {
+      hfz_set_error("hfz_edge_record_batch: prev table allocation failed (%llu bytes)",
+                    (unsigned long long)grid * stride * 4);
+      return HFZ_ENOMEM;
+    }
+    ctx->edge_prev_words = (uint64_t)grid * stride;
   }
+  uint32_t* d_prev = ctx->edge_prev;
+  cudaError_t e = cudaSuccess;
   EdgeParams p;
   p.launch_off = launch_off;
   p.dims = dims;
@@ -388,7 +422,7 @@ extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, c
   p.warp_events = warp_events_out;
   p.prev_scratch = d_prev;
   p.prev_stride = stride;
-  const size_t wsmem = (size_t)kEdgeWarps * (kTC * 8 + kTC * 32 * 4 + 64);
+  const size_t wsmem = (size_t)kEdgeWarps * kWarpTab;
   const bool smem_hist = ctx->H <= kSmemSlots;
   const size_t smem = wsmem + (smem_hist ? (size_t)ctx->H * 4 : 0);
   if (smem_hist) {
@@ -400,8 +434,6 @@ extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, c
   }
   ++ctx->launches;
   if (e == cudaSuccess) e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);  // d_prev must outlive the kernel
-  cudaFree(d_prev);
   if (e != cudaSuccess) return hfz_cuda_fail(e, "hfz_edge_record_batch");
   return HFZ_OK;
 }
