@@ -62,6 +62,7 @@ struct hfz_ctx {
   int scan_prefetch = 1;  // L2 prefetch of the row after next
   int virgin_smem = 1;    // stage V0 in shared memory when it fits
   int time_scan = 0;      // bracket scan launches with events (bench roofline)
+  int64_t scan_small = -1; // batches up to this many execs use the warp-per-map kernel (-1 = auto)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> scan_events;
 };
 

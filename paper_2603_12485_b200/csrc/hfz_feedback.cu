@@ -153,11 +153,15 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
   bool virgin_ready = !VSMEM;
 
   // even split of the batch over all warps of the grid
-  const uint64_t W = (uint64_t)gridDim.x * nwarps;
+  // Small batches keep the groups full (32 lanes) on fewer warps instead of a few maps on
+  // every warp: SIMD efficiency of phase B matters more than occupancy there.
+  const uint64_t Wall = (uint64_t)gridDim.x * nwarps;
+  const uint64_t groups = (p.n_exec + 31) / 32;
+  const uint64_t W = groups < Wall ? groups : Wall;
   const uint64_t wg = (uint64_t)warp * gridDim.x + blockIdx.x;
   const uint64_t per = p.n_exec / W, rem = p.n_exec % W;
   const uint64_t start = wg * per + (wg < rem ? wg : rem);
-  const uint64_t cnt = per + (wg < rem ? 1 : 0);
+  const uint64_t cnt = wg < W ? per + (wg < rem ? 1 : 0) : 0;
   const uint32_t rows_host = p.H / ROW;
   const uint32_t rows = (uint32_t)(rec / ROW);
   const uint8_t* my_slot = s_buf + lane * C::kSlot;
@@ -277,6 +281,155 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
     }
   }
   if (!virgin_ready) hfz_mbar_wait(bar_virgin, 0);  // never leave the bulk copy in flight
+}
+
+// ---------------------------------------------------------------------------
+// K2 scan for SMALL batches ("warp-per-map").  With fewer maps than ~6 per warp of the grid the
+// lane-per-map kernel above is latency-bound (one warp walks 320+ rows serially).  Here every
+// warp owns ONE map: the 32 lanes stream it coalesced and compact the non-zero slots, in index
+// order, into a per-warp shared list (classification, virgin test and first-occurrence update
+// happen in parallel on the way); then lanes 0 and 1 run the Full and the Simple FNV chain over
+// the list.  ~5x more instructions per map than lane-per-map, but the latency of a batch drops
+// from rows x row-latency to one map's chain (~20 us).
+constexpr uint32_t kListCap = 2048;  // entries per warp: idx (24 bits) | rung << 24
+
+template <bool VSMEM, bool CLASSED>
+__global__ void __launch_bounds__(512, 1) hfz_k_scan_wpm(const ScanParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  uint8_t* s_virgin = smem;
+  uint32_t* list = reinterpret_cast<uint32_t*>(smem + (VSMEM ? p.S : 0)) + (size_t)warp * kListCap;
+  uint64_t* bar_virgin =
+      reinterpret_cast<uint64_t*>(smem + (VSMEM ? p.S : 0) + (size_t)nwarps * kListCap * 4);
+  if (VSMEM) {
+    if (threadIdx.x == 0) {
+      hfz_mbar_init(bar_virgin, 1);
+      hfz_fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint64_t pol = hfz_policy_evict_last();
+      hfz_mbar_expect_tx(bar_virgin, p.S);
+      for (uint32_t off = 0; off < p.S; off += 16384u) {
+        const uint32_t n = p.S - off < 16384u ? p.S - off : 16384u;
+        hfz_bulk_g2s_stream(s_virgin + off, p.v0 + off, n, bar_virgin, pol);
+      }
+    }
+    hfz_mbar_wait(bar_virgin, 0);
+  }
+  const uint8_t* virgin = VSMEM ? s_virgin : p.v0;
+  const uint32_t lane_lt = (1u << lane) - 1u;
+
+  for (uint64_t e64 = (uint64_t)blockIdx.x * nwarps + warp; e64 < p.n_exec;
+       e64 += (uint64_t)gridDim.x * nwarps) {
+    const uint32_t e = (uint32_t)e64;
+    const uint4* src = reinterpret_cast<const uint4*>(p.raw + e64 * p.rec_bytes);
+    uint8_t* classed_row = CLASSED ? p.classed + e64 * p.S : nullptr;
+    uint64_t h = HFZ_FNV_OFFSET;  // lane 0: Full chain, lane 1: Simple chain
+    uint32_t fill = 0, nnz = 0, novel = 0;
+
+    auto drain = [&]() {
+      __syncwarp();
+      if (lane < 2) {
+#pragma unroll 4
+        for (uint32_t i = 0; i < fill; ++i) {
+          const uint32_t en = list[i];
+          const uint32_t idx = en & 0xffffffu;
+          h = hfz_fnv(hfz_fnv(h, idx & 0xffu), (idx >> 8) & 0xffu);
+          if (lane == 0) h = hfz_fnv(h, 1u << (en >> 24));
+        }
+      }
+      fill = 0;
+      __syncwarp();
+    };
+    // one element (count c at logical slot idx): everything except the hash chains
+    auto element = [&](uint32_t idx, uint32_t klass, uint32_t pos) {
+      list[pos] = idx | ((31 - __clz(klass)) << 24);
+      const uint32_t known = VSMEM ? (uint32_t)virgin[idx] : (uint32_t)__ldg(virgin + idx);
+      if (klass & ~known) {
+        novel = 1;
+        atomicMin(p.first + (size_t)idx * 8 + (31 - __clz(klass)), e);
+      }
+      if (CLASSED) classed_row[idx] = (uint8_t)klass;
+    };
+
+    const uint32_t host_vecs = p.H / 16, total_vecs = (uint32_t)(p.rec_bytes / 16);
+    auto load8 = [&](uint4* x, uint32_t v0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t v = v0 + j * 32 + lane;
+        x[j] = v < total_vecs ? hfz_ldg_stream(src + v) : make_uint4(0, 0, 0, 0);
+      }
+    };
+    auto process8 = [&](const uint4* x, uint32_t v0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t vb = v0 + j * 32;  // first vector of this warp-wide load (uniform)
+        if (vb < total_vecs) {
+          const bool host = vb < host_vecs;  // H is a multiple of 512: a load never straddles the halves
+          const uint32_t w[4] = {x[j].x, x[j].y, x[j].z, x[j].w};
+          uint32_t c;
+          if (host)
+            c = __popc(nz_bytes(w[0])) + __popc(nz_bytes(w[1])) + __popc(nz_bytes(w[2])) + __popc(nz_bytes(w[3]));
+          else
+            c = (w[0] != 0u) + (w[1] != 0u) + (w[2] != 0u) + (w[3] != 0u);
+          if (__any_sync(0xffffffffu, c != 0u)) {
+            // warp-wide exclusive prefix sum of the per-lane element counts
+            uint32_t inc = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+              const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+              if (lane >= d) inc += o;
+            }
+            const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+            if (fill + tot > kListCap) drain();
+            uint32_t pos = fill + inc - c;
+            if (c) {
+              const uint32_t v = vb + lane;
+              if (host) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  uint32_t bm = nz_bytes(w[k]);
+                  while (bm) {
+                    const uint32_t b = __ffs(bm) - 1;
+                    bm &= bm - 1;
+                    element(v * 16 + k * 4 + b, hfz_class_host((w[k] >> (8 * b)) & 0xffu), pos++);
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                  if (w[k]) element(p.H + (v - host_vecs) * 4 + k, hfz_class_device(w[k]), pos++);
+              }
+            }
+            fill += tot;
+            nnz += tot;
+          }
+        }
+      }
+    };
+    uint4 xa[8], xb[8];
+    load8(xa, 0);
+    for (uint32_t v0 = 0; v0 < total_vecs; v0 += 2 * 256) {
+      load8(xb, v0 + 256);
+      process8(xa, v0);
+      load8(xa, v0 + 512);
+      process8(xb, v0 + 256);
+    }
+    drain();
+    const uint64_t h_simple = __shfl_sync(0xffffffffu, h, 1);
+    const uint32_t any_novel = __any_sync(0xffffffffu, novel != 0u);
+    if (lane == 0) {
+      p.sig_full[e64] = h;
+      p.sig_simple[e64] = h_simple;
+      if (p.nnz) p.nnz[e64] = nnz;
+      if (any_novel) {
+        const uint32_t ci = atomicAdd(p.cand_count, 1u);
+        p.cand_list[ci] = e;
+        p.cand_flags[ci] = 0;
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -432,7 +585,8 @@ int launch_scan_t(hfz_ctx* ctx, const ScanParams& p) {
   const size_t smem = scan_smem_bytes<ROW>(p.S, VSMEM, warps);
   HFZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   uint64_t grid = (uint64_t)ctx->num_sms;
-  if (grid * warps > p.n_exec) grid = (p.n_exec + warps - 1) / warps;  // >= one map per warp
+  const uint64_t groups = (p.n_exec + 31) / 32;
+  if (grid > groups) grid = groups;  // warp w of CTA b owns work slice w * grid + b
   kern<<<(uint32_t)grid, warps * 32, smem, ctx->stream>>>(p);
   ++ctx->launches;
   HFZ_CUDA(cudaGetLastError());
@@ -449,9 +603,34 @@ int launch_scan_r(hfz_ctx* ctx, const ScanParams& p, int row) {
                  : launch_scan_t<REC_CT, 512, VSMEM, false>(ctx, p);
 }
 
+template <bool VSMEM, bool CLASSED>
+int launch_scan_wpm_t(hfz_ctx* ctx, const ScanParams& p) {
+  auto kern = hfz_k_scan_wpm<VSMEM, CLASSED>;
+  // spread a small batch over all SMs: as few warps per CTA as cover the batch (4..16)
+  int warps = (int)((p.n_exec + ctx->num_sms - 1) / ctx->num_sms);
+  warps = warps < 4 ? 4 : (warps > 16 ? 16 : warps);
+  const size_t smem = (VSMEM ? p.S : 0) + (size_t)warps * kListCap * 4 + 16;
+  HFZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  uint64_t grid = (p.n_exec + warps - 1) / warps;
+  if (grid > (uint64_t)ctx->num_sms) grid = (uint64_t)ctx->num_sms;
+  kern<<<(uint32_t)grid, warps * 32, smem, ctx->stream>>>(p);
+  ++ctx->launches;
+  HFZ_CUDA(cudaGetLastError());
+  return HFZ_OK;
+}
+
 int launch_scan(hfz_ctx* ctx, const ScanParams& p) {
   // virgin copy in shared memory whenever it leaves room for the per-warp slots
   const bool vsmem = ctx->virgin_smem && p.S <= 65536u;
+  // small batches: one warp per map (latency), else 32 maps per warp (throughput).  Measured
+  // crossover on B200 at 65,536 slots: 1,024 maps 0.31 vs 0.54 ms, 4,096 maps 0.70 vs 0.55 ms.
+  const uint64_t small_limit = ctx->scan_small >= 0 ? (uint64_t)ctx->scan_small
+                                                    : (uint64_t)ctx->num_sms * 14 * 65536u / p.S;
+  if (p.n_exec <= small_limit) {
+    const bool classed = p.classed != nullptr;
+    if (vsmem) return classed ? launch_scan_wpm_t<true, true>(ctx, p) : launch_scan_wpm_t<true, false>(ctx, p);
+    return classed ? launch_scan_wpm_t<false, true>(ctx, p) : launch_scan_wpm_t<false, false>(ctx, p);
+  }
   const int row = ctx->scan_row == 256 ? 256 : 512;
   if (p.S == 65536u && vsmem) return launch_scan_r<163840, true>(ctx, p, row);
   if (p.S == 262144u && !vsmem) return launch_scan_r<655360, false>(ctx, p, row);

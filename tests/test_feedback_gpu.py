@@ -14,6 +14,15 @@ pytestmark = pytest.mark.gpu
 S = 65536
 
 
+@pytest.fixture(autouse=True, params=["lane_per_map", "warp_per_map"])
+def scan_kernel(request, ctx):
+    """Every test runs against both scan kernels: the throughput kernel (32 maps per warp) and
+    the small-batch kernel (one warp per map); by default the library picks by batch size."""
+    ctx.set_option("scan_small", 0 if request.param == "lane_per_map" else 1 << 40)
+    yield request.param
+    ctx.set_option("scan_small", -1)
+
+
 def run_gpu(ctx, raw, virgin0=None, counts0=None, want_classed=True):
     d_raw = torch.from_numpy(raw).to(ctx.device)
     virgin = ctx.new_virgin() if virgin0 is None else torch.from_numpy(virgin0).to(ctx.device)
@@ -144,7 +153,7 @@ def test_host_buffer_path(ctx, checker):
     assert np.array_equal(v, cv) and np.array_equal(c, cc)
 
 
-def test_sharded_scan_resolve_equals_sequential(ctx, checker):
+def test_sharded_scan_resolve_equals_sequential(ctx, checker, scan_kernel):
     """R simulated ranks on one GPU -- per-rank scan against V0, 'allgather' of
     the deltas by concatenation, resolve in rank order -- must reproduce the single-rank
     sequential Admit codes, virgin and counters."""
@@ -160,6 +169,8 @@ def test_sharded_scan_resolve_equals_sequential(ctx, checker):
     d_v0 = torch.from_numpy(v0).to(ctx.device)
     import paper_2603_12485_b200 as hfz
     ctxs = [hfz.Context(0) for _ in range(R)]
+    for i, c in enumerate(ctxs):
+        c.set_option("scan_small", 0 if (i % 2) == (scan_kernel == "lane_per_map") else 1 << 40)
     try:
         scans = [ctxs[r].feedback_scan(shards[r], d_v0) for r in range(R)]
         deltas = torch.cat([s["delta"] for s in scans])
@@ -206,13 +217,14 @@ def test_many_maps_per_warp(ctx, checker):
         ctx.set_option("scan_warps", 0)
 
 
-def test_large_map_262144(checker):
+def test_large_map_262144(checker, scan_kernel):
     """BASELINE.json configs[2] map size: 262,144 slots (virgin no longer fits shared memory)."""
     import paper_2603_12485_b200 as hfz
     from oracle import pyoracle
     S2 = 262144
     ck = pyoracle.Ref(S2) if pyoracle.Ref.available(S2) else pyoracle.Port()
     c2 = hfz.Context(0, S2)
+    c2.set_option("scan_small", 0 if scan_kernel == "lane_per_map" else 1 << 40)
     try:
         raw = synth.maps_iid(48, S2, density=0.01, seed=3)
         g = run_gpu(c2, raw)
