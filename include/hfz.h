@@ -199,6 +199,13 @@ HFZ_API int hfz_havoc_batch(hfz_ctx* ctx, const uint8_t* in_bytes, const uint64_
                             uint64_t n, uint64_t* rng_state_inout, uint8_t* out_bytes,
                             const uint64_t* out_off, uint64_t* out_len, uint32_t* draws_out);
 
+/* Serial-stream mode: ONE Rng threaded through n mutants in slot order, as
+ * Campaign::fuzz_entry does (src/engine.cpp:561-562).  A length-only dry run of every slot on the
+ * device yields the state each slot starts from (slot_states_out, feed it to hfz_havoc_batch) and
+ * leaves the stream's state after the n-th mutant in stream_state_inout (device, 1 x u64). */
+HFZ_API int hfz_havoc_serial_plan(hfz_ctx* ctx, const uint64_t* in_off, uint64_t n,
+                                  uint64_t* stream_state_inout, uint64_t* slot_states_out);
+
 /* splice_mutant (engine.hpp:33-35, src/engine.cpp:195-204): slot j splices
  * a = input a_idx[j], b = input b_idx[j] of the same packed input set. */
 HFZ_API int hfz_splice_batch(hfz_ctx* ctx, const uint8_t* in_bytes, const uint64_t* in_off,
@@ -223,6 +230,25 @@ HFZ_API int hfz_splice_batch_host(hfz_ctx* ctx, const uint8_t* in_bytes, const u
                                   const uint64_t* out_off, uint64_t* out_len);
 HFZ_API int hfz_deterministic_host(hfz_ctx* ctx, const uint8_t* in, uint64_t in_len, uint8_t* out,
                                    uint64_t count);
+
+/* ------------------------------------------------------------------------- */
+/* Signature seen-sets and dispatch flags: the std::set<uint64_t> pair of
+ * Campaign (src/engine.cpp:319) with count()-then-insert() semantics in exec order
+ * (src/engine.cpp:474-478) and should_sanitize (src/sanitizers.cpp:283-296), on the device.
+ * capacity: power of two; a set refuses to grow past 3/4 of it (HFZ_ECAP). */
+typedef struct hfz_sigset hfz_sigset;
+HFZ_API int hfz_sigset_create(hfz_ctx* ctx, uint64_t capacity, hfz_sigset** out);
+HFZ_API int hfz_sigset_destroy(hfz_sigset* set);
+HFZ_API int hfz_sigset_size(hfz_sigset* set, uint64_t* size_out); /* synchronises */
+/* seen_out[i] = 1 iff sigs[i] was in the set before the call or equals sigs[j], j < i */
+HFZ_API int hfz_sigset_seen_insert(hfz_ctx* ctx, hfz_sigset* set, const uint64_t* sigs, uint64_t n,
+                                   uint8_t* seen_out);
+/* strategy: 0 AllTrace, 1 UniqueTrace, 2 SimpleTrace, 3 CoverageIncrease (sanitizers.hpp:70-75) */
+HFZ_API int hfz_dispatch_batch(hfz_ctx* ctx, hfz_sigset* full_set, hfz_sigset* simple_set,
+                               const uint64_t* sig_full, const uint64_t* sig_simple,
+                               const uint8_t* admit, uint64_t n, int strategy,
+                               uint8_t* full_seen_out, uint8_t* simple_seen_out,
+                               uint8_t* sanitize_out);
 
 /* Rng helpers (host side, O(1)): rng.hpp:15-21,39-42.  State after k draws =
  * state + k*gamma; split() child seed of the tag-th split from a parent state. */

@@ -10,7 +10,7 @@ Importing the package loads the shared library and fails loudly if it has not
 been built; there is no CPU fallback anywhere in the product path.
 """
 from ._lib import HfzError, LIB_PATH, lib  # noqa: F401  (loads libhfz.so or raises)
-from .api import (Context, GAMMA, HOST_SLOTS, MAP_SIZE, MAX_INPUT_BYTES, i64_to_u64,  # noqa: F401
+from .api import (Context, SigSet, dispatch_batch, GAMMA, HOST_SLOTS, MAP_SIZE, MAX_INPUT_BYTES, i64_to_u64,  # noqa: F401
                   record_bytes, rng_jump, rng_split, u64_to_i64)
 from .binding import (TargetError, deterministic_mutants, havoc_mutant, splice_mutant,  # noqa: F401
                       feedback_batch, havoc_batch, default_context)

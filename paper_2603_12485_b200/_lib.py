@@ -47,6 +47,12 @@ PROTOTYPES = {
     "hfz_havoc_batch_host": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp]),
     "hfz_splice_batch_host": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
     "hfz_deterministic_host": (C.c_int, [_vp, _vp, _u64, _vp, _u64]),
+    "hfz_havoc_serial_plan": (C.c_int, [_vp, _vp, _u64, _vp, _vp]),
+    "hfz_sigset_create": (C.c_int, [_vp, _u64, C.POINTER(_vp)]),
+    "hfz_sigset_destroy": (C.c_int, [_vp]),
+    "hfz_sigset_size": (C.c_int, [_vp, C.POINTER(_u64)]),
+    "hfz_sigset_seen_insert": (C.c_int, [_vp, _vp, _vp, _u64, _vp]),
+    "hfz_dispatch_batch": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _u64, C.c_int, _vp, _vp, _vp]),
     "hfz_rng_jump": (_u64, [_u64, _u64]),
     "hfz_rng_next": (_u64, [C.POINTER(_u64)]),
     "hfz_rng_below": (_u64, [C.POINTER(_u64), _u64]),

@@ -224,6 +224,16 @@ class Context:
                                   _ptr(out_bytes), _ptr(out_off), _ptr(out_len), _ptr(draws)))
         return out_bytes, out_off, out_len, draws
 
+    def havoc_serial_plan(self, in_off, stream_state):
+        """Serial-stream mode: `stream_state` (1-element int64 device tensor) is the campaign's single
+        Rng; returns the per-slot start states for havoc_batch and advances stream_state past all
+        n mutants (Campaign::fuzz_entry, src/engine.cpp:561-562)."""
+        n = in_off.numel() - 1
+        states = torch.empty(n, dtype=torch.int64, device=self.device)
+        self._sync_stream()
+        check(lib.hfz_havoc_serial_plan(self._h, _ptr(in_off), n, _ptr(stream_state), _ptr(states)))
+        return states
+
     def splice_batch(self, in_bytes, in_off, a_idx, b_idx, rng_state):
         _dev(in_bytes, self.device, torch.uint8)
         n = a_idx.numel()
@@ -254,6 +264,50 @@ class Context:
         check(lib.hfz_deterministic_batch(self._h, _ptr(dev_in), L, C.c_void_p(host.ctypes.data),
                                           _ptr(out), cnt))
         return cnt, out
+
+
+class SigSet:
+    """Device-resident std::set<uint64_t> stand-in with count()-then-insert() batch semantics."""
+
+    def __init__(self, ctx: Context, capacity: int = 1 << 22):
+        self.ctx = ctx
+        h = C.c_void_p()
+        check(lib.hfz_sigset_create(ctx._h, capacity, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) and lib is not None:
+            lib.hfz_sigset_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def __len__(self):
+        v = C.c_uint64(0)
+        check(lib.hfz_sigset_size(self._h, C.byref(v)))
+        return int(v.value)
+
+    def seen_insert(self, sigs: torch.Tensor) -> torch.Tensor:
+        seen = torch.empty(sigs.numel(), dtype=torch.uint8, device=sigs.device)
+        self.ctx._sync_stream()
+        check(lib.hfz_sigset_seen_insert(self.ctx._h, self._h, _ptr(sigs), sigs.numel(), _ptr(seen)))
+        return seen
+
+
+STRATEGIES = {"all-trace": 0, "unique-trace": 1, "simple-trace": 2, "coverage-increase": 3}
+
+
+def dispatch_batch(ctx: Context, full_set: SigSet, simple_set: SigSet, sig_full, sig_simple, admit,
+                   strategy: str = "simple-trace"):
+    """engine.cpp:474-478 + should_sanitize for a whole batch: (full_seen, simple_seen, sanitize)."""
+    n = admit.numel()
+    fs = torch.empty(n, dtype=torch.uint8, device=admit.device)
+    ss = torch.empty(n, dtype=torch.uint8, device=admit.device)
+    sz = torch.empty(n, dtype=torch.uint8, device=admit.device)
+    ctx._sync_stream()
+    check(lib.hfz_dispatch_batch(ctx._h, full_set._h, simple_set._h, _ptr(sig_full), _ptr(sig_simple),
+                                 _ptr(admit), n, STRATEGIES[strategy], _ptr(fs), _ptr(ss), _ptr(sz)))
+    return fs, ss, sz
 
 
 # ---- scalar Rng helpers (host arithmetic, rng.hpp) ------------------------------------

@@ -107,6 +107,107 @@ __device__ __forceinline__ uint64_t havoc_cap(uint64_t len) {
   return m > kMaxInput ? kMaxInput : m;
 }
 
+// The stacked-havoc edit loop of one slot (src/engine.cpp:120-191).  DRY = true runs only the
+// Rng draws and the length bookkeeping -- every below() bound depends on the current length
+// alone, never on the bytes -- which is what a serial-stream plan needs (hfz_havoc_serial_plan).
+template <bool DRY>
+__device__ __forceinline__ uint64_t havoc_edit(uint8_t* v, uint64_t len, WarpRng& rng, int lane) {
+  const uint64_t ops = 1 + rng.below(64);
+  for (uint64_t op = 0; op < ops; ++op) {
+    if (len == 0) {  // engine.cpp:124-129 (no 1 MiB clamp on this branch)
+      const uint64_t cnt = 1 + rng.below(8);
+      for (uint64_t i = 0; i < cnt; ++i) {
+        const uint8_t b = (uint8_t)rng.below(256);
+        if (!DRY && lane == 0) v[len] = b;
+        ++len;
+      }
+      if (!DRY) __syncwarp();
+      continue;
+    }
+    switch ((uint32_t)rng.below(9)) {
+      case 0: {  // flip one bit, MSB-first numbering
+        const uint64_t pos = rng.below(len * 8);
+        if (!DRY && lane == 0) v[pos / 8] ^= (uint8_t)(0x80u >> (pos % 8));
+        break;
+      }
+      case 1: {  // random byte: the VALUE is drawn before the index (C++17 sequencing of '=')
+        const uint8_t val = (uint8_t)rng.below(256);
+        const uint64_t i = rng.below(len);
+        if (!DRY && lane == 0) v[i] = val;
+        break;
+      }
+      case 2: {  // byte +/- delta
+        const uint8_t d = (uint8_t)(1 + rng.below(35));
+        const uint64_t i = rng.below(len);
+        const bool add = rng.below(2) < 1;
+        if (!DRY && lane == 0) v[i] = (uint8_t)(add ? v[i] + d : v[i] - d);
+        break;
+      }
+      case 3: {  // interesting 16-bit, little endian
+        if (len < 2) break;
+        const uint64_t off = rng.below(len - 1);
+        const uint16_t val = (uint16_t)c_interesting16[rng.below(10)];
+        if (!DRY && lane < 2) v[off + lane] = (uint8_t)(val >> (8 * lane));
+        break;
+      }
+      case 4: {  // interesting 32-bit, little endian
+        if (len < 4) break;
+        const uint64_t off = rng.below(len - 3);
+        const uint32_t val = (uint32_t)c_interesting32[rng.below(8)];
+        if (!DRY && lane < 4) v[off + lane] = (uint8_t)(val >> (8 * lane));
+        break;
+      }
+      case 5: {  // delete a block
+        if (len < 2) break;
+        const uint64_t off = rng.below(len);
+        const uint64_t q = len / 4 ? len / 4 : 1;
+        const uint64_t max_n = len - off < q ? len - off : q;
+        const uint64_t cnt = 1 + rng.below(max_n);
+        if (!DRY) __syncwarp();
+        if (!DRY) warp_move_down(v, off, off + cnt, len - off - cnt, lane);
+        len -= cnt;
+        break;
+      }
+      case 6: {  // duplicate a block elsewhere (copy first, then insert)
+        const uint64_t src = rng.below(len);
+        const uint64_t lim = len - src < 16 ? len - src : 16;
+        const uint64_t cnt = 1 + rng.below(lim);
+        const uint64_t dst = rng.below(len + 1);
+        if (!DRY) __syncwarp();
+        const uint8_t blk = (!DRY && (uint64_t)lane < cnt) ? v[src + lane] : 0;
+        // insert with the 1 MiB clamp folded in: bytes that would land past the cap are dropped
+        const uint64_t new_len = len + cnt > kMaxInput ? kMaxInput : len + cnt;
+        if (!DRY) __syncwarp();
+        if (!DRY && new_len > dst + cnt) warp_move_up(v, dst + cnt, dst, new_len - dst - cnt, lane);
+        if (!DRY && (uint64_t)lane < cnt && dst + lane < new_len) v[dst + lane] = blk;
+        len = new_len;
+        break;
+      }
+      case 7: {  // constant fill
+        const uint64_t off = rng.below(len);
+        const uint64_t lim = len - off < 16 ? len - off : 16;
+        const uint64_t cnt = 1 + rng.below(lim);
+        const uint8_t b = (uint8_t)rng.below(256);
+        if (!DRY && (uint64_t)lane < cnt) v[off + lane] = b;
+        break;
+      }
+      default: {  // 8: swap two bytes
+        const uint64_t i = rng.below(len);
+        const uint64_t k = rng.below(len);
+        if (!DRY && lane == 0) {
+          const uint8_t t = v[i];
+          v[i] = v[k];
+          v[k] = t;
+        }
+        break;
+      }
+    }
+    if (!DRY) __syncwarp();
+    if (len > kMaxInput) len = kMaxInput;
+  }
+  return len;
+}
+
 __global__ void __launch_bounds__(kHavocWarps * 32) hfz_k_havoc(
     const uint8_t* __restrict__ in_bytes, const uint64_t* __restrict__ in_off, uint64_t n,
     uint64_t* __restrict__ state, uint8_t* __restrict__ out_bytes,
@@ -127,99 +228,7 @@ __global__ void __launch_bounds__(kHavocWarps * 32) hfz_k_havoc(
     WarpRng rng;
     rng.s = state[j];
     rng.draws = 0;
-    const uint64_t ops = 1 + rng.below(64);
-    for (uint64_t op = 0; op < ops; ++op) {
-      if (len == 0) {  // engine.cpp:124-129 (no 1 MiB clamp on this branch)
-        const uint64_t cnt = 1 + rng.below(8);
-        for (uint64_t i = 0; i < cnt; ++i) {
-          const uint8_t b = (uint8_t)rng.below(256);
-          if (lane == 0) v[len] = b;
-          ++len;
-        }
-        __syncwarp();
-        continue;
-      }
-      switch ((uint32_t)rng.below(9)) {
-        case 0: {  // flip one bit, MSB-first numbering
-          const uint64_t pos = rng.below(len * 8);
-          if (lane == 0) v[pos / 8] ^= (uint8_t)(0x80u >> (pos % 8));
-          break;
-        }
-        case 1: {  // random byte: the VALUE is drawn before the index (C++17 sequencing of '=')
-          const uint8_t val = (uint8_t)rng.below(256);
-          const uint64_t i = rng.below(len);
-          if (lane == 0) v[i] = val;
-          break;
-        }
-        case 2: {  // byte +/- delta
-          const uint8_t d = (uint8_t)(1 + rng.below(35));
-          const uint64_t i = rng.below(len);
-          const bool add = rng.below(2) < 1;
-          if (lane == 0) v[i] = (uint8_t)(add ? v[i] + d : v[i] - d);
-          break;
-        }
-        case 3: {  // interesting 16-bit, little endian
-          if (len < 2) break;
-          const uint64_t off = rng.below(len - 1);
-          const uint16_t val = (uint16_t)c_interesting16[rng.below(10)];
-          if (lane < 2) v[off + lane] = (uint8_t)(val >> (8 * lane));
-          break;
-        }
-        case 4: {  // interesting 32-bit, little endian
-          if (len < 4) break;
-          const uint64_t off = rng.below(len - 3);
-          const uint32_t val = (uint32_t)c_interesting32[rng.below(8)];
-          if (lane < 4) v[off + lane] = (uint8_t)(val >> (8 * lane));
-          break;
-        }
-        case 5: {  // delete a block
-          if (len < 2) break;
-          const uint64_t off = rng.below(len);
-          const uint64_t q = len / 4 ? len / 4 : 1;
-          const uint64_t max_n = len - off < q ? len - off : q;
-          const uint64_t cnt = 1 + rng.below(max_n);
-          __syncwarp();
-          warp_move_down(v, off, off + cnt, len - off - cnt, lane);
-          len -= cnt;
-          break;
-        }
-        case 6: {  // duplicate a block elsewhere (copy first, then insert)
-          const uint64_t src = rng.below(len);
-          const uint64_t lim = len - src < 16 ? len - src : 16;
-          const uint64_t cnt = 1 + rng.below(lim);
-          const uint64_t dst = rng.below(len + 1);
-          __syncwarp();
-          const uint8_t blk = (uint64_t)lane < cnt ? v[src + lane] : 0;
-          // insert with the 1 MiB clamp folded in: bytes that would land past the cap are dropped
-          const uint64_t new_len = len + cnt > kMaxInput ? kMaxInput : len + cnt;
-          __syncwarp();
-          if (new_len > dst + cnt) warp_move_up(v, dst + cnt, dst, new_len - dst - cnt, lane);
-          if ((uint64_t)lane < cnt && dst + lane < new_len) v[dst + lane] = blk;
-          len = new_len;
-          break;
-        }
-        case 7: {  // constant fill
-          const uint64_t off = rng.below(len);
-          const uint64_t lim = len - off < 16 ? len - off : 16;
-          const uint64_t cnt = 1 + rng.below(lim);
-          const uint8_t b = (uint8_t)rng.below(256);
-          if ((uint64_t)lane < cnt) v[off + lane] = b;
-          break;
-        }
-        default: {  // 8: swap two bytes
-          const uint64_t i = rng.below(len);
-          const uint64_t k = rng.below(len);
-          if (lane == 0) {
-            const uint8_t t = v[i];
-            v[i] = v[k];
-            v[k] = t;
-          }
-          break;
-        }
-      }
-      __syncwarp();
-      if (len > kMaxInput) len = kMaxInput;
-    }
+    len = havoc_edit<false>(v, len, rng, lane);
     if (in_smem) {
       warp_copy(out, v, len, lane);
       __syncwarp();
@@ -230,6 +239,21 @@ __global__ void __launch_bounds__(kHavocWarps * 32) hfz_k_havoc(
       if (draws_out) draws_out[j] = rng.draws;
     }
   }
+}
+
+// Serial-stream plan: ONE Rng threaded through n mutants in slot order, as Campaign::fuzz_entry
+// does (src/engine.cpp:561-562).  A dry run per slot yields the state each slot starts from.
+__global__ void hfz_k_havoc_plan(const uint64_t* __restrict__ in_off, uint64_t n,
+                                 uint64_t* __restrict__ stream_state, uint64_t* __restrict__ slot_states) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  WarpRng rng;
+  rng.s = *stream_state;
+  rng.draws = 0;
+  for (uint64_t j = 0; j < n; ++j) {
+    slot_states[j] = rng.s;
+    havoc_edit<true>(nullptr, in_off[j + 1] - in_off[j], rng, 0);
+  }
+  *stream_state = rng.s;
 }
 
 __global__ void __launch_bounds__(256) hfz_k_splice(
@@ -353,6 +377,19 @@ extern "C" int hfz_havoc_batch(hfz_ctx* ctx, const uint8_t* in_bytes, const uint
   if (blocks > maxb) blocks = maxb;
   hfz_k_havoc<<<(uint32_t)blocks, kHavocWarps * 32, 0, ctx->stream>>>(
       in_bytes, in_off, n, rng_state_inout, out_bytes, out_off, out_len, draws_out);
+  ++ctx->launches;
+  HFZ_CUDA(cudaGetLastError());
+  return HFZ_OK;
+}
+
+extern "C" int hfz_havoc_serial_plan(hfz_ctx* ctx, const uint64_t* in_off, uint64_t n,
+                                     uint64_t* stream_state_inout, uint64_t* slot_states_out) {
+  if (!ctx || !stream_state_inout || (n && (!in_off || !slot_states_out))) {
+    hfz_set_error("hfz_havoc_serial_plan: null argument");
+    return HFZ_EINVAL;
+  }
+  HFZ_CUDA(cudaSetDevice(ctx->device));
+  hfz_k_havoc_plan<<<1, 32, 0, ctx->stream>>>(in_off, n, stream_state_inout, slot_states_out);
   ++ctx->launches;
   HFZ_CUDA(cudaGetLastError());
   return HFZ_OK;
