@@ -114,9 +114,9 @@ __device__ __forceinline__ uint64_t general_path(WarpTable& tab, const uint32_t*
   uint64_t bumps = 0;
   const uint32_t lane_le = 0xffffffffu >> (31 - lane);
   const uint32_t ev_total = __reduce_add_sync(0xffffffffu, n_ev);
-  const bool may_overflow = ev_total > kFill;  // distinct sites <= events
+  // initial depth: every partition would fit even if all its events were distinct sites
   uint32_t d0 = 0;
-  while (d0 < 26 && (ev_total >> d0) > kFill * 2) ++d0;  // assume some repetition; splits fix the rest
+  while (d0 < 26 && (ev_total >> d0) > kFill) ++d0;
   uint32_t stk_prefix[36], stk_depth[36];
   for (uint32_t root = 0; root < (1u << d0); ++root) {
     int sp = 1;
@@ -125,14 +125,22 @@ __device__ __forceinline__ uint64_t general_path(WarpTable& tab, const uint32_t*
     while (sp > 0) {
       --sp;
       const uint32_t prefix = stk_prefix[sp], depth = stk_depth[sp];
+      // events of this partition (an upper bound of its distinct sites): no table can overflow
+      // when they fit, otherwise a dry run inserts the sites to find out
+      uint32_t mine_cnt = n_ev;
+      if (depth) {
+        mine_cnt = 0;
+        for (uint32_t i = 0; i < n_ev; ++i) mine_cnt += (mix32(sites[e0 + i]) >> (32 - depth)) == prefix;
+      }
+      const uint32_t part_events = __reduce_add_sync(0xffffffffu, mine_cnt);
+      if (part_events == 0) continue;
       for (uint32_t i = lane; i < kRows; i += 32) {
         tab.keys[i] = 0;
         tab.stamp[i] = 0xffffffffu;  // row never touched in this partition: m = c = 0
       }
       if (lane == 0) *tab.used = 0;
       __syncwarp();
-      if (may_overflow) {
-        // dry run: insert this partition's sites only, to know that the table holds them
+      if (part_events > kRows - 16) {
         bool full = false;
         for (uint32_t i = 0; i < n_ev && !full; ++i) {
           const uint32_t s = sites[e0 + i];
@@ -141,7 +149,7 @@ __device__ __forceinline__ uint64_t general_path(WarpTable& tab, const uint32_t*
           full = table_insert(tab, s, h) == kRows;
         }
         __syncwarp();
-        if (__any_sync(0xffffffffu, full) || (*tab.used > kFill && depth < 32)) {
+        if (__any_sync(0xffffffffu, full) || (*tab.used > kRows - 16 && depth < 32)) {
           stk_prefix[sp] = prefix * 2 + 1;
           stk_depth[sp] = depth + 1;
           stk_prefix[sp + 1] = prefix * 2;
@@ -196,6 +204,15 @@ __device__ __forceinline__ uint64_t general_path(WarpTable& tab, const uint32_t*
   return bumps;
 }
 
+// exact a / b for a < 2^23, b >= 1: float quotient is within 1 of the true one
+__device__ __forceinline__ uint32_t div_small(uint32_t a, uint32_t b, float rb) {
+  uint32_t q = (uint32_t)((float)a * rb);
+  const uint32_t r = a - q * b;
+  if ((int32_t)r < 0) --q;             // overshoot by one
+  else if (r >= b) ++q;                // undershoot by one
+  return q;
+}
+
 template <bool SMEM_HIST>
 __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const EdgeParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -246,6 +263,8 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
         const uint32_t tpb = bdx * bdy * bdz, blocks = gx * gy * d[2];
         const uint32_t wpb = (tpb + 31) / 32;
         const uint32_t n_sw = blocks * wpb;
+        const float r_wpb = 1.0f / (float)wpb, r_gx = 1.0f / (float)gx, r_gy = 1.0f / (float)gy,
+                    r_bdx = 1.0f / (float)bdx, r_bdy = 1.0f / (float)bdy;
         const uint64_t t0 = p.thread_off[l];
         // simulated warps are handed out dynamically: divergent ones take far longer
         for (;;) {
@@ -253,7 +272,7 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
           if (lane == 0) sw = atomicAdd(&s_next, 1u);
           sw = __shfl_sync(0xffffffffu, sw, 0);
           if (sw >= n_sw) break;
-          const uint32_t bl = sw / wpb, tl = (sw - bl * wpb) * 32 + lane;
+          const uint32_t bl = div_small(sw, wpb, r_wpb), tl = (sw - bl * wpb) * 32 + lane;
           const bool active = tl < tpb;
           uint64_t e0 = 0, e1 = 0, gtid = 0;
           if (active) {
@@ -261,8 +280,10 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
             e0 = p.ev_off[t];
             e1 = p.ev_off[t + 1];
             if (multi) {
-              const uint32_t bxy = bl / gx, bx = bl - bxy * gx, bz = bxy / gy, by = bxy - bz * gy;
-              const uint32_t txy = tl / bdx, tx = tl - txy * bdx, tz = txy / bdy, ty = txy - tz * bdy;
+              const uint32_t bxy = div_small(bl, gx, r_gx), bx = bl - bxy * gx;
+              const uint32_t bz = div_small(bxy, gy, r_gy), by = bxy - bz * gy;
+              const uint32_t txy = div_small(tl, bdx, r_bdx), tx = tl - txy * bdx;
+              const uint32_t tz = div_small(txy, bdy, r_bdy), ty = txy - tz * bdy;
               const uint64_t rowx = (uint64_t)bdx * gx;  // threads per grid row
               gtid = tx + (uint64_t)bx * bdx + (ty + (uint64_t)by * bdy) * rowx +
                      (tz + (uint64_t)bz * bdz) * rowx * bdy * gy;

@@ -32,7 +32,7 @@ if what in ("all", "havoc"):
     tot = int(off[-1]) + int(ol.sum().item())
     print(f"K3 havoc: {n} seeds, {ms:.3f} ms -> {n/ms*1e3/1e6:.2f} M mutants/s, sum(in+out) {tot/ms/1e6:.1f} GB/s, mean draws {dr.float().mean().item():.1f}")
 if what in ("all", "edge"):
-    for n_exec in (512,):
+    for n_exec in (int(os.environ.get("EDGE_N", "2048")),):
         t = time.time()
         tr = synth.bb_traces(n_exec, seed=44)
         print(f"generated traces for {n_exec} execs in {time.time()-t:.1f}s: {tr['sites'].size/n_exec:.0f} events/exec")
