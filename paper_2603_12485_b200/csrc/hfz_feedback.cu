@@ -51,12 +51,12 @@ template <bool VSMEM, bool CLASSED>
 struct Lane {
   uint64_t hf, hs;
   uint32_t nnz, novel;
-  __device__ __forceinline__ void visit(uint32_t idx, uint32_t klass, const uint8_t* virgin,
-                                        uint32_t* first, uint32_t e, uint8_t* classed_row) {
+  // one non-zero slot: both FNV chains, novelty versus V0 (`known` = V0[idx]), optional class store
+  __device__ __forceinline__ void visit(uint32_t idx, uint32_t klass, uint32_t known, uint32_t* first,
+                                        uint32_t e, uint8_t* classed_row) {
     const uint32_t b0 = idx & 0xffu, b1 = (idx >> 8) & 0xffu;
     hf = hfz_fnv(hfz_fnv(hfz_fnv(hf, b0), b1), klass);
     hs = hfz_fnv(hfz_fnv(hs, b0), b1);
-    const uint32_t known = VSMEM ? (uint32_t)virgin[idx] : (uint32_t)__ldg(virgin + idx);
     ++nnz;
     if (klass & ~known) {
       novel = 1;
@@ -93,9 +93,13 @@ __device__ __forceinline__ void phase_b(const uint8_t* slot, uint32_t vm, uint32
                                         Lane<VSMEM, CLASSED>& st, const uint8_t* virgin,
                                         uint32_t* first, uint32_t e, uint8_t* classed_row) {
   // Warp-uniform loop (exit by vote) so the warp is provably converged around it; lanes that
-  // have run out of entries are predicated off inside.
+  // have run out of entries are predicated off inside.  Software-pipelined: the shared-memory
+  // loads of the NEXT non-zero slot (vector, element, virgin byte) are issued before the FNV
+  // chains of the current one, so their latency hides behind the dependent multiplies.
   uint32_t em = 0, vpos = 0;  // remaining non-zero elements of the current vector
-  while (__any_sync(0xffffffffu, (vm | em) != 0u)) {
+  uint32_t n_idx = 0, n_c = 0, n_known = 0;
+  bool n_valid = false;
+  auto fetch = [&]() {
     if (em == 0 && vm != 0) {
       vpos = __ffs(vm) - 1;
       vm &= vm - 1;
@@ -105,17 +109,26 @@ __device__ __forceinline__ void phase_b(const uint8_t* slot, uint32_t vm, uint32
       else
         em = min(v.x, 1u) | (min(v.y, 1u) << 1) | (min(v.z, 1u) << 2) | (min(v.w, 1u) << 3);
     }
-    if (em != 0) {
+    n_valid = em != 0;
+    if (n_valid) {
       const uint32_t k = __ffs(em) - 1;
       em &= em - 1;
       if (HOST) {
-        const uint32_t c = slot[vpos * 16 + k];
-        st.visit(slot_base + vpos * 16 + k, hfz_class_host(c), virgin, first, e, classed_row);
+        n_c = slot[vpos * 16 + k];
+        n_idx = slot_base + vpos * 16 + k;
       } else {
-        const uint32_t c = *reinterpret_cast<const uint32_t*>(slot + vpos * 16 + k * 4);
-        st.visit(slot_base + vpos * 4 + k, hfz_class_device(c), virgin, first, e, classed_row);
+        n_c = *reinterpret_cast<const uint32_t*>(slot + vpos * 16 + k * 4);
+        n_idx = slot_base + vpos * 4 + k;
       }
+      n_known = VSMEM ? (uint32_t)virgin[n_idx] : (uint32_t)__ldg(virgin + n_idx);
     }
+  };
+  fetch();
+  while (__any_sync(0xffffffffu, n_valid)) {
+    const bool valid = n_valid;
+    const uint32_t idx = n_idx, c = n_c, known = n_known;
+    fetch();
+    if (valid) st.visit(idx, HOST ? hfz_class_host(c) : hfz_class_device(c), known, first, e, classed_row);
   }
 }
 
@@ -153,15 +166,17 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
   bool virgin_ready = !VSMEM;
 
   // even split of the batch over all warps of the grid
-  // Small batches keep the groups full (32 lanes) on fewer warps instead of a few maps on
-  // every warp: SIMD efficiency of phase B matters more than occupancy there.
+  // Work split: every active warp gets g full groups of 32 maps (g = the fewest groups per warp
+  // that cover the batch); a partial group costs as much as a full one (absent maps alias the
+  // last one), so warps are left idle rather than given a few maps each.  Only the last active
+  // warp sees a partial group.
   const uint64_t Wall = (uint64_t)gridDim.x * nwarps;
   const uint64_t groups = (p.n_exec + 31) / 32;
-  const uint64_t W = groups < Wall ? groups : Wall;
+  const uint64_t g = (groups + Wall - 1) / Wall;
   const uint64_t wg = (uint64_t)warp * gridDim.x + blockIdx.x;
-  const uint64_t per = p.n_exec / W, rem = p.n_exec % W;
-  const uint64_t start = wg * per + (wg < rem ? wg : rem);
-  const uint64_t cnt = wg < W ? per + (wg < rem ? 1 : 0) : 0;
+  const uint64_t start = wg * g * 32 < p.n_exec ? wg * g * 32 : p.n_exec;
+  const uint64_t stop = (wg + 1) * g * 32 < p.n_exec ? (wg + 1) * g * 32 : p.n_exec;
+  const uint64_t cnt = stop - start;
   const uint32_t rows_host = p.H / ROW;
   const uint32_t rows = (uint32_t)(rec / ROW);
   const uint8_t* my_slot = s_buf + lane * C::kSlot;
@@ -631,7 +646,7 @@ int launch_scan(hfz_ctx* ctx, const ScanParams& p) {
     if (vsmem) return classed ? launch_scan_wpm_t<true, true>(ctx, p) : launch_scan_wpm_t<true, false>(ctx, p);
     return classed ? launch_scan_wpm_t<false, true>(ctx, p) : launch_scan_wpm_t<false, false>(ctx, p);
   }
-  const int row = ctx->scan_row == 256 ? 256 : 512;
+  const int row = ctx->scan_row == 512 ? 512 : 256;
   if (p.S == 65536u && vsmem) return launch_scan_r<163840, true>(ctx, p, row);
   if (p.S == 262144u && !vsmem) return launch_scan_r<655360, false>(ctx, p, row);
   return vsmem ? launch_scan_r<0, true>(ctx, p, row) : launch_scan_r<0, false>(ctx, p, row);

@@ -9,6 +9,7 @@ from paper_2603_12485_b200 import synth
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=16384)
+ap.add_argument("--ns", default="", help="comma separated batch sizes to time with the defaults (prefixes of the generated batch)")
 ap.add_argument("--mode", default="campaign")
 ap.add_argument("--configs", default="row=512;row=256", help="; separated, each k=v,k=v over scan_row/scan_warps/scan_prefetch/virgin_smem")
 ap.add_argument("--reps", type=int, default=5)
@@ -29,7 +30,7 @@ warm = torch.from_numpy(gen(4096, S, first=1 << 20)).to(ctx.device)
 ctx.feedback_batch(warm, virgin, counts)
 v0 = virgin.clone()
 ALIAS = dict(row="scan_row", warps="scan_warps", prefetch="scan_prefetch", vsmem="virgin_smem")
-DEFAULTS = dict(scan_row=512, scan_warps=0, scan_prefetch=1, virgin_smem=1)
+DEFAULTS = dict(scan_row=256, scan_warps=0, scan_prefetch=1, virgin_smem=1)
 for cfg in a.configs.split(";"):
     opts = dict(DEFAULTS)
     for kv in filter(None, cfg.split(",")):
@@ -52,3 +53,21 @@ for cfg in a.configs.split(";"):
     cand = int((out["admit"] != 0).sum())
     print(f"{cfg:40s}: {ms:8.3f} ms  {a.n/ms*1e3/1e6:7.3f} M evals/s  "
           f"{a.n*rec/ms/1e6:8.1f} GB/s ({a.n*rec/ms/1e6/6544.7*100:4.1f}% of 6544.7)  admits {cand}", flush=True)
+
+if a.ns:
+    for k, v in DEFAULTS.items():
+        ctx.set_option(k, v)
+    for n in [int(x) for x in a.ns.split(",")]:
+        sub = raw[: n * rec]
+        ts = []
+        for r in range(a.reps + 2):
+            virgin.copy_(v0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            o = ctx.feedback_batch(sub, virgin, counts)
+            e1.record()
+            torch.cuda.synchronize()
+            if r >= 2:
+                ts.append(e0.elapsed_time(e1))
+        ms = min(ts)
+        print(f"n={n:7d}: {ms:8.3f} ms  {n/ms*1e3/1e6:7.3f} M evals/s  {n*rec/ms/1e6:8.1f} GB/s ({n*rec/ms/1e6/6544.7*100:4.1f}%)", flush=True)

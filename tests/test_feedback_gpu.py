@@ -191,8 +191,8 @@ def test_sharded_scan_resolve_equals_sequential(ctx, checker, scan_kernel):
             c.close()
 
 
-@pytest.mark.parametrize("opts", [dict(scan_row=256), dict(scan_row=512, scan_prefetch=0),
-                                  dict(scan_row=512, virgin_smem=0), dict(scan_row=256, scan_warps=3)])
+@pytest.mark.parametrize("opts", [dict(scan_row=512), dict(scan_row=256, scan_prefetch=0), dict(scan_row=512, scan_prefetch=0),
+                                  dict(scan_row=512, virgin_smem=0), dict(scan_row=256, virgin_smem=0), dict(scan_row=256, scan_warps=3)])
 def test_scan_tunings_agree(ctx, checker, opts):
     """Every tuning of the scan kernel (row size, warps, L2 prefetch, virgin in smem or not)
     is the same function."""
@@ -202,7 +202,7 @@ def test_scan_tunings_agree(ctx, checker, opts):
     try:
         assert_same(run_gpu(ctx, raw), run_cpu(checker, raw, 200))
     finally:
-        for k, v in dict(scan_row=512, scan_warps=0, scan_prefetch=1, virgin_smem=1).items():
+        for k, v in dict(scan_row=256, scan_warps=0, scan_prefetch=1, virgin_smem=1).items():
             ctx.set_option(k, v)
 
 
