@@ -62,7 +62,7 @@ extern "C" int hfz_ctx_create(hfz_ctx** out, int device, uint32_t map_slots, voi
   c->num_sms = prop.multiProcessorCount;
   c->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
   cudaError_t a = cudaMalloc(&c->first, (size_t)map_slots * 8 * sizeof(uint32_t));
-  if (a == cudaSuccess) a = cudaMalloc(&c->cand_count, sizeof(uint32_t));
+  if (a == cudaSuccess) a = cudaMalloc(&c->cand_count, 2 * sizeof(uint32_t));
   if (a == cudaSuccess) a = cudaMalloc(&c->prior, map_slots);
   if (a == cudaSuccess) a = cudaMalloc(&c->delta, map_slots);
   if (a == cudaSuccess) a = cudaMalloc(&c->v0, map_slots);
@@ -130,7 +130,7 @@ extern "C" int hfz_ctx_set_option(hfz_ctx* c, const char* key, int64_t value) {
     if (value < 0 || value > 32) return HFZ_EINVAL;
     c->scan_warps = (int)value;
   } else if (!strcmp(key, "scan_row")) {
-    if (value != 256 && value != 512) return HFZ_EINVAL;
+    if (value != 0 && value != 256 && value != 512) return HFZ_EINVAL;
     c->scan_row = (int)value;
   } else if (!strcmp(key, "scan_prefetch")) {
     c->scan_prefetch = value != 0;

@@ -21,6 +21,7 @@
 namespace {
 
 constexpr uint32_t kNone = 0xffffffffu;
+constexpr uint32_t kNovMax = 8;  // novel entries kept per map; more -> resolve re-reads the map
 constexpr int kPad = 16;  // per-lane slot padding: makes 128-bit shared loads conflict-free
 
 struct ScanParams {
@@ -31,8 +32,11 @@ struct ScanParams {
   const uint8_t* v0;
   uint32_t* first;
   uint32_t* cand_list;
-  uint32_t* cand_count;
+  uint32_t* cand_count;  // [0] candidates, [1] candidates that need the map re-read
   uint32_t* cand_flags;
+  uint32_t* cand_nov;    // novel entries recorded for candidate ci (kNovMax + 1 = re-read the map)
+  uint32_t* slow_list;   // candidate indices whose map must be re-read
+  uint32_t* novel_ent;   // [n_exec][kNovMax] idx | rung << 24 of the slots novel versus V0
   uint64_t* sig_full;
   uint64_t* sig_simple;
   uint32_t* nnz;
@@ -53,14 +57,16 @@ struct Lane {
   uint32_t nnz, novel;
   // one non-zero slot: both FNV chains, novelty versus V0 (`known` = V0[idx]), optional class store
   __device__ __forceinline__ void visit(uint32_t idx, uint32_t klass, uint32_t known, uint32_t* first,
-                                        uint32_t e, uint8_t* classed_row) {
+                                        uint32_t e, uint8_t* classed_row, uint32_t* nov_row) {
     const uint32_t b0 = idx & 0xffu, b1 = (idx >> 8) & 0xffu;
     hf = hfz_fnv(hfz_fnv(hfz_fnv(hf, b0), b1), klass);
     hs = hfz_fnv(hfz_fnv(hs, b0), b1);
     ++nnz;
     if (klass & ~known) {
-      novel = 1;
-      atomicMin(first + (size_t)idx * 8 + (31 - __clz(klass)), e);
+      const uint32_t rung = 31 - __clz(klass);
+      if (novel < kNovMax) nov_row[novel] = idx | (rung << 24);
+      ++novel;
+      atomicMin(first + (size_t)idx * 8 + rung, e);
     }
     if (CLASSED) classed_row[idx] = (uint8_t)klass;
   }
@@ -91,7 +97,8 @@ struct RowCfg {
 template <bool HOST, int ROW, bool VSMEM, bool CLASSED>
 __device__ __forceinline__ void phase_b(const uint8_t* slot, uint32_t vm, uint32_t slot_base,
                                         Lane<VSMEM, CLASSED>& st, const uint8_t* virgin,
-                                        uint32_t* first, uint32_t e, uint8_t* classed_row) {
+                                        uint32_t* first, uint32_t e, uint8_t* classed_row,
+                                        uint32_t* nov_row) {
   // Warp-uniform loop (exit by vote) so the warp is provably converged around it; lanes that
   // have run out of entries are predicated off inside.  Software-pipelined: the shared-memory
   // loads of the NEXT non-zero slot (vector, element, virgin byte) are issued before the FNV
@@ -128,7 +135,7 @@ __device__ __forceinline__ void phase_b(const uint8_t* slot, uint32_t vm, uint32
     const bool valid = n_valid;
     const uint32_t idx = n_idx, c = n_c, known = n_known;
     fetch();
-    if (valid) st.visit(idx, HOST ? hfz_class_host(c) : hfz_class_device(c), known, first, e, classed_row);
+    if (valid) st.visit(idx, HOST ? hfz_class_host(c) : hfz_class_device(c), known, first, e, classed_row, nov_row);
   }
 }
 
@@ -190,6 +197,7 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
     const uint64_t e64 = base + lane;
     const uint32_t e = (uint32_t)e64;
     uint8_t* classed_row = CLASSED ? p.classed + e64 * p.S : nullptr;
+    uint32_t* nov_row = p.novel_ent + (valid ? e64 : base) * kNovMax;
     // lane's source for load i: map (i*kMapsPerLoad + sub), unit `unit`
     const uint8_t* gsrc = p.raw + (base + sub) * rec + unit * 16;
 
@@ -266,10 +274,10 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
         uint32_t vm = s_mask[lane];
         if (!FULL && !valid) vm = 0;  // no branch on `valid`: idle lanes just see an empty mask
         if (r < rows_host)
-          phase_b<true, ROW, VSMEM, CLASSED>(my_slot, vm, r * ROW, st, virgin, p.first, e, classed_row);
+          phase_b<true, ROW, VSMEM, CLASSED>(my_slot, vm, r * ROW, st, virgin, p.first, e, classed_row, nov_row);
         else
           phase_b<false, ROW, VSMEM, CLASSED>(my_slot, vm, p.H + (r - rows_host) * (ROW / 4), st,
-                                              virgin, p.first, e, classed_row);
+                                              virgin, p.first, e, classed_row, nov_row);
         __syncwarp();
       }
     };
@@ -292,6 +300,8 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
         const uint32_t ci = basei + __popc(cm & ((1u << lane) - 1u));
         p.cand_list[ci] = e;
         p.cand_flags[ci] = 0;
+        p.cand_nov[ci] = st.novel <= kNovMax ? st.novel : kNovMax + 1;
+        if (st.novel > kNovMax) p.slow_list[atomicAdd(p.cand_count + 1, 1u)] = ci;
       }
     }
   }
@@ -438,10 +448,12 @@ __global__ void __launch_bounds__(512, 1) hfz_k_scan_wpm(const ScanParams p) {
       p.sig_full[e64] = h;
       p.sig_simple[e64] = h_simple;
       if (p.nnz) p.nnz[e64] = nnz;
-      if (any_novel) {
+      if (any_novel) {  // this kernel does not record the novel slots: resolve re-reads the map
         const uint32_t ci = atomicAdd(p.cand_count, 1u);
         p.cand_list[ci] = e;
         p.cand_flags[ci] = 0;
+        p.cand_nov[ci] = kNovMax + 1;
+        p.slow_list[atomicAdd(p.cand_count + 1, 1u)] = ci;
       }
     }
   }
@@ -506,6 +518,9 @@ struct ResolveParams {
   const uint32_t* cand_list;
   const uint32_t* cand_count;
   uint32_t* cand_flags;
+  const uint32_t* cand_nov;
+  const uint32_t* slow_list;
+  const uint32_t* novel_ent;
   uint8_t* admit;
 };
 
@@ -532,9 +547,9 @@ __global__ void __launch_bounds__(256) hfz_k_resolve(const ResolveParams p, uint
   const uint32_t total_warps = (gridDim.x * blockDim.x) >> 5;
   const uint32_t pieces = (uint32_t)(p.rec_bytes / piece);
   const uint32_t host_pieces = p.H / piece;
-  const uint64_t items = (uint64_t)(*p.cand_count) * pieces;
+  const uint64_t items = (uint64_t)p.cand_count[1] * pieces;
   for (uint64_t it = warp; it < items; it += total_warps) {
-    const uint32_t ci = (uint32_t)(it / pieces), pc = (uint32_t)(it % pieces);
+    const uint32_t ci = p.slow_list[it / pieces], pc = (uint32_t)(it % pieces);
     const uint32_t e = p.cand_list[ci];
     const uint4* src = reinterpret_cast<const uint4*>(p.raw + (uint64_t)e * p.rec_bytes + (uint64_t)pc * piece);
     uint32_t flags = 0;
@@ -570,6 +585,21 @@ __global__ void __launch_bounds__(256) hfz_k_resolve(const ResolveParams p, uint
     }
     flags = __reduce_or_sync(0xffffffffu, flags);
     if (lane == 0 && flags) atomicOr(p.cand_flags + ci, flags);
+  }
+}
+
+// candidates with at most kNovMax novel slots: the scan recorded them, no need to read the map again
+__global__ void __launch_bounds__(256) hfz_k_resolve_fast(const ResolveParams p) {
+  const uint64_t n = (uint64_t)p.cand_count[0] * kNovMax;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t ci = (uint32_t)(t / kNovMax), k = (uint32_t)(t % kNovMax);
+    const uint32_t cnt = p.cand_nov[ci];
+    if (cnt > kNovMax || k >= cnt) continue;
+    const uint32_t e = p.cand_list[ci];
+    const uint32_t en = p.novel_ent[(size_t)e * kNovMax + k];
+    const uint32_t f = resolve_entry(p, en & 0xffffffu, 1u << (en >> 24), e);
+    if (f) atomicOr(p.cand_flags + ci, f);
   }
 }
 
@@ -646,7 +676,11 @@ int launch_scan(hfz_ctx* ctx, const ScanParams& p) {
     if (vsmem) return classed ? launch_scan_wpm_t<true, true>(ctx, p) : launch_scan_wpm_t<true, false>(ctx, p);
     return classed ? launch_scan_wpm_t<false, true>(ctx, p) : launch_scan_wpm_t<false, false>(ctx, p);
   }
-  const int row = ctx->scan_row == 512 ? 512 : 256;
+  // 256-byte rows let 18 warps/SM hide the shared-memory latency of phase B (best when every SM
+  // has more than 9 groups to run); 512-byte rows halve the number of rows a warp walks, which
+  // wins while a batch gives each SM at most 9 groups anyway (latency-bound regime).
+  int row = ctx->scan_row;
+  if (row != 256 && row != 512) row = ((p.n_exec + 31) / 32 <= (uint64_t)ctx->num_sms * 9) ? 512 : 256;
   if (p.S == 65536u && vsmem) return launch_scan_r<163840, true>(ctx, p, row);
   if (p.S == 262144u && !vsmem) return launch_scan_r<655360, false>(ctx, p, row);
   return vsmem ? launch_scan_r<0, true>(ctx, p, row) : launch_scan_r<0, false>(ctx, p, row);
@@ -658,7 +692,7 @@ int ensure_cand(hfz_ctx* ctx, uint64_t n_exec) {
   ctx->cand_list = nullptr;
   ctx->cand_cap = 0;
   const uint64_t cap = n_exec < 1024 ? 1024 : n_exec;
-  if (cudaMalloc(&ctx->cand_list, 2 * cap * sizeof(uint32_t)) != cudaSuccess) {
+  if (cudaMalloc(&ctx->cand_list, (4 + kNovMax) * cap * sizeof(uint32_t)) != cudaSuccess) {
     hfz_set_error("cudaMalloc(cand_list, %llu) failed", (unsigned long long)cap * 4);
     return HFZ_ENOMEM;
   }
@@ -688,7 +722,7 @@ extern "C" int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t
   int rc = ensure_cand(ctx, n_exec);
   if (rc) return rc;
   HFZ_CUDA(cudaMemsetAsync(ctx->first, 0xff, (size_t)ctx->S * 8 * sizeof(uint32_t), ctx->stream));
-  HFZ_CUDA(cudaMemsetAsync(ctx->cand_count, 0, sizeof(uint32_t), ctx->stream));
+  HFZ_CUDA(cudaMemsetAsync(ctx->cand_count, 0, 2 * sizeof(uint32_t), ctx->stream));
   if (classed_out && n_exec)
     HFZ_CUDA(cudaMemsetAsync(classed_out, 0, n_exec * (size_t)ctx->S, ctx->stream));
   if (n_exec) {
@@ -703,6 +737,9 @@ extern "C" int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t
     p.cand_list = ctx->cand_list;
     p.cand_count = ctx->cand_count;
     p.cand_flags = ctx->cand_list + ctx->cand_cap;
+    p.cand_nov = ctx->cand_list + 2 * ctx->cand_cap;
+    p.slow_list = ctx->cand_list + 3 * ctx->cand_cap;
+    p.novel_ent = ctx->cand_list + 4 * ctx->cand_cap;
     p.sig_full = sig_full_out;
     p.sig_simple = sig_simple_out;
     p.nnz = nnz_out;
@@ -770,7 +807,13 @@ extern "C" int hfz_feedback_resolve(hfz_ctx* ctx, const uint8_t* raw_maps, uint6
     p.cand_list = ctx->cand_list;
     p.cand_count = ctx->cand_count;
     p.cand_flags = ctx->cand_list + ctx->cand_cap;
+    p.cand_nov = ctx->cand_list + 2 * ctx->cand_cap;
+    p.slow_list = ctx->cand_list + 3 * ctx->cand_cap;
+    p.novel_ent = ctx->cand_list + 4 * ctx->cand_cap;
     p.admit = admit_out;
+    hfz_k_resolve_fast<<<(uint32_t)ctx->num_sms * 2, 256, 0, ctx->stream>>>(p);
+    ++ctx->launches;
+    HFZ_CUDA(cudaGetLastError());
     uint32_t piece = kPiece;
     while (ctx->H % piece) piece >>= 1;  // H is a power of two >= 512
     hfz_k_resolve<<<(uint32_t)ctx->num_sms * 4, 256, 0, ctx->stream>>>(p, piece);

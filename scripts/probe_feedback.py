@@ -30,7 +30,7 @@ warm = torch.from_numpy(gen(4096, S, first=1 << 20)).to(ctx.device)
 ctx.feedback_batch(warm, virgin, counts)
 v0 = virgin.clone()
 ALIAS = dict(row="scan_row", warps="scan_warps", prefetch="scan_prefetch", vsmem="virgin_smem")
-DEFAULTS = dict(scan_row=256, scan_warps=0, scan_prefetch=1, virgin_smem=1)
+DEFAULTS = dict(scan_row=0, scan_warps=0, scan_prefetch=1, virgin_smem=1)
 for cfg in a.configs.split(";"):
     opts = dict(DEFAULTS)
     for kv in filter(None, cfg.split(",")):

@@ -202,7 +202,7 @@ def test_scan_tunings_agree(ctx, checker, opts):
     try:
         assert_same(run_gpu(ctx, raw), run_cpu(checker, raw, 200))
     finally:
-        for k, v in dict(scan_row=256, scan_warps=0, scan_prefetch=1, virgin_smem=1).items():
+        for k, v in dict(scan_row=0, scan_warps=0, scan_prefetch=1, virgin_smem=1).items():
             ctx.set_option(k, v)
 
 
