@@ -42,7 +42,8 @@ struct WarpRng {
   }
 };
 
-// non-overlapping copy by one warp
+// non-overlapping copy by one warp; loads are issued in batches of 8 per lane so that a
+// misaligned (byte-granular) copy from global memory still has 8 requests in flight per lane
 __device__ __forceinline__ void warp_copy(uint8_t* dst, const uint8_t* src, uint64_t n, int lane) {
   if ((((uintptr_t)dst ^ (uintptr_t)src) & 15) == 0 && n >= 64) {
     uint64_t head = (16 - ((uintptr_t)dst & 15)) & 15;
@@ -51,10 +52,55 @@ __device__ __forceinline__ void warp_copy(uint8_t* dst, const uint8_t* src, uint
     const uint64_t body = (n - head) / 16;
     const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
     uint4* d4 = reinterpret_cast<uint4*>(dst + head);
-    for (uint64_t i = lane; i < body; i += 32) d4[i] = s4[i];
+    for (uint64_t b0 = 0; b0 < body; b0 += 32 * 4) {
+      uint4 t[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t i = b0 + k * 32 + lane;
+        if (i < body) t[k] = s4[i];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t i = b0 + k * 32 + lane;
+        if (i < body) d4[i] = t[k];
+      }
+    }
     for (uint64_t i = head + body * 16 + lane; i < n; i += 32) dst[i] = src[i];
+  } else if ((((uintptr_t)dst ^ (uintptr_t)src) & 3) == 0 && n >= 16) {
+    uint64_t head = (4 - ((uintptr_t)dst & 3)) & 3;
+    if (head > n) head = n;
+    if ((uint64_t)lane < head) dst[lane] = src[lane];
+    const uint64_t body = (n - head) / 4;
+    const uint32_t* s1 = reinterpret_cast<const uint32_t*>(src + head);
+    uint32_t* d1 = reinterpret_cast<uint32_t*>(dst + head);
+    for (uint64_t b0 = 0; b0 < body; b0 += 32 * 8) {
+      uint32_t t[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint64_t i = b0 + k * 32 + lane;
+        if (i < body) t[k] = s1[i];
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint64_t i = b0 + k * 32 + lane;
+        if (i < body) d1[i] = t[k];
+      }
+    }
+    for (uint64_t i = head + body * 4 + lane; i < n; i += 32) dst[i] = src[i];
   } else {
-    for (uint64_t i = lane; i < n; i += 32) dst[i] = src[i];
+    for (uint64_t b0 = 0; b0 < n; b0 += 32 * 8) {
+      uint8_t t[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint64_t i = b0 + k * 32 + lane;
+        if (i < n) t[k] = src[i];
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint64_t i = b0 + k * 32 + lane;
+        if (i < n) dst[i] = t[k];
+      }
+    }
   }
 }
 
