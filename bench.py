@@ -188,6 +188,40 @@ def workload_name(args):
 
 
 # --------------------------------------------------------------------------- GPU arm
+def sparse_lists_from_device(raw, n, dev):
+    """Touched-slot lists of the first n records of `raw` (device tensor): pinned host tensors
+    (entries (N, 2) int32, entry_off (n+1) int64).  The pairs of an exec are put in a random order.
+    Data preparation, outside every timed region."""
+    import torch
+    H = S // 2
+    ents, counts = [], []
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234)
+    for i in range(0, n, 2048):
+        m = min(2048, n - i)
+        rec = raw[i * REC:(i + m) * REC].view(m, REC)
+        host = rec[:, :H]
+        devh = rec[:, H:].contiguous().view(torch.int32)
+        hr, hc = torch.nonzero(host, as_tuple=True)
+        dr, dc = torch.nonzero(devh, as_tuple=True)
+        rows = torch.cat([hr, dr])
+        slots = torch.cat([hc, dc + H]).to(torch.int32)
+        cnts = torch.cat([host[hr, hc].to(torch.int32), devh[dr, dc]])
+        key = (rows << 32) | torch.randint(0, 1 << 31, rows.shape, device=dev, generator=g)
+        order = torch.argsort(key)
+        ents.append(torch.stack([slots[order], cnts[order]], dim=1).cpu())
+        counts.append(torch.bincount(rows, minlength=m).cpu())
+    total = sum(int(e.shape[0]) for e in ents)
+    ent = torch.empty((total, 2), dtype=torch.int32, pin_memory=True)
+    off = torch.zeros(n + 1, dtype=torch.int64, pin_memory=True)
+    p = 0
+    for e in ents:
+        ent[p:p + e.shape[0]] = e
+        p += e.shape[0]
+    off[1:] = torch.cumsum(torch.cat(counts), 0)
+    return ent, off
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -301,32 +335,63 @@ def run_ours(args):
     value = world * n / (ms_per_step / 1e3)
     admits = int((out["admit"] != 0).sum().item())
 
-    # --- end-to-end through the C-ABI with HOST buffers (pinned), copies inside the timed region
+    # --- end-to-end through the C-ABI with HOST buffers (pinned), copies inside the timed region.
+    # Two host forms of the same batch: (a) touched-slot lists (slot, count) -- what
+    # hetfuzz::b200::SparseBatch keeps per CoverageMap -- through hfz_feedback_batch_sparse_host;
+    # (b) dense 163,840-byte records through hfz_feedback_batch_host (PCIe-bound).
     e2e = None
+    e2e_dense = None
     if not args.no_e2e:
         n_e2e = args.e2e_execs or n
-        pinned = torch.empty(n_e2e * REC, dtype=torch.uint8, pin_memory=True)
-        pinned.copy_(raw[: n_e2e * REC])
-        raw_host = pinned.numpy()
         v0_host = v0.cpu().numpy()
         c0_host = c0.cpu().numpy().view(np.uint64)
-        ts = []
-        for i in range(1 + args.e2e_steps):
-            vh, ch = v0_host.copy(), c0_host.copy()
-            barrier()
-            t1 = time.perf_counter()
-            res = ctx.feedback_batch_host(raw_host, vh, ch)
-            dt = time.perf_counter() - t1
-            if i:
-                ts.append(dt)
-        te = torch.tensor([float(np.mean(ts))], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * n_e2e / float(te.item()), "unit": UNIT,
-               "h2d_bytes_per_step": int(n_e2e * REC + S + 16),
-               "d2h_bytes_per_step": int(n_e2e * (1 + 8 + 8 + 4) + S + 16),
-               "execs_per_step": n_e2e, "api": "hfz_feedback_batch_host (pinned host buffers, chunked overlapped H2D)"}
-        del pinned
+
+        def timed(call):
+            ts, res = [], None
+            for i in range(1 + args.e2e_steps):
+                vh, ch = v0_host.copy(), c0_host.copy()
+                barrier()
+                t1 = time.perf_counter()
+                res = call(vh, ch)
+                dt = time.perf_counter() - t1
+                if i:
+                    ts.append(dt)
+            te = torch.tensor([float(np.mean(ts))], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            return float(te.item()), res
+
+        # (a) sparse lists, built outside the timed region from the same maps
+        ent_t, off_t = sparse_lists_from_device(raw, n_e2e, dev)
+        ent_np, off_np = ent_t.numpy().view(np.uint32), off_t.numpy().view(np.uint64)
+        sec, res = timed(lambda vh, ch: ctx.feedback_batch_sparse_host(ent_np, off_np, vh, ch))
+        same = bool(np.array_equal(res["admit"], out["admit"][:n_e2e].cpu().numpy())
+                    and np.array_equal(res["sig_full"], out["sig_full"][:n_e2e].cpu().numpy().view(np.uint64))
+                    and np.array_equal(res["sig_simple"], out["sig_simple"][:n_e2e].cpu().numpy().view(np.uint64)))
+        if not same:
+            raise SystemExit("bench.py: sparse e2e results differ from the device-resident dense fold")
+        e2e = {"value": world * n_e2e / sec, "unit": UNIT,
+               "h2d_bytes_per_step": int(ent_np.nbytes + off_np.nbytes + S + 16),
+               "d2h_bytes_per_step": int(n_e2e * (1 + 8 + 8 + 4) + S + 16 + 8),
+               "execs_per_step": n_e2e, "host_form": "touched-slot lists: (u32 slot, u32 count) pairs per exec, "
+               "random order inside an exec, pinned host memory",
+               "pairs_per_exec": float(ent_np.shape[0]) / n_e2e,
+               "equals_device_fold": same,
+               "api": "hfz_feedback_batch_sparse_host (pairs streamed H2D chunk by chunk, expanded and folded "
+                      "on the device)"}
+        del ent_t, off_t, ent_np, off_np
+        # (b) dense records
+        if not args.no_e2e_dense:
+            pinned = torch.empty(n_e2e * REC, dtype=torch.uint8, pin_memory=True)
+            pinned.copy_(raw[: n_e2e * REC])
+            raw_host = pinned.numpy()
+            sec, res = timed(lambda vh, ch: ctx.feedback_batch_host(raw_host, vh, ch))
+            e2e_dense = {"value": world * n_e2e / sec, "unit": UNIT,
+                         "h2d_bytes_per_step": int(n_e2e * REC + S + 16),
+                         "d2h_bytes_per_step": int(n_e2e * (1 + 8 + 8 + 4) + S + 16),
+                         "execs_per_step": n_e2e, "host_form": "dense 163,840-byte records, pinned host memory",
+                         "api": "hfz_feedback_batch_host (chunked overlapped H2D); PCIe-bound"}
+            del pinned
 
     if rank == 0:
         peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -366,7 +431,8 @@ def run_ours(args):
                        "l2_policy": "inputs larger than L2 (10.7 GB per GPU per step)",
                        "admits_per_step_rank0": admits, "parallelism": f"exec-sharded x{world}",
                        "gen_seconds": round(gen_s, 1), "parity_checked": parity},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_dense": e2e_dense,
+            "gpu_launches": launches,
             "clocks": clocks,
             "hbm_gbs_algorithmic": world * n * REC / (ms_per_step / 1e3) / 1e9,
             "logical_map_gbs": world * n * S / (ms_per_step / 1e3) / 1e9,
@@ -391,6 +457,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-execs", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-e2e-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true")
     args = ap.parse_args()

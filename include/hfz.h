@@ -79,7 +79,7 @@ HFZ_API int hfz_ctx_set_stream(hfz_ctx* ctx, void* stream);
 HFZ_API int hfz_ctx_sync(hfz_ctx* ctx);
 HFZ_API uint32_t hfz_ctx_map_slots(const hfz_ctx* ctx);
 HFZ_API uint64_t hfz_record_bytes(uint32_t map_slots);
-/* Tuning knobs, mostly for bench/profiling: key in {"scan_warps","scan_row","scan_prefetch","virgin_smem","time_scan","stage_execs"} */
+/* Tuning knobs, mostly for bench/profiling: key in {"scan_warps","scan_row","scan_prefetch","virgin_smem","scan_small","time_scan","stage_execs","sparse_chunk"} */
 HFZ_API int hfz_ctx_set_option(hfz_ctx* ctx, const char* key, int64_t value);
 /* Kernels launched by this context since creation (for bench.py's gpu_launches). */
 HFZ_API uint64_t hfz_ctx_launch_count(const hfz_ctx* ctx);
@@ -118,6 +118,46 @@ HFZ_API int hfz_feedback_batch_host(hfz_ctx* ctx, const uint8_t* raw_maps_host, 
                                     uint8_t* classed_out_host, uint8_t* admit_out_host,
                                     uint64_t* sig_full_out_host, uint64_t* sig_simple_out_host,
                                     uint32_t* nnz_out_host);
+
+/* ------------------------------------------------------------------------- */
+/* Sparse ingest: the same fold, fed with per-exec TOUCHED-SLOT LISTS instead of dense records.
+ * A raw map is ~2 % dense; the reference's runtime already keeps a dirty-slot list beside its
+ * device counters (Runtime::bump_counter / reset_device_coverage, src/hdvm.cpp:356-366) and
+ * classify_trace reduces a map to its non-zero list (src/coverage.cpp:58-72).  A list ships
+ * ~10 KB per exec over PCIe instead of 163,840 B.
+ *
+ *   entries    n_total x {u32 slot, u32 count} pairs, 8-byte aligned.  Exec e owns pairs
+ *              [entry_off[e], entry_off[e+1]); ANY order inside an exec; a slot may appear at
+ *              most once per exec (repeats: one of them wins).  slot < S/2 is a host counter
+ *              (count & 0xff is stored, CoverageMap::host_), S/2 <= slot < S a device counter
+ *              (full u32, CoverageMap::device_).  count 0 leaves the slot unvisited.  Pairs
+ *              with slot >= S are ignored and counted: the _host call then returns HFZ_EINVAL
+ *              after completing the fold.
+ *   entry_off  (n_exec+1) x u64, entry_off[0] = 0, non-decreasing
+ * Outputs and in/out state exactly as hfz_feedback_batch: results are bit-identical to the
+ * dense call on the maps the lists describe.  The lists are expanded chunk by chunk into a
+ * context-owned, all-zero staging buffer (option "sparse_chunk" = execs per chunk, default
+ * ~1.25 GB of records) which the K2 scan then streams.
+ */
+HFZ_API int hfz_feedback_batch_sparse(hfz_ctx* ctx, const uint32_t* entries, const uint64_t* entry_off,
+                                      uint64_t n_exec, uint8_t* virgin_inout,
+                                      uint64_t* edge_counts_inout, uint8_t* classed_out,
+                                      uint8_t* admit_out, uint64_t* sig_full_out,
+                                      uint64_t* sig_simple_out, uint32_t* nnz_out);
+/* HOST buffers (pinned for full PCIe speed, see hfz_host_alloc): the pairs stream in on a copy
+ * stream chunk by chunk while earlier chunks are folded; synchronous. */
+HFZ_API int hfz_feedback_batch_sparse_host(hfz_ctx* ctx, const uint32_t* entries_host,
+                                           const uint64_t* entry_off_host, uint64_t n_exec,
+                                           uint8_t* virgin_inout_host, uint64_t* edge_counts_inout_host,
+                                           uint8_t* classed_out_host, uint8_t* admit_out_host,
+                                           uint64_t* sig_full_out_host, uint64_t* sig_simple_out_host,
+                                           uint32_t* nnz_out_host);
+/* lists -> dense records (device buffers; raw_maps_out is overwritten, n_exec records) */
+HFZ_API int hfz_expand_sparse(hfz_ctx* ctx, const uint32_t* entries, const uint64_t* entry_off,
+                              uint64_t n_exec, uint8_t* raw_maps_out);
+/* Page-locked host memory for hosts that do not link the CUDA runtime themselves. */
+HFZ_API int hfz_host_alloc(void** out, uint64_t bytes);
+HFZ_API int hfz_host_free(void* p);
 
 /* The two halves of hfz_feedback_batch, exposed for multi-GPU sharding
  * (SURVEY.md 8e).  Rank r owns a contiguous exec range of the global batch.

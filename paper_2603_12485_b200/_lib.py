@@ -33,6 +33,11 @@ PROTOTYPES = {
     "hfz_ctx_get_stat": (C.c_int, [_vp, C.c_char_p, C.POINTER(C.c_double)]),
     "hfz_feedback_batch": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hfz_feedback_batch_host": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hfz_feedback_batch_sparse": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hfz_feedback_batch_sparse_host": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hfz_expand_sparse": (C.c_int, [_vp, _vp, _vp, _u64, _vp]),
+    "hfz_host_alloc": (C.c_int, [C.POINTER(_vp), _u64]),
+    "hfz_host_free": (C.c_int, [_vp]),
     "hfz_feedback_scan": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hfz_feedback_resolve": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _u32, _u32, _vp]),
     "hfz_virgin_merge": (C.c_int, [_vp, _vp, _vp, _vp, _u32]),

@@ -174,6 +174,62 @@ class Context:
             o["classed"] = classed
         return o
 
+    # ---- sparse ingest ------------------------------------------------------
+    def feedback_batch_sparse(self, entries: torch.Tensor, entry_off: torch.Tensor, virgin: torch.Tensor,
+                              edge_counts: torch.Tensor, want_classed: bool = False, out: dict | None = None):
+        """feedback_batch fed with per-exec touched-slot lists: `entries` is an (N, 2) int32 device
+        tensor of (slot, count) bit patterns, `entry_off` an int64 device tensor of n_exec+1 offsets."""
+        _dev(entries, self.device, torch.int32)
+        _dev(entry_off, self.device, torch.int64)
+        n = entry_off.numel() - 1
+        o = out or {}
+        if "admit" not in o:
+            o["admit"] = torch.empty(n, dtype=torch.uint8, device=self.device)
+            o["sig_full"] = torch.empty(n, dtype=torch.int64, device=self.device)
+            o["sig_simple"] = torch.empty(n, dtype=torch.int64, device=self.device)
+            o["nnz"] = torch.empty(n, dtype=torch.int32, device=self.device)
+        if want_classed and "classed" not in o:
+            o["classed"] = torch.empty((n, self.S), dtype=torch.uint8, device=self.device)
+        self._sync_stream()
+        check(lib.hfz_feedback_batch_sparse(self._h, _ptr(entries), _ptr(entry_off), n, _ptr(virgin),
+                                            _ptr(edge_counts), _ptr(o.get("classed")) if want_classed else None,
+                                            _ptr(o["admit"]), _ptr(o["sig_full"]), _ptr(o["sig_simple"]),
+                                            _ptr(o["nnz"])))
+        return o
+
+    def feedback_batch_sparse_host(self, entries: np.ndarray, entry_off: np.ndarray, virgin: np.ndarray,
+                                   edge_counts: np.ndarray, want_classed: bool = False):
+        """Same through HOST buffers: entries (N, 2) uint32, entry_off (n_exec+1) uint64 (numpy,
+        ideally views of pinned memory): the sparse e2e path of bench.py."""
+        n = entry_off.size - 1
+        assert entries.dtype == np.uint32 and entries.flags.c_contiguous and entries.size % 2 == 0
+        assert entry_off.dtype == np.uint64 and entry_off.flags.c_contiguous and n >= 0
+        assert virgin.dtype == np.uint8 and virgin.size == self.S
+        assert edge_counts.dtype == np.uint64 and edge_counts.size == 2
+        admit = np.empty(n, np.uint8)
+        sf = np.empty(n, np.uint64)
+        ss = np.empty(n, np.uint64)
+        nnz = np.empty(n, np.uint32)
+        classed = np.empty((n, self.S), np.uint8) if want_classed else None
+        vp = lambda a: None if a is None else C.c_void_p(a.ctypes.data)
+        self._sync_stream()
+        check(lib.hfz_feedback_batch_sparse_host(self._h, vp(entries), vp(entry_off), n, vp(virgin),
+                                                 vp(edge_counts), vp(classed), vp(admit), vp(sf), vp(ss),
+                                                 vp(nnz)))
+        o = dict(admit=admit, sig_full=sf, sig_simple=ss, nnz=nnz)
+        if want_classed:
+            o["classed"] = classed
+        return o
+
+    def expand_sparse(self, entries: torch.Tensor, entry_off: torch.Tensor, raw: torch.Tensor | None = None):
+        """Touched-slot lists -> dense raw records on the device."""
+        n = entry_off.numel() - 1
+        if raw is None:
+            raw = torch.empty(n * self.rec, dtype=torch.uint8, device=self.device)
+        self._sync_stream()
+        check(lib.hfz_expand_sparse(self._h, _ptr(entries), _ptr(entry_off), n, _ptr(raw)))
+        return raw
+
     # ---- K1 -----------------------------------------------------------------
     def edge_record_batch(self, launch_off, dims, thread_off, ev_off, sites, n_exec, raw=None,
                           want_events=True):

@@ -104,6 +104,10 @@ extern "C" int hfz_ctx_destroy(hfz_ctx* c) {
   cudaFree(c->d_sigs);
   cudaFree(c->d_nnz);
   cudaFree(c->d_classed);
+  cudaFree(c->sp_dense);
+  cudaFree(c->sp_entries);
+  cudaFree(c->sp_off);
+  for (cudaEvent_t ev : c->sp_events) cudaEventDestroy(ev);
   delete c;
   return HFZ_OK;
 }
@@ -140,6 +144,9 @@ extern "C" int hfz_ctx_set_option(hfz_ctx* c, const char* key, int64_t value) {
     c->scan_small = value;
   } else if (!strcmp(key, "time_scan")) {
     c->time_scan = value != 0;
+  } else if (!strcmp(key, "sparse_chunk")) {
+    if (value < 0 || (value && value < 32) || c->sp_dense) return HFZ_EINVAL;
+    c->sparse_chunk = (uint64_t)value / 32 * 32;
   } else if (!strcmp(key, "stage_execs")) {
     if (value < 32 || c->stage_raw[0]) return HFZ_EINVAL;
     c->stage_execs = (uint64_t)value;
@@ -178,19 +185,9 @@ extern "C" int hfz_ctx_get_stat(hfz_ctx* c, const char* key, double* out) {
 // ---------------------------------------------------------------------------
 // Host-buffer front-end: chunked, double-buffered H2D overlapped with the kernels.
 
-static int ensure_host_path(hfz_ctx* c, uint64_t n_exec, bool want_classed) {
-  if (!c->stage_raw[0]) {
-    if (c->stage_execs == 0) {
-      // ~256 MB per staging buffer
-      uint64_t se = (256ull << 20) / c->rec_bytes;
-      se = se < 32 ? 32 : (se / 32) * 32;
-      c->stage_execs = se;
-    }
-    for (int i = 0; i < 2; ++i) {
-      HFZ_CUDA(cudaMalloc(&c->stage_raw[i], c->stage_execs * c->rec_bytes));
-      HFZ_CUDA(cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming));
-      HFZ_CUDA(cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming));
-    }
+// copy stream, device copies of virgin / counters and per-exec outputs shared by the _host calls
+int hfz_ensure_host_common(hfz_ctx* c, uint64_t n_exec) {
+  if (!c->copy_stream) {
     HFZ_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     HFZ_CUDA(cudaMalloc(&c->d_virgin, c->S));
     HFZ_CUDA(cudaMalloc(&c->d_counts, 2 * sizeof(uint64_t)));
@@ -211,10 +208,36 @@ static int ensure_host_path(hfz_ctx* c, uint64_t n_exec, bool want_classed) {
     HFZ_CUDA(cudaMalloc(&c->d_nnz, cap * 4));
     c->d_out_cap = cap;
   }
-  if (want_classed && !c->d_classed) {
-    HFZ_CUDA(cudaMalloc(&c->d_classed, c->stage_execs * (uint64_t)c->S));
-    c->d_classed_cap = c->stage_execs;
+  return HFZ_OK;
+}
+
+int hfz_ensure_classed_stage(hfz_ctx* c, uint64_t execs) {
+  if (c->d_classed_cap >= execs) return HFZ_OK;
+  cudaFree(c->d_classed);
+  c->d_classed = nullptr;
+  c->d_classed_cap = 0;
+  HFZ_CUDA(cudaMalloc(&c->d_classed, execs * (uint64_t)c->S));
+  c->d_classed_cap = execs;
+  return HFZ_OK;
+}
+
+static int ensure_host_path(hfz_ctx* c, uint64_t n_exec, bool want_classed) {
+  int rc = hfz_ensure_host_common(c, n_exec);
+  if (rc) return rc;
+  if (!c->stage_raw[0]) {
+    if (c->stage_execs == 0) {
+      // ~256 MB per staging buffer
+      uint64_t se = (256ull << 20) / c->rec_bytes;
+      se = se < 32 ? 32 : (se / 32) * 32;
+      c->stage_execs = se;
+    }
+    for (int i = 0; i < 2; ++i) {
+      HFZ_CUDA(cudaMalloc(&c->stage_raw[i], c->stage_execs * c->rec_bytes));
+      HFZ_CUDA(cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming));
+      HFZ_CUDA(cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming));
+    }
   }
+  if (want_classed) return hfz_ensure_classed_stage(c, c->stage_execs);
   return HFZ_OK;
 }
 

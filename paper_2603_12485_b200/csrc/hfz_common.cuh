@@ -56,6 +56,17 @@ struct hfz_ctx {
   uint64_t d_out_cap = 0;
   uint64_t d_classed_cap = 0;
 
+  // sparse ingest (hfz_sparse.cu; owned, lazily allocated)
+  uint8_t* sp_dense = nullptr;     // dense expansion staging, all-zero between calls
+  uint64_t sp_dense_execs = 0;     // records it holds
+  bool sp_dirty = false;           // an error path left entries behind: memset before reuse
+  uint64_t sparse_chunk = 0;       // execs expanded per chunk (0 = ~1.25 GB of records)
+  uint32_t* sp_entries = nullptr;  // device copy of host (slot, count) pairs
+  uint64_t sp_entries_cap = 0;     // pairs
+  uint64_t* sp_off = nullptr;
+  uint64_t sp_off_cap = 0;
+  std::vector<cudaEvent_t> sp_events;  // one "entries of chunk k copied" event per chunk
+
   // tuning
   int scan_warps = 0;     // 0 = as many as fit
   int scan_row = 0;       // bytes per map per row: 0 = auto, 256 (18 warps/SM) or 512 (9 warps/SM)
@@ -68,6 +79,8 @@ struct hfz_ctx {
 
 void hfz_set_error(const char* fmt, ...);
 int hfz_cuda_fail(cudaError_t e, const char* what);
+int hfz_ensure_host_common(hfz_ctx* c, uint64_t n_exec);   // hfz_api.cu
+int hfz_ensure_classed_stage(hfz_ctx* c, uint64_t execs);  // hfz_api.cu
 
 #define HFZ_CUDA(call)                                   \
   do {                                                   \

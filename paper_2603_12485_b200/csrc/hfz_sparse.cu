@@ -1,0 +1,284 @@
+// hfz_sparse.cu -- sparse ingest of raw maps: per-exec touched-slot lists instead of dense records.
+//
+// A raw map is ~2 % dense, so shipping it dense costs 163,840 B per exec over PCIe (the e2e
+// bound of hfz_feedback_batch_host) for ~1,300 non-zero counters.  The reference's own runtime
+// already keeps a dirty-slot list beside its device counters (Runtime::bump_counter /
+// reset_device_coverage, /root/reference/proj/src/hdvm.cpp:356-366) and classify_trace reduces
+// a map to its ascending non-zero list (src/coverage.cpp:58-72).  Here the host hands over, per
+// exec, the (slot, count) pairs of the slots it touched, in ANY order; the device scatters
+// them into an all-zero dense staging record and runs the same K2 scan / K2b resolve / K4 merge
+// on it, so results are bit-identical to the dense call by construction.  After each chunk the
+// same pairs are scattered back as zeros (the staging buffer stays all-zero between calls, no
+// 1.3 GB memset per chunk).
+#include "hfz_common.cuh"
+
+namespace {
+
+// One warp per exec, lanes stride over the exec's pairs (coalesced 8-byte loads, 4 in flight).
+// ZERO = true writes zeros instead of the counts (cleanup pass).
+template <bool ZERO>
+__global__ void __launch_bounds__(256) hfz_k_expand(const uint2* __restrict__ entries,
+                                                    const uint64_t* __restrict__ off, uint64_t n_exec,
+                                                    uint8_t* __restrict__ dense, uint32_t S, uint32_t H,
+                                                    uint64_t rec, unsigned long long* __restrict__ bad) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  uint32_t nbad = 0;
+  for (uint64_t e = warp; e < n_exec; e += nwarps) {
+    const uint64_t b = off[e], t = off[e + 1];
+    uint8_t* r = dense + e * rec;
+    for (uint64_t i0 = b; i0 < t; i0 += 128) {
+      uint2 x[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t i = i0 + j * 32 + lane;
+        x[j] = i < t ? __ldcs(entries + i) : make_uint2(0xffffffffu, 0u);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t slot = x[j].x, c = ZERO ? 0u : x[j].y;
+        if (slot < H) {
+          r[slot] = (uint8_t)c;  // host half: u8 counters (CoverageMap::host_, coverage.hpp:19)
+        } else if (slot < S) {
+          *reinterpret_cast<uint32_t*>(r + H + (size_t)(slot - H) * 4) = c;  // device half: u32
+        } else if (!ZERO && i0 + j * 32 + lane < t) {
+          ++nbad;
+        }
+      }
+    }
+  }
+  if (!ZERO) {
+    nbad = __reduce_add_sync(0xffffffffu, nbad);
+    if (lane == 0 && nbad) atomicAdd(bad, (unsigned long long)nbad);
+  }
+}
+
+constexpr int kBadSlot = 4;  // ctx->d_small[4]: out-of-range pairs seen by the expand kernel
+
+uint64_t chunk_execs(const hfz_ctx* c) {
+  if (c->sparse_chunk) return c->sparse_chunk;
+  uint64_t n = (1280ull << 20) / c->rec_bytes;  // 8,192 records of 163,840 B
+  return n < 32 ? 32 : n / 32 * 32;
+}
+
+int ensure_dense(hfz_ctx* c, uint64_t n_exec) {
+  uint64_t want = chunk_execs(c);
+  if (n_exec < want) want = (n_exec + 31) / 32 * 32;
+  if (want < 32) want = 32;
+  if (c->sp_dense_execs < want) {
+    cudaFree(c->sp_dense);
+    c->sp_dense = nullptr;
+    c->sp_dense_execs = 0;
+    cudaError_t e = cudaMalloc(&c->sp_dense, want * c->rec_bytes);
+    if (e != cudaSuccess) {
+      hfz_set_error("sparse ingest: cudaMalloc of %llu staging bytes failed (%s)",
+                    (unsigned long long)(want * c->rec_bytes), cudaGetErrorString(e));
+      return HFZ_ENOMEM;
+    }
+    c->sp_dense_execs = want;
+    c->sp_dirty = true;
+  }
+  if (c->sp_dirty) {
+    HFZ_CUDA(cudaMemsetAsync(c->sp_dense, 0, c->sp_dense_execs * c->rec_bytes, c->stream));
+    c->sp_dirty = false;
+  }
+  return HFZ_OK;
+}
+
+template <bool ZERO>
+int launch_expand(hfz_ctx* c, const uint32_t* entries, const uint64_t* off, uint64_t n) {
+  uint64_t blocks = (n + 7) / 8;  // 8 warps per block, one exec per warp
+  const uint64_t cap = (uint64_t)c->num_sms * 8;
+  if (blocks > cap) blocks = cap;
+  hfz_k_expand<ZERO><<<(uint32_t)blocks, 256, 0, c->stream>>>(
+      reinterpret_cast<const uint2*>(entries), off, n, c->sp_dense, c->S, c->H, c->rec_bytes,
+      c->d_small + kBadSlot);
+  ++c->launches;
+  HFZ_CUDA(cudaGetLastError());
+  return HFZ_OK;
+}
+
+// Folds execs [0, n_exec) given device pairs / offsets, chunk by chunk.  `events` (may be
+// null) holds one event per chunk that the stream must wait for before touching the chunk's
+// pairs; classed_host (may be null) receives the classed maps through ctx->d_classed.
+int fold_chunks(hfz_ctx* c, const uint32_t* entries, const uint64_t* off, uint64_t n_exec,
+                uint8_t* virgin, uint64_t* counts, uint8_t* classed_dev, uint8_t* classed_host,
+                uint8_t* admit, uint64_t* sigf, uint64_t* sigs, uint32_t* nnz,
+                const cudaEvent_t* events) {
+  const uint64_t C = c->sp_dense_execs;
+  c->sp_dirty = true;  // until the last cleanup pass has been enqueued
+  uint64_t k = 0;
+  for (uint64_t done = 0; done < n_exec; done += C, ++k) {
+    const uint64_t n = n_exec - done < C ? n_exec - done : C;
+    if (events) HFZ_CUDA(cudaStreamWaitEvent(c->stream, events[k], 0));
+    int rc = launch_expand<false>(c, entries, off + done, n);
+    if (rc) return rc;
+    uint8_t* cls = classed_dev ? classed_dev + done * (uint64_t)c->S : (classed_host ? c->d_classed : nullptr);
+    rc = hfz_feedback_batch(c, c->sp_dense, n, virgin, counts, cls, admit + done, sigf + done,
+                            sigs + done, nnz ? nnz + done : nullptr);
+    if (rc) return rc;
+    if (classed_host)
+      HFZ_CUDA(cudaMemcpyAsync(classed_host + done * (uint64_t)c->S, c->d_classed, n * (uint64_t)c->S,
+                               cudaMemcpyDeviceToHost, c->stream));
+    rc = launch_expand<true>(c, entries, off + done, n);
+    if (rc) return rc;
+  }
+  c->sp_dirty = false;
+  return HFZ_OK;
+}
+
+}  // namespace
+
+extern "C" int hfz_feedback_batch_sparse(hfz_ctx* c, const uint32_t* entries, const uint64_t* entry_off,
+                                         uint64_t n_exec, uint8_t* virgin_inout,
+                                         uint64_t* edge_counts_inout, uint8_t* classed_out,
+                                         uint8_t* admit_out, uint64_t* sig_full_out,
+                                         uint64_t* sig_simple_out, uint32_t* nnz_out) {
+  if (!c || !virgin_inout || !edge_counts_inout ||
+      (n_exec && (!entry_off || !admit_out || !sig_full_out || !sig_simple_out))) {
+    hfz_set_error("hfz_feedback_batch_sparse: null argument");
+    return HFZ_EINVAL;
+  }
+  if ((uintptr_t)entries & 7) {
+    hfz_set_error("hfz_feedback_batch_sparse: entries must be 8-byte aligned");
+    return HFZ_EINVAL;
+  }
+  HFZ_CUDA(cudaSetDevice(c->device));
+  if (n_exec == 0) return HFZ_OK;
+  int rc = ensure_dense(c, n_exec);
+  if (rc) return rc;
+  HFZ_CUDA(cudaMemsetAsync(c->d_small + kBadSlot, 0, sizeof(unsigned long long), c->stream));
+  return fold_chunks(c, entries, entry_off, n_exec, virgin_inout, edge_counts_inout, classed_out, nullptr,
+                     admit_out, sig_full_out, sig_simple_out, nnz_out, nullptr);
+}
+
+extern "C" int hfz_feedback_batch_sparse_host(hfz_ctx* c, const uint32_t* entries, const uint64_t* entry_off,
+                                              uint64_t n_exec, uint8_t* virgin, uint64_t* counts,
+                                              uint8_t* classed, uint8_t* admit, uint64_t* sigf,
+                                              uint64_t* sigs, uint32_t* nnz) {
+  if (!c || !virgin || !counts || (n_exec && (!entry_off || !admit || !sigf || !sigs))) {
+    hfz_set_error("hfz_feedback_batch_sparse_host: null argument");
+    return HFZ_EINVAL;
+  }
+  if (n_exec == 0) return HFZ_OK;
+  const uint64_t total = entry_off[n_exec];
+  if (entry_off[0] != 0 || (total && !entries)) {
+    hfz_set_error("hfz_feedback_batch_sparse_host: entry_off[0] must be 0 and entries non-null");
+    return HFZ_EINVAL;
+  }
+  for (uint64_t e = 0; e < n_exec; ++e) {
+    if (entry_off[e + 1] < entry_off[e]) {
+      hfz_set_error("hfz_feedback_batch_sparse_host: entry_off is not non-decreasing at exec %llu",
+                    (unsigned long long)e);
+      return HFZ_EINVAL;
+    }
+  }
+  HFZ_CUDA(cudaSetDevice(c->device));
+  int rc = hfz_ensure_host_common(c, n_exec);
+  if (rc) return rc;
+  rc = ensure_dense(c, n_exec);
+  if (rc) return rc;
+  const uint64_t C = c->sp_dense_execs;
+  const uint64_t n_chunks = (n_exec + C - 1) / C;
+  if (classed && (rc = hfz_ensure_classed_stage(c, n_exec < C ? n_exec : C))) return rc;
+  if (c->sp_entries_cap < total) {
+    cudaFree(c->sp_entries);
+    c->sp_entries = nullptr;
+    c->sp_entries_cap = 0;
+    const uint64_t cap = total + total / 8 + 1024;
+    HFZ_CUDA(cudaMalloc(&c->sp_entries, cap * 8));
+    c->sp_entries_cap = cap;
+  }
+  if (c->sp_off_cap < n_exec + 1) {
+    cudaFree(c->sp_off);
+    c->sp_off = nullptr;
+    c->sp_off_cap = 0;
+    HFZ_CUDA(cudaMalloc(&c->sp_off, (n_exec + 1 + 1024) * 8));
+    c->sp_off_cap = n_exec + 1 + 1024;
+  }
+  while (c->sp_events.size() < n_chunks) {
+    cudaEvent_t ev;
+    HFZ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    c->sp_events.push_back(ev);
+  }
+  cudaStream_t st = c->stream;
+  // small inputs first: the H2D copy engine serves copies in issue order, so queueing them
+  // behind the pairs would hold the first chunk's kernels back until every pair has arrived
+  HFZ_CUDA(cudaMemcpyAsync(c->sp_off, entry_off, (n_exec + 1) * 8, cudaMemcpyHostToDevice, st));
+  HFZ_CUDA(cudaMemcpyAsync(c->d_virgin, virgin, c->S, cudaMemcpyHostToDevice, st));
+  HFZ_CUDA(cudaMemcpyAsync(c->d_counts, counts, 16, cudaMemcpyHostToDevice, st));
+  HFZ_CUDA(cudaMemsetAsync(c->d_small + kBadSlot, 0, sizeof(unsigned long long), st));
+  // the pairs stream in on the copy stream, one event per chunk; everything else on `st`
+  for (uint64_t k = 0; k < n_chunks; ++k) {
+    const uint64_t e0 = k * C, e1 = e0 + C < n_exec ? e0 + C : n_exec;
+    const uint64_t b = entry_off[e0], t = entry_off[e1];
+    if (t > b)
+      HFZ_CUDA(cudaMemcpyAsync(c->sp_entries + 2 * b, entries + 2 * b, (t - b) * 8, cudaMemcpyHostToDevice,
+                               c->copy_stream));
+    HFZ_CUDA(cudaEventRecord(c->sp_events[k], c->copy_stream));
+  }
+  rc = fold_chunks(c, c->sp_entries, c->sp_off, n_exec, c->d_virgin, c->d_counts, nullptr, classed,
+                   c->d_admit, c->d_sigf, c->d_sigs, c->d_nnz, c->sp_events.data());
+  if (rc) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamSynchronize(st);
+    return rc;
+  }
+  unsigned long long bad = 0;
+  HFZ_CUDA(cudaMemcpyAsync(admit, c->d_admit, n_exec, cudaMemcpyDeviceToHost, st));
+  HFZ_CUDA(cudaMemcpyAsync(sigf, c->d_sigf, n_exec * 8, cudaMemcpyDeviceToHost, st));
+  HFZ_CUDA(cudaMemcpyAsync(sigs, c->d_sigs, n_exec * 8, cudaMemcpyDeviceToHost, st));
+  if (nnz) HFZ_CUDA(cudaMemcpyAsync(nnz, c->d_nnz, n_exec * 4, cudaMemcpyDeviceToHost, st));
+  HFZ_CUDA(cudaMemcpyAsync(virgin, c->d_virgin, c->S, cudaMemcpyDeviceToHost, st));
+  HFZ_CUDA(cudaMemcpyAsync(counts, c->d_counts, 16, cudaMemcpyDeviceToHost, st));
+  HFZ_CUDA(cudaMemcpyAsync(&bad, c->d_small + kBadSlot, sizeof(bad), cudaMemcpyDeviceToHost, st));
+  HFZ_CUDA(cudaStreamSynchronize(st));
+  if (bad) {
+    hfz_set_error("hfz_feedback_batch_sparse_host: %llu pairs name a slot >= %u (ignored)", bad, c->S);
+    return HFZ_EINVAL;
+  }
+  return HFZ_OK;
+}
+
+extern "C" int hfz_expand_sparse(hfz_ctx* c, const uint32_t* entries, const uint64_t* entry_off,
+                                 uint64_t n_exec, uint8_t* raw_maps_out) {
+  if (!c || (n_exec && (!entry_off || !raw_maps_out))) {
+    hfz_set_error("hfz_expand_sparse: null argument");
+    return HFZ_EINVAL;
+  }
+  if (((uintptr_t)entries & 7) || ((uintptr_t)raw_maps_out & 15)) {
+    hfz_set_error("hfz_expand_sparse: entries must be 8-byte, raw_maps_out 16-byte aligned");
+    return HFZ_EINVAL;
+  }
+  HFZ_CUDA(cudaSetDevice(c->device));
+  if (n_exec == 0) return HFZ_OK;
+  HFZ_CUDA(cudaMemsetAsync(raw_maps_out, 0, n_exec * c->rec_bytes, c->stream));
+  uint64_t blocks = (n_exec + 7) / 8;
+  const uint64_t cap = (uint64_t)c->num_sms * 8;
+  if (blocks > cap) blocks = cap;
+  hfz_k_expand<false><<<(uint32_t)blocks, 256, 0, c->stream>>>(
+      reinterpret_cast<const uint2*>(entries), entry_off, n_exec, raw_maps_out, c->S, c->H, c->rec_bytes,
+      c->d_small + kBadSlot);
+  ++c->launches;
+  HFZ_CUDA(cudaGetLastError());
+  return HFZ_OK;
+}
+
+// Pinned host memory for C/C++ hosts that do not link the CUDA runtime themselves.
+extern "C" int hfz_host_alloc(void** out, uint64_t bytes) {
+  if (!out) return HFZ_EINVAL;
+  *out = nullptr;
+  cudaError_t e = cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocDefault);
+  if (e != cudaSuccess) {
+    hfz_set_error("hfz_host_alloc(%llu): %s", (unsigned long long)bytes, cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? HFZ_ENOMEM : HFZ_ECUDA;
+  }
+  return HFZ_OK;
+}
+
+extern "C" int hfz_host_free(void* p) {
+  if (!p) return HFZ_OK;
+  HFZ_CUDA(cudaFreeHost(p));
+  return HFZ_OK;
+}

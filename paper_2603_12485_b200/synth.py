@@ -161,6 +161,31 @@ def maps_edge_cases(S: int = 65536):
     return np.concatenate(recs), len(recs)
 
 
+def to_sparse(raw: np.ndarray, n_exec: int, S: int = 65536, shuffle_seed: int | None = 1):
+    """Dense records -> per-exec touched-slot lists for the sparse ingest calls: returns
+    (entries (N, 2) uint32 of (slot, count), entry_off (n_exec+1) uint64).  The pairs of an exec
+    are put in a seeded random order (touch order is arbitrary); shuffle_seed=None keeps them
+    ascending."""
+    H = S // 2
+    host, dev = _split_views(raw, n_exec, S)
+    hr, hc = np.nonzero(host)
+    dr, dc = np.nonzero(dev)
+    rows = np.concatenate([hr, dr])
+    slots = np.concatenate([hc, dc + H]).astype(np.uint32)
+    cnts = np.concatenate([host[hr, hc].astype(np.uint32), dev[dr, dc]])
+    if shuffle_seed is None:
+        order = np.lexsort((slots, rows))
+    else:
+        key = sm64(np.uint64(shuffle_seed), np.arange(rows.size, dtype=np.uint64))
+        order = np.lexsort((key, rows))
+    entries = np.empty((rows.size, 2), np.uint32)
+    entries[:, 0] = slots[order]
+    entries[:, 1] = cnts[order]
+    off = np.zeros(n_exec + 1, np.uint64)
+    np.cumsum(np.bincount(rows, minlength=n_exec), out=off[1:])
+    return entries, off
+
+
 # ---- havoc seeds (config 4) ---------------------------------------------------
 
 def havoc_inputs(n: int, seed: int = 45, lo: int = 1024, hi: int = 4096):

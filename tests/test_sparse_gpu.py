@@ -1,0 +1,166 @@
+"""Sparse ingest parity: per-exec touched-slot lists through hfz_feedback_batch_sparse{,_host}
+must give exactly what the CPU oracle gives on the dense maps the lists describe (classed
+bytes, Admit codes in order, both signatures, nnz, final virgin, edge counters)."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2603_12485_b200 as hfz
+from paper_2603_12485_b200 import synth
+from paper_2603_12485_b200._lib import HFZ_EINVAL, HfzError
+
+pytestmark = pytest.mark.gpu
+
+S = 65536
+
+
+def cpu(checker, raw, n, S_=S, want_classed=True):
+    v = np.zeros(S_, np.uint8)
+    c = np.zeros(2, np.uint64)
+    return checker.feedback_batch(raw, n, S_, v, c, want_classed=want_classed), v, c
+
+
+def check_host(c, got, gv, gc, want):
+    wo, wv, wc = want
+    for k in wo:
+        assert np.array_equal(got[k], wo[k]), f"{k} differs at {np.nonzero(got[k] != wo[k])[0][:8]}"
+    assert np.array_equal(gv, wv), "virgin differs"
+    assert np.array_equal(gc, wc), f"edge counts differ {gc} vs {wc}"
+
+
+@pytest.fixture()
+def sctx():
+    """Own context per test: the sparse chunk size can only be set before first use."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = hfz.Context(0)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("mode,shuffle", [("campaign", 1), ("iid", 7), ("campaign", None)])
+def test_sparse_host_equals_oracle(sctx, checker, mode, shuffle):
+    n = 700
+    raw = synth.maps_iid(n, S) if mode == "iid" else synth.maps_campaign(n, S, p_extra=16, p_rare=16)
+    entries, off = synth.to_sparse(raw, n, S, shuffle_seed=shuffle)
+    v = np.zeros(S, np.uint8)
+    c = np.zeros(2, np.uint64)
+    got = sctx.feedback_batch_sparse_host(entries, off, v, c, want_classed=True)
+    check_host(sctx, got, v, c, cpu(checker, raw, n))
+    assert len(set(got["admit"].tolist())) >= 2
+
+
+def test_sparse_chunking_and_reuse(sctx, checker):
+    """Several chunks per call (chunk = 64 execs), the staging buffer must come back all-zero:
+    a second, different batch through the same context must still be exact."""
+    sctx.set_option("sparse_chunk", 64)
+    for seed, n in ((5, 333), (6, 190), (7, 64), (8, 1)):
+        raw = synth.maps_campaign(n, S, seed=seed, p_extra=8, p_rare=8)
+        entries, off = synth.to_sparse(raw, n, S, shuffle_seed=seed)
+        v = np.zeros(S, np.uint8)
+        c = np.zeros(2, np.uint64)
+        got = sctx.feedback_batch_sparse_host(entries, off, v, c, want_classed=True)
+        check_host(sctx, got, v, c, cpu(checker, raw, n))
+
+
+def test_sparse_edge_vectors_and_empty_execs(sctx, checker):
+    """All-zero map (empty list), full-density map, rung boundaries, last/first slots; plus
+    explicit count-0 pairs, which must read as unvisited."""
+    raw, n = synth.maps_edge_cases(S)
+    entries, off = synth.to_sparse(raw, n, S)
+    assert off[1] == 0  # the all-zero map has an empty list
+    # append two count-0 pairs to the last exec
+    entries = np.concatenate([entries, np.array([[77, 0], [S - 5, 0]], np.uint32)])
+    off = off.copy()
+    off[-1] += 2
+    v = np.zeros(S, np.uint8)
+    c = np.zeros(2, np.uint64)
+    got = sctx.feedback_batch_sparse_host(entries, off, v, c, want_classed=True)
+    check_host(sctx, got, v, c, cpu(checker, raw, n))
+
+
+def test_sparse_device_call_equals_dense_call(sctx):
+    """Device-buffer form against the dense device call, with a pre-warmed virgin map."""
+    n = 300
+    warm = synth.maps_campaign(256, S, seed=90)
+    raw = synth.maps_campaign(n, S, seed=91, p_extra=8, p_rare=8)
+    dev = sctx.device
+    results = []
+    for sparse in (False, True):
+        virgin, counts = sctx.new_virgin(), sctx.new_edge_counts()
+        sctx.feedback_batch(torch.from_numpy(warm).to(dev), virgin, counts)
+        if sparse:
+            entries, off = synth.to_sparse(raw, n, S, shuffle_seed=3)
+            o = sctx.feedback_batch_sparse(torch.from_numpy(entries.view(np.int32)).to(dev),
+                                           torch.from_numpy(off.view(np.int64)).to(dev), virgin, counts,
+                                           want_classed=True)
+        else:
+            o = sctx.feedback_batch(torch.from_numpy(raw).to(dev), virgin, counts, want_classed=True)
+        sctx.synchronize()
+        results.append({k: t.cpu().numpy() for k, t in o.items()} | {"virgin": virgin.cpu().numpy(),
+                                                                      "counts": counts.cpu().numpy()})
+    for k in results[0]:
+        assert np.array_equal(results[0][k], results[1][k]), k
+
+
+def test_expand_sparse_reproduces_records(sctx):
+    n = 100
+    raw = synth.maps_iid(n, S, seed=11)
+    entries, off = synth.to_sparse(raw, n, S, shuffle_seed=2)
+    out = sctx.expand_sparse(torch.from_numpy(entries.view(np.int32)).to(sctx.device),
+                             torch.from_numpy(off.view(np.int64)).to(sctx.device))
+    sctx.synchronize()
+    assert np.array_equal(out.cpu().numpy(), raw)
+
+
+def test_sparse_out_of_range_pairs_are_reported(sctx, checker):
+    """Pairs naming a slot >= S are ignored, the fold completes, and the host call says so."""
+    n = 40
+    raw = synth.maps_campaign(n, S, seed=21)
+    entries, off = synth.to_sparse(raw, n, S)
+    bad = np.concatenate([entries, np.array([[S, 3], [0xFFFFFFFF, 1]], np.uint32)])
+    off2 = off.copy()
+    off2[-1] += 2
+    v = np.zeros(S, np.uint8)
+    c = np.zeros(2, np.uint64)
+    with pytest.raises(HfzError) as ei:
+        sctx.feedback_batch_sparse_host(bad, off2, v, c)
+    assert ei.value.code == HFZ_EINVAL
+    wo, wv, wc = cpu(checker, raw, n, want_classed=False)
+    assert np.array_equal(v, wv) and np.array_equal(c, wc)
+    # and the context is still usable and exact afterwards
+    v = np.zeros(S, np.uint8)
+    c = np.zeros(2, np.uint64)
+    got = sctx.feedback_batch_sparse_host(entries, off, v, c)
+    assert np.array_equal(got["admit"], wo["admit"]) and np.array_equal(got["sig_full"], wo["sig_full"])
+
+
+def test_sparse_bad_offsets_rejected(sctx):
+    entries = np.zeros((4, 2), np.uint32)
+    v = np.zeros(S, np.uint8)
+    c = np.zeros(2, np.uint64)
+    with pytest.raises(HfzError):
+        sctx.feedback_batch_sparse_host(entries, np.array([0, 3, 2], np.uint64), v, c)
+    with pytest.raises(HfzError):
+        sctx.feedback_batch_sparse_host(entries, np.array([1, 2, 4], np.uint64), v, c)
+
+
+def test_sparse_large_map():
+    """262,144-slot map (BASELINE.json configs[2])."""
+    from oracle import pyoracle
+    S2 = 262144
+    checker_large = pyoracle.best_checker(S2)
+    c2 = hfz.Context(0, S2)
+    try:
+        n = 48
+        raw = synth.maps_iid(n, S2, seed=31)
+        entries, off = synth.to_sparse(raw, n, S2, shuffle_seed=4)
+        v = np.zeros(S2, np.uint8)
+        c = np.zeros(2, np.uint64)
+        got = c2.feedback_batch_sparse_host(entries, off, v, c)
+        wo, wv, wc = cpu(checker_large, raw, n, S2, want_classed=False)
+        for k in wo:
+            assert np.array_equal(got[k], wo[k]), k
+        assert np.array_equal(v, wv) and np.array_equal(c, wc)
+    finally:
+        c2.close()
