@@ -31,6 +31,7 @@ class CoverageMap {
       ++host_violations_;
       idx &= kHostSlots - 1;
     }
+    if (host_[idx] == 0) touched_.push_back(idx);
     const std::uint8_t next = static_cast<std::uint8_t>(host_[idx] + 1);
     host_[idx] = next == 0 ? 1 : next;  // a wrap never reads as "unvisited"
   }
@@ -39,7 +40,9 @@ class CoverageMap {
       ++device_violations_;
       logical_idx = kDeviceIndexBase + logical_idx % (kMapSize - kHostSlots);
     }
-    device_[logical_idx - kDeviceIndexBase] = count;
+    std::uint32_t& d = device_[logical_idx - kDeviceIndexBase];
+    if (d == 0 && count != 0) touched_.push_back(logical_idx);
+    d = count;
   }
   std::uint8_t host_at(std::uint32_t idx) const { return host_[idx]; }
   std::uint32_t device_at(std::uint32_t logical_idx) const { return device_[logical_idx - kDeviceIndexBase]; }
@@ -51,6 +54,10 @@ class CoverageMap {
   std::uint64_t host_partition_violations() const { return host_violations_; }
   std::uint64_t device_partition_violations() const { return device_violations_; }
 
+  // Logical slots in first-touch order: the dirty list the reference's runtime keeps beside its
+  // device counters (src/hdvm.cpp:356-366), here for both halves.  Feeds b200::SparseBatch.
+  const std::vector<std::uint32_t>& touched() const { return touched_; }
+
   // raw record in the library's layout: [host u8 x H][device u32 x H]
   void pack(std::uint8_t* rec) const {
     std::memcpy(rec, host_.data(), kHostSlots);
@@ -60,8 +67,86 @@ class CoverageMap {
  private:
   std::vector<std::uint8_t> host_;
   std::vector<std::uint32_t> device_;
+  std::vector<std::uint32_t> touched_;
   std::uint64_t host_violations_ = 0, device_violations_ = 0;
 };
+
+namespace b200 {
+
+// A batch of executions in the sparse host form of include/hfz.h: per exec the (slot, count)
+// pairs of the slots its CoverageMap touched, packed back to back in page-locked memory.
+// append() right after an execution costs one ~10 KB copy while the map is still cache-hot;
+// the batch then crosses PCIe at ~10 KB per exec instead of 163,840 B.
+class SparseBatch {
+ public:
+  SparseBatch() = default;
+  SparseBatch(const SparseBatch&) = delete;
+  SparseBatch& operator=(const SparseBatch&) = delete;
+  ~SparseBatch() {
+    hfz_host_free(pairs_);
+    hfz_host_free(off_);
+  }
+  void append(const CoverageMap& m) {
+    const std::vector<std::uint32_t>& t = m.touched();
+    reserve_pairs(n_pairs_ + t.size());
+    reserve_execs(n_exec_ + 1);
+    std::uint32_t* p = pairs_ + 2 * n_pairs_;
+    for (std::uint32_t slot : t) {
+      *p++ = slot;
+      *p++ = static_cast<std::uint32_t>(m.count_at(slot));
+    }
+    n_pairs_ += t.size();
+    off_[++n_exec_] = n_pairs_;
+  }
+  void clear() { n_exec_ = n_pairs_ = 0; }
+  std::uint64_t size() const { return n_exec_; }
+  std::uint64_t pairs() const { return n_pairs_; }
+  const std::uint32_t* entries() const { return pairs_; }
+  const std::uint64_t* offsets() const { return off_ ? off_ : &zero_; }
+
+ private:
+  template <class T>
+  static void grow(T*& buf, std::uint64_t& cap, std::uint64_t used, std::uint64_t want, std::uint64_t unit) {
+    if (want <= cap) return;
+    std::uint64_t ncap = cap ? cap : 4096;
+    while (ncap < want) ncap *= 2;
+    void* nb = nullptr;
+    check(hfz_host_alloc(&nb, ncap * unit * sizeof(T)), "hfz_host_alloc");
+    if (used) std::memcpy(nb, buf, used * unit * sizeof(T));
+    hfz_host_free(buf);
+    buf = static_cast<T*>(nb);
+    cap = ncap;
+  }
+  void reserve_pairs(std::uint64_t want) { grow(pairs_, cap_pairs_, n_pairs_, want, 2); }
+  void reserve_execs(std::uint64_t want) {
+    const bool fresh = off_ == nullptr;
+    grow(off_, cap_execs_, fresh ? 0 : n_exec_ + 1, want + 1, 1);
+    if (fresh) off_[0] = 0;
+  }
+  std::uint32_t* pairs_ = nullptr;
+  std::uint64_t* off_ = nullptr;
+  std::uint64_t cap_pairs_ = 0, cap_execs_ = 0, n_pairs_ = 0, n_exec_ = 0;
+  std::uint64_t zero_ = 0;
+};
+
+// Folds the batch into virgin / edge_counts in exec order (engine.cpp:471-478 per exec).
+inline FeedbackResult feedback_batch(Context& ctx, const SparseBatch& batch, std::uint8_t* virgin,
+                                     std::uint64_t* edge_counts, bool want_classed = false) {
+  const std::uint64_t n = batch.size();
+  FeedbackResult r;
+  r.admit.resize(n);
+  r.sig_full.resize(n);
+  r.sig_simple.resize(n);
+  r.nnz.resize(n);
+  if (want_classed) r.classed.resize(n * std::uint64_t(ctx.map_slots()));
+  check(hfz_feedback_batch_sparse_host(ctx.get(), batch.entries(), batch.offsets(), n, virgin, edge_counts,
+                                       want_classed ? r.classed.data() : nullptr, r.admit.data(),
+                                       r.sig_full.data(), r.sig_simple.data(), r.nnz.data()),
+        "hfz_feedback_batch_sparse_host");
+  return r;
+}
+
+}  // namespace b200
 
 struct HostEdgeState {
   std::uint16_t prev_loc = 0;
@@ -168,12 +253,12 @@ inline void record_from_classed(const ClassedTrace& t, std::vector<std::uint8_t>
 }  // namespace detail
 
 inline ClassedTrace classify_trace(const CoverageMap& map) {
-  std::vector<std::uint8_t> rec(std::size_t(kHostSlots) * 5);
-  map.pack(rec.data());
+  b200::SparseBatch one;
+  one.append(map);
   std::vector<std::uint8_t> scratch_virgin(kMapSize, 0);
   std::uint64_t counts[2] = {0, 0};
   b200::FeedbackResult r =
-      b200::feedback_batch(b200::default_context(), rec.data(), 1, scratch_virgin.data(), counts, true);
+      b200::feedback_batch(b200::default_context(), one, scratch_virgin.data(), counts, true);
   ClassedTrace out;
   out.classed = std::move(r.classed);
   out.nonzero.reserve(r.nnz[0]);

@@ -239,7 +239,27 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
     // prev is carried across launches per flattened gtid (hdvm.cpp:376,426-430): only needed
     // when the exec has more than one launch
     const bool multi = l1 - l0 > 1;
+    // Launches of one exec usually share one geometry.  Thread j then has the same flattened
+    // gtid in every launch, so its carried prev is the last site of thread j in the nearest
+    // earlier launch where it ran any events -- read straight from the trace.  No prev table,
+    // no ordering between launches: all simulated warps of the exec go into ONE work queue and
+    // the few long (divergent) warps of a launch no longer hold the others at a barrier.
+    bool uniform = multi;
     if (multi) {
+      const uint32_t* d0 = p.dims + l0 * 6;
+      uniform = launch_valid(d0);
+      if (uniform) {  // the shared work counter is 32 bits wide
+        const uint64_t tpb0 = (uint64_t)d0[3] * d0[4] * d0[5];
+        const uint64_t nsw0 = (uint64_t)d0[0] * d0[1] * d0[2] * ((tpb0 + 31) / 32);
+        uniform = nsw0 * (l1 - l0) < (1ull << 31);
+      }
+      for (uint64_t l = l0 + 1; l < l1 && uniform; ++l) {
+        const uint32_t* d = p.dims + l * 6;
+        uniform = d[0] == d0[0] && d[1] == d0[1] && d[2] == d0[2] && d[3] == d0[3] && d[4] == d0[4] &&
+                  d[5] == d0[5];
+      }
+    }
+    if (multi && !uniform) {
       uint64_t mx = 0;
       for (uint64_t l = l0; l < l1; ++l) {
         const uint32_t* d = p.dims + l * 6;
@@ -253,7 +273,9 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
     __syncthreads();
 
     uint64_t my_events = 0;
-    for (uint64_t l = l0; l < l1; ++l) {
+    // uniform: one pass over all launches (sw runs over launch-major simulated warps)
+    const uint64_t l_step = uniform ? (l1 - l0) : 1;
+    for (uint64_t l = l0; l < l1; l += l_step) {
       const uint32_t* d = p.dims + l * 6;
       if (threadIdx.x == 0) s_next = 0;
       __syncthreads();
@@ -262,24 +284,39 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
         const uint32_t gx = d[0], gy = d[1], bdx = d[3], bdy = d[4], bdz = d[5];
         const uint32_t tpb = bdx * bdy * bdz, blocks = gx * gy * d[2];
         const uint32_t wpb = (tpb + 31) / 32;
-        const uint32_t n_sw = blocks * wpb;
+        const uint32_t n_sw = blocks * wpb;  // <= 2^22 (launch_valid)
         const float r_wpb = 1.0f / (float)wpb, r_gx = 1.0f / (float)gx, r_gy = 1.0f / (float)gy,
                     r_bdx = 1.0f / (float)bdx, r_bdy = 1.0f / (float)bdy;
-        const uint64_t t0 = p.thread_off[l];
+        const uint64_t n_q = (uint64_t)n_sw * l_step;
         // simulated warps are handed out dynamically: divergent ones take far longer
         for (;;) {
-          uint32_t sw = 0;
-          if (lane == 0) sw = atomicAdd(&s_next, 1u);
-          sw = __shfl_sync(0xffffffffu, sw, 0);
-          if (sw >= n_sw) break;
+          uint32_t q = 0;
+          if (lane == 0) q = atomicAdd(&s_next, 1u);
+          q = __shfl_sync(0xffffffffu, q, 0);
+          if (q >= n_q) break;  // n_q < 2^31 (checked where `uniform` is set; n_sw <= 2^22 otherwise)
+          const uint32_t lq = uniform ? q / n_sw : 0u;  // launch within the exec (uniform pass only)
+          const uint32_t sw = q - lq * n_sw;
+          const uint64_t t0 = p.thread_off[l + lq];
           const uint32_t bl = div_small(sw, wpb, r_wpb), tl = (sw - bl * wpb) * 32 + lane;
           const bool active = tl < tpb;
           uint64_t e0 = 0, e1 = 0, gtid = 0;
+          uint32_t prev_u = 0;
           if (active) {
-            const uint64_t t = t0 + (uint64_t)bl * tpb + tl;
+            const uint64_t j = (uint64_t)bl * tpb + tl;  // thread index within its launch
+            const uint64_t t = t0 + j;
             e0 = p.ev_off[t];
             e1 = p.ev_off[t + 1];
-            if (multi) {
+            if (uniform) {
+              for (uint32_t lb = lq; lb > 0;) {  // nearest earlier launch where thread j ran events
+                --lb;
+                const uint64_t tb = p.thread_off[l + lb] + j;
+                const uint64_t b1 = p.ev_off[tb + 1];
+                if (b1 > p.ev_off[tb]) {
+                  prev_u = p.sites[b1 - 1] >> 1;
+                  break;
+                }
+              }
+            } else if (multi) {
               const uint32_t bxy = div_small(bl, gx, r_gx), bx = bl - bxy * gx;
               const uint32_t bz = div_small(bxy, gy, r_gy), by = bxy - bz * gy;
               const uint32_t txy = div_small(tl, bdx, r_bdx), tx = tl - txy * bdx;
@@ -290,7 +327,8 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
             }
           }
           const uint32_t n_ev = (uint32_t)(e1 - e0);
-          uint32_t prev0 = (multi && active) ? prev_tab[gtid] : 0;
+          const bool use_tab = multi && !uniform;
+          uint32_t prev0 = uniform ? prev_u : ((use_tab && active) ? prev_tab[gtid] : 0);
           const uint32_t amask = __ballot_sync(0xffffffffu, active);
           const int lead = __ffs(amask) - 1;  // lowest active lane (always lane 0 of the sim warp)
 
@@ -318,13 +356,13 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
               bump(&counters[(pv ^ s) & hmask]);
             }
             if (lane == 0) my_events += n_lead;
-            if (multi && active && n_ev) prev_tab[gtid] = sm[n_ev - 1] >> 1;
+            if (use_tab && active && n_ev) prev_tab[gtid] = sm[n_ev - 1] >> 1;
             continue;
           }
 
           // ---- general path
           my_events += general_path(tab, p.sites, e0, n_ev, prev0, counters, hmask, lane);
-          if (multi && active && n_ev) prev_tab[gtid] = p.sites[e1 - 1] >> 1;
+          if (use_tab && active && n_ev) prev_tab[gtid] = p.sites[e1 - 1] >> 1;
         }
       }
       __syncthreads();  // prev table and counters are launch-ordered

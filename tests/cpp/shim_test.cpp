@@ -99,6 +99,43 @@ int main() {
     auto hb = havoc_batch({base, base}, rr);
     REQUIRE(hb[0] == h && hb[1].size() == 32);
   }
+  {  // sparse host form: SparseBatch of CoverageMaps == the dense records of the same maps
+    Rng rng(0x5151);
+    const int n = 200;
+    std::vector<CoverageMap> maps(n);
+    std::vector<std::uint8_t> raw(std::size_t(n) * kHostSlots * 5);
+    b200::SparseBatch batch;
+    for (int e = 0; e < n; ++e) {
+      const int hits = e == 7 ? 0 : 200 + int(rng.below(800));  // exec 7 touches nothing
+      for (int i = 0; i < hits; ++i) {
+        if (rng.chance(1, 2)) {
+          const std::uint32_t idx = std::uint32_t(rng.below(64) * 97 + rng.below(3)) % kHostSlots;
+          const int reps = 1 + int(rng.below(300));  // wraps past 255 now and then
+          for (int k = 0; k < reps; ++k) maps[e].host_increment(idx);
+        } else {
+          const std::uint32_t idx = kDeviceIndexBase + std::uint32_t(rng.below(64) * 131 + rng.below(3)) % kHostSlots;
+          maps[e].device_store(idx, std::uint32_t(rng.below(3) == 0 ? 0 : 1 + rng.below(100000)));
+        }
+      }
+      maps[e].pack(&raw[std::size_t(e) * kHostSlots * 5]);
+      batch.append(maps[e]);
+    }
+    REQUIRE(batch.size() == std::uint64_t(n));
+    VirginMap va, vb;
+    b200::FeedbackResult a = b200::feedback_batch(b200::default_context(), raw.data(), n, va.data(), va.edge_counts(), true);
+    b200::FeedbackResult b = b200::feedback_batch(b200::default_context(), batch, vb.data(), vb.edge_counts(), true);
+    REQUIRE(a.admit == b.admit);
+    REQUIRE(a.sig_full == b.sig_full);
+    REQUIRE(a.sig_simple == b.sig_simple);
+    REQUIRE(a.nnz == b.nnz);
+    REQUIRE(a.classed == b.classed);
+    REQUIRE(a.nnz[7] == 0 && a.sig_full[7] == 14695981039346656037ULL);
+    REQUIRE(va.host_edges() == vb.host_edges() && va.device_edges() == vb.device_edges());
+    bool same = true;
+    for (std::uint32_t i = 0; i < kMapSize; ++i) same = same && va.at(i) == vb.at(i);
+    REQUIRE(same);
+    REQUIRE(va.host_edges() > 0 && va.device_edges() > 0);
+  }
   if (g_fail) {
     std::printf("%d check(s) failed\n", g_fail);
     return 1;

@@ -105,6 +105,32 @@ def test_random_3d_multi_launch(ctx, port):
     check(ctx, port, pack(execs), len(execs))
 
 
+def test_uniform_launches_with_idle_threads(ctx, port):
+    """Same geometry in every launch (one work queue across launches, prev read from the trace):
+    threads that run no events in some launches must carry prev from the last launch where they
+    did; 3-D geometry so the thread index <-> gtid mapping matters; divergent and coherent warps."""
+    rng = np.random.default_rng(14)
+    execs = []
+    for ex in range(12):
+        d = [2, 2, 1, 8, 3, 2] if ex % 2 else [3, 1, 1, 48, 1, 1]
+        threads = int(np.prod(d))
+        n_launch = int(rng.integers(2, 6))
+        ev, sites = [0], []
+        common = rng.integers(1, 300, 6).tolist()
+        for l in range(n_launch):
+            for t in range(threads):
+                r = rng.random()
+                if r < 0.35:
+                    pass                                    # idle in this launch
+                elif r < 0.75:
+                    sites.extend(common[: 1 + (l % 5)])     # coherent-looking sequence
+                else:
+                    sites.extend(rng.integers(1, 300, int(rng.integers(1, 9))).tolist())
+                ev.append(len(sites))
+        execs.append((np.array([d] * n_launch, np.uint32), ev, sites))
+    check(ctx, port, pack(execs), len(execs))
+
+
 def test_many_distinct_sites_forces_partitioning(ctx, port):
     """Fully divergent warps with far more distinct sites than the per-warp table holds."""
     rng = np.random.default_rng(12)
