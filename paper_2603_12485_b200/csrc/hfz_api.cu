@@ -142,6 +142,8 @@ extern "C" int hfz_ctx_set_option(hfz_ctx* c, const char* key, int64_t value) {
     c->virgin_smem = value != 0;
   } else if (!strcmp(key, "scan_small")) {
     c->scan_small = value;
+  } else if (!strcmp(key, "scan_pipe")) {
+    c->scan_pipe = value;
   } else if (!strcmp(key, "time_scan")) {
     c->time_scan = value != 0;
   } else if (!strcmp(key, "sparse_chunk")) {

@@ -74,6 +74,7 @@ struct hfz_ctx {
   int virgin_smem = 1;    // stage V0 in shared memory when it fits
   int time_scan = 0;      // bracket scan launches with events (bench roofline)
   int64_t scan_small = -1; // batches up to this many execs use the warp-per-map kernel (-1 = auto)
+  int64_t scan_pipe = -1;  // batches of up to this many 32-map groups per SM use the pipelined kernel (-1 = auto)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> scan_events;
 };
 
@@ -153,6 +154,9 @@ __device__ __forceinline__ bool hfz_mbar_try_wait(uint64_t* bar, uint32_t parity
       : "r"(hfz_smem_u32(bar)), "r"(parity)
       : "memory");
   return ok != 0;
+}
+__device__ __forceinline__ void hfz_mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(hfz_smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void hfz_mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!hfz_mbar_try_wait(bar, parity)) {

@@ -114,9 +114,11 @@ __device__ __forceinline__ uint64_t general_path(WarpTable& tab, const uint32_t*
   uint64_t bumps = 0;
   const uint32_t lane_le = 0xffffffffu >> (31 - lane);
   const uint32_t ev_total = __reduce_add_sync(0xffffffffu, n_ev);
-  // initial depth: every partition would fit even if all its events were distinct sites
+  // initial depth: the expected events per partition fit the table even if all were distinct
+  // sites (a replay costs the same however few of its events belong to the partition, so start
+  // as shallow as possible; a partition that does overflow is found by the dry run and split)
   uint32_t d0 = 0;
-  while (d0 < 26 && (ev_total >> d0) > kFill) ++d0;
+  while (d0 < 26 && (ev_total >> d0) > kRows - 32) ++d0;
   uint32_t stk_prefix[36], stk_depth[36];
   for (uint32_t root = 0; root < (1u << d0); ++root) {
     int sp = 1;

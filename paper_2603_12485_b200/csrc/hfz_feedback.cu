@@ -309,6 +309,156 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
 }
 
 // ---------------------------------------------------------------------------
+// K2 scan for MEDIUM batches ("pipelined lane-per-map").  With only a few 32-map groups per SM
+// the kernel above is latency-bound: the warp that owns a group issues a row's loads, waits for
+// them, scatters, and only then runs the 32 FNV chains over that row.  Here the two halves are
+// split between warps of a TEAM that owns one group: P producer warps stream the group's rows
+// (row r by producer r % P: 32 maps x ROW bytes, coalesced 128-bit loads, ballot, scatter of the
+// non-zero vectors into ring slot r % P in shared memory) and ONE consumer warp runs phase B --
+// the serial chains -- row after row without ever waiting for HBM.  Full/empty hand-over per
+// ring slot through mbarriers.  A CTA holds G teams; per-group latency drops from
+// rows x (load latency + phase B) to rows x phase B.
+template <int REC_CT, int ROW, int P, bool VSMEM, bool CLASSED>
+__global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan_pipe(const ScanParams p, const int G) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  using C = RowCfg<ROW>;
+  constexpr int LB = C::kLoads / 2;
+  constexpr int SLOT = 32 * C::kSlot + 128;  // one row of a group: 32 padded lane slots + 32 masks
+  constexpr int TEAM = 1 + P;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = warp / TEAM, role = warp % TEAM;
+  const uint64_t rec = REC_CT ? (uint64_t)REC_CT : p.rec_bytes;
+  uint8_t* s_virgin = smem;
+  uint8_t* s_ring = smem + (VSMEM ? p.S : 0) + (size_t)g * P * SLOT;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (VSMEM ? p.S : 0) + (size_t)G * P * SLOT);
+  uint64_t* bar_virgin = bars;
+  uint64_t* full = bars + 1 + (size_t)g * 2 * P;
+  uint64_t* empty = full + P;
+  if (threadIdx.x == 0) {
+    hfz_mbar_init(bar_virgin, 1);
+    for (int i = 0; i < G * 2 * P; ++i) hfz_mbar_init(bars + 1 + i, 32);
+    hfz_fence_barrier_init();
+  }
+  __syncthreads();
+  if (VSMEM && threadIdx.x == 0) {  // thread 0 = consumer lane of team 0, whose group always exists
+    const uint64_t pol = hfz_policy_evict_last();
+    hfz_mbar_expect_tx(bar_virgin, p.S);
+    for (uint32_t off = 0; off < p.S; off += 16384u) {
+      const uint32_t n = p.S - off < 16384u ? p.S - off : 16384u;
+      hfz_bulk_g2s_stream(s_virgin + off, p.v0 + off, n, bar_virgin, pol);
+    }
+  }
+  const uint64_t base = ((uint64_t)g * gridDim.x + blockIdx.x) * 32;  // team g of CTA b owns group g * grid + b
+  if (base >= p.n_exec) return;
+  const uint32_t nm = (uint32_t)min((uint64_t)32, p.n_exec - base);
+  const uint32_t rows = (uint32_t)(rec / ROW), rows_host = p.H / ROW;
+
+  if (role != 0) {
+    // ---- producer: rows pr, pr + P, ... into ring slot pr
+    const int pr = role - 1;
+    uint8_t* slot = s_ring + (size_t)pr * SLOT;
+    uint32_t* s_mask = reinterpret_cast<uint32_t*>(slot + 32 * C::kSlot);
+    const uint32_t sub = lane / C::kLanesPerMap, unit = lane % C::kLanesPerMap;
+    uint8_t* scat = slot + sub * C::kSlot + unit * 16;
+    const uint8_t* gsrc = p.raw + (base + sub) * rec + unit * 16;
+    const uint32_t last = nm - 1;
+    auto run = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
+      uint4 A[LB], B[LB];
+      auto load = [&](uint4* X, uint32_t row, int half) {
+        const uint8_t* src = gsrc + (size_t)row * ROW;
+#pragma unroll
+        for (int i = 0; i < LB; ++i) {
+          const uint32_t m0 = (half * LB + i) * C::kMapsPerLoad;
+          if (FULL) {
+            X[i] = hfz_ldg_stream(reinterpret_cast<const uint4*>(src + (size_t)m0 * rec));
+          } else {  // maps >= nm alias the group's last map; their votes are masked below
+            const uint32_t m = min(m0 + sub, last) - sub;
+            X[i] = hfz_ldg_stream(reinterpret_cast<const uint4*>(src + (int64_t)(int32_t)m * (int64_t)rec));
+          }
+        }
+      };
+      auto scatter = [&](const uint4* X, int half) {
+#pragma unroll
+        for (int i = 0; i < LB; ++i) {
+          const uint32_t m0 = (half * LB + i) * C::kMapsPerLoad;
+          bool nz = (X[i].x | X[i].y | X[i].z | X[i].w) != 0u;
+          if (!FULL) nz = nz && (m0 + sub < nm);
+          const uint32_t b = __ballot_sync(0xffffffffu, nz);
+          if (lane == 0) {
+            if (C::kMapsPerLoad == 1)
+              s_mask[m0] = b;
+            else
+              *reinterpret_cast<uint2*>(s_mask + m0) = make_uint2(b & 0xffffu, b >> 16);
+          }
+          if (nz) *reinterpret_cast<uint4*>(scat + m0 * C::kSlot) = X[i];
+        }
+      };
+      uint32_t it = 0;
+      for (uint32_t r = pr; r < rows; r += P, ++it) {
+        load(A, r, 0);
+        load(B, r, 1);
+        if (it) hfz_mbar_wait(&empty[pr], (it - 1) & 1u);  // the consumer is done with the slot's previous row
+        scatter(A, 0);
+        scatter(B, 1);
+        hfz_mbar_arrive(&full[pr]);
+      }
+    };
+    if (nm == 32)
+      run(std::true_type{});
+    else
+      run(std::false_type{});
+    return;
+  }
+
+  // ---- consumer: lane m runs map m's chains over the rows in order
+  const bool valid = (uint32_t)lane < nm;
+  const uint64_t e64 = base + lane;
+  const uint32_t e = (uint32_t)e64;
+  uint8_t* classed_row = CLASSED ? p.classed + e64 * p.S : nullptr;
+  uint32_t* nov_row = p.novel_ent + (valid ? e64 : base) * kNovMax;
+  Lane<VSMEM, CLASSED> st;
+  st.hf = HFZ_FNV_OFFSET;
+  st.hs = HFZ_FNV_OFFSET;
+  st.nnz = 0;
+  st.novel = 0;
+  if (VSMEM) hfz_mbar_wait(bar_virgin, 0);
+  const uint8_t* virgin = VSMEM ? s_virgin : p.v0;
+  for (uint32_t r = 0; r < rows; ++r) {
+    const uint32_t s = r % P, it = r / P;
+    const uint8_t* slot = s_ring + (size_t)s * SLOT;
+    hfz_mbar_wait(&full[s], it & 1u);
+    uint32_t vm = reinterpret_cast<const uint32_t*>(slot + 32 * C::kSlot)[lane];
+    if (!valid) vm = 0;
+    const uint8_t* my_slot = slot + lane * C::kSlot;
+    if (r < rows_host)
+      phase_b<true, ROW, VSMEM, CLASSED>(my_slot, vm, r * ROW, st, virgin, p.first, e, classed_row, nov_row);
+    else
+      phase_b<false, ROW, VSMEM, CLASSED>(my_slot, vm, p.H + (r - rows_host) * (ROW / 4), st, virgin,
+                                          p.first, e, classed_row, nov_row);
+    hfz_mbar_arrive(&empty[s]);
+  }
+  if (valid) {
+    p.sig_full[e64] = st.hf;
+    p.sig_simple[e64] = st.hs;
+    if (p.nnz) p.nnz[e64] = st.nnz;
+  }
+  const uint32_t cm = __ballot_sync(0xffffffffu, valid && st.novel);
+  if (cm) {
+    uint32_t basei = 0;
+    if (lane == 0) basei = atomicAdd(p.cand_count, __popc(cm));
+    basei = __shfl_sync(0xffffffffu, basei, 0);
+    if (valid && st.novel) {
+      const uint32_t ci = basei + __popc(cm & ((1u << lane) - 1u));
+      p.cand_list[ci] = e;
+      p.cand_flags[ci] = 0;
+      p.cand_nov[ci] = st.novel <= kNovMax ? st.novel : kNovMax + 1;
+      if (st.novel > kNovMax) p.slow_list[atomicAdd(p.cand_count + 1, 1u)] = ci;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K2 scan for SMALL batches ("warp-per-map").  With fewer maps than ~6 per warp of the grid the
 // lane-per-map kernel above is latency-bound (one warp walks 320+ rows serially).  Here every
 // warp owns ONE map: the 32 lanes stream it coalesced and compact the non-zero slots, in index
@@ -664,6 +814,37 @@ int launch_scan_wpm_t(hfz_ctx* ctx, const ScanParams& p) {
   return HFZ_OK;
 }
 
+constexpr int kPipeP = 4;  // producer warps per team
+
+template <int REC_CT, int ROW, bool VSMEM, bool CLASSED>
+int launch_scan_pipe_t(hfz_ctx* ctx, const ScanParams& p) {
+  auto kern = hfz_k_scan_pipe<REC_CT, ROW, kPipeP, VSMEM, CLASSED>;
+  constexpr int SLOT = 32 * RowCfg<ROW>::kSlot + 128;
+  const uint64_t groups = (p.n_exec + 31) / 32;
+  int gmax = (ROW == 512 ? 320 : 640) / (32 * (1 + kPipeP));  // teams the launch bounds allow
+  auto smem_for = [&](int G) { return (size_t)(VSMEM ? p.S : 0) + (size_t)G * kPipeP * SLOT + 8 * (1 + 2 * kPipeP * G) + 16; };
+  while (gmax > 1 && smem_for(gmax) > (size_t)ctx->max_smem_optin) --gmax;
+  int G = (int)((groups + ctx->num_sms - 1) / ctx->num_sms);
+  G = G < 1 ? 1 : (G > gmax ? gmax : G);
+  const size_t smem = smem_for(G);
+  HFZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const uint64_t grid = (groups + G - 1) / G;
+  kern<<<(uint32_t)grid, G * (1 + kPipeP) * 32, smem, ctx->stream>>>(p, G);
+  ++ctx->launches;
+  HFZ_CUDA(cudaGetLastError());
+  return HFZ_OK;
+}
+
+template <int REC_CT, bool VSMEM>
+int launch_scan_pipe_r(hfz_ctx* ctx, const ScanParams& p, int row) {
+  const bool classed = p.classed != nullptr;
+  if (row == 256)
+    return classed ? launch_scan_pipe_t<REC_CT, 256, VSMEM, true>(ctx, p)
+                   : launch_scan_pipe_t<REC_CT, 256, VSMEM, false>(ctx, p);
+  return classed ? launch_scan_pipe_t<REC_CT, 512, VSMEM, true>(ctx, p)
+                 : launch_scan_pipe_t<REC_CT, 512, VSMEM, false>(ctx, p);
+}
+
 int launch_scan(hfz_ctx* ctx, const ScanParams& p) {
   // virgin copy in shared memory whenever it leaves room for the per-warp slots
   const bool vsmem = ctx->virgin_smem && p.S <= 65536u;
@@ -675,6 +856,17 @@ int launch_scan(hfz_ctx* ctx, const ScanParams& p) {
     const bool classed = p.classed != nullptr;
     if (vsmem) return classed ? launch_scan_wpm_t<true, true>(ctx, p) : launch_scan_wpm_t<true, false>(ctx, p);
     return classed ? launch_scan_wpm_t<false, true>(ctx, p) : launch_scan_wpm_t<false, false>(ctx, p);
+  }
+  // medium batches: pipelined lane-per-map (producer warps stream, one consumer warp per group)
+  const uint64_t groups = (p.n_exec + 31) / 32;
+  const uint64_t pipe_limit = ctx->scan_pipe >= 0 ? (uint64_t)ctx->scan_pipe : 2;  // groups per SM
+  if (groups <= pipe_limit * (uint64_t)ctx->num_sms) {
+    // 512-byte rows (2 teams per CTA) up to 2 groups per SM, 256-byte rows (4 teams) beyond
+    int row = ctx->scan_row;
+    if (row != 256 && row != 512) row = groups <= 2ull * ctx->num_sms ? 512 : 256;
+    if (p.S == 65536u && vsmem) return launch_scan_pipe_r<163840, true>(ctx, p, row);
+    if (p.S == 262144u && !vsmem) return launch_scan_pipe_r<655360, false>(ctx, p, row);
+    return vsmem ? launch_scan_pipe_r<0, true>(ctx, p, row) : launch_scan_pipe_r<0, false>(ctx, p, row);
   }
   // 256-byte rows let 18 warps/SM hide the shared-memory latency of phase B (best when every SM
   // has more than 9 groups to run); 512-byte rows halve the number of rows a warp walks, which
