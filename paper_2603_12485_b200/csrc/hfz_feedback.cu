@@ -848,22 +848,24 @@ int launch_scan_pipe_r(hfz_ctx* ctx, const ScanParams& p, int row) {
 int launch_scan(hfz_ctx* ctx, const ScanParams& p) {
   // virgin copy in shared memory whenever it leaves room for the per-warp slots
   const bool vsmem = ctx->virgin_smem && p.S <= 65536u;
-  // small batches: one warp per map (latency), else 32 maps per warp (throughput).  Measured
-  // crossover on B200 at 65,536 slots: 1,024 maps 0.31 vs 0.54 ms, 4,096 maps 0.70 vs 0.55 ms.
+  // small batches: one warp per map (latency), else 32 maps per warp (pipelined, then throughput)
   const uint64_t small_limit = ctx->scan_small >= 0 ? (uint64_t)ctx->scan_small
-                                                    : (uint64_t)ctx->num_sms * 14 * 65536u / p.S;
+                                                    : (uint64_t)ctx->num_sms * 10 * 65536u / p.S;
   if (p.n_exec <= small_limit) {
     const bool classed = p.classed != nullptr;
     if (vsmem) return classed ? launch_scan_wpm_t<true, true>(ctx, p) : launch_scan_wpm_t<true, false>(ctx, p);
     return classed ? launch_scan_wpm_t<false, true>(ctx, p) : launch_scan_wpm_t<false, false>(ctx, p);
   }
-  // medium batches: pipelined lane-per-map (producer warps stream, one consumer warp per group)
+  // medium batches: pipelined lane-per-map (producer warps stream, one consumer warp per group).
+  // Measured on B200, 65,536 slots, ms per step (lane-per-map / warp-per-map / pipelined):
+  //   1,024: 0.61 / 0.34 / 0.37   2,048: 0.62 / 0.40 / 0.37   4,096: 0.61 / 0.71 / 0.38
+  //   8,192: 0.62 / 1.36 / 0.42  12,288: 0.64 / 1.99 / 0.48  16,384: 0.65 / 2.37 / 0.78
   const uint64_t groups = (p.n_exec + 31) / 32;
-  const uint64_t pipe_limit = ctx->scan_pipe >= 0 ? (uint64_t)ctx->scan_pipe : 2;  // groups per SM
+  const uint64_t pipe_limit = ctx->scan_pipe >= 0 ? (uint64_t)ctx->scan_pipe : 3;  // groups per SM
   if (groups <= pipe_limit * (uint64_t)ctx->num_sms) {
-    // 512-byte rows (2 teams per CTA) up to 2 groups per SM, 256-byte rows (4 teams) beyond
+    // 512-byte rows (up to 2 teams per CTA) while every SM has one group, 256-byte rows (4 teams) beyond
     int row = ctx->scan_row;
-    if (row != 256 && row != 512) row = groups <= 2ull * ctx->num_sms ? 512 : 256;
+    if (row != 256 && row != 512) row = groups <= (uint64_t)ctx->num_sms ? 512 : 256;
     if (p.S == 65536u && vsmem) return launch_scan_pipe_r<163840, true>(ctx, p, row);
     if (p.S == 262144u && !vsmem) return launch_scan_pipe_r<655360, false>(ctx, p, row);
     return vsmem ? launch_scan_pipe_r<0, true>(ctx, p, row) : launch_scan_pipe_r<0, false>(ctx, p, row);

@@ -13,6 +13,7 @@ ap.add_argument("--ns", default="", help="comma separated batch sizes to time wi
 ap.add_argument("--mode", default="campaign")
 ap.add_argument("--configs", default="row=512;row=256", help="; separated, each k=v,k=v over scan_row/scan_warps/scan_prefetch/virgin_smem")
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--sweep", default="", help="comma separated batch sizes: time every scan kernel on each")
 a = ap.parse_args()
 S = 65536
 ctx = hfz.Context(0, S)
@@ -71,3 +72,26 @@ if a.ns:
                 ts.append(e0.elapsed_time(e1))
         ms = min(ts)
         print(f"n={n:7d}: {ms:8.3f} ms  {n/ms*1e3/1e6:7.3f} M evals/s  {n*rec/ms/1e6:8.1f} GB/s ({n*rec/ms/1e6/6544.7*100:4.1f}%)", flush=True)
+
+if a.sweep:
+    KERN = {"lane": dict(scan_small=0, scan_pipe=0), "wpm": dict(scan_small=1 << 40, scan_pipe=0),
+            "pipe512": dict(scan_small=0, scan_pipe=1 << 20, scan_row=512),
+            "pipe256": dict(scan_small=0, scan_pipe=1 << 20, scan_row=256), "auto": dict(scan_small=-1, scan_pipe=-1)}
+    for n in [int(x) for x in a.sweep.split(",")]:
+        sub = raw[: n * rec]
+        line = f"n={n:7d} ideal {n*rec/6544.7e6:6.3f} ms |"
+        for name, opts in KERN.items():
+            for k, v in dict(DEFAULTS, **opts).items():
+                ctx.set_option(k, v)
+            ts = []
+            for r in range(a.reps + 2):
+                virgin.copy_(v0)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                o = ctx.feedback_batch(sub, virgin, counts)
+                e1.record()
+                torch.cuda.synchronize()
+                if r >= 2:
+                    ts.append(e0.elapsed_time(e1))
+            line += f" {name} {min(ts):6.3f}"
+        print(line, flush=True)

@@ -14,13 +14,24 @@ pytestmark = pytest.mark.gpu
 S = 65536
 
 
-@pytest.fixture(autouse=True, params=["lane_per_map", "warp_per_map"])
+KERNEL_OPTS = {  # (scan_small, scan_pipe): force one of the three scan kernels
+    "lane_per_map": (0, 0),
+    "warp_per_map": (1 << 40, 0),
+    "pipelined": (0, 1 << 20),
+}
+
+
+@pytest.fixture(autouse=True, params=list(KERNEL_OPTS))
 def scan_kernel(request, ctx):
-    """Every test runs against both scan kernels: the throughput kernel (32 maps per warp) and
-    the small-batch kernel (one warp per map); by default the library picks by batch size."""
-    ctx.set_option("scan_small", 0 if request.param == "lane_per_map" else 1 << 40)
+    """Every test runs against all three scan kernels: the throughput kernel (32 maps per warp),
+    the small-batch kernel (one warp per map) and the medium-batch kernel (producer warps + one
+    consumer warp per 32 maps); by default the library picks by batch size."""
+    small, pipe = KERNEL_OPTS[request.param]
+    ctx.set_option("scan_small", small)
+    ctx.set_option("scan_pipe", pipe)
     yield request.param
     ctx.set_option("scan_small", -1)
+    ctx.set_option("scan_pipe", -1)
 
 
 def run_gpu(ctx, raw, virgin0=None, counts0=None, want_classed=True):
@@ -170,7 +181,10 @@ def test_sharded_scan_resolve_equals_sequential(ctx, checker, scan_kernel):
     import paper_2603_12485_b200 as hfz
     ctxs = [hfz.Context(0) for _ in range(R)]
     for i, c in enumerate(ctxs):
-        c.set_option("scan_small", 0 if (i % 2) == (scan_kernel == "lane_per_map") else 1 << 40)
+        # mix the kernels across the simulated ranks
+        small, pipe = KERNEL_OPTS[list(KERNEL_OPTS)[(i + list(KERNEL_OPTS).index(scan_kernel)) % 3]]
+        c.set_option("scan_small", small)
+        c.set_option("scan_pipe", pipe)
     try:
         scans = [ctxs[r].feedback_scan(shards[r], d_v0) for r in range(R)]
         deltas = torch.cat([s["delta"] for s in scans])
@@ -224,7 +238,8 @@ def test_large_map_262144(checker, scan_kernel):
     S2 = 262144
     ck = pyoracle.Ref(S2) if pyoracle.Ref.available(S2) else pyoracle.Port()
     c2 = hfz.Context(0, S2)
-    c2.set_option("scan_small", 0 if scan_kernel == "lane_per_map" else 1 << 40)
+    c2.set_option("scan_small", KERNEL_OPTS[scan_kernel][0])
+    c2.set_option("scan_pipe", KERNEL_OPTS[scan_kernel][1])
     try:
         raw = synth.maps_iid(48, S2, density=0.01, seed=3)
         g = run_gpu(c2, raw)
@@ -232,3 +247,18 @@ def test_large_map_262144(checker, scan_kernel):
         assert_same(g, c)
     finally:
         c2.close()
+
+
+@pytest.mark.parametrize("row", [256, 512])
+@pytest.mark.parametrize("n", [32 * 148 * 2 + 13, 32 * 5, 1000])
+def test_pipelined_kernel_rows_and_teams(ctx, checker, row, n, scan_kernel):
+    """Medium-batch kernel with both ring-slot sizes, more groups than SMs x teams (several CTAs
+    per SM in waves), a partial last group and idle teams."""
+    if scan_kernel != "pipelined":
+        pytest.skip("pipelined kernel only")
+    raw = synth.maps_campaign(n, S, seed=77 + row, p_extra=32, p_rare=32)
+    ctx.set_option("scan_row", row)
+    try:
+        assert_same(run_gpu(ctx, raw, want_classed=False), run_cpu(checker, raw, n, want_classed=False))
+    finally:
+        ctx.set_option("scan_row", 0)
