@@ -54,6 +54,21 @@ class CoverageMap {
   std::uint64_t host_partition_violations() const { return host_violations_; }
   std::uint64_t device_partition_violations() const { return device_violations_; }
 
+  // --- additions for batched hosts
+  // Back to the all-zero map in O(touched slots): the reference's runtime resets its device
+  // counters the same way (reset_device_coverage, src/hdvm.cpp:356-360).
+  void reset() {
+    for (std::uint32_t s : touched_) {
+      if (s < kHostSlots) host_[s] = 0; else device_[s - kDeviceIndexBase] = 0;
+    }
+    touched_.clear();
+    host_violations_ = device_violations_ = 0;
+  }
+  // Sets a host counter to a final value (importing a map recorded elsewhere).
+  void host_assign(std::uint32_t idx, std::uint8_t value) {
+    if (host_[idx] == 0 && value != 0) touched_.push_back(idx);
+    host_[idx] = value;
+  }
   // Logical slots in first-touch order: the dirty list the reference's runtime keeps beside its
   // device counters (src/hdvm.cpp:356-366), here for both halves.  Feeds b200::SparseBatch.
   const std::vector<std::uint32_t>& touched() const { return touched_; }

@@ -6,7 +6,7 @@
  * hot path sits behind the C++ headers proj/include/hetfuzz/{coverage,rng,
  * engine}.hpp (statically linked, proj/CMakeLists.txt:14-23) and the pybind11
  * module proj/python/bindings.cpp:310-350.  Each entry point below names the
- * reference interface it replaces; include/hetfuzz_b200/*.hpp re-creates the
+ * reference interface it replaces; the headers under include/hetfuzz/ re-create the
  * reference's C++ API on top of these calls and INTEGRATION.md shows the
  * binding a maintainer of the reference would add.
  *
@@ -133,7 +133,8 @@ HFZ_API int hfz_feedback_batch_host(hfz_ctx* ctx, const uint8_t* raw_maps_host, 
  *              (full u32, CoverageMap::device_).  count 0 leaves the slot unvisited.  Pairs
  *              with slot >= S are ignored and counted: the _host call then returns HFZ_EINVAL
  *              after completing the fold.
- *   entry_off  (n_exec+1) x u64, entry_off[0] = 0, non-decreasing
+ *   entry_off  (n_exec+1) x u64, non-decreasing absolute indices into `entries` (entry_off[0] need
+ *              not be 0: pass entry_off + k to fold execs k.. of a larger batch)
  * Outputs and in/out state exactly as hfz_feedback_batch: results are bit-identical to the
  * dense call on the maps the lists describe.  The lists are expanded chunk by chunk into a
  * context-owned, all-zero staging buffer (option "sparse_chunk" = execs per chunk, default
@@ -245,6 +246,13 @@ HFZ_API int hfz_havoc_batch(hfz_ctx* ctx, const uint8_t* in_bytes, const uint64_
  * leaves the stream's state after the n-th mutant in stream_state_inout (device, 1 x u64). */
 HFZ_API int hfz_havoc_serial_plan(hfz_ctx* ctx, const uint64_t* in_off, uint64_t n,
                                   uint64_t* stream_state_inout, uint64_t* slot_states_out);
+
+/* Serial-stream havoc with HOST buffers: plan + batch in one synchronous call.  The n mutants
+ * consume ONE Rng in slot order exactly like the havoc loop of Campaign::fuzz_entry
+ * (src/engine.cpp:561-562); *stream_state_inout (host) is the campaign Rng's state. */
+HFZ_API int hfz_havoc_serial_host(hfz_ctx* ctx, const uint8_t* in_bytes, const uint64_t* in_off,
+                                  uint64_t n, uint64_t* stream_state_inout, uint8_t* out_bytes,
+                                  const uint64_t* out_off, uint64_t* out_len);
 
 /* splice_mutant (engine.hpp:33-35, src/engine.cpp:195-204): slot j splices
  * a = input a_idx[j], b = input b_idx[j] of the same packed input set. */

@@ -9,7 +9,9 @@
 // Used (a) to validate the plain-C restatement in hfz_oracle.c, (b) to generate
 // tests/golden/ fixtures, (c) as the "reference" CPU baseline in bench.py.
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <iterator>
 #include <memory>
 #include <string>
 #include <vector>
@@ -222,6 +224,204 @@ REF_API std::uint64_t ref_deterministic(const std::uint8_t* in, std::uint64_t in
     for (std::size_t i = 0; i < ms.size(); ++i)
       if (in_len) std::memcpy(out + i * in_len, ms[i].data(), in_len);
   return ms.size();
+}
+
+
+// ---- campaign + single executions (checker for the batch-aware campaign loop) ----
+// ref_campaign_run forwards to run_campaign (engine.hpp:105); ref_execute / ref_shadow forward to
+// hdvm::execute with the ExecOptions Campaign uses (engine.cpp:346-348, 396-399) plus
+// derive_crash_finding / run_all_tools / dedup_key.  A test drives include/hetfuzz/campaign.hpp
+// with these as its Executor and compares every field with the reference's own campaign.
+
+namespace {
+
+struct RefCampaign {
+  CampaignConfig cfg;
+  CampaignResult res;
+  std::vector<std::string> texts;  // crash_report_text per crash, in map order
+  std::string json, csv;
+};
+
+// findings as text: one per record-separator, fields split by unit-separator:
+// key(hex16) US tool US kind US detail US site frames split by group-separator
+void append_finding(std::string& out, const Finding& f) {
+  char key[17];
+  std::snprintf(key, sizeof key, "%016llx", static_cast<unsigned long long>(dedup_key(f)));
+  out += key;
+  out += '\x1f';
+  out += to_string(f.tool);
+  out += '\x1f';
+  out += to_string(f.kind);
+  out += '\x1f';
+  out += f.detail;
+  out += '\x1f';
+  for (std::size_t i = 0; i < f.site.size(); ++i) {
+    if (i) out += '\x1d';
+    out += f.site[i];
+  }
+  out += '\x1e';
+}
+
+int copy_text(const std::string& s, char* out, std::uint64_t cap) {
+  if (s.size() + 1 > cap) return 20;
+  std::memcpy(out, s.data(), s.size());
+  out[s.size()] = 0;
+  return 0;
+}
+
+}  // namespace
+
+REF_API void* ref_campaign_run(const char* target, const std::uint8_t* seeds_blob,
+                               const std::uint64_t* seed_off, std::uint32_t n_seeds, std::uint64_t rng_seed,
+                               int strategy, int sanitizers, int device_coverage, int budget_kind,
+                               std::uint64_t budget, int sequential_queue, int workers,
+                               std::uint64_t stats_every, const char* out_dir) {
+  auto* c = new RefCampaign;
+  c->cfg.target = target;
+  for (std::uint32_t i = 0; i < n_seeds; ++i)
+    c->cfg.seeds.emplace_back(seeds_blob + seed_off[i], seeds_blob + seed_off[i + 1]);
+  c->cfg.rng_seed = rng_seed;
+  c->cfg.strategy = static_cast<Strategy>(strategy);
+  c->cfg.sanitizers = sanitizers != 0;
+  c->cfg.device_coverage = device_coverage != 0;
+  c->cfg.budget_kind = static_cast<BudgetKind>(budget_kind);
+  c->cfg.budget = budget;
+  c->cfg.sequential_queue = sequential_queue != 0;
+  c->cfg.workers = workers;
+  c->cfg.stats_every = stats_every;
+  c->cfg.out_dir = out_dir ? out_dir : "";
+  try {
+    c->res = run_campaign(c->cfg);
+  } catch (const std::exception&) {
+    delete c;
+    return nullptr;
+  }
+  for (const auto& kv : c->res.crashes) c->texts.push_back(crash_report_text(kv.second));
+  c->json = campaign_json(c->cfg, c->res);
+  c->csv = plot_data_csv(c->res.stats);
+  return c;
+}
+REF_API void ref_campaign_free(void* h) { delete static_cast<RefCampaign*>(h); }
+
+// out[9]: execs, virtual_time, sanitizer_execs, queue size, host_edges, device_edges,
+// partition_violations, crashes, stats rows
+REF_API void ref_campaign_totals(void* h, std::uint64_t* out) {
+  const CampaignResult& r = static_cast<RefCampaign*>(h)->res;
+  out[0] = r.execs;
+  out[1] = r.virtual_time;
+  out[2] = r.sanitizer_execs;
+  out[3] = r.queue.size();
+  out[4] = r.virgin.host_edges();
+  out[5] = r.virgin.device_edges();
+  out[6] = r.partition_violations;
+  out[7] = r.crashes.size();
+  out[8] = r.stats.size();
+}
+// meta[7]: id, full_sig, simple_sig, admit_reason, discovered_at, parent (~0 = none), exec_cost
+REF_API void ref_campaign_queue_entry(void* h, std::uint64_t i, std::uint64_t* meta,
+                                      const std::uint8_t** data, std::uint64_t* len) {
+  const QueueEntry& e = static_cast<RefCampaign*>(h)->res.queue[i];
+  meta[0] = e.id;
+  meta[1] = e.full_sig;
+  meta[2] = e.simple_sig;
+  meta[3] = static_cast<std::uint64_t>(e.admit_reason);
+  meta[4] = e.discovered_at;
+  meta[5] = e.parent ? *e.parent : ~0ull;
+  meta[6] = e.exec_cost;
+  *data = e.input.data();
+  *len = e.input.size();
+}
+REF_API void ref_campaign_stats_row(void* h, std::uint64_t i, std::uint64_t* row) {
+  const StatsRow& r = static_cast<RefCampaign*>(h)->res.stats[i];
+  row[0] = r.virtual_time;
+  row[1] = r.execs;
+  row[2] = r.host_edges;
+  row[3] = r.device_edges;
+  row[4] = r.unique_inputs;
+  row[5] = r.crashes;
+  row[6] = r.sanitizer_execs;
+}
+// meta[4]: key, first_exposed, hits, false_positive; *text = crash_report_text
+REF_API void ref_campaign_crash(void* h, std::uint64_t i, std::uint64_t* meta, const char** text) {
+  auto* c = static_cast<RefCampaign*>(h);
+  auto it = c->res.crashes.begin();
+  std::advance(it, i);
+  meta[0] = it->first;
+  meta[1] = it->second.first_exposed;
+  meta[2] = it->second.hits;
+  meta[3] = it->second.false_positive ? 1 : 0;
+  *text = c->texts[i].c_str();
+}
+REF_API void ref_campaign_virgin(void* h, std::uint8_t* out) {
+  const VirginMap& v = static_cast<RefCampaign*>(h)->res.virgin;
+  for (std::uint32_t i = 0; i < kMapSize; ++i) out[i] = v.at(i);
+}
+REF_API const char* ref_campaign_json(void* h) { return static_cast<RefCampaign*>(h)->json.c_str(); }
+REF_API const char* ref_campaign_csv(void* h) { return static_cast<RefCampaign*>(h)->csv.c_str(); }
+
+// The target's canonical seed corpus (TargetInfo::seeds, targets.hpp:27).
+REF_API int ref_target_seeds(const char* target, std::uint8_t* blob, std::uint64_t blob_cap,
+                             std::uint64_t* off, std::uint32_t* n) {
+  const TargetInfo* info = find_target(target);
+  if (!info) return 21;
+  std::uint64_t pos = 0;
+  off[0] = 0;
+  *n = static_cast<std::uint32_t>(info->seeds.size());
+  for (std::size_t i = 0; i < info->seeds.size(); ++i) {
+    if (pos + info->seeds[i].size() > blob_cap) return 20;
+    std::memcpy(blob + pos, info->seeds[i].data(), info->seeds[i].size());
+    pos += info->seeds[i].size();
+    off[i + 1] = pos;
+  }
+  return 0;
+}
+
+// One plain execution as Campaign::run_one performs it (whole-program mode, fresh process).
+// raw_out: the raw record in the library layout.  out[4]: virtual_cost, partition violations,
+// exit clean?, has crash finding?; text: the crash finding (see append_finding) or empty.
+REF_API int ref_execute(const char* target, const std::uint8_t* in, std::uint64_t len,
+                        int device_coverage, std::uint8_t* raw_out, std::uint64_t* out, char* text,
+                        std::uint64_t text_cap) {
+  const TargetInfo* info = find_target(target);
+  if (!info) return 21;
+  hdvm::ExecOptions opts;
+  opts.host_coverage = true;
+  opts.device_coverage = device_coverage != 0;
+  opts.shadow = false;
+  hdvm::ExecutionReport rep = hdvm::execute(info->program, std::vector<std::uint8_t>(in, in + len), opts);
+  std::memcpy(raw_out, rep.raw_map.host_half().data(), kHostSlots);
+  std::memcpy(raw_out + kHostSlots, rep.raw_map.device_half().data(), std::uint64_t(kMapSize - kHostSlots) * 4);
+  out[0] = rep.virtual_cost;
+  out[1] = rep.raw_map.host_partition_violations() + rep.raw_map.device_partition_violations();
+  out[2] = rep.exit.kind == hdvm::ExitKind::Clean ? 1 : 0;
+  out[3] = 0;
+  std::string t;
+  if (rep.exit.kind != hdvm::ExitKind::Clean) {
+    if (auto crash = derive_crash_finding(rep)) {
+      out[3] = 1;
+      append_finding(t, *crash);
+    }
+  }
+  return copy_text(t, text, text_cap);
+}
+
+// One shadow execution + all four tools (Campaign::drain_sanitizers, engine.cpp:396-417).
+// out[2]: virtual_cost + records_examined, number of findings.
+REF_API int ref_shadow(const char* target, const std::uint8_t* in, std::uint64_t len, std::uint64_t* out,
+                       char* text, std::uint64_t text_cap) {
+  const TargetInfo* info = find_target(target);
+  if (!info) return 21;
+  hdvm::ExecOptions opts;
+  opts.host_coverage = false;
+  opts.device_coverage = false;
+  opts.shadow = true;
+  hdvm::ExecutionReport rep = hdvm::execute(info->program, std::vector<std::uint8_t>(in, in + len), opts);
+  SanitizerSweep sweep = run_all_tools(rep);
+  out[0] = rep.virtual_cost + sweep.records_examined;
+  out[1] = sweep.findings.size();
+  std::string t;
+  for (const Finding& f : sweep.findings) append_finding(t, f);
+  return copy_text(t, text, text_cap);
 }
 
 #endif  // REF_NO_ENGINE

@@ -52,6 +52,7 @@ PROTOTYPES = {
     "hfz_havoc_batch_host": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp]),
     "hfz_splice_batch_host": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
     "hfz_deterministic_host": (C.c_int, [_vp, _vp, _u64, _vp, _u64]),
+    "hfz_havoc_serial_host": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
     "hfz_havoc_serial_plan": (C.c_int, [_vp, _vp, _u64, _vp, _vp]),
     "hfz_sigset_create": (C.c_int, [_vp, _u64, C.POINTER(_vp)]),
     "hfz_sigset_destroy": (C.c_int, [_vp]),

@@ -550,6 +550,41 @@ extern "C" int hfz_havoc_batch_host(hfz_ctx* ctx, const uint8_t* in_bytes, const
   return HFZ_OK;
 }
 
+extern "C" int hfz_havoc_serial_host(hfz_ctx* ctx, const uint8_t* in_bytes, const uint64_t* in_off,
+                                     uint64_t n, uint64_t* stream_state_inout, uint8_t* out_bytes,
+                                     const uint64_t* out_off, uint64_t* out_len) {
+  if (!ctx || !stream_state_inout || (n && (!in_off || !out_bytes || !out_off || !out_len))) {
+    hfz_set_error("hfz_havoc_serial_host: null argument");
+    return HFZ_EINVAL;
+  }
+  if (n == 0) return HFZ_OK;
+  HFZ_TRY(cudaSetDevice(ctx->device));
+  const uint64_t in_total = in_off[n], out_total = out_off[n];
+  DevBuf d_in, d_ioff, d_stream, d_state, d_out, d_ooff, d_olen;
+  HFZ_TRY(d_in.alloc(in_total + 16));
+  HFZ_TRY(d_ioff.alloc((n + 1) * 8));
+  HFZ_TRY(d_stream.alloc(8));
+  HFZ_TRY(d_state.alloc(n * 8));
+  HFZ_TRY(d_out.alloc(out_total + 16));
+  HFZ_TRY(d_ooff.alloc((n + 1) * 8));
+  HFZ_TRY(d_olen.alloc(n * 8));
+  cudaStream_t st = ctx->stream;
+  if (in_total) HFZ_TRY(cudaMemcpyAsync(d_in.p, in_bytes, in_total, cudaMemcpyHostToDevice, st));
+  HFZ_TRY(cudaMemcpyAsync(d_ioff.p, in_off, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+  HFZ_TRY(cudaMemcpyAsync(d_stream.p, stream_state_inout, 8, cudaMemcpyHostToDevice, st));
+  HFZ_TRY(cudaMemcpyAsync(d_ooff.p, out_off, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+  int rc = hfz_havoc_serial_plan(ctx, d_ioff.as<uint64_t>(), n, d_stream.as<uint64_t>(), d_state.as<uint64_t>());
+  if (rc) return rc;
+  rc = hfz_havoc_batch(ctx, d_in.as<uint8_t>(), d_ioff.as<uint64_t>(), n, d_state.as<uint64_t>(),
+                       d_out.as<uint8_t>(), d_ooff.as<uint64_t>(), d_olen.as<uint64_t>(), nullptr);
+  if (rc) return rc;
+  if (out_total) HFZ_TRY(cudaMemcpyAsync(out_bytes, d_out.p, out_total, cudaMemcpyDeviceToHost, st));
+  HFZ_TRY(cudaMemcpyAsync(out_len, d_olen.p, n * 8, cudaMemcpyDeviceToHost, st));
+  HFZ_TRY(cudaMemcpyAsync(stream_state_inout, d_stream.p, 8, cudaMemcpyDeviceToHost, st));
+  HFZ_TRY(cudaStreamSynchronize(st));
+  return HFZ_OK;
+}
+
 extern "C" int hfz_splice_batch_host(hfz_ctx* ctx, const uint8_t* in_bytes, const uint64_t* in_off,
                                      uint64_t n_inputs, const uint32_t* a_idx, const uint32_t* b_idx,
                                      uint64_t n, uint64_t* rng_state_inout, uint8_t* out_bytes,

@@ -162,9 +162,12 @@ extern "C" int hfz_feedback_batch_sparse_host(hfz_ctx* c, const uint32_t* entrie
     return HFZ_EINVAL;
   }
   if (n_exec == 0) return HFZ_OK;
+  // entry_off indexes `entries` absolutely, so a sub-range of a larger batch is folded by
+  // passing entry_off + first_exec; only pairs [entry_off[0], entry_off[n_exec]) are copied
+  const uint64_t first_pair = entry_off[0];
   const uint64_t total = entry_off[n_exec];
-  if (entry_off[0] != 0 || (total && !entries)) {
-    hfz_set_error("hfz_feedback_batch_sparse_host: entry_off[0] must be 0 and entries non-null");
+  if (total > first_pair && !entries) {
+    hfz_set_error("hfz_feedback_batch_sparse_host: entries is null");
     return HFZ_EINVAL;
   }
   for (uint64_t e = 0; e < n_exec; ++e) {
@@ -182,6 +185,7 @@ extern "C" int hfz_feedback_batch_sparse_host(hfz_ctx* c, const uint32_t* entrie
   const uint64_t C = c->sp_dense_execs;
   const uint64_t n_chunks = (n_exec + C - 1) / C;
   if (classed && (rc = hfz_ensure_classed_stage(c, n_exec < C ? n_exec : C))) return rc;
+  (void)first_pair;  // the device copy keeps the absolute indexing: pairs below first_pair are never read
   if (c->sp_entries_cap < total) {
     cudaFree(c->sp_entries);
     c->sp_entries = nullptr;

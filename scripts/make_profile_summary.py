@@ -61,3 +61,25 @@ if os.path.exists(launches):
 reg = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_regions.py"), rep], capture_output=True, text=True).stdout
 open(os.path.join(out, f"{rnd}_scan_regions.txt"), "w").write(reg)
 print(json.dumps({k: summary[k] for k in ("duration_s_under_ncu", "dram_bytes_per_launch", "traffic_over_algorithmic", "dram_gbs_under_ncu", "sectors_per_global_load_request") if k in summary}))
+
+
+# ---- secondary kernels: one compact summary per extra report found in gpurun_out/
+EXTRA = {"scan_pipe": "scripts/probe_feedback.py --n 4096 --configs '' --reps 1 --sweep 4096 (-k regex:hfz_k_scan_pipe -s 2 -c 1)",
+         "expand": "scripts/probe_sparse.py --execs 16384 --chunks 8192 (-k regex:hfz_k_expand -s 2 -c 2)",
+         "edge": "scripts/probe_k1k3.py edge (-k regex:hfz_k_edge_record -c 1)"}
+for name, cmd in EXTRA.items():
+    rp = os.path.join(ROOT, "gpurun_out", f"{rnd}_{name}.ncu-rep")
+    if not os.path.exists(rp):
+        continue
+    raw2 = subprocess.run(["ncu", "-i", rp, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows2 = list(csv.reader(raw2.splitlines()))
+    hdr2, units2 = rows2[0], rows2[1]
+    outl = []
+    for vals2 in rows2[2:]:
+        mm = {h: (vals2[i], units2[i]) for i, h in enumerate(hdr2)}
+        sel2 = {k: {"value": mm[k][0], "unit": mm[k][1]} for k in keys if k in mm}
+        st2 = {h: mm[h][0] for h in hdr2 if "issue_stalled" in h and h.endswith("_per_warp_active.pct")}
+        top = dict(sorted(st2.items(), key=lambda kv: -float(kv[1].replace(",", "") or 0))[:6])
+        outl.append({"kernel": mm.get("Kernel Name", ("?",))[0], "metrics": sel2, "top_stalls_pct_per_warp_active": top})
+    json.dump({"round": rnd, "command": "ncu --set full --clock-control none python " + cmd, "launches": outl},
+              open(os.path.join(out, f"{rnd}_{name}_summary.json"), "w"), indent=1)

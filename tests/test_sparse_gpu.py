@@ -141,8 +141,22 @@ def test_sparse_bad_offsets_rejected(sctx):
     c = np.zeros(2, np.uint64)
     with pytest.raises(HfzError):
         sctx.feedback_batch_sparse_host(entries, np.array([0, 3, 2], np.uint64), v, c)
-    with pytest.raises(HfzError):
-        sctx.feedback_batch_sparse_host(entries, np.array([1, 2, 4], np.uint64), v, c)
+
+
+def test_sparse_subrange_folds_equal_one_fold(sctx, checker):
+    """entry_off indexes the pairs absolutely: folding execs [0,k) and then [k,n) through
+    entry_off[k:] (entry_off[0] != 0) equals one fold of the whole batch."""
+    n, k = 150, 61
+    raw = synth.maps_campaign(n, S, seed=41, p_extra=8, p_rare=8)
+    entries, off = synth.to_sparse(raw, n, S, shuffle_seed=9)
+    v = np.zeros(S, np.uint8)
+    c = np.zeros(2, np.uint64)
+    a = sctx.feedback_batch_sparse_host(entries, off[:k + 1].copy(), v, c)
+    b = sctx.feedback_batch_sparse_host(entries, off[k:].copy(), v, c)
+    wo, wv, wc = cpu(checker, raw, n, want_classed=False)
+    for key in wo:
+        assert np.array_equal(np.concatenate([a[key], b[key]]), wo[key]), key
+    assert np.array_equal(v, wv) and np.array_equal(c, wc)
 
 
 def test_sparse_large_map():
