@@ -149,7 +149,7 @@ struct CampaignResult {  // engine.hpp:93-103
   std::uint64_t execs = 0, virtual_time = 0, sanitizer_execs = 0, partition_violations = 0,
                 persistent_processes = 0;
   // batching telemetry (not part of the reference's result)
-  std::uint64_t folds = 0, rollbacks = 0, gpu_mutants = 0;
+  std::uint64_t folds = 0, rollbacks = 0, splice_cuts = 0, gpu_mutants = 0;
 };
 
 inline std::uint64_t hash_input(const Bytes& input) {  // sanitizers.cpp:298-300
@@ -283,6 +283,19 @@ class BatchCampaign {
     }
     if (cfg_.budget_kind == BudgetKind::Execs && cfg_.budget - res_.execs < n)
       n = static_cast<std::size_t>(cfg_.budget - res_.execs);  // never execute past an exec budget
+    if (cfg_.budget_kind == BudgetKind::VirtualTime && n > kTimeBudgetBatch) {
+      // a time budget can run out anywhere: bound how far past it the executor may run by
+      // handing a long stage over in pieces (consecutive run_one calls either way)
+      std::size_t done = 0;
+      while (done < inputs.size() && !stop_) {
+        const std::size_t m = std::min(kTimeBudgetBatch, inputs.size() - done);
+        const std::vector<Bytes> piece(inputs.begin() + done, inputs.begin() + done + m);
+        const std::size_t used = run_batch(piece, parent, force_admit, cut_on_admit);
+        done += used;
+        if (used < m) break;  // stopped, or cut at an admission
+      }
+      return done;
+    }
     batch_.clear();
     std::vector<ExecOutcome> out(n);
     for (std::size_t i = 0; i < n; ++i) {
@@ -314,7 +327,8 @@ class BatchCampaign {
         }
         const bool admitted = account(inputs[i], out[i], static_cast<Admit>(fb.admit[i - p]), fb.sig_full[i - p],
                                       fb.sig_simple[i - p], parent, force_admit);
-        if (cut_on_admit && admitted && i + 1 < n) {
+        if (cut_on_admit && admitted && i + 1 < inputs.size()) {  // later mutants were drawn for a shorter queue
+          ++res_.splice_cuts;
           if (i + 1 < end) refold(p, i + 1);
           return i + 1;
         }
@@ -473,6 +487,7 @@ class BatchCampaign {
     return res;
   }
 
+  static constexpr std::size_t kTimeBudgetBatch = 256;
   const CampaignConfig& cfg_;
   Executor& exec_;
   Context& ctx_;

@@ -51,6 +51,9 @@ def test_batched_campaign_equals_serial_reference(tmp_path):
     print(r.stdout[-6000:])
     assert r.returncode == 0, r.stdout[-6000:] + r.stderr[-2000:]
     assert "all checks passed" in r.stdout
+    import re
+    m = re.search(r"splice cuts (\d+), rollbacks (\d+)", r.stdout)
+    assert m and int(m.group(2)) > 0, "no rollback was exercised"
     cases = sorted(d[:-4] for d in os.listdir(out) if d.endswith("_ref"))
     assert len(cases) >= 5
     for c in cases:
