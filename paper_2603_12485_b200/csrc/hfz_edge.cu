@@ -32,9 +32,14 @@
 namespace {
 
 constexpr int kEdgeWarps = 16;
-constexpr uint32_t kRows = 256;        // per-warp site table rows
-constexpr uint32_t kFill = 192;        // rows in use before a partition is split
-constexpr uint32_t kWarpTab = kRows * (8 + 4 + 4 + 4) + 64;  // keys u64, m u32, c u32, stamp u32, used
+constexpr uint32_t kRows = 256;        // site table rows
+// One table serves either general-path variant:
+//   transposed replay: keys u64[kRows] + per-row byte matrix [kRows][32]  (2 KB + 8 KB)
+//   partitioned replay (fallback): keys u64, m u32, c u32, stamp u32       (5 KB)
+// Only non-coherent simulated warps need one, so the CTA keeps a POOL of kPool tables that its
+// 16 warps borrow (free-mask in shared memory) instead of one table per warp.
+constexpr uint32_t kTabBytes = kRows * (8 + 32) + 64;
+constexpr int kPool = 8;
 constexpr uint32_t kSmemSlots = 32768; // device slots whose counters fit in shared memory
 constexpr uint32_t kMaxBlockThreads = 1024;         // hdvm.hpp:167
 constexpr uint64_t kMaxLaunchThreads = 1ull << 22;  // hdvm.hpp:168
@@ -206,6 +211,103 @@ __device__ __forceinline__ uint64_t general_path(WarpTable& tab, const uint32_t*
   return bumps;
 }
 
+// Transposed general path: real lane L plays simulated lane L.
+//   phase 1  every lane walks its own events and counts its visits per site in a nibble matrix
+//            cnt[row(site)][L] (shared-memory atomics on the 32-bit word that holds the nibble);
+//   row pass c_L(s) -> d_L(s) = max(0, c_L(s) - max_{L' < L} c_{L'}(s)): the number of bumps lane L
+//            owes for site s (its visits k = M_L(s)+1 .. c_L(s)); exclusive prefix max over the 32
+//            lanes of a row with SIMD byte ops, saturating byte subtract;
+//   phase 2  every lane walks its events BACKWARDS and hands out its d_L(s) bumps to the last
+//            d_L(s) visits of s -- exactly the visits with k > M_L(s); slot uses that visit's own
+//            prev.  Bumps commute (saturating adds), so their order is free.
+// Table: kTRows x {u32 site key, 16 bytes of nibbles}; byte b holds lane b (low nibble) and lane
+// b + 16 (high nibble).  Returns false (nothing bumped) when the table fills up or a lane visits a
+// site more than 15 times: the caller then runs the partitioned replay, which has neither limit.
+constexpr uint32_t kTRows = 512;
+constexpr uint32_t kTEmpty = 0xffffffffu;  // key of a free row; the site 0xffffffff gets row kTRows
+static_assert((kTRows + 1) * (4 + 16) <= kTabBytes, "transposed table must fit a pool table");
+
+__device__ __forceinline__ bool transposed_path(uint8_t* tab, const uint32_t* sites, uint64_t e0, uint32_t n_ev,
+                                                uint32_t prev0, uint32_t* counters, uint32_t hmask, int lane,
+                                                uint64_t& bumps_out) {
+  uint32_t* keys = reinterpret_cast<uint32_t*>(tab);                    // [kTRows + 1]
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(tab + (kTRows + 4) * 4);  // [kTRows + 1][4], 16-byte aligned
+  for (uint32_t i = lane; i < kTRows + 1; i += 32) keys[i] = kTEmpty;
+  uint4* clr = reinterpret_cast<uint4*>(cnt);
+  for (uint32_t i = lane; i < kTRows + 1; i += 32) clr[i] = make_uint4(0, 0, 0, 0);
+  __syncwarp();
+  const uint32_t b = lane & 15;
+  const uint32_t word = b >> 2, shift = (b & 3) * 8 + (lane >> 4) * 4;
+  const uint32_t max_n = __reduce_max_sync(0xffffffffu, n_ev);
+  auto find = [&](uint32_t s, bool insert) -> uint32_t {
+    if (s == kTEmpty) return kTRows;
+    uint32_t r = mix32(s) & (kTRows - 1);
+    for (uint32_t probe = 0; probe < kTRows; ++probe) {
+      const uint32_t cur = keys[r];
+      if (cur == s) return r;
+      if (insert && cur == kTEmpty) {
+        const uint32_t old = atomicCAS(&keys[r], kTEmpty, s);
+        if (old == kTEmpty || old == s) return r;
+      }
+      r = (r + 1) & (kTRows - 1);
+    }
+    return kTRows + 1;  // full
+  };
+  bool bad = false;
+  for (uint32_t i = 0; i < max_n; ++i) {
+    if (i < n_ev && !bad) {
+      const uint32_t r = find(sites[e0 + i], true);
+      if (r > kTRows) {
+        bad = true;
+      } else {
+        const uint32_t old = atomicAdd(&cnt[r * 4 + word], 1u << shift);
+        bad = ((old >> shift) & 15u) == 15u;  // nibble overflow: the table is abandoned
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad)) return false;
+  __syncwarp();
+  // rows -> owed bumps.  Lane order inside a row: low nibbles of words 0..3, then high nibbles.
+  for (uint32_t r = lane; r < kTRows + 1; r += 32) {
+    uint4 x = reinterpret_cast<uint4*>(cnt)[r];
+    if ((x.x | x.y | x.z | x.w) == 0u) continue;
+    uint32_t w[4] = {x.x, x.y, x.z, x.w}, d[4] = {0, 0, 0, 0};
+    uint32_t carry = 0;  // max count among the lanes seen so far
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t v = (w[k] >> (4 * half)) & 0x0f0f0f0fu;
+        uint32_t pm = __vmaxu4(v, v << 8);
+        pm = __vmaxu4(pm, pm << 16);                     // inclusive prefix max inside the word
+        pm = __vmaxu4(pm, carry * 0x01010101u);          // ... including the earlier lanes
+        const uint32_t ex = (pm << 8) | carry;           // exclusive prefix max per lane
+        d[k] |= __vsubus4(v, ex) << (4 * half);
+        carry = pm >> 24;
+      }
+    }
+    reinterpret_cast<uint4*>(cnt)[r] = make_uint4(d[0], d[1], d[2], d[3]);
+  }
+  __syncwarp();
+  uint32_t bumps = 0;
+  for (uint32_t i = max_n; i-- > 0;) {
+    if (i < n_ev) {
+      const uint32_t s = sites[e0 + i];
+      const uint32_t r = find(s, false);  // present since phase 1
+      uint32_t* c = &cnt[r * 4 + word];
+      if ((*reinterpret_cast<volatile uint32_t*>(c) >> shift) & 15u) {  // only this lane changes its nibble
+        atomicSub(c, 1u << shift);
+        const uint32_t pv = i ? (sites[e0 + i - 1] >> 1) : prev0;
+        bump(&counters[(pv ^ s) & hmask]);
+        ++bumps;
+      }
+    }
+  }
+  bumps_out += bumps;
+  __syncwarp();
+  return true;
+}
+
 // exact a / b for a < 2^23, b >= 1: float quotient is within 1 of the true one
 __device__ __forceinline__ uint32_t div_small(uint32_t a, uint32_t b, float rb) {
   uint32_t q = (uint32_t)((float)a * rb);
@@ -219,16 +321,12 @@ template <bool SMEM_HIST>
 __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const EdgeParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint32_t* hist = SMEM_HIST ? reinterpret_cast<uint32_t*>(smem) : nullptr;
-  uint8_t* wbase = smem + (SMEM_HIST ? (size_t)p.H * 4 : 0);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  WarpTable tab;
-  tab.keys = reinterpret_cast<unsigned long long*>(wbase + (size_t)warp * kWarpTab);
-  tab.m = reinterpret_cast<uint32_t*>(tab.keys + kRows);
-  tab.c = tab.m + kRows;
-  tab.stamp = tab.c + kRows;
-  tab.used = tab.stamp + kRows;
+  uint8_t* pool = smem + (SMEM_HIST ? (size_t)p.H * 4 : 0);
+  const int lane = threadIdx.x & 31;
   __shared__ unsigned long long s_events;
   __shared__ uint32_t s_next;
+  __shared__ uint32_t s_free;  // bit t set = pool table t is free
+  if (threadIdx.x == 0) s_free = (1u << kPool) - 1u;
   uint32_t* prev_tab = p.prev_scratch + (size_t)blockIdx.x * p.prev_stride;
   const uint32_t hmask = p.H - 1;
 
@@ -362,8 +460,35 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
             continue;
           }
 
-          // ---- general path
-          my_events += general_path(tab, p.sites, e0, n_ev, prev0, counters, hmask, lane);
+          // ---- general path: borrow a table from the CTA's pool
+          uint32_t t = 0;
+          if (lane == 0) {
+            for (;;) {
+              const uint32_t m = *reinterpret_cast<volatile uint32_t*>(&s_free);
+              if (m == 0) {
+                __nanosleep(100);
+                continue;
+              }
+              t = __ffs(m) - 1;
+              if (atomicAnd(&s_free, ~(1u << t)) & (1u << t)) break;
+            }
+          }
+          t = __shfl_sync(0xffffffffu, t, 0);
+          uint8_t* tmem = pool + (size_t)t * kTabBytes;
+          if (!transposed_path(tmem, p.sites, e0, n_ev, prev0, counters, hmask, lane, my_events)) {
+            WarpTable tab;
+            tab.keys = reinterpret_cast<unsigned long long*>(tmem);
+            tab.m = reinterpret_cast<uint32_t*>(tab.keys + kRows);
+            tab.c = tab.m + kRows;
+            tab.stamp = tab.c + kRows;
+            tab.used = tab.stamp + kRows;
+            my_events += general_path(tab, p.sites, e0, n_ev, prev0, counters, hmask, lane);
+          }
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence_block();
+            atomicOr(&s_free, 1u << t);
+          }
           if (use_tab && active && n_ev) prev_tab[gtid] = p.sites[e1 - 1] >> 1;
         }
       }
@@ -483,7 +608,7 @@ extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, c
   p.warp_events = warp_events_out;
   p.prev_scratch = d_prev;
   p.prev_stride = stride;
-  const size_t wsmem = (size_t)kEdgeWarps * kWarpTab;
+  const size_t wsmem = (size_t)kPool * kTabBytes;
   const bool smem_hist = ctx->H <= kSmemSlots;
   const size_t smem = wsmem + (smem_hist ? (size_t)ctx->H * 4 : 0);
   if (smem_hist) {

@@ -131,6 +131,30 @@ def test_uniform_launches_with_idle_threads(ctx, port):
     check(ctx, port, pack(execs), len(execs))
 
 
+def test_divergent_warps_small_tables(ctx, port):
+    """Divergent warps that fit the transposed replay's table (a few hundred distinct sites, at
+    most 15 visits per lane and site), including the site id 0xffffffff (the table's free-row
+    marker) and lanes that differ only in their last event."""
+    rng = np.random.default_rng(15)
+    execs = []
+    for ex in range(6):
+        dims = np.array([[2, 1, 1, 64, 1, 1]] * 2, np.uint32)
+        pool = np.concatenate([rng.integers(0, 2 ** 32, 300, dtype=np.uint64), [0xFFFFFFFF, 0, 1]])
+        ev, sites = [0], []
+        for l in range(2):
+            for t in range(128):
+                n = int(rng.integers(0, 24))
+                seq = pool[rng.integers(0, len(pool) if ex % 2 else 40, n)].tolist()
+                if t % 7 == 0:
+                    seq += [0xFFFFFFFF] * int(rng.integers(1, 6))
+                if ex == 5:
+                    seq = [5, 6, 7, 8, 9, 10 + (t % 3)]     # nearly coherent: same prefix, 3 endings
+                sites.extend(int(x) for x in seq)
+                ev.append(len(sites))
+        execs.append((dims, ev, sites))
+    check(ctx, port, pack(execs), len(execs))
+
+
 def test_many_distinct_sites_forces_partitioning(ctx, port):
     """Fully divergent warps with far more distinct sites than the per-warp table holds."""
     rng = np.random.default_rng(12)
