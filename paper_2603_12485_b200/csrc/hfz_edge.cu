@@ -268,21 +268,36 @@ __device__ __forceinline__ bool transposed_path(uint8_t* tab, const uint32_t* si
   if (__any_sync(0xffffffffu, bad)) return false;
   __syncwarp();
   // rows -> owed bumps.  Lane order inside a row: low nibbles of words 0..3, then high nibbles.
+  // Most rows of a divergent warp were visited by ONE lane only (d = c, nothing to do); the
+  // byte-wise max / saturating subtract are plain SWAR arithmetic (values <= 15 leave bit 7 of
+  // every byte free as a borrow guard; the video intrinsics are emulated on sm_100).
+  auto max4 = [](uint32_t a, uint32_t b2) {
+    const uint32_t ge = (((a | 0x80808080u) - b2) >> 7) & 0x01010101u;  // 1 where a >= b
+    const uint32_t m = ge * 0xffu;
+    return (a & m) | (b2 & ~m);
+  };
   for (uint32_t r = lane; r < kTRows + 1; r += 32) {
-    uint4 x = reinterpret_cast<uint4*>(cnt)[r];
-    if ((x.x | x.y | x.z | x.w) == 0u) continue;
-    uint32_t w[4] = {x.x, x.y, x.z, x.w}, d[4] = {0, 0, 0, 0};
+    const uint4 x = reinterpret_cast<uint4*>(cnt)[r];
+    const uint32_t any = x.x | x.y | x.z | x.w;
+    if (any == 0u) continue;
+    // non-zero nibble flags of each word, then: exactly one visiting lane?
+    auto nzn = [](uint32_t v) { return (v | (v >> 1) | (v >> 2) | (v >> 3)) & 0x11111111u; };
+    if (__popc(nzn(x.x)) + __popc(nzn(x.y)) + __popc(nzn(x.z)) + __popc(nzn(x.w)) == 1) continue;
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+    uint32_t d[4] = {0, 0, 0, 0};
     uint32_t carry = 0;  // max count among the lanes seen so far
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint32_t v = (w[k] >> (4 * half)) & 0x0f0f0f0fu;
-        uint32_t pm = __vmaxu4(v, v << 8);
-        pm = __vmaxu4(pm, pm << 16);                     // inclusive prefix max inside the word
-        pm = __vmaxu4(pm, carry * 0x01010101u);          // ... including the earlier lanes
-        const uint32_t ex = (pm << 8) | carry;           // exclusive prefix max per lane
-        d[k] |= __vsubus4(v, ex) << (4 * half);
+        uint32_t pm = max4(v, v << 8);
+        pm = max4(pm, pm << 16);                          // inclusive prefix max inside the word
+        pm = max4(pm, carry * 0x01010101u);               // ... including the earlier lanes
+        const uint32_t ex = (pm << 8) | carry;            // exclusive prefix max per lane
+        const uint32_t t = (v | 0x80808080u) - ex;        // per byte: v - ex with a borrow guard
+        const uint32_t ge = (t >> 7) & 0x01010101u;       // 1 where v >= ex
+        d[k] |= (t & 0x0f0f0f0fu & (ge * 0xffu)) << (4 * half);
         carry = pm >> 24;
       }
     }
@@ -427,6 +442,23 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
             }
           }
           const uint32_t n_ev = (uint32_t)(e1 - e0);
+          {
+            // Traces are contiguous in thread order and the CTA's warps pop simulated warps in
+            // order, so what the pop kEdgeWarps ahead will read lies about kEdgeWarps times this
+            // warp's own span further on: pull it (and its offsets) into L2 now.
+            const uint64_t first = __shfl_sync(0xffffffffu, e0, 0);
+            const uint64_t last = __shfl_sync(0xffffffffu, e1, 31);
+            const uint64_t span = (last - first) * 4;
+            if (span) {
+              const uint64_t lines = min((span + 127) / 128, (uint64_t)32);
+              if ((uint64_t)lane < lines)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint8_t*>(p.sites + last) +
+                                                              span * (kEdgeWarps - 1) + (uint64_t)lane * 128));
+            }
+            if (lane < 2)
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint8_t*>(
+                  p.ev_off + t0 + (uint64_t)bl * tpb + (uint64_t)(sw - bl * wpb) * 32 + (uint64_t)kEdgeWarps * 32) + lane * 128));
+          }
           const bool use_tab = multi && !uniform;
           uint32_t prev0 = uniform ? prev_u : ((use_tab && active) ? prev_tab[gtid] : 0);
           const uint32_t amask = __ballot_sync(0xffffffffu, active);
@@ -466,7 +498,7 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
             for (;;) {
               const uint32_t m = *reinterpret_cast<volatile uint32_t*>(&s_free);
               if (m == 0) {
-                __nanosleep(100);
+                __nanosleep(400);
                 continue;
               }
               t = __ffs(m) - 1;
