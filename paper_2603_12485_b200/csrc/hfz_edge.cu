@@ -39,7 +39,7 @@ constexpr uint32_t kRows = 256;        // site table rows
 // Only non-coherent simulated warps need one, so the CTA keeps a POOL of kPool tables that its
 // 16 warps borrow (free-mask in shared memory) instead of one table per warp.
 constexpr uint32_t kTabBytes = kRows * (8 + 32) + 64;
-constexpr int kPool = 8;
+constexpr int kPool = 9;
 constexpr uint32_t kSmemSlots = 32768; // device slots whose counters fit in shared memory
 constexpr uint32_t kMaxBlockThreads = 1024;         // hdvm.hpp:167
 constexpr uint64_t kMaxLaunchThreads = 1ull << 22;  // hdvm.hpp:168
