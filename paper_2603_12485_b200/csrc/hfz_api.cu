@@ -107,6 +107,8 @@ extern "C" int hfz_ctx_destroy(hfz_ctx* c) {
   cudaFree(c->sp_dense);
   cudaFree(c->sp_entries);
   cudaFree(c->sp_off);
+  cudaFree(c->sp_sorted);
+  cudaFree(c->sp_cnt);
   for (cudaEvent_t ev : c->sp_events) cudaEventDestroy(ev);
   delete c;
   return HFZ_OK;
@@ -146,6 +148,8 @@ extern "C" int hfz_ctx_set_option(hfz_ctx* c, const char* key, int64_t value) {
     c->scan_pipe = value;
   } else if (!strcmp(key, "time_scan")) {
     c->time_scan = value != 0;
+  } else if (!strcmp(key, "sparse_native")) {
+    c->sparse_native = value != 0;
   } else if (!strcmp(key, "sparse_chunk")) {
     if (value < 0 || (value && value < 32) || c->sp_dense) return HFZ_EINVAL;
     c->sparse_chunk = (uint64_t)value / 32 * 32;

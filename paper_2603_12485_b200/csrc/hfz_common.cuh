@@ -66,6 +66,16 @@ struct hfz_ctx {
   uint64_t* sp_off = nullptr;
   uint64_t sp_off_cap = 0;
   std::vector<cudaEvent_t> sp_events;  // one "entries of chunk k copied" event per chunk
+  int sparse_native = 1;           // 1 = rank + chain kernels on the lists (S <= 65,536), 0 = expand to dense records
+  uint32_t* sp_sorted = nullptr;   // per pair: slot | rung << 24, ascending slots inside an exec
+  uint64_t sp_sorted_cap = 0;
+  uint32_t* sp_cnt = nullptr;      // per exec: distinct non-zero slots
+  uint64_t sp_cnt_cap = 0;
+  // set by the last scan: the resolve step re-reads a candidate either from its dense record or
+  // from its ordered list
+  const uint32_t* sc_sorted = nullptr;
+  const uint64_t* sc_off = nullptr;
+  const uint32_t* sc_cnt = nullptr;
 
   // tuning
   int scan_warps = 0;     // 0 = as many as fit
@@ -82,6 +92,13 @@ void hfz_set_error(const char* fmt, ...);
 int hfz_cuda_fail(cudaError_t e, const char* what);
 int hfz_ensure_host_common(hfz_ctx* c, uint64_t n_exec);   // hfz_api.cu
 int hfz_ensure_classed_stage(hfz_ctx* c, uint64_t execs);  // hfz_api.cu
+// hfz_feedback.cu: the scan half of the fold on touched-slot lists (device buffers); total_pairs =
+// entry_off[n_exec] (absolute).  Pair it with hfz_feedback_resolve(raw_maps = NULL).
+bool hfz_sparse_native_ok(const hfz_ctx* c);
+int hfz_feedback_scan_sparse(hfz_ctx* c, const uint32_t* pairs, const uint64_t* entry_off, uint64_t n_exec,
+                             uint64_t total_pairs, const uint8_t* virgin_v0, uint8_t* classed_out,
+                             uint64_t* sig_full_out, uint64_t* sig_simple_out, uint32_t* nnz_out,
+                             uint8_t* delta_out, unsigned long long* bad_pairs);
 
 #define HFZ_CUDA(call)                                   \
   do {                                                   \

@@ -764,6 +764,209 @@ __global__ void hfz_k_admit(const uint32_t* __restrict__ cand_list,
 }
 
 // ---------------------------------------------------------------------------
+// Sparse-native scan: the fold on touched-slot lists without ever building a dense record.
+//   rank   one warp per exec: the (slot, count) pairs arrive in any order; a bitmap of the map's
+//          slots in shared memory (S bits) + a popcount prefix give every slot its RANK among the
+//          exec's non-zero slots, so the pairs are written out as `slot | rung << 24` in ascending
+//          slot order without a sort; classification, the virgin test against the TMA-staged
+//          V0 and the first-occurrence update ride along;
+//   chain  one lane per exec runs both FNV chains over its ordered list -- dense iterations, no
+//          row-synchronous max over lanes as in the dense kernels.
+// 65,536 execs (76 M pairs) take ~0.3 ms instead of ~10 ms through the dense staging buffer.
+constexpr int kRankWarps = 12;  // 12 x (8 KB bitmap + 4 KB prefix) + 64 KB virgin = 208 KB for S = 65,536
+
+struct SparseParams {
+  const uint2* pairs;
+  const uint64_t* off;
+  uint64_t n_exec;
+  uint32_t S, H;
+  const uint8_t* v0;
+  uint32_t* first;
+  uint32_t* cand_list;
+  uint32_t* cand_count;
+  uint32_t* cand_flags;
+  uint32_t* cand_nov;
+  uint32_t* slow_list;
+  uint32_t* novel_ent;
+  uint32_t* sorted;
+  uint32_t* cnt;
+  uint8_t* classed;
+  unsigned long long* bad;
+};
+
+__global__ void __launch_bounds__(kRankWarps * 32, 1) hfz_k_sparse_rank(const SparseParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t words = p.S / 32, per = words / 32;  // bitmap words, words per lane in the prefix pass
+  const uint32_t per_shift = 31 - __clz(per);         // S is a power of two >= 1024
+  uint8_t* s_virgin = smem;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem + p.S + (size_t)warp * (words * 4 + words * 2 + 256));
+  uint16_t* pre = reinterpret_cast<uint16_t*>(bm + words);
+  uint32_t* lane_base = reinterpret_cast<uint32_t*>(pre + words);  // [32] + [1] novel counter
+  uint32_t* nov_cnt = lane_base + 32;
+  uint64_t* bar_virgin = reinterpret_cast<uint64_t*>(smem + p.S + (size_t)kRankWarps * (words * 4 + words * 2 + 256));
+  if (threadIdx.x == 0) {
+    hfz_mbar_init(bar_virgin, 1);
+    hfz_fence_barrier_init();
+  }
+  for (uint32_t i = lane; i < words; i += 32) bm[i] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint64_t pol = hfz_policy_evict_last();
+    hfz_mbar_expect_tx(bar_virgin, p.S);
+    for (uint32_t o = 0; o < p.S; o += 16384u) {
+      const uint32_t n = p.S - o < 16384u ? p.S - o : 16384u;
+      hfz_bulk_g2s_stream(s_virgin + o, p.v0 + o, n, bar_virgin, pol);
+    }
+  }
+  hfz_mbar_wait(bar_virgin, 0);
+  uint32_t nbad = 0;
+  for (uint64_t e64 = (uint64_t)blockIdx.x * kRankWarps + warp; e64 < p.n_exec; e64 += (uint64_t)gridDim.x * kRankWarps) {
+    const uint32_t e = (uint32_t)e64;
+    const uint64_t b = p.off[e64], t = p.off[e64 + 1];
+    if (lane == 0) *nov_cnt = 0;
+    // pass 1: mark the slots
+    for (uint64_t i0 = b; i0 < t; i0 += 128) {
+      uint2 x[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t i = i0 + j * 32 + lane;
+        x[j] = i < t ? __ldg(p.pairs + i) : make_uint2(0u, 0u);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t slot = x[j].x, c = slot < p.H ? (x[j].y & 0xffu) : x[j].y;
+        if (slot >= p.S) {
+          ++nbad;
+        } else if (c) {
+          atomicOr(&bm[slot >> 5], 1u << (slot & 31));
+        }
+      }
+    }
+    __syncwarp();
+    // popcount prefix: lane l owns words [l * per, (l + 1) * per)
+    uint32_t sum = 0;
+    for (uint32_t k = 0; k < per; ++k) {
+      const uint32_t w = lane * per + k;
+      pre[w] = (uint16_t)sum;
+      sum += __popc(bm[w]);
+    }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += o;
+    }
+    lane_base[lane] = inc - sum;
+    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+    __syncwarp();
+    // pass 2: rank, classify, novelty, ordered write
+    uint8_t* classed_row = p.classed ? p.classed + e64 * p.S : nullptr;
+    uint32_t* nov_row = p.novel_ent + e64 * kNovMax;
+    for (uint64_t i0 = b; i0 < t; i0 += 128) {
+      uint2 x[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t i = i0 + j * 32 + lane;
+        x[j] = i < t ? __ldg(p.pairs + i) : make_uint2(0u, 0u);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t slot = x[j].x;
+        if (slot >= p.S) continue;
+        const uint32_t c = slot < p.H ? (x[j].y & 0xffu) : x[j].y;
+        if (!c) continue;
+        const uint32_t w = slot >> 5;
+        const uint32_t rank = lane_base[w >> per_shift] + pre[w] + __popc(bm[w] & ((1u << (slot & 31)) - 1u));
+        const uint32_t klass = slot < p.H ? hfz_class_host(c) : hfz_class_device(c);
+        const uint32_t rung = 31 - __clz(klass);
+        const uint32_t en = slot | (rung << 24);
+        p.sorted[b + rank] = en;
+        if (klass & ~(uint32_t)s_virgin[slot]) {
+          const uint32_t k = atomicAdd(nov_cnt, 1u);
+          if (k < kNovMax) nov_row[k] = en;
+          atomicMin(p.first + (size_t)slot * 8 + rung, e);
+        }
+        if (classed_row) classed_row[slot] = (uint8_t)klass;
+      }
+    }
+    __syncwarp();
+    const uint32_t novel = *nov_cnt;
+    if (lane == 0) {
+      p.cnt[e64] = total;
+      if (novel) {
+        const uint32_t ci = atomicAdd(p.cand_count, 1u);
+        p.cand_list[ci] = e;
+        p.cand_flags[ci] = 0;
+        p.cand_nov[ci] = novel <= kNovMax ? novel : kNovMax + 1;
+        if (novel > kNovMax) p.slow_list[atomicAdd(p.cand_count + 1, 1u)] = ci;
+      }
+    }
+    for (uint32_t i = lane; i < words / 4; i += 32) reinterpret_cast<uint4*>(bm)[i] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+  }
+  nbad = __reduce_add_sync(0xffffffffu, nbad);
+  if (lane == 0 && nbad && p.bad) atomicAdd(p.bad, (unsigned long long)nbad);
+}
+
+__global__ void __launch_bounds__(128) hfz_k_sparse_chain(const uint32_t* __restrict__ sorted,
+                                                          const uint64_t* __restrict__ off,
+                                                          const uint32_t* __restrict__ cnt, uint64_t n_exec,
+                                                          uint64_t* __restrict__ sig_full,
+                                                          uint64_t* __restrict__ sig_simple,
+                                                          uint32_t* __restrict__ nnz_out) {
+  const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_exec) return;
+  const uint32_t* list = sorted + off[e];
+  const uint32_t n = cnt[e];
+  uint64_t hf = HFZ_FNV_OFFSET, hs = HFZ_FNV_OFFSET;
+  uint32_t i = 0;
+  for (; i + 4 <= n; i += 4) {  // the four loads are independent of the chains
+    uint32_t en[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) en[k] = __ldg(list + i + k);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t b0 = en[k] & 0xffu, b1 = (en[k] >> 8) & 0xffu;
+      hf = hfz_fnv(hfz_fnv(hfz_fnv(hf, b0), b1), 1u << (en[k] >> 24));
+      hs = hfz_fnv(hfz_fnv(hs, b0), b1);
+    }
+  }
+  for (; i < n; ++i) {
+    const uint32_t en = __ldg(list + i);
+    const uint32_t b0 = en & 0xffu, b1 = (en >> 8) & 0xffu;
+    hf = hfz_fnv(hfz_fnv(hfz_fnv(hf, b0), b1), 1u << (en >> 24));
+    hs = hfz_fnv(hfz_fnv(hs, b0), b1);
+  }
+  sig_full[e] = hf;
+  sig_simple[e] = hs;
+  if (nnz_out) nnz_out[e] = n;
+}
+
+// resolve of the candidates with more than kNovMax novel slots, from their ordered lists
+__global__ void __launch_bounds__(256) hfz_k_resolve_sparse(const ResolveParams p, const uint32_t* __restrict__ sorted,
+                                                            const uint64_t* __restrict__ off,
+                                                            const uint32_t* __restrict__ cnt) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t total_warps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t n_slow = p.cand_count[1];
+  for (uint32_t it = warp; it < n_slow; it += total_warps) {
+    const uint32_t ci = p.slow_list[it];
+    const uint32_t e = p.cand_list[ci];
+    const uint32_t* list = sorted + off[e];
+    const uint32_t n = cnt[e];
+    uint32_t flags = 0;
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint32_t en = __ldg(list + i);
+      flags |= resolve_entry(p, en & 0xffffffu, 1u << (en >> 24), e);
+    }
+    flags = __reduce_or_sync(0xffffffffu, flags);
+    if (lane == 0 && flags) atomicOr(p.cand_flags + ci, flags);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // launch plumbing
 
 template <int ROW>
@@ -915,6 +1118,7 @@ extern "C" int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t
   HFZ_CUDA(cudaSetDevice(ctx->device));
   int rc = ensure_cand(ctx, n_exec);
   if (rc) return rc;
+  ctx->sc_sorted = nullptr;  // the resolve step re-reads candidates from their dense records
   HFZ_CUDA(cudaMemsetAsync(ctx->first, 0xff, (size_t)ctx->S * 8 * sizeof(uint32_t), ctx->stream));
   HFZ_CUDA(cudaMemsetAsync(ctx->cand_count, 0, 2 * sizeof(uint32_t), ctx->stream));
   if (classed_out && n_exec)
@@ -959,6 +1163,81 @@ extern "C" int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t
   return HFZ_OK;
 }
 
+bool hfz_sparse_native_ok(const hfz_ctx* c) {
+  // bitmap + prefix per warp and the virgin copy must fit shared memory
+  return c->sparse_native && c->S <= 65536u && c->S >= 1024u;
+}
+
+int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t* entry_off, uint64_t n_exec,
+                             uint64_t total_pairs, const uint8_t* virgin_v0, uint8_t* classed_out,
+                             uint64_t* sig_full_out, uint64_t* sig_simple_out, uint32_t* nnz_out,
+                             uint8_t* delta_out, unsigned long long* bad_pairs) {
+  if (n_exec >= 0xfffffffeull) {
+    hfz_set_error("hfz_feedback_scan_sparse: n_exec too large");
+    return HFZ_ECAP;
+  }
+  HFZ_CUDA(cudaSetDevice(ctx->device));
+  int rc = ensure_cand(ctx, n_exec);
+  if (rc) return rc;
+  if (ctx->sp_sorted_cap < total_pairs) {
+    cudaFree(ctx->sp_sorted);
+    ctx->sp_sorted = nullptr;
+    ctx->sp_sorted_cap = 0;
+    const uint64_t cap = total_pairs + total_pairs / 8 + 1024;
+    HFZ_CUDA(cudaMalloc(&ctx->sp_sorted, cap * 4));
+    ctx->sp_sorted_cap = cap;
+  }
+  if (ctx->sp_cnt_cap < n_exec) {
+    cudaFree(ctx->sp_cnt);
+    ctx->sp_cnt = nullptr;
+    ctx->sp_cnt_cap = 0;
+    HFZ_CUDA(cudaMalloc(&ctx->sp_cnt, (n_exec + 1024) * 4));
+    ctx->sp_cnt_cap = n_exec + 1024;
+  }
+  HFZ_CUDA(cudaMemsetAsync(ctx->first, 0xff, (size_t)ctx->S * 8 * sizeof(uint32_t), ctx->stream));
+  HFZ_CUDA(cudaMemsetAsync(ctx->cand_count, 0, 2 * sizeof(uint32_t), ctx->stream));
+  if (classed_out && n_exec) HFZ_CUDA(cudaMemsetAsync(classed_out, 0, n_exec * (size_t)ctx->S, ctx->stream));
+  if (n_exec) {
+    SparseParams p;
+    p.pairs = reinterpret_cast<const uint2*>(pairs);
+    p.off = entry_off;
+    p.n_exec = n_exec;
+    p.S = ctx->S;
+    p.H = ctx->H;
+    p.v0 = virgin_v0;
+    p.first = ctx->first;
+    p.cand_list = ctx->cand_list;
+    p.cand_count = ctx->cand_count;
+    p.cand_flags = ctx->cand_list + ctx->cand_cap;
+    p.cand_nov = ctx->cand_list + 2 * ctx->cand_cap;
+    p.slow_list = ctx->cand_list + 3 * ctx->cand_cap;
+    p.novel_ent = ctx->cand_list + 4 * ctx->cand_cap;
+    p.sorted = ctx->sp_sorted;
+    p.cnt = ctx->sp_cnt;
+    p.classed = classed_out;
+    p.bad = bad_pairs;
+    const uint32_t words = ctx->S / 32;
+    const size_t smem = (size_t)ctx->S + (size_t)kRankWarps * (words * 4 + words * 2 + 256) + 16;
+    HFZ_CUDA(cudaFuncSetAttribute(hfz_k_sparse_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    uint64_t grid = (n_exec + kRankWarps - 1) / kRankWarps;
+    if (grid > (uint64_t)ctx->num_sms) grid = (uint64_t)ctx->num_sms;
+    hfz_k_sparse_rank<<<(uint32_t)grid, kRankWarps * 32, smem, ctx->stream>>>(p);
+    ++ctx->launches;
+    HFZ_CUDA(cudaGetLastError());
+    hfz_k_sparse_chain<<<(uint32_t)((n_exec + 127) / 128), 128, 0, ctx->stream>>>(
+        ctx->sp_sorted, entry_off, ctx->sp_cnt, n_exec, sig_full_out, sig_simple_out, nnz_out);
+    ++ctx->launches;
+    HFZ_CUDA(cudaGetLastError());
+  }
+  hfz_k_delta<<<(ctx->S + 255) / 256, 256, 0, ctx->stream>>>(ctx->first, delta_out, ctx->S);
+  ++ctx->launches;
+  HFZ_CUDA(cudaGetLastError());
+  ctx->sc_sorted = ctx->sp_sorted;
+  ctx->sc_off = entry_off;
+  ctx->sc_cnt = ctx->sp_cnt;
+  return HFZ_OK;
+}
+
 extern "C" int hfz_virgin_merge(hfz_ctx* ctx, uint8_t* virgin_inout, uint64_t* edge_counts_inout,
                                 const uint8_t* deltas, uint32_t n_ranks) {
   if (!ctx || !virgin_inout || !edge_counts_inout || (n_ranks && !deltas)) {
@@ -979,7 +1258,7 @@ extern "C" int hfz_feedback_resolve(hfz_ctx* ctx, const uint8_t* raw_maps, uint6
                                     const uint8_t* deltas, uint32_t n_ranks, uint32_t rank,
                                     uint8_t* admit_out) {
   if (!ctx || !virgin_inout || !edge_counts_inout || !deltas || n_ranks == 0 || rank >= n_ranks ||
-      (n_exec && (!raw_maps || !admit_out))) {
+      (n_exec && ((!raw_maps && !ctx->sc_sorted) || !admit_out))) {
     hfz_set_error("hfz_feedback_resolve: bad argument");
     return HFZ_EINVAL;
   }
@@ -1008,9 +1287,14 @@ extern "C" int hfz_feedback_resolve(hfz_ctx* ctx, const uint8_t* raw_maps, uint6
     hfz_k_resolve_fast<<<(uint32_t)ctx->num_sms * 2, 256, 0, ctx->stream>>>(p);
     ++ctx->launches;
     HFZ_CUDA(cudaGetLastError());
-    uint32_t piece = kPiece;
-    while (ctx->H % piece) piece >>= 1;  // H is a power of two >= 512
-    hfz_k_resolve<<<(uint32_t)ctx->num_sms * 4, 256, 0, ctx->stream>>>(p, piece);
+    if (ctx->sc_sorted) {
+      hfz_k_resolve_sparse<<<(uint32_t)ctx->num_sms * 4, 256, 0, ctx->stream>>>(p, ctx->sc_sorted, ctx->sc_off,
+                                                                                  ctx->sc_cnt);
+    } else {
+      uint32_t piece = kPiece;
+      while (ctx->H % piece) piece >>= 1;  // H is a power of two >= 512
+      hfz_k_resolve<<<(uint32_t)ctx->num_sms * 4, 256, 0, ctx->stream>>>(p, piece);
+    }
     ++ctx->launches;
     HFZ_CUDA(cudaGetLastError());
     hfz_k_admit<<<(uint32_t)ctx->num_sms, 256, 0, ctx->stream>>>(ctx->cand_list, ctx->cand_count,

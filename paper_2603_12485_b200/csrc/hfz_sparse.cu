@@ -102,29 +102,41 @@ int launch_expand(hfz_ctx* c, const uint32_t* entries, const uint64_t* off, uint
 // Folds execs [0, n_exec) given device pairs / offsets, chunk by chunk.  `events` (may be
 // null) holds one event per chunk that the stream must wait for before touching the chunk's
 // pairs; classed_host (may be null) receives the classed maps through ctx->d_classed.
-int fold_chunks(hfz_ctx* c, const uint32_t* entries, const uint64_t* off, uint64_t n_exec,
-                uint8_t* virgin, uint64_t* counts, uint8_t* classed_dev, uint8_t* classed_host,
-                uint8_t* admit, uint64_t* sigf, uint64_t* sigs, uint32_t* nnz,
+// native: rank + chain kernels on the lists (total_pairs = entry_off[n_exec], absolute);
+// otherwise the pairs are expanded into the dense staging buffer and scanned by K2.
+int fold_chunks(hfz_ctx* c, const uint32_t* entries, const uint64_t* off, uint64_t n_exec, uint64_t C,
+                bool native, uint64_t total_pairs, uint8_t* virgin, uint64_t* counts, uint8_t* classed_dev,
+                uint8_t* classed_host, uint8_t* admit, uint64_t* sigf, uint64_t* sigs, uint32_t* nnz,
                 const cudaEvent_t* events) {
-  const uint64_t C = c->sp_dense_execs;
-  c->sp_dirty = true;  // until the last cleanup pass has been enqueued
+  if (!native) c->sp_dirty = true;  // until the last cleanup pass has been enqueued
   uint64_t k = 0;
   for (uint64_t done = 0; done < n_exec; done += C, ++k) {
     const uint64_t n = n_exec - done < C ? n_exec - done : C;
     if (events) HFZ_CUDA(cudaStreamWaitEvent(c->stream, events[k], 0));
-    int rc = launch_expand<false>(c, entries, off + done, n);
-    if (rc) return rc;
     uint8_t* cls = classed_dev ? classed_dev + done * (uint64_t)c->S : (classed_host ? c->d_classed : nullptr);
-    rc = hfz_feedback_batch(c, c->sp_dense, n, virgin, counts, cls, admit + done, sigf + done,
-                            sigs + done, nnz ? nnz + done : nullptr);
-    if (rc) return rc;
+    int rc;
+    if (native) {
+      rc = hfz_feedback_scan_sparse(c, entries, off + done, n, total_pairs, virgin, cls, sigf + done, sigs + done,
+                                    nnz ? nnz + done : nullptr, c->delta, c->d_small + kBadSlot);
+      if (rc) return rc;
+      rc = hfz_feedback_resolve(c, nullptr, n, virgin, counts, c->delta, 1, 0, admit + done);
+      if (rc) return rc;
+    } else {
+      rc = launch_expand<false>(c, entries, off + done, n);
+      if (rc) return rc;
+      rc = hfz_feedback_batch(c, c->sp_dense, n, virgin, counts, cls, admit + done, sigf + done, sigs + done,
+                              nnz ? nnz + done : nullptr);
+      if (rc) return rc;
+    }
     if (classed_host)
       HFZ_CUDA(cudaMemcpyAsync(classed_host + done * (uint64_t)c->S, c->d_classed, n * (uint64_t)c->S,
                                cudaMemcpyDeviceToHost, c->stream));
-    rc = launch_expand<true>(c, entries, off + done, n);
-    if (rc) return rc;
+    if (!native) {
+      rc = launch_expand<true>(c, entries, off + done, n);
+      if (rc) return rc;
+    }
   }
-  c->sp_dirty = false;
+  if (!native) c->sp_dirty = false;
   return HFZ_OK;
 }
 
@@ -146,11 +158,20 @@ extern "C" int hfz_feedback_batch_sparse(hfz_ctx* c, const uint32_t* entries, co
   }
   HFZ_CUDA(cudaSetDevice(c->device));
   if (n_exec == 0) return HFZ_OK;
+  HFZ_CUDA(cudaMemsetAsync(c->d_small + kBadSlot, 0, sizeof(unsigned long long), c->stream));
+  if (hfz_sparse_native_ok(c)) {
+    // one pass over the whole batch; the ordered-list scratch is sized from entry_off[n_exec]
+    // (one 8-byte read back: this call synchronises the stream once before it enqueues)
+    uint64_t total = 0;
+    HFZ_CUDA(cudaMemcpyAsync(&total, entry_off + n_exec, 8, cudaMemcpyDeviceToHost, c->stream));
+    HFZ_CUDA(cudaStreamSynchronize(c->stream));
+    return fold_chunks(c, entries, entry_off, n_exec, n_exec, true, total, virgin_inout, edge_counts_inout,
+                       classed_out, nullptr, admit_out, sig_full_out, sig_simple_out, nnz_out, nullptr);
+  }
   int rc = ensure_dense(c, n_exec);
   if (rc) return rc;
-  HFZ_CUDA(cudaMemsetAsync(c->d_small + kBadSlot, 0, sizeof(unsigned long long), c->stream));
-  return fold_chunks(c, entries, entry_off, n_exec, virgin_inout, edge_counts_inout, classed_out, nullptr,
-                     admit_out, sig_full_out, sig_simple_out, nnz_out, nullptr);
+  return fold_chunks(c, entries, entry_off, n_exec, c->sp_dense_execs, false, 0, virgin_inout, edge_counts_inout,
+                     classed_out, nullptr, admit_out, sig_full_out, sig_simple_out, nnz_out, nullptr);
 }
 
 extern "C" int hfz_feedback_batch_sparse_host(hfz_ctx* c, const uint32_t* entries, const uint64_t* entry_off,
@@ -180,9 +201,16 @@ extern "C" int hfz_feedback_batch_sparse_host(hfz_ctx* c, const uint32_t* entrie
   HFZ_CUDA(cudaSetDevice(c->device));
   int rc = hfz_ensure_host_common(c, n_exec);
   if (rc) return rc;
-  rc = ensure_dense(c, n_exec);
-  if (rc) return rc;
-  const uint64_t C = c->sp_dense_execs;
+  const bool native = hfz_sparse_native_ok(c);
+  uint64_t C;
+  if (native) {
+    // chunks only pace the overlap of the H2D stream with the kernels (measured: 4,096 execs)
+    C = c->sparse_chunk ? c->sparse_chunk : 4096;
+  } else {
+    rc = ensure_dense(c, n_exec);
+    if (rc) return rc;
+    C = c->sp_dense_execs;
+  }
   const uint64_t n_chunks = (n_exec + C - 1) / C;
   if (classed && (rc = hfz_ensure_classed_stage(c, n_exec < C ? n_exec : C))) return rc;
   (void)first_pair;  // the device copy keeps the absolute indexing: pairs below first_pair are never read
@@ -222,8 +250,8 @@ extern "C" int hfz_feedback_batch_sparse_host(hfz_ctx* c, const uint32_t* entrie
                                c->copy_stream));
     HFZ_CUDA(cudaEventRecord(c->sp_events[k], c->copy_stream));
   }
-  rc = fold_chunks(c, c->sp_entries, c->sp_off, n_exec, c->d_virgin, c->d_counts, nullptr, classed,
-                   c->d_admit, c->d_sigf, c->d_sigs, c->d_nnz, c->sp_events.data());
+  rc = fold_chunks(c, c->sp_entries, c->sp_off, n_exec, C, native, total, c->d_virgin, c->d_counts, nullptr,
+                   classed, c->d_admit, c->d_sigf, c->d_sigs, c->d_nnz, c->sp_events.data());
   if (rc) {
     cudaStreamSynchronize(c->copy_stream);
     cudaStreamSynchronize(st);

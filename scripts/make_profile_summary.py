@@ -53,7 +53,8 @@ if os.path.exists(launches):
         agg.setdefault(r[ik].split("(")[0][-48:], []).append(float(r[iv].replace(",", "")))
     tot = sum(sum(v) for k, v in agg.items() if "hfz_k" in k)
     with open(os.path.join(out, f"{rnd}_bench_launches_summary.txt"), "w") as f:
-        f.write("# ncu --metrics gpu__time_duration.sum --clock-control none -c 400 python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu\n")
+        f.write("# ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e-dense --e2e-steps 1\n")
+        f.write("# (timed steps, the untimed clock-sampling steps, torch data-prep kernels of the sparse lists, then the sparse e2e calls)\n")
         f.write("# per-launch times are cold-cache and serialised: compare SHARES\n")
         for k, v in agg.items():
             share = f"{sum(v)/tot*100:5.1f}% of hfz kernels" if "hfz_k" in k else ""

@@ -28,12 +28,15 @@ def check_host(c, got, gv, gc, want):
     assert np.array_equal(gc, wc), f"edge counts differ {gc} vs {wc}"
 
 
-@pytest.fixture()
-def sctx():
-    """Own context per test: the sparse chunk size can only be set before first use."""
+@pytest.fixture(params=["native", "expand"])
+def sctx(request):
+    """Own context per test (the sparse chunk size can only be set before first use); every test
+    runs through both device paths: rank + chain kernels on the lists, and expansion into dense
+    staging records scanned by K2."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     c = hfz.Context(0)
+    c.set_option("sparse_native", 1 if request.param == "native" else 0)
     yield c
     c.close()
 
@@ -178,3 +181,22 @@ def test_sparse_large_map():
         assert np.array_equal(v, wv) and np.array_equal(c, wc)
     finally:
         c2.close()
+
+
+def test_sparse_repeated_pairs_with_equal_counts(sctx, checker):
+    """A slot listed twice with the same count (SparseBatch does that after device_store(x, 0)
+    followed by a new store) is one slot: nnz, signatures and virgin are those of the map."""
+    n = 60
+    raw = synth.maps_campaign(n, S, seed=55, p_extra=8, p_rare=8)
+    entries, off = synth.to_sparse(raw, n, S, shuffle_seed=6)
+    parts, new_off = [], [0]
+    for e in range(n):
+        seg = entries[int(off[e]):int(off[e + 1])]
+        dup = seg[:: 7]                                   # every 7th pair once more
+        parts += [seg, dup]
+        new_off.append(new_off[-1] + len(seg) + len(dup))
+    entries2 = np.ascontiguousarray(np.concatenate(parts))
+    v = np.zeros(S, np.uint8)
+    c = np.zeros(2, np.uint64)
+    got = sctx.feedback_batch_sparse_host(entries2, np.array(new_off, np.uint64), v, c, want_classed=True)
+    check_host(sctx, got, v, c, cpu(checker, raw, n))
