@@ -79,7 +79,7 @@ HFZ_API int hfz_ctx_set_stream(hfz_ctx* ctx, void* stream);
 HFZ_API int hfz_ctx_sync(hfz_ctx* ctx);
 HFZ_API uint32_t hfz_ctx_map_slots(const hfz_ctx* ctx);
 HFZ_API uint64_t hfz_record_bytes(uint32_t map_slots);
-/* Tuning knobs, mostly for bench/profiling: key in {"scan_warps","scan_row","scan_prefetch","virgin_smem","scan_small","time_scan","stage_execs","sparse_chunk"} */
+/* Tuning knobs, mostly for bench/profiling: key in {"scan_warps","scan_row","scan_prefetch","virgin_smem","scan_small","time_scan","stage_execs","sparse_chunk","sparse_native","scan_pipe"} */
 HFZ_API int hfz_ctx_set_option(hfz_ctx* ctx, const char* key, int64_t value);
 /* Kernels launched by this context since creation (for bench.py's gpu_launches). */
 HFZ_API uint64_t hfz_ctx_launch_count(const hfz_ctx* ctx);
@@ -127,8 +127,9 @@ HFZ_API int hfz_feedback_batch_host(hfz_ctx* ctx, const uint8_t* raw_maps_host, 
  * ~10 KB per exec over PCIe instead of 163,840 B.
  *
  *   entries    n_total x {u32 slot, u32 count} pairs, 8-byte aligned.  Exec e owns pairs
- *              [entry_off[e], entry_off[e+1]); ANY order inside an exec; a slot may appear at
- *              most once per exec (repeats: one of them wins).  slot < S/2 is a host counter
+ *              [entry_off[e], entry_off[e+1]); ANY order inside an exec.  Listing a slot twice
+ *              with the SAME count is harmless (it is one slot); with different counts it is
+ *              unspecified which one each output uses.  slot < S/2 is a host counter
  *              (count & 0xff is stored, CoverageMap::host_), S/2 <= slot < S a device counter
  *              (full u32, CoverageMap::device_).  count 0 leaves the slot unvisited.  Pairs
  *              with slot >= S are ignored and counted: the _host call then returns HFZ_EINVAL
@@ -136,7 +137,10 @@ HFZ_API int hfz_feedback_batch_host(hfz_ctx* ctx, const uint8_t* raw_maps_host, 
  *   entry_off  (n_exec+1) x u64, non-decreasing absolute indices into `entries` (entry_off[0] need
  *              not be 0: pass entry_off + k to fold execs k.. of a larger batch)
  * Outputs and in/out state exactly as hfz_feedback_batch: results are bit-identical to the
- * dense call on the maps the lists describe.  The lists are expanded chunk by chunk into a
+ * dense call on the maps the lists describe.  For S <= 65,536 the lists are folded directly
+ * (rank + chain kernels, option "sparse_native" = 1, the default; the device-buffer call reads
+ * entry_off[n_exec] back once to size its scratch, i.e. it synchronises the stream before it
+ * enqueues); otherwise, or with "sparse_native" = 0, they are expanded chunk by chunk into a
  * context-owned, all-zero staging buffer (option "sparse_chunk" = execs per chunk, default
  * ~1.25 GB of records) which the K2 scan then streams.
  */
