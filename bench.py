@@ -391,7 +391,8 @@ def run_ours(args):
                       "on the device)"}
         del ent_t, off_t, ent_np, off_np
         # (b) dense records
-        if not args.no_e2e_dense:
+        # the dense form pins 10.7 GB of host memory per rank: single-rank runs only
+        if not args.no_e2e_dense and world == 1:
             pinned = torch.empty(n_e2e * REC, dtype=torch.uint8, pin_memory=True)
             pinned.copy_(raw[: n_e2e * REC])
             raw_host = pinned.numpy()
