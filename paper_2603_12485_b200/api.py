@@ -258,14 +258,22 @@ class Context:
         return raw
 
     # ---- K3 -----------------------------------------------------------------
-    def havoc_batch(self, in_bytes, in_off, rng_state, want_draws=True):
+    def havoc_batch(self, in_bytes, in_off, rng_state, want_draws=True, out=None):
         """Batched havoc_mutant.  in_off / rng_state are int64 device tensors (u64 bit
         patterns); rng_state is advanced in place.  Returns (out_bytes, out_off, out_len, draws):
-        slot j's mutant is out_bytes[out_off[j] : out_off[j] + out_len[j]]."""
+        slot j's mutant is out_bytes[out_off[j] : out_off[j] + out_len[j]].  `out` = the tuple a
+        previous call with the same in_off returned: its buffers are reused (no allocation, no
+        host synchronisation to size them)."""
         _dev(in_bytes, self.device, torch.uint8)
         _dev(in_off, self.device, torch.int64)
         _dev(rng_state, self.device, torch.int64)
         n = in_off.numel() - 1
+        if out is not None:
+            out_bytes, out_off, out_len, draws = out
+            self._sync_stream()
+            check(lib.hfz_havoc_batch(self._h, _ptr(in_bytes), _ptr(in_off), n, _ptr(rng_state),
+                                      _ptr(out_bytes), _ptr(out_off), _ptr(out_len), _ptr(draws)))
+            return out
         lens = in_off[1:] - in_off[:-1]
         caps = torch.clamp(lens + 1024, max=MAX_INPUT_BYTES)
         caps = (caps + 15) // 16 * 16  # keep every slot 16-byte aligned

@@ -27,13 +27,33 @@ __constant__ int16_t c_interesting16[10] = {-32768, -129, 128, 255, 256, 512, 10
 __constant__ int32_t c_interesting32[8] = {(-2147483647 - 1), -100663046, -32769, 32768,
                                            65535,             65536,      100663045, 2147483647};
 
+// The slot's splitmix64 stream, warp-uniform.  The state after k draws is seed + k * gamma
+// (rng.hpp:15-21), so the warp computes the next 32 outputs at once -- lane i mixes
+// s + (i + 1) * gamma -- and hands them out one per draw by shuffle: a draw costs two shuffles
+// instead of two 64-bit multiplies on every lane.  next() must be called by the whole warp.
 struct WarpRng {
-  uint64_t s;
+  uint64_t s;      // reference state: seed + draws * gamma
   uint32_t draws;
+  uint64_t buf;    // this lane's output of the current batch
+  uint32_t pos;    // next unread output of the batch; 32 = none left
+  uint32_t lane;
+  __device__ __forceinline__ void init(uint64_t state, int lane_) {
+    s = state;
+    draws = 0;
+    pos = 32;
+    lane = (uint32_t)lane_;
+    buf = 0;
+  }
   __device__ __forceinline__ uint64_t next() {
+    if (pos == 32) {
+      buf = hfz_sm64_mix(s + (uint64_t)(lane + 1) * HFZ_GAMMA);
+      pos = 0;
+    }
+    const uint64_t r = __shfl_sync(0xffffffffu, buf, (int)pos);
+    ++pos;
     s += HFZ_GAMMA;
     ++draws;
-    return hfz_sm64_mix(s);
+    return r;
   }
   // below(n): n <= 1 returns 0 WITHOUT drawing (rng.hpp:24-28)
   __device__ __forceinline__ uint64_t below(uint64_t n) {
@@ -272,8 +292,7 @@ __global__ void __launch_bounds__(kHavocWarps * 32) hfz_k_havoc(
     __syncwarp();
 
     WarpRng rng;
-    rng.s = state[j];
-    rng.draws = 0;
+    rng.init(state[j], lane);
     len = havoc_edit<false>(v, len, rng, lane);
     if (in_smem) {
       warp_copy(out, v, len, lane);
@@ -291,15 +310,17 @@ __global__ void __launch_bounds__(kHavocWarps * 32) hfz_k_havoc(
 // does (src/engine.cpp:561-562).  A dry run per slot yields the state each slot starts from.
 __global__ void hfz_k_havoc_plan(const uint64_t* __restrict__ in_off, uint64_t n,
                                  uint64_t* __restrict__ stream_state, uint64_t* __restrict__ slot_states) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;  // one warp: the draws are handed out by shuffle
+  const int lane = threadIdx.x;
   WarpRng rng;
-  rng.s = *stream_state;
-  rng.draws = 0;
+  rng.init(*stream_state, lane);
+  __syncwarp();
   for (uint64_t j = 0; j < n; ++j) {
-    slot_states[j] = rng.s;
-    havoc_edit<true>(nullptr, in_off[j + 1] - in_off[j], rng, 0);
+    if (lane == 0) slot_states[j] = rng.s;
+    havoc_edit<true>(nullptr, in_off[j + 1] - in_off[j], rng, lane);
   }
-  *stream_state = rng.s;
+  __syncwarp();
+  if (lane == 0) *stream_state = rng.s;
 }
 
 __global__ void __launch_bounds__(256) hfz_k_splice(
@@ -314,8 +335,7 @@ __global__ void __launch_bounds__(256) hfz_k_splice(
     const uint64_t a0 = in_off[a_idx[j]], alen = in_off[a_idx[j] + 1] - a0;
     const uint64_t b0 = in_off[b_idx[j]], blen = in_off[b_idx[j] + 1] - b0;
     WarpRng rng;
-    rng.s = state[j];
-    rng.draws = 0;
+    rng.init(state[j], lane);
     const uint64_t ca = rng.below(alen + 1);
     const uint64_t cb = rng.below(blen + 1);
     const uint64_t total = ca + (blen - cb);

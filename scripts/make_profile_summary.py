@@ -68,6 +68,7 @@ print(json.dumps({k: summary[k] for k in ("duration_s_under_ncu", "dram_bytes_pe
 EXTRA = {"scan_pipe": "scripts/probe_feedback.py --n 4096 --configs '' --reps 1 --sweep 4096 (-k regex:hfz_k_scan_pipe -s 2 -c 1)",
          "expand": "scripts/probe_sparse.py --execs 16384 --chunks 8192 (-k regex:hfz_k_expand -s 2 -c 2)",
          "edge": "scripts/probe_k1k3.py edge (-k regex:hfz_k_edge_record -c 1)",
+         "havoc": "scripts/probe_k1k3.py havoc (-k regex:hfz_k_havoc -s 2 -c 1)",
          "sparse": "scripts/probe_sparse.py --chunks 65536 (-k regex:hfz_k_sparse -s 6 -c 2: rank + chain of one 65,536-exec device call)"}
 for name, cmd in EXTRA.items():
     rp = os.path.join(ROOT, "gpurun_out", f"{rnd}_{name}.ncu-rep")

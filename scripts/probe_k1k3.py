@@ -24,9 +24,10 @@ if what in ("all", "havoc"):
     seeds = torch.from_numpy(api.u64_to_i64(np.arange(1000, 1000 + n, dtype=np.uint64))).to(dev)
     st = seeds.clone()
     res = {}
+    res["o"] = ctx.havoc_batch(d_in, d_off, st)  # sizes the output buffers once (host sync)
     def run():
         st.copy_(seeds)
-        res["o"] = ctx.havoc_batch(d_in, d_off, st)
+        res["o"] = ctx.havoc_batch(d_in, d_off, st, out=res["o"])  # the kernel alone
     ms = timeit(run)
     ob, oo, ol, dr = res["o"]
     tot = int(off[-1]) + int(ol.sum().item())
