@@ -73,6 +73,7 @@ struct hfz_ctx {
   uint64_t sp_cnt_cap = 0;
   // set by the last scan: the resolve step re-reads a candidate either from its dense record or
   // from its ordered list
+  bool sc_sparse = false;
   const uint32_t* sc_sorted = nullptr;
   const uint64_t* sc_off = nullptr;
   const uint32_t* sc_cnt = nullptr;

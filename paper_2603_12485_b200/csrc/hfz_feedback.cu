@@ -1118,7 +1118,7 @@ extern "C" int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t
   HFZ_CUDA(cudaSetDevice(ctx->device));
   int rc = ensure_cand(ctx, n_exec);
   if (rc) return rc;
-  ctx->sc_sorted = nullptr;  // the resolve step re-reads candidates from their dense records
+  ctx->sc_sparse = false;  // the resolve step re-reads candidates from their dense records
   HFZ_CUDA(cudaMemsetAsync(ctx->first, 0xff, (size_t)ctx->S * 8 * sizeof(uint32_t), ctx->stream));
   HFZ_CUDA(cudaMemsetAsync(ctx->cand_count, 0, 2 * sizeof(uint32_t), ctx->stream));
   if (classed_out && n_exec)
@@ -1232,6 +1232,7 @@ int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t
   hfz_k_delta<<<(ctx->S + 255) / 256, 256, 0, ctx->stream>>>(ctx->first, delta_out, ctx->S);
   ++ctx->launches;
   HFZ_CUDA(cudaGetLastError());
+  ctx->sc_sparse = true;
   ctx->sc_sorted = ctx->sp_sorted;
   ctx->sc_off = entry_off;
   ctx->sc_cnt = ctx->sp_cnt;
@@ -1258,7 +1259,7 @@ extern "C" int hfz_feedback_resolve(hfz_ctx* ctx, const uint8_t* raw_maps, uint6
                                     const uint8_t* deltas, uint32_t n_ranks, uint32_t rank,
                                     uint8_t* admit_out) {
   if (!ctx || !virgin_inout || !edge_counts_inout || !deltas || n_ranks == 0 || rank >= n_ranks ||
-      (n_exec && ((!raw_maps && !ctx->sc_sorted) || !admit_out))) {
+      (n_exec && ((!raw_maps && !ctx->sc_sparse) || !admit_out))) {
     hfz_set_error("hfz_feedback_resolve: bad argument");
     return HFZ_EINVAL;
   }
@@ -1287,7 +1288,7 @@ extern "C" int hfz_feedback_resolve(hfz_ctx* ctx, const uint8_t* raw_maps, uint6
     hfz_k_resolve_fast<<<(uint32_t)ctx->num_sms * 2, 256, 0, ctx->stream>>>(p);
     ++ctx->launches;
     HFZ_CUDA(cudaGetLastError());
-    if (ctx->sc_sorted) {
+    if (ctx->sc_sparse) {
       hfz_k_resolve_sparse<<<(uint32_t)ctx->num_sms * 4, 256, 0, ctx->stream>>>(p, ctx->sc_sorted, ctx->sc_off,
                                                                                   ctx->sc_cnt);
     } else {

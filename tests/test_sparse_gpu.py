@@ -200,3 +200,39 @@ def test_sparse_repeated_pairs_with_equal_counts(sctx, checker):
     c = np.zeros(2, np.uint64)
     got = sctx.feedback_batch_sparse_host(entries2, np.array(new_off, np.uint64), v, c, want_classed=True)
     check_host(sctx, got, v, c, cpu(checker, raw, n))
+
+
+@pytest.mark.parametrize("S_small", [1024, 4096, 32768])
+@pytest.mark.parametrize("native", [1, 0])
+def test_small_map_sizes(port, S_small, native):
+    """Map sizes below the reference's 65,536 (run-time parameter of the C restatement): the
+    bitmap / prefix geometry of the rank kernel and the dense kernels' row walk must adapt."""
+    c2 = hfz.Context(0, S_small)
+    c2.set_option("sparse_native", native)
+    try:
+        n = 90
+        raw = synth.maps_iid(n, S_small, density=0.05, seed=61)
+        entries, off = synth.to_sparse(raw, n, S_small, shuffle_seed=8)
+        v, c = np.zeros(S_small, np.uint8), np.zeros(2, np.uint64)
+        got = c2.feedback_batch_sparse_host(entries, off, v, c, want_classed=True)
+        wv, wc = np.zeros(S_small, np.uint8), np.zeros(2, np.uint64)
+        want = port.feedback_batch(raw, n, S_small, wv, wc, want_classed=True)
+        for k in want:
+            assert np.array_equal(got[k], want[k]), k
+        assert np.array_equal(v, wv) and np.array_equal(c, wc)
+        # and the dense host path on the same maps
+        v2, c3 = np.zeros(S_small, np.uint8), np.zeros(2, np.uint64)
+        got2 = c2.feedback_batch_host(raw, v2, c3)
+        assert np.array_equal(got2["admit"], want["admit"]) and np.array_equal(got2["sig_full"], want["sig_full"])
+        assert np.array_equal(v2, wv)
+    finally:
+        c2.close()
+
+
+def test_sparse_empty_batch_and_all_empty_lists(sctx):
+    v, c = np.zeros(S, np.uint8), np.zeros(2, np.uint64)
+    got = sctx.feedback_batch_sparse_host(np.zeros((0, 2), np.uint32), np.zeros(1, np.uint64), v, c)
+    assert got["admit"].size == 0 and not v.any()
+    got = sctx.feedback_batch_sparse_host(np.zeros((0, 2), np.uint32), np.zeros(6, np.uint64), v, c)
+    assert got["admit"].tolist() == [0] * 5 and got["nnz"].tolist() == [0] * 5
+    assert all(int(x) == 14695981039346656037 for x in got["sig_full"]) and not v.any() and not c.any()
