@@ -108,6 +108,8 @@ extern "C" int hfz_ctx_destroy(hfz_ctx* c) {
   cudaFree(c->sp_entries);
   cudaFree(c->sp_off);
   cudaFree(c->sp_sorted);
+  cudaFree(c->ts_sorted);
+  cudaFree(c->ts_cnt);
   cudaFree(c->sp_cnt);
   for (cudaEvent_t ev : c->sp_events) cudaEventDestroy(ev);
   delete c;
@@ -146,6 +148,8 @@ extern "C" int hfz_ctx_set_option(hfz_ctx* c, const char* key, int64_t value) {
     c->scan_small = value;
   } else if (!strcmp(key, "scan_pipe")) {
     c->scan_pipe = value;
+  } else if (!strcmp(key, "scan_two_stage")) {
+    c->scan_two_stage = value;
   } else if (!strcmp(key, "time_scan")) {
     c->time_scan = value != 0;
   } else if (!strcmp(key, "sparse_native")) {

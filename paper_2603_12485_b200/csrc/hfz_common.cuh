@@ -86,6 +86,11 @@ struct hfz_ctx {
   int time_scan = 0;      // bracket scan launches with events (bench roofline)
   int64_t scan_small = -1; // batches up to this many execs use the warp-per-map kernel (-1 = auto)
   int64_t scan_pipe = -1;  // batches of up to this many 32-map groups per SM use the pipelined kernel (-1 = auto)
+  int64_t scan_two_stage = -1;  // batches of up to this many execs use compact + chain (-1 = auto, 0 = off)
+  uint32_t* ts_sorted = nullptr;  // two-stage scratch: [n_exec][S] entries (only the used prefix of each piece is touched)
+  uint64_t ts_sorted_cap = 0;     // entries
+  uint32_t* ts_cnt = nullptr;     // [n_exec][pieces] entries per piece, then [n_exec] novel-slot counters
+  uint64_t ts_cnt_cap = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> scan_events;
 };
 

@@ -909,6 +909,35 @@ __global__ void __launch_bounds__(kRankWarps * 32, 1) hfz_k_sparse_rank(const Sp
   if (lane == 0 && nbad && p.bad) atomicAdd(p.bad, (unsigned long long)nbad);
 }
 
+// Both FNV chains over `n` ordered entries (slot | rung << 24).  The next four entries are
+// loaded BEFORE the chains of the current four run, so their latency (the lists usually sit in
+// L2) hides behind the dependent multiplies.
+__device__ __forceinline__ void chain_list(const uint32_t* __restrict__ list, uint32_t n, uint64_t& hf, uint64_t& hs) {
+  auto step = [&](uint32_t en) {
+    const uint32_t b0 = en & 0xffu, b1 = (en >> 8) & 0xffu;
+    hf = hfz_fnv(hfz_fnv(hfz_fnv(hf, b0), b1), 1u << (en >> 24));
+    hs = hfz_fnv(hfz_fnv(hs, b0), b1);
+  };
+  uint32_t cur[4], nxt[4];
+  uint32_t i = 0;
+  if (n >= 4) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cur[k] = __ldg(list + k);
+    for (; i + 8 <= n; i += 4) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) nxt[k] = __ldg(list + i + 4 + k);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) step(cur[k]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cur[k] = nxt[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) step(cur[k]);
+    i += 4;
+  }
+  for (; i < n; ++i) step(__ldg(list + i));
+}
+
 __global__ void __launch_bounds__(128) hfz_k_sparse_chain(const uint32_t* __restrict__ sorted,
                                                           const uint64_t* __restrict__ off,
                                                           const uint32_t* __restrict__ cnt, uint64_t n_exec,
@@ -920,27 +949,143 @@ __global__ void __launch_bounds__(128) hfz_k_sparse_chain(const uint32_t* __rest
   const uint32_t* list = sorted + off[e];
   const uint32_t n = cnt[e];
   uint64_t hf = HFZ_FNV_OFFSET, hs = HFZ_FNV_OFFSET;
-  uint32_t i = 0;
-  for (; i + 4 <= n; i += 4) {  // the four loads are independent of the chains
-    uint32_t en[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) en[k] = __ldg(list + i + k);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t b0 = en[k] & 0xffu, b1 = (en[k] >> 8) & 0xffu;
-      hf = hfz_fnv(hfz_fnv(hfz_fnv(hf, b0), b1), 1u << (en[k] >> 24));
-      hs = hfz_fnv(hfz_fnv(hs, b0), b1);
-    }
-  }
-  for (; i < n; ++i) {
-    const uint32_t en = __ldg(list + i);
-    const uint32_t b0 = en & 0xffu, b1 = (en >> 8) & 0xffu;
-    hf = hfz_fnv(hfz_fnv(hfz_fnv(hf, b0), b1), 1u << (en >> 24));
-    hs = hfz_fnv(hfz_fnv(hs, b0), b1);
-  }
+  chain_list(list, n, hf, hs);
   sig_full[e] = hf;
   sig_simple[e] = hs;
   if (nnz_out) nnz_out[e] = n;
+}
+
+// ---------------------------------------------------------------------------
+// Two-stage scan of DENSE records for small and medium batches ("compact + chain").
+//   compact  work item = (map, 16 KB piece of its record), one warp each: the piece is streamed
+//            coalesced (4 x 128-bit loads in flight per lane), the non-zero slots are compacted IN
+//            ORDER (warp scan of the per-lane element counts) as `slot | rung << 24` into the
+//            piece's own slot range of a scratch list [n_exec][S] -- no offsets to compute, only
+//            the used prefix of a range is ever touched; classification, the virgin test and the
+//            first-occurrence update ride along;
+//   chain    one lane per map walks its pieces' lists and runs both FNV chains.
+// Nothing is row-synchronous and every warp of the grid has work from the first microsecond, so
+// a batch costs its HBM time plus one map's chain (~50 us) instead of rows x row latency.
+constexpr uint32_t kTsPiece = 16384;  // bytes per piece (divides H and 4H for H >= 16,384; halved otherwise)
+
+struct CompactParams {
+  const uint8_t* raw;
+  uint64_t n_exec, rec_bytes;
+  uint32_t S, H, piece, host_pieces, pieces;
+  const uint8_t* v0;
+  uint32_t* first;
+  uint32_t* novel_ent;
+  uint32_t* sorted;   // [n_exec][S]
+  uint32_t* cnt;      // [n_exec][pieces]
+  uint32_t* nov_cnt;  // [n_exec]
+  uint8_t* classed;
+};
+
+__global__ void __launch_bounds__(256) hfz_k_compact(const CompactParams p) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t items = p.n_exec * p.pieces;
+  const uint32_t lane_lt = (1u << lane) - 1u;
+  (void)lane_lt;
+  for (uint64_t it = warp; it < items; it += nwarps) {
+    const uint64_t e64 = it / p.pieces;
+    const uint32_t pc = (uint32_t)(it - e64 * p.pieces), e = (uint32_t)e64;
+    const bool host = pc < p.host_pieces;
+    const uint32_t slot0 = host ? pc * p.piece : p.H + (pc - p.host_pieces) * (p.piece / 4);
+    const uint4* src = reinterpret_cast<const uint4*>(p.raw + e64 * p.rec_bytes + (uint64_t)pc * p.piece);
+    uint32_t* out = p.sorted + e64 * p.S + slot0;
+    uint8_t* classed_row = p.classed ? p.classed + e64 * p.S : nullptr;
+    uint32_t fill = 0;
+    const uint32_t vecs = p.piece / 16;
+    for (uint32_t v0 = 0; v0 < vecs; v0 += 128) {
+      uint4 x[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t v = v0 + j * 32 + lane;
+        x[j] = v < vecs ? hfz_ldg_stream(src + v) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t w[4] = {x[j].x, x[j].y, x[j].z, x[j].w};
+        // element mask of this lane's vector: 16 bits (host bytes) or 4 bits (device words)
+        uint32_t m;
+        if (host)
+          m = nz_bytes(w[0]) | (nz_bytes(w[1]) << 4) | (nz_bytes(w[2]) << 8) | (nz_bytes(w[3]) << 12);
+        else
+          m = (w[0] != 0u) | ((w[1] != 0u) << 1) | ((w[2] != 0u) << 2) | ((w[3] != 0u) << 3);
+        if (!__any_sync(0xffffffffu, m != 0u)) continue;
+        const uint32_t c = __popc(m);
+        uint32_t inc = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+          if (lane >= d) inc += o;
+        }
+        uint32_t pos = fill + inc - c;
+        fill += __shfl_sync(0xffffffffu, inc, 31);
+        const uint32_t v = v0 + j * 32 + lane;
+        while (m) {
+          const uint32_t b = __ffs(m) - 1;
+          m &= m - 1;
+          uint32_t idx, klass;
+          // word b >> 2 (host) / b (device) of the vector, by selects (no local-memory indexing)
+          const uint32_t wi = host ? (b >> 2) : b;
+          const uint32_t word = wi == 0 ? w[0] : (wi == 1 ? w[1] : (wi == 2 ? w[2] : w[3]));
+          if (host) {
+            idx = slot0 + v * 16 + b;
+            klass = hfz_class_host((word >> (8 * (b & 3))) & 0xffu);
+          } else {
+            idx = slot0 + v * 4 + b;
+            klass = hfz_class_device(word);
+          }
+          const uint32_t rung = 31 - __clz(klass);
+          const uint32_t en = idx | (rung << 24);
+          out[pos++] = en;
+          if (klass & ~(uint32_t)__ldg(p.v0 + idx)) {
+            const uint32_t k = atomicAdd(p.nov_cnt + e64, 1u);
+            if (k < kNovMax) p.novel_ent[e64 * kNovMax + k] = en;
+            atomicMin(p.first + (size_t)idx * 8 + rung, e);
+          }
+          if (classed_row) classed_row[idx] = (uint8_t)klass;
+        }
+      }
+    }
+    if (lane == 0) p.cnt[it] = fill;
+  }
+}
+
+// one lane per map: chains over the map's piece lists, nnz, candidate bookkeeping
+__global__ void __launch_bounds__(128) hfz_k_chain_pieces(const CompactParams p, uint32_t* __restrict__ cand_list,
+                                                          uint32_t* __restrict__ cand_count,
+                                                          uint32_t* __restrict__ cand_flags,
+                                                          uint32_t* __restrict__ cand_nov,
+                                                          uint32_t* __restrict__ slow_list,
+                                                          uint64_t* __restrict__ sig_full,
+                                                          uint64_t* __restrict__ sig_simple,
+                                                          uint32_t* __restrict__ nnz_out) {
+  const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= p.n_exec) return;
+  uint64_t hf = HFZ_FNV_OFFSET, hs = HFZ_FNV_OFFSET;
+  uint32_t nnz = 0;
+  for (uint32_t pc = 0; pc < p.pieces; ++pc) {
+    const uint32_t slot0 = pc < p.host_pieces ? pc * p.piece : p.H + (pc - p.host_pieces) * (p.piece / 4);
+    const uint32_t* list = p.sorted + e * p.S + slot0;
+    const uint32_t n = p.cnt[e * p.pieces + pc];
+    nnz += n;
+    chain_list(list, n, hf, hs);
+  }
+  sig_full[e] = hf;
+  sig_simple[e] = hs;
+  if (nnz_out) nnz_out[e] = nnz;
+  const uint32_t novel = p.nov_cnt[e];
+  if (novel) {
+    const uint32_t ci = atomicAdd(cand_count, 1u);
+    cand_list[ci] = (uint32_t)e;
+    cand_flags[ci] = 0;
+    cand_nov[ci] = novel <= kNovMax ? novel : kNovMax + 1;
+    if (novel > kNovMax) slow_list[atomicAdd(cand_count + 1, 1u)] = ci;
+  }
 }
 
 // resolve of the candidates with more than kNovMax novel slots, from their ordered lists
@@ -1048,12 +1193,75 @@ int launch_scan_pipe_r(hfz_ctx* ctx, const ScanParams& p, int row) {
                  : launch_scan_pipe_t<REC_CT, 512, VSMEM, false>(ctx, p);
 }
 
+// compact + chain for a dense batch; false when the scratch it would need is not allowed
+bool two_stage_fits(const hfz_ctx* ctx, uint64_t n_exec) {
+  return n_exec * (uint64_t)ctx->S <= (1ull << 30);  // <= 4 GB of u32 entries
+}
+
+int launch_scan_two_stage(hfz_ctx* ctx, const ScanParams& sp) {
+  CompactParams p;
+  p.raw = sp.raw;
+  p.n_exec = sp.n_exec;
+  p.rec_bytes = sp.rec_bytes;
+  p.S = sp.S;
+  p.H = sp.H;
+  uint32_t piece = kTsPiece;
+  while (sp.H % piece) piece >>= 1;  // H is a power of two >= 512
+  p.piece = piece;
+  p.host_pieces = sp.H / piece;
+  p.pieces = (uint32_t)(sp.rec_bytes / piece);
+  p.v0 = sp.v0;
+  p.first = sp.first;
+  p.novel_ent = sp.novel_ent;
+  p.classed = sp.classed;
+  const uint64_t need = sp.n_exec * (uint64_t)sp.S;
+  if (ctx->ts_sorted_cap < need) {
+    cudaFree(ctx->ts_sorted);
+    ctx->ts_sorted = nullptr;
+    ctx->ts_sorted_cap = 0;
+    cudaError_t e = cudaMalloc(&ctx->ts_sorted, need * 4);
+    if (e != cudaSuccess) {
+      hfz_set_error("two-stage scan: cudaMalloc of %llu scratch bytes failed (%s)", (unsigned long long)need * 4,
+                    cudaGetErrorString(e));
+      return HFZ_ENOMEM;
+    }
+    ctx->ts_sorted_cap = need;
+  }
+  const uint64_t need_cnt = sp.n_exec * (uint64_t)(p.pieces + 1);
+  if (ctx->ts_cnt_cap < need_cnt) {
+    cudaFree(ctx->ts_cnt);
+    ctx->ts_cnt = nullptr;
+    ctx->ts_cnt_cap = 0;
+    HFZ_CUDA(cudaMalloc(&ctx->ts_cnt, (need_cnt + 1024) * 4));
+    ctx->ts_cnt_cap = need_cnt + 1024;
+  }
+  p.sorted = ctx->ts_sorted;
+  p.cnt = ctx->ts_cnt;
+  p.nov_cnt = ctx->ts_cnt + sp.n_exec * (uint64_t)p.pieces;
+  HFZ_CUDA(cudaMemsetAsync(p.nov_cnt, 0, sp.n_exec * 4, ctx->stream));
+  const uint64_t items = sp.n_exec * p.pieces;
+  uint64_t blocks = (items + 7) / 8;
+  const uint64_t cap = (uint64_t)ctx->num_sms * 8;  // 64 warps per SM
+  if (blocks > cap) blocks = cap;
+  hfz_k_compact<<<(uint32_t)blocks, 256, 0, ctx->stream>>>(p);
+  ++ctx->launches;
+  HFZ_CUDA(cudaGetLastError());
+  hfz_k_chain_pieces<<<(uint32_t)((sp.n_exec + 127) / 128), 128, 0, ctx->stream>>>(
+      p, sp.cand_list, sp.cand_count, sp.cand_flags, sp.cand_nov, sp.slow_list, sp.sig_full, sp.sig_simple, sp.nnz);
+  ++ctx->launches;
+  HFZ_CUDA(cudaGetLastError());
+  return HFZ_OK;
+}
+
 int launch_scan(hfz_ctx* ctx, const ScanParams& p) {
   // virgin copy in shared memory whenever it leaves room for the per-warp slots
   const bool vsmem = ctx->virgin_smem && p.S <= 65536u;
   // small batches: one warp per map (latency), else 32 maps per warp (pipelined, then throughput)
   const uint64_t small_limit = ctx->scan_small >= 0 ? (uint64_t)ctx->scan_small
                                                     : (uint64_t)ctx->num_sms * 10 * 65536u / p.S;
+  // small and medium batches: compact + chain (two-stage)
+  const uint64_t ts_limit = ctx->scan_two_stage >= 0 ? (uint64_t)ctx->scan_two_stage : 3072;
+  if (p.n_exec <= ts_limit && two_stage_fits(ctx, p.n_exec)) return launch_scan_two_stage(ctx, p);
   if (p.n_exec <= small_limit) {
     const bool classed = p.classed != nullptr;
     if (vsmem) return classed ? launch_scan_wpm_t<true, true>(ctx, p) : launch_scan_wpm_t<true, false>(ctx, p);

@@ -74,9 +74,11 @@ if a.ns:
         print(f"n={n:7d}: {ms:8.3f} ms  {n/ms*1e3/1e6:7.3f} M evals/s  {n*rec/ms/1e6:8.1f} GB/s ({n*rec/ms/1e6/6544.7*100:4.1f}%)", flush=True)
 
 if a.sweep:
-    KERN = {"lane": dict(scan_small=0, scan_pipe=0), "wpm": dict(scan_small=1 << 40, scan_pipe=0),
-            "pipe512": dict(scan_small=0, scan_pipe=1 << 20, scan_row=512),
-            "pipe256": dict(scan_small=0, scan_pipe=1 << 20, scan_row=256), "auto": dict(scan_small=-1, scan_pipe=-1)}
+    KERN = {"lane": dict(scan_small=0, scan_pipe=0, scan_two_stage=0), "wpm": dict(scan_small=1 << 40, scan_pipe=0, scan_two_stage=0),
+            "pipe512": dict(scan_small=0, scan_pipe=1 << 20, scan_row=512, scan_two_stage=0),
+            "pipe256": dict(scan_small=0, scan_pipe=1 << 20, scan_row=256, scan_two_stage=0),
+            "two": dict(scan_small=0, scan_pipe=0, scan_two_stage=1 << 40),
+            "auto": dict(scan_small=-1, scan_pipe=-1, scan_two_stage=-1)}
     for n in [int(x) for x in a.sweep.split(",")]:
         sub = raw[: n * rec]
         line = f"n={n:7d} ideal {n*rec/6544.7e6:6.3f} ms |"

@@ -14,24 +14,30 @@ pytestmark = pytest.mark.gpu
 S = 65536
 
 
-KERNEL_OPTS = {  # (scan_small, scan_pipe): force one of the three scan kernels
-    "lane_per_map": (0, 0),
-    "warp_per_map": (1 << 40, 0),
-    "pipelined": (0, 1 << 20),
+KERNEL_OPTS = {  # (scan_small, scan_pipe, scan_two_stage): force one of the four scan kernels
+    "lane_per_map": (0, 0, 0),
+    "warp_per_map": (1 << 40, 0, 0),
+    "pipelined": (0, 1 << 20, 0),
+    "two_stage": (0, 0, 1 << 40),
 }
+
+
+def force_kernel(c, name):
+    small, pipe, two = KERNEL_OPTS[name]
+    c.set_option("scan_small", small)
+    c.set_option("scan_pipe", pipe)
+    c.set_option("scan_two_stage", two)
 
 
 @pytest.fixture(autouse=True, params=list(KERNEL_OPTS))
 def scan_kernel(request, ctx):
-    """Every test runs against all three scan kernels: the throughput kernel (32 maps per warp),
-    the small-batch kernel (one warp per map) and the medium-batch kernel (producer warps + one
-    consumer warp per 32 maps); by default the library picks by batch size."""
-    small, pipe = KERNEL_OPTS[request.param]
-    ctx.set_option("scan_small", small)
-    ctx.set_option("scan_pipe", pipe)
+    """Every test runs against all four scan kernels: the throughput kernel (32 maps per warp),
+    the warp-per-map kernel, the pipelined kernel (producer warps + one consumer warp per 32 maps)
+    and the two-stage path (compact + chain); by default the library picks by batch size."""
+    force_kernel(ctx, request.param)
     yield request.param
-    ctx.set_option("scan_small", -1)
-    ctx.set_option("scan_pipe", -1)
+    for k in ("scan_small", "scan_pipe", "scan_two_stage"):
+        ctx.set_option(k, -1)
 
 
 def run_gpu(ctx, raw, virgin0=None, counts0=None, want_classed=True):
@@ -182,9 +188,7 @@ def test_sharded_scan_resolve_equals_sequential(ctx, checker, scan_kernel):
     ctxs = [hfz.Context(0) for _ in range(R)]
     for i, c in enumerate(ctxs):
         # mix the kernels across the simulated ranks
-        small, pipe = KERNEL_OPTS[list(KERNEL_OPTS)[(i + list(KERNEL_OPTS).index(scan_kernel)) % 3]]
-        c.set_option("scan_small", small)
-        c.set_option("scan_pipe", pipe)
+        force_kernel(c, list(KERNEL_OPTS)[(i + list(KERNEL_OPTS).index(scan_kernel)) % len(KERNEL_OPTS)])
     try:
         scans = [ctxs[r].feedback_scan(shards[r], d_v0) for r in range(R)]
         deltas = torch.cat([s["delta"] for s in scans])
@@ -238,8 +242,7 @@ def test_large_map_262144(checker, scan_kernel):
     S2 = 262144
     ck = pyoracle.Ref(S2) if pyoracle.Ref.available(S2) else pyoracle.Port()
     c2 = hfz.Context(0, S2)
-    c2.set_option("scan_small", KERNEL_OPTS[scan_kernel][0])
-    c2.set_option("scan_pipe", KERNEL_OPTS[scan_kernel][1])
+    force_kernel(c2, scan_kernel)
     try:
         raw = synth.maps_iid(48, S2, density=0.01, seed=3)
         g = run_gpu(c2, raw)
