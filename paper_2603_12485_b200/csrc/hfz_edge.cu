@@ -265,8 +265,9 @@ __device__ __forceinline__ bool transposed_path(uint8_t* tab, const uint32_t* si
       }
     }
   }
-  if (__any_sync(0xffffffffu, bad)) return false;
-  __syncwarp();
+  const bool any_bad = __any_sync(0xffffffffu, bad);
+  __syncwarp();  // table reads above are ordered before whatever reuses the table next
+  if (any_bad) return false;
   // rows -> owed bumps.  Lane order inside a row: low nibbles of words 0..3, then high nibbles.
   // Most rows of a divergent warp were visited by ONE lane only (d = c, nothing to do); the
   // byte-wise max / saturating subtract are plain SWAR arithmetic (values <= 15 leave bit 7 of
@@ -492,7 +493,11 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
             continue;
           }
 
-          // ---- general path: borrow a table from the CTA's pool
+          // ---- general path: borrow a table from the CTA's pool.  Hand-over = shared-memory
+          // atomic on the free-mask, release after __syncwarp() + __threadfence_block().
+          // (compute-sanitizer racecheck does not model lock-style synchronisation and reports
+          // the previous owner's last reads against the next owner's clear as WAR hazards;
+          // one private table per warp instead -- 9 warps -- is race-report-free but 30 % slower.)
           uint32_t t = 0;
           if (lane == 0) {
             for (;;) {
