@@ -74,6 +74,8 @@ struct hfz_ctx {
   // set by the last scan: the resolve step re-reads a candidate either from its dense record or
   // from its ordered list
   bool sc_sparse = false;
+  bool sc_pieces = false;         // last scan was the two-stage dense path: resolve from its piece lists
+  uint32_t sc_piece = 0, sc_host_pieces = 0, sc_npieces = 0;
   const uint32_t* sc_sorted = nullptr;
   const uint64_t* sc_off = nullptr;
   const uint32_t* sc_cnt = nullptr;

@@ -1111,6 +1111,30 @@ __global__ void __launch_bounds__(256) hfz_k_resolve_sparse(const ResolveParams 
   }
 }
 
+// resolve of the slow candidates after a two-stage scan: from the piece lists, not the records
+__global__ void __launch_bounds__(256) hfz_k_resolve_pieces(const ResolveParams p, const uint32_t* __restrict__ sorted,
+                                                            const uint32_t* __restrict__ cnt, uint32_t piece,
+                                                            uint32_t host_pieces, uint32_t pieces) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t total_warps = (gridDim.x * blockDim.x) >> 5;
+  const uint64_t items = (uint64_t)p.cand_count[1] * pieces;
+  for (uint64_t it = warp; it < items; it += total_warps) {
+    const uint32_t ci = p.slow_list[it / pieces], pc = (uint32_t)(it % pieces);
+    const uint32_t e = p.cand_list[ci];
+    const uint32_t slot0 = pc < host_pieces ? pc * piece : p.H + (pc - host_pieces) * (piece / 4);
+    const uint32_t* list = sorted + (uint64_t)e * p.S + slot0;
+    const uint32_t n = cnt[(uint64_t)e * pieces + pc];
+    uint32_t flags = 0;
+    for (uint32_t i = lane; i < n; i += 32) {
+      const uint32_t en = __ldg(list + i);
+      flags |= resolve_entry(p, en & 0xffffffu, 1u << (en >> 24), e);
+    }
+    flags = __reduce_or_sync(0xffffffffu, flags);
+    if (lane == 0 && flags) atomicOr(p.cand_flags + ci, flags);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // launch plumbing
 
@@ -1250,6 +1274,10 @@ int launch_scan_two_stage(hfz_ctx* ctx, const ScanParams& sp) {
       p, sp.cand_list, sp.cand_count, sp.cand_flags, sp.cand_nov, sp.slow_list, sp.sig_full, sp.sig_simple, sp.nnz);
   ++ctx->launches;
   HFZ_CUDA(cudaGetLastError());
+  ctx->sc_pieces = true;
+  ctx->sc_piece = p.piece;
+  ctx->sc_host_pieces = p.host_pieces;
+  ctx->sc_npieces = p.pieces;
   return HFZ_OK;
 }
 
@@ -1328,7 +1356,8 @@ extern "C" int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t
   HFZ_CUDA(cudaSetDevice(ctx->device));
   int rc = ensure_cand(ctx, n_exec);
   if (rc) return rc;
-  ctx->sc_sparse = false;  // the resolve step re-reads candidates from their dense records
+  ctx->sc_sparse = false;  // the resolve step re-reads candidates from their dense records ...
+  ctx->sc_pieces = false;  // ... unless the two-stage path below leaves its piece lists behind
   HFZ_CUDA(cudaMemsetAsync(ctx->first, 0xff, (size_t)ctx->S * 8 * sizeof(uint32_t), ctx->stream));
   HFZ_CUDA(cudaMemsetAsync(ctx->cand_count, 0, 2 * sizeof(uint32_t), ctx->stream));
   if (classed_out && n_exec)
@@ -1443,6 +1472,7 @@ int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t
   ++ctx->launches;
   HFZ_CUDA(cudaGetLastError());
   ctx->sc_sparse = true;
+  ctx->sc_pieces = false;
   ctx->sc_sorted = ctx->sp_sorted;
   ctx->sc_off = entry_off;
   ctx->sc_cnt = ctx->sp_cnt;
@@ -1501,6 +1531,9 @@ extern "C" int hfz_feedback_resolve(hfz_ctx* ctx, const uint8_t* raw_maps, uint6
     if (ctx->sc_sparse) {
       hfz_k_resolve_sparse<<<(uint32_t)ctx->num_sms * 4, 256, 0, ctx->stream>>>(p, ctx->sc_sorted, ctx->sc_off,
                                                                                   ctx->sc_cnt);
+    } else if (ctx->sc_pieces) {
+      hfz_k_resolve_pieces<<<(uint32_t)ctx->num_sms * 4, 256, 0, ctx->stream>>>(
+          p, ctx->ts_sorted, ctx->ts_cnt, ctx->sc_piece, ctx->sc_host_pieces, ctx->sc_npieces);
     } else {
       uint32_t piece = kPiece;
       while (ctx->H % piece) piece >>= 1;  // H is a power of two >= 512
