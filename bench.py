@@ -222,6 +222,26 @@ def sparse_lists_from_device(raw, n, dev):
     return ent, off
 
 
+def compact_lists(ent, off):
+    """8-byte pairs -> the 4-byte list form: compact words slot | count << 16 for counts below
+    65,536 plus wide pairs for the rest (pinned host tensors; data preparation)."""
+    import torch
+    n = off.numel() - 1
+    rows = torch.repeat_interleave(torch.arange(n), off[1:] - off[:-1])
+    cnt = ent[:, 1]
+    big = (cnt < 0) | (cnt >= 65536)          # int32 view of u32 counts
+    small = ~big
+    comp = torch.empty(int(small.sum()), dtype=torch.int32, pin_memory=True)
+    comp.copy_(ent[small, 0] | (ent[small, 1] << 16))
+    wide = torch.empty((int(big.sum()), 2), dtype=torch.int32, pin_memory=True)
+    wide.copy_(ent[big])
+    coff = torch.zeros(n + 1, dtype=torch.int64, pin_memory=True)
+    woff = torch.zeros(n + 1, dtype=torch.int64, pin_memory=True)
+    coff[1:] = torch.cumsum(torch.bincount(rows[small], minlength=n), 0)
+    woff[1:] = torch.cumsum(torch.bincount(rows[big], minlength=n), 0)
+    return comp, coff, wide, woff
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -346,10 +366,12 @@ def run_ours(args):
     admits = int((out["admit"] != 0).sum().item())
 
     # --- end-to-end through the C-ABI with HOST buffers (pinned), copies inside the timed region.
-    # Two host forms of the same batch: (a) touched-slot lists (slot, count) -- what
-    # hetfuzz::b200::SparseBatch keeps per CoverageMap -- through hfz_feedback_batch_sparse_host;
-    # (b) dense 163,840-byte records through hfz_feedback_batch_host (PCIe-bound).
+    # Host forms of the same batch: (a) touched-slot lists -- what hetfuzz::b200::CompactBatch /
+    # SparseBatch keep per CoverageMap -- at 4 bytes per pair (hfz_feedback_batch_compact_host) and at
+    # 8 bytes per pair (hfz_feedback_batch_sparse_host); (b) dense 163,840-byte records through
+    # hfz_feedback_batch_host (PCIe-bound).
     e2e = None
+    e2e_pairs = None
     e2e_dense = None
     if not args.no_e2e:
         n_e2e = args.e2e_execs or n
@@ -371,25 +393,45 @@ def run_ours(args):
                 dist.all_reduce(te, op=dist.ReduceOp.MAX)
             return float(te.item()), res
 
-        # (a) sparse lists, built outside the timed region from the same maps
+        # (a) touched-slot lists, built outside the timed region from the same maps
         ent_t, off_t = sparse_lists_from_device(raw, n_e2e, dev)
         ent_np, off_np = ent_t.numpy().view(np.uint32), off_t.numpy().view(np.uint64)
-        sec, res = timed(lambda vh, ch: ctx.feedback_batch_sparse_host(ent_np, off_np, vh, ch))
-        same = bool(np.array_equal(res["admit"], out["admit"][:n_e2e].cpu().numpy())
-                    and np.array_equal(res["sig_full"], out["sig_full"][:n_e2e].cpu().numpy().view(np.uint64))
-                    and np.array_equal(res["sig_simple"], out["sig_simple"][:n_e2e].cpu().numpy().view(np.uint64)))
+
+        def same_as_device_fold(res):
+            return bool(np.array_equal(res["admit"], out["admit"][:n_e2e].cpu().numpy())
+                        and np.array_equal(res["sig_full"], out["sig_full"][:n_e2e].cpu().numpy().view(np.uint64))
+                        and np.array_equal(res["sig_simple"], out["sig_simple"][:n_e2e].cpu().numpy().view(np.uint64)))
+
+        # (a1) 4 bytes per pair: compact words + wide pairs for counts >= 65,536
+        comp_t, coff_t, wide_t, woff_t = compact_lists(ent_t, off_t)
+        comp_np, coff_np = comp_t.numpy().view(np.uint32), coff_t.numpy().view(np.uint64)
+        wide_np, woff_np = wide_t.numpy().view(np.uint32), woff_t.numpy().view(np.uint64)
+        sec, res = timed(lambda vh, ch: ctx.feedback_batch_compact_host(comp_np, coff_np, wide_np, woff_np, vh, ch))
+        same = same_as_device_fold(res)
         if not same:
-            raise SystemExit("bench.py: sparse e2e results differ from the device-resident dense fold")
+            raise SystemExit("bench.py: compact-list e2e results differ from the device-resident dense fold")
         e2e = {"value": world * n_e2e / sec, "unit": UNIT,
-               "h2d_bytes_per_step": int(ent_np.nbytes + off_np.nbytes + S + 16),
+               "h2d_bytes_per_step": int(comp_np.nbytes + coff_np.nbytes + wide_np.nbytes + woff_np.nbytes + S + 16),
                "d2h_bytes_per_step": int(n_e2e * (1 + 8 + 8 + 4) + S + 16 + 8),
-               "execs_per_step": n_e2e, "host_form": "touched-slot lists: (u32 slot, u32 count) pairs per exec, "
-               "random order inside an exec, pinned host memory",
+               "execs_per_step": n_e2e,
+               "host_form": "touched-slot lists, 4 bytes per pair: u32 slot | count << 16 (counts < 65,536) + "
+                            "(u32 slot, u32 count) pairs for larger device counters; random order inside an exec; "
+                            "pinned host memory",
                "pairs_per_exec": float(ent_np.shape[0]) / n_e2e,
+               "wide_pairs_per_exec": float(wide_np.shape[0]) / n_e2e,
                "equals_device_fold": same,
-               "api": "hfz_feedback_batch_sparse_host (pairs streamed H2D chunk by chunk, expanded and folded "
-                      "on the device)"}
-        del ent_t, off_t, ent_np, off_np
+               "api": "hfz_feedback_batch_compact_host (lists streamed H2D chunk by chunk, ranked and folded on "
+                      "the device)"}
+        # (a2) the same lists at 8 bytes per pair
+        sec, res = timed(lambda vh, ch: ctx.feedback_batch_sparse_host(ent_np, off_np, vh, ch))
+        if not same_as_device_fold(res):
+            raise SystemExit("bench.py: sparse e2e results differ from the device-resident dense fold")
+        e2e_pairs = {"value": world * n_e2e / sec, "unit": UNIT,
+                     "h2d_bytes_per_step": int(ent_np.nbytes + off_np.nbytes + S + 16),
+                     "d2h_bytes_per_step": int(n_e2e * (1 + 8 + 8 + 4) + S + 16 + 8), "execs_per_step": n_e2e,
+                     "host_form": "touched-slot lists, 8 bytes per pair: (u32 slot, u32 count)",
+                     "api": "hfz_feedback_batch_sparse_host"}
+        del ent_t, off_t, ent_np, off_np, comp_t, coff_t, wide_t, woff_t, comp_np, coff_np, wide_np, woff_np
         # (b) dense records
         # the dense form pins 10.7 GB of host memory per rank: single-rank runs only
         if not args.no_e2e_dense and world == 1:
@@ -443,7 +485,7 @@ def run_ours(args):
                                      else f"inputs of {n * REC / 1e6:.0f} MB per GPU may stay L2-resident (not a bench configuration)"),
                        "admits_per_step_rank0": admits, "parallelism": f"exec-sharded x{world}",
                        "gen_seconds": round(gen_s, 1), "parity_checked": parity},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_dense": e2e_dense,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_pairs": e2e_pairs, "e2e_dense": e2e_dense,
             "gpu_launches": launches,
             "clocks": clocks,
             "hbm_gbs_algorithmic": world * n * REC / (ms_per_step / 1e3) / 1e9,

@@ -346,10 +346,11 @@ class BatchCampaign {
     r.admit.resize(n);
     r.sig_full.resize(n);
     r.sig_simple.resize(n);
-    check(hfz_feedback_batch_sparse_host(ctx_.get(), batch_.entries(), batch_.offsets() + first, n,
-                                         res_.virgin.data(), res_.virgin.edge_counts(), nullptr, r.admit.data(),
-                                         r.sig_full.data(), r.sig_simple.data(), nullptr),
-          "hfz_feedback_batch_sparse_host");
+    check(hfz_feedback_batch_compact_host(ctx_.get(), batch_.compact(), batch_.compact_offsets() + first,
+                                          batch_.wide(), batch_.wide_offsets() + first, n, res_.virgin.data(),
+                                          res_.virgin.edge_counts(), nullptr, r.admit.data(), r.sig_full.data(),
+                                          r.sig_simple.data(), nullptr),
+          "hfz_feedback_batch_compact_host");
     return r;
   }
   void save_virgin() {
@@ -504,7 +505,7 @@ class BatchCampaign {
   bool have_medians_ = false;
   std::size_t medians_at_queue_ = 0;
   CoverageMap map_;
-  SparseBatch batch_;
+  CompactBatch batch_;
   std::vector<std::uint8_t> saved_bits_;
   std::uint64_t saved_edges_[2] = {0, 0};
 };

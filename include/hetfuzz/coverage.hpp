@@ -88,60 +88,111 @@ class CoverageMap {
 
 namespace b200 {
 
+namespace detail {
+// growable array in page-locked host memory (hfz_host_alloc): full PCIe speed for the H2D stream
+template <class T>
+class PinnedVec {
+ public:
+  PinnedVec() = default;
+  PinnedVec(const PinnedVec&) = delete;
+  PinnedVec& operator=(const PinnedVec&) = delete;
+  ~PinnedVec() { hfz_host_free(buf_); }
+  void push_back(T v) {
+    if (n_ == cap_) reserve(n_ + 1);
+    buf_[n_++] = v;
+  }
+  void reserve(std::uint64_t want) {
+    if (want <= cap_) return;
+    std::uint64_t ncap = cap_ ? cap_ : 4096;
+    while (ncap < want) ncap *= 2;
+    void* nb = nullptr;
+    check(hfz_host_alloc(&nb, ncap * sizeof(T)), "hfz_host_alloc");
+    if (n_) std::memcpy(nb, buf_, n_ * sizeof(T));
+    hfz_host_free(buf_);
+    buf_ = static_cast<T*>(nb);
+    cap_ = ncap;
+  }
+  void clear() { n_ = 0; }
+  std::uint64_t size() const { return n_; }
+  const T* data() const { return buf_; }
+  T* data() { return buf_; }
+
+ private:
+  T* buf_ = nullptr;
+  std::uint64_t cap_ = 0, n_ = 0;
+};
+}  // namespace detail
+
 // A batch of executions in the sparse host form of include/hfz.h: per exec the (slot, count)
 // pairs of the slots its CoverageMap touched, packed back to back in page-locked memory.
 // append() right after an execution costs one ~10 KB copy while the map is still cache-hot;
 // the batch then crosses PCIe at ~10 KB per exec instead of 163,840 B.
 class SparseBatch {
  public:
-  SparseBatch() = default;
-  SparseBatch(const SparseBatch&) = delete;
-  SparseBatch& operator=(const SparseBatch&) = delete;
-  ~SparseBatch() {
-    hfz_host_free(pairs_);
-    hfz_host_free(off_);
-  }
+  SparseBatch() { off_.push_back(0); }
   void append(const CoverageMap& m) {
     const std::vector<std::uint32_t>& t = m.touched();
-    reserve_pairs(n_pairs_ + t.size());
-    reserve_execs(n_exec_ + 1);
-    std::uint32_t* p = pairs_ + 2 * n_pairs_;
+    pairs_.reserve(pairs_.size() + 2 * t.size());
     for (std::uint32_t slot : t) {
-      *p++ = slot;
-      *p++ = static_cast<std::uint32_t>(m.count_at(slot));
+      pairs_.push_back(slot);
+      pairs_.push_back(static_cast<std::uint32_t>(m.count_at(slot)));
     }
-    n_pairs_ += t.size();
-    off_[++n_exec_] = n_pairs_;
+    off_.push_back(pairs_.size() / 2);
   }
-  void clear() { n_exec_ = n_pairs_ = 0; }
-  std::uint64_t size() const { return n_exec_; }
-  std::uint64_t pairs() const { return n_pairs_; }
-  const std::uint32_t* entries() const { return pairs_; }
-  const std::uint64_t* offsets() const { return off_ ? off_ : &zero_; }
+  void clear() {
+    pairs_.clear();
+    off_.clear();
+    off_.push_back(0);
+  }
+  std::uint64_t size() const { return off_.size() - 1; }
+  std::uint64_t pairs() const { return pairs_.size() / 2; }
+  const std::uint32_t* entries() const { return pairs_.data(); }
+  const std::uint64_t* offsets() const { return off_.data(); }
 
  private:
-  template <class T>
-  static void grow(T*& buf, std::uint64_t& cap, std::uint64_t used, std::uint64_t want, std::uint64_t unit) {
-    if (want <= cap) return;
-    std::uint64_t ncap = cap ? cap : 4096;
-    while (ncap < want) ncap *= 2;
-    void* nb = nullptr;
-    check(hfz_host_alloc(&nb, ncap * unit * sizeof(T)), "hfz_host_alloc");
-    if (used) std::memcpy(nb, buf, used * unit * sizeof(T));
-    hfz_host_free(buf);
-    buf = static_cast<T*>(nb);
-    cap = ncap;
+  detail::PinnedVec<std::uint32_t> pairs_;
+  detail::PinnedVec<std::uint64_t> off_;
+};
+
+// The same batch at four bytes per pair (include/hfz.h, hfz_feedback_batch_compact_host): counts
+// below 65,536 go into `slot | count << 16` words, the rare larger device counters into wide
+// {slot, count} pairs.  kMapSize = 65,536 slots fit the 16-bit slot field exactly.
+class CompactBatch {
+ public:
+  CompactBatch() {
+    coff_.push_back(0);
+    woff_.push_back(0);
   }
-  void reserve_pairs(std::uint64_t want) { grow(pairs_, cap_pairs_, n_pairs_, want, 2); }
-  void reserve_execs(std::uint64_t want) {
-    const bool fresh = off_ == nullptr;
-    grow(off_, cap_execs_, fresh ? 0 : n_exec_ + 1, want + 1, 1);
-    if (fresh) off_[0] = 0;
+  void append(const CoverageMap& m) {
+    for (std::uint32_t slot : m.touched()) {
+      const std::uint32_t c = static_cast<std::uint32_t>(m.count_at(slot));
+      if (c < 65536u) {
+        compact_.push_back(slot | (c << 16));
+      } else {
+        wide_.push_back(slot);
+        wide_.push_back(c);
+      }
+    }
+    coff_.push_back(compact_.size());
+    woff_.push_back(wide_.size() / 2);
   }
-  std::uint32_t* pairs_ = nullptr;
-  std::uint64_t* off_ = nullptr;
-  std::uint64_t cap_pairs_ = 0, cap_execs_ = 0, n_pairs_ = 0, n_exec_ = 0;
-  std::uint64_t zero_ = 0;
+  void clear() {
+    compact_.clear();
+    wide_.clear();
+    coff_.clear();
+    woff_.clear();
+    coff_.push_back(0);
+    woff_.push_back(0);
+  }
+  std::uint64_t size() const { return coff_.size() - 1; }
+  const std::uint32_t* compact() const { return compact_.data(); }
+  const std::uint64_t* compact_offsets() const { return coff_.data(); }
+  const std::uint32_t* wide() const { return wide_.data(); }
+  const std::uint64_t* wide_offsets() const { return woff_.data(); }
+
+ private:
+  detail::PinnedVec<std::uint32_t> compact_, wide_;
+  detail::PinnedVec<std::uint64_t> coff_, woff_;
 };
 
 // Folds the batch into virgin / edge_counts in exec order (engine.cpp:471-478 per exec).
@@ -158,6 +209,23 @@ inline FeedbackResult feedback_batch(Context& ctx, const SparseBatch& batch, std
                                        want_classed ? r.classed.data() : nullptr, r.admit.data(),
                                        r.sig_full.data(), r.sig_simple.data(), r.nnz.data()),
         "hfz_feedback_batch_sparse_host");
+  return r;
+}
+
+inline FeedbackResult feedback_batch(Context& ctx, const CompactBatch& batch, std::uint8_t* virgin,
+                                     std::uint64_t* edge_counts, bool want_classed = false) {
+  const std::uint64_t n = batch.size();
+  FeedbackResult r;
+  r.admit.resize(n);
+  r.sig_full.resize(n);
+  r.sig_simple.resize(n);
+  r.nnz.resize(n);
+  if (want_classed) r.classed.resize(n * std::uint64_t(ctx.map_slots()));
+  check(hfz_feedback_batch_compact_host(ctx.get(), batch.compact(), batch.compact_offsets(), batch.wide(),
+                                        batch.wide_offsets(), n, virgin, edge_counts,
+                                        want_classed ? r.classed.data() : nullptr, r.admit.data(),
+                                        r.sig_full.data(), r.sig_simple.data(), r.nnz.data()),
+        "hfz_feedback_batch_compact_host");
   return r;
 }
 

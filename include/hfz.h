@@ -157,6 +157,20 @@ HFZ_API int hfz_feedback_batch_sparse_host(hfz_ctx* ctx, const uint32_t* entries
                                            uint8_t* classed_out_host, uint8_t* admit_out_host,
                                            uint64_t* sig_full_out_host, uint64_t* sig_simple_out_host,
                                            uint32_t* nnz_out_host);
+/* Compact lists, for maps of at most 65,536 slots: the same touched-slot lists at FOUR bytes per
+ * pair.  compact = u32 words `slot | count << 16` for counts below 65,536 (host counters always
+ * fit); wide = {u32 slot, u32 count} pairs as above for the larger device counters (wide and
+ * wide_off may be NULL when there are none).  Exec e owns compact[compact_off[e] ..
+ * compact_off[e+1]) and wide[wide_off[e] .. wide_off[e+1]); a slot belongs in ONE of the two lists.
+ * Everything else as hfz_feedback_batch_sparse_host; needs the list-native fold (HFZ_EINVAL when
+ * map_slots > 65,536 or option "sparse_native" = 0). */
+HFZ_API int hfz_feedback_batch_compact_host(hfz_ctx* ctx, const uint32_t* compact_host,
+                                            const uint64_t* compact_off_host, const uint32_t* wide_host,
+                                            const uint64_t* wide_off_host, uint64_t n_exec,
+                                            uint8_t* virgin_inout_host, uint64_t* edge_counts_inout_host,
+                                            uint8_t* classed_out_host, uint8_t* admit_out_host,
+                                            uint64_t* sig_full_out_host, uint64_t* sig_simple_out_host,
+                                            uint32_t* nnz_out_host);
 /* lists -> dense records (device buffers; raw_maps_out is overwritten, n_exec records) */
 HFZ_API int hfz_expand_sparse(hfz_ctx* ctx, const uint32_t* entries, const uint64_t* entry_off,
                               uint64_t n_exec, uint8_t* raw_maps_out);

@@ -221,6 +221,36 @@ class Context:
             o["classed"] = classed
         return o
 
+    def feedback_batch_compact_host(self, compact: np.ndarray, compact_off: np.ndarray, wide: np.ndarray | None,
+                                    wide_off: np.ndarray | None, virgin: np.ndarray, edge_counts: np.ndarray,
+                                    want_classed: bool = False):
+        """Touched-slot lists at 4 bytes per pair (maps of <= 65,536 slots): compact = uint32 words
+        slot | count << 16 for counts below 65,536, wide = (M, 2) uint32 (slot, count) pairs for the
+        larger device counters (None when there are none); one uint64 offsets array per list."""
+        n = compact_off.size - 1
+        assert compact.dtype == np.uint32 and compact.flags.c_contiguous
+        assert compact_off.dtype == np.uint64 and compact_off.flags.c_contiguous
+        if wide_off is not None:
+            assert wide is not None and wide.dtype == np.uint32 and wide.flags.c_contiguous
+            assert wide_off.dtype == np.uint64 and wide_off.size == n + 1 and wide_off.flags.c_contiguous
+        assert virgin.dtype == np.uint8 and virgin.size == self.S
+        assert edge_counts.dtype == np.uint64 and edge_counts.size == 2
+        admit = np.empty(n, np.uint8)
+        sf = np.empty(n, np.uint64)
+        ss = np.empty(n, np.uint64)
+        nnz = np.empty(n, np.uint32)
+        classed = np.empty((n, self.S), np.uint8) if want_classed else None
+        vp = lambda a: None if a is None else C.c_void_p(a.ctypes.data)
+        self._sync_stream()
+        check(lib.hfz_feedback_batch_compact_host(self._h, vp(compact), vp(compact_off),
+                                                  vp(wide) if wide_off is not None else None, vp(wide_off), n,
+                                                  vp(virgin), vp(edge_counts), vp(classed), vp(admit), vp(sf), vp(ss),
+                                                  vp(nnz)))
+        o = dict(admit=admit, sig_full=sf, sig_simple=ss, nnz=nnz)
+        if want_classed:
+            o["classed"] = classed
+        return o
+
     def expand_sparse(self, entries: torch.Tensor, entry_off: torch.Tensor, raw: torch.Tensor | None = None):
         """Touched-slot lists -> dense raw records on the device."""
         n = entry_off.numel() - 1

@@ -65,6 +65,10 @@ struct hfz_ctx {
   uint64_t sp_entries_cap = 0;     // pairs
   uint64_t* sp_off = nullptr;
   uint64_t sp_off_cap = 0;
+  uint32_t* sp_compact = nullptr;  // device copy of host compact pairs (slot | count << 16)
+  uint64_t sp_compact_cap = 0;
+  uint64_t* sp_coff = nullptr;
+  uint64_t sp_coff_cap = 0;
   std::vector<cudaEvent_t> sp_events;  // one "entries of chunk k copied" event per chunk
   int sparse_native = 1;           // 1 = rank + chain kernels on the lists (S <= 65,536), 0 = expand to dense records
   uint32_t* sp_sorted = nullptr;   // per pair: slot | rung << 24, ascending slots inside an exec
@@ -78,6 +82,7 @@ struct hfz_ctx {
   uint32_t sc_piece = 0, sc_host_pieces = 0, sc_npieces = 0;
   const uint32_t* sc_sorted = nullptr;
   const uint64_t* sc_off = nullptr;
+  const uint64_t* sc_coff = nullptr;
   const uint32_t* sc_cnt = nullptr;
 
   // tuning
@@ -103,7 +108,10 @@ int hfz_ensure_classed_stage(hfz_ctx* c, uint64_t execs);  // hfz_api.cu
 // hfz_feedback.cu: the scan half of the fold on touched-slot lists (device buffers); total_pairs =
 // entry_off[n_exec] (absolute).  Pair it with hfz_feedback_resolve(raw_maps = NULL).
 bool hfz_sparse_native_ok(const hfz_ctx* c);
-int hfz_feedback_scan_sparse(hfz_ctx* c, const uint32_t* pairs, const uint64_t* entry_off, uint64_t n_exec,
+// pairs / entry_off = wide {slot, count} pairs, compact / compact_off = slot | count << 16 words;
+// either list may be absent (null); total_pairs = the sum of both lists' end offsets (absolute).
+int hfz_feedback_scan_sparse(hfz_ctx* c, const uint32_t* pairs, const uint64_t* entry_off,
+                             const uint32_t* compact, const uint64_t* compact_off, uint64_t n_exec,
                              uint64_t total_pairs, const uint8_t* virgin_v0, uint8_t* classed_out,
                              uint64_t* sig_full_out, uint64_t* sig_simple_out, uint32_t* nnz_out,
                              uint8_t* delta_out, unsigned long long* bad_pairs);

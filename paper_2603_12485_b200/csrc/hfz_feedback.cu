@@ -776,8 +776,10 @@ __global__ void hfz_k_admit(const uint32_t* __restrict__ cand_list,
 constexpr int kRankWarps = 12;  // 12 x (8 KB bitmap + 4 KB prefix) + 64 KB virgin = 208 KB for S = 65,536
 
 struct SparseParams {
-  const uint2* pairs;
+  const uint2* pairs;       // wide pairs {slot, count}; may be null
   const uint64_t* off;
+  const uint32_t* cpairs;   // compact pairs slot | count << 16; may be null
+  const uint64_t* coff;
   uint64_t n_exec;
   uint32_t S, H;
   const uint8_t* v0;
@@ -823,26 +825,42 @@ __global__ void __launch_bounds__(kRankWarps * 32, 1) hfz_k_sparse_rank(const Sp
   uint32_t nbad = 0;
   for (uint64_t e64 = (uint64_t)blockIdx.x * kRankWarps + warp; e64 < p.n_exec; e64 += (uint64_t)gridDim.x * kRankWarps) {
     const uint32_t e = (uint32_t)e64;
-    const uint64_t b = p.off[e64], t = p.off[e64 + 1];
+    // exec e owns wide pairs [b, t) and compact pairs [cb, ct); its ordered list starts at b + cb
+    const uint64_t b = p.off ? p.off[e64] : 0, t = p.off ? p.off[e64 + 1] : 0;
+    const uint64_t cb = p.coff ? p.coff[e64] : 0, ct = p.coff ? p.coff[e64 + 1] : 0;
     if (lane == 0) *nov_cnt = 0;
-    // pass 1: mark the slots
-    for (uint64_t i0 = b; i0 < t; i0 += 128) {
-      uint2 x[4];
+    // calls f(slot, count) for every pair of the exec, four loads in flight per lane
+    auto for_pairs = [&](auto&& f) {
+      for (uint64_t i0 = b; i0 < t; i0 += 128) {
+        uint2 x[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint64_t i = i0 + j * 32 + lane;
-        x[j] = i < t ? __ldg(p.pairs + i) : make_uint2(0u, 0u);
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t slot = x[j].x, c = slot < p.H ? (x[j].y & 0xffu) : x[j].y;
-        if (slot >= p.S) {
-          ++nbad;
-        } else if (c) {
-          atomicOr(&bm[slot >> 5], 1u << (slot & 31));
+        for (int j = 0; j < 4; ++j) {
+          const uint64_t i = i0 + j * 32 + lane;
+          x[j] = i < t ? __ldg(p.pairs + i) : make_uint2(0u, 0u);
         }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) f(x[j].x, x[j].y);
       }
-    }
+      for (uint64_t i0 = cb; i0 < ct; i0 += 128) {
+        uint32_t x[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint64_t i = i0 + j * 32 + lane;
+          x[j] = i < ct ? __ldg(p.cpairs + i) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) f(x[j] & 0xffffu, x[j] >> 16);
+      }
+    };
+    // pass 1: mark the slots (padding pairs are {0, 0}: count 0 = unvisited)
+    for_pairs([&](uint32_t slot, uint32_t cnt_raw) {
+      const uint32_t c = slot < p.H ? (cnt_raw & 0xffu) : cnt_raw;
+      if (slot >= p.S) {
+        ++nbad;
+      } else if (c) {
+        atomicOr(&bm[slot >> 5], 1u << (slot & 31));
+      }
+    });
     __syncwarp();
     // popcount prefix: lane l owns words [l * per, (l + 1) * per)
     uint32_t sum = 0;
@@ -863,33 +881,24 @@ __global__ void __launch_bounds__(kRankWarps * 32, 1) hfz_k_sparse_rank(const Sp
     // pass 2: rank, classify, novelty, ordered write
     uint8_t* classed_row = p.classed ? p.classed + e64 * p.S : nullptr;
     uint32_t* nov_row = p.novel_ent + e64 * kNovMax;
-    for (uint64_t i0 = b; i0 < t; i0 += 128) {
-      uint2 x[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint64_t i = i0 + j * 32 + lane;
-        x[j] = i < t ? __ldg(p.pairs + i) : make_uint2(0u, 0u);
+    uint32_t* out = p.sorted + b + cb;
+    for_pairs([&](uint32_t slot, uint32_t cnt_raw) {
+      if (slot >= p.S) return;
+      const uint32_t c = slot < p.H ? (cnt_raw & 0xffu) : cnt_raw;
+      if (!c) return;
+      const uint32_t w = slot >> 5;
+      const uint32_t rank = lane_base[w >> per_shift] + pre[w] + __popc(bm[w] & ((1u << (slot & 31)) - 1u));
+      const uint32_t klass = slot < p.H ? hfz_class_host(c) : hfz_class_device(c);
+      const uint32_t rung = 31 - __clz(klass);
+      const uint32_t en = slot | (rung << 24);
+      out[rank] = en;
+      if (klass & ~(uint32_t)s_virgin[slot]) {
+        const uint32_t k = atomicAdd(nov_cnt, 1u);
+        if (k < kNovMax) nov_row[k] = en;
+        atomicMin(p.first + (size_t)slot * 8 + rung, e);
       }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t slot = x[j].x;
-        if (slot >= p.S) continue;
-        const uint32_t c = slot < p.H ? (x[j].y & 0xffu) : x[j].y;
-        if (!c) continue;
-        const uint32_t w = slot >> 5;
-        const uint32_t rank = lane_base[w >> per_shift] + pre[w] + __popc(bm[w] & ((1u << (slot & 31)) - 1u));
-        const uint32_t klass = slot < p.H ? hfz_class_host(c) : hfz_class_device(c);
-        const uint32_t rung = 31 - __clz(klass);
-        const uint32_t en = slot | (rung << 24);
-        p.sorted[b + rank] = en;
-        if (klass & ~(uint32_t)s_virgin[slot]) {
-          const uint32_t k = atomicAdd(nov_cnt, 1u);
-          if (k < kNovMax) nov_row[k] = en;
-          atomicMin(p.first + (size_t)slot * 8 + rung, e);
-        }
-        if (classed_row) classed_row[slot] = (uint8_t)klass;
-      }
-    }
+      if (classed_row) classed_row[slot] = (uint8_t)klass;
+    });
     __syncwarp();
     const uint32_t novel = *nov_cnt;
     if (lane == 0) {
@@ -940,13 +949,14 @@ __device__ __forceinline__ void chain_list(const uint32_t* __restrict__ list, ui
 
 __global__ void __launch_bounds__(128) hfz_k_sparse_chain(const uint32_t* __restrict__ sorted,
                                                           const uint64_t* __restrict__ off,
+                                                          const uint64_t* __restrict__ coff,
                                                           const uint32_t* __restrict__ cnt, uint64_t n_exec,
                                                           uint64_t* __restrict__ sig_full,
                                                           uint64_t* __restrict__ sig_simple,
                                                           uint32_t* __restrict__ nnz_out) {
   const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n_exec) return;
-  const uint32_t* list = sorted + off[e];
+  const uint32_t* list = sorted + (off ? off[e] : 0) + (coff ? coff[e] : 0);
   const uint32_t n = cnt[e];
   uint64_t hf = HFZ_FNV_OFFSET, hs = HFZ_FNV_OFFSET;
   chain_list(list, n, hf, hs);
@@ -1091,6 +1101,7 @@ __global__ void __launch_bounds__(128) hfz_k_chain_pieces(const CompactParams p,
 // resolve of the candidates with more than kNovMax novel slots, from their ordered lists
 __global__ void __launch_bounds__(256) hfz_k_resolve_sparse(const ResolveParams p, const uint32_t* __restrict__ sorted,
                                                             const uint64_t* __restrict__ off,
+                                                            const uint64_t* __restrict__ coff,
                                                             const uint32_t* __restrict__ cnt) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1099,7 +1110,7 @@ __global__ void __launch_bounds__(256) hfz_k_resolve_sparse(const ResolveParams 
   for (uint32_t it = warp; it < n_slow; it += total_warps) {
     const uint32_t ci = p.slow_list[it];
     const uint32_t e = p.cand_list[ci];
-    const uint32_t* list = sorted + off[e];
+    const uint32_t* list = sorted + (off ? off[e] : 0) + (coff ? coff[e] : 0);
     const uint32_t n = cnt[e];
     uint32_t flags = 0;
     for (uint32_t i = lane; i < n; i += 32) {
@@ -1407,7 +1418,8 @@ bool hfz_sparse_native_ok(const hfz_ctx* c) {
   return c->sparse_native && c->S <= 65536u && c->S >= 1024u;
 }
 
-int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t* entry_off, uint64_t n_exec,
+int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t* entry_off,
+                             const uint32_t* compact, const uint64_t* compact_off, uint64_t n_exec,
                              uint64_t total_pairs, const uint8_t* virgin_v0, uint8_t* classed_out,
                              uint64_t* sig_full_out, uint64_t* sig_simple_out, uint32_t* nnz_out,
                              uint8_t* delta_out, unsigned long long* bad_pairs) {
@@ -1440,6 +1452,8 @@ int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t
     SparseParams p;
     p.pairs = reinterpret_cast<const uint2*>(pairs);
     p.off = entry_off;
+    p.cpairs = compact;
+    p.coff = compact_off;
     p.n_exec = n_exec;
     p.S = ctx->S;
     p.H = ctx->H;
@@ -1464,7 +1478,7 @@ int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t
     ++ctx->launches;
     HFZ_CUDA(cudaGetLastError());
     hfz_k_sparse_chain<<<(uint32_t)((n_exec + 127) / 128), 128, 0, ctx->stream>>>(
-        ctx->sp_sorted, entry_off, ctx->sp_cnt, n_exec, sig_full_out, sig_simple_out, nnz_out);
+        ctx->sp_sorted, entry_off, compact_off, ctx->sp_cnt, n_exec, sig_full_out, sig_simple_out, nnz_out);
     ++ctx->launches;
     HFZ_CUDA(cudaGetLastError());
   }
@@ -1475,6 +1489,7 @@ int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t
   ctx->sc_pieces = false;
   ctx->sc_sorted = ctx->sp_sorted;
   ctx->sc_off = entry_off;
+  ctx->sc_coff = compact_off;
   ctx->sc_cnt = ctx->sp_cnt;
   return HFZ_OK;
 }
@@ -1530,7 +1545,7 @@ extern "C" int hfz_feedback_resolve(hfz_ctx* ctx, const uint8_t* raw_maps, uint6
     HFZ_CUDA(cudaGetLastError());
     if (ctx->sc_sparse) {
       hfz_k_resolve_sparse<<<(uint32_t)ctx->num_sms * 4, 256, 0, ctx->stream>>>(p, ctx->sc_sorted, ctx->sc_off,
-                                                                                  ctx->sc_cnt);
+                                                                                  ctx->sc_coff, ctx->sc_cnt);
     } else if (ctx->sc_pieces) {
       hfz_k_resolve_pieces<<<(uint32_t)ctx->num_sms * 4, 256, 0, ctx->stream>>>(
           p, ctx->ts_sorted, ctx->ts_cnt, ctx->sc_piece, ctx->sc_host_pieces, ctx->sc_npieces);

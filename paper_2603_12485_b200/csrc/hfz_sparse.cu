@@ -104,7 +104,8 @@ int launch_expand(hfz_ctx* c, const uint32_t* entries, const uint64_t* off, uint
 // pairs; classed_host (may be null) receives the classed maps through ctx->d_classed.
 // native: rank + chain kernels on the lists (total_pairs = entry_off[n_exec], absolute);
 // otherwise the pairs are expanded into the dense staging buffer and scanned by K2.
-int fold_chunks(hfz_ctx* c, const uint32_t* entries, const uint64_t* off, uint64_t n_exec, uint64_t C,
+int fold_chunks(hfz_ctx* c, const uint32_t* entries, const uint64_t* off, const uint32_t* compact,
+                const uint64_t* coff, uint64_t n_exec, uint64_t C,
                 bool native, uint64_t total_pairs, uint8_t* virgin, uint64_t* counts, uint8_t* classed_dev,
                 uint8_t* classed_host, uint8_t* admit, uint64_t* sigf, uint64_t* sigs, uint32_t* nnz,
                 const cudaEvent_t* events) {
@@ -116,7 +117,8 @@ int fold_chunks(hfz_ctx* c, const uint32_t* entries, const uint64_t* off, uint64
     uint8_t* cls = classed_dev ? classed_dev + done * (uint64_t)c->S : (classed_host ? c->d_classed : nullptr);
     int rc;
     if (native) {
-      rc = hfz_feedback_scan_sparse(c, entries, off + done, n, total_pairs, virgin, cls, sigf + done, sigs + done,
+      rc = hfz_feedback_scan_sparse(c, entries, off ? off + done : nullptr, compact, coff ? coff + done : nullptr, n,
+                                    total_pairs, virgin, cls, sigf + done, sigs + done,
                                     nnz ? nnz + done : nullptr, c->delta, c->d_small + kBadSlot);
       if (rc) return rc;
       rc = hfz_feedback_resolve(c, nullptr, n, virgin, counts, c->delta, 1, 0, admit + done);
@@ -165,43 +167,68 @@ extern "C" int hfz_feedback_batch_sparse(hfz_ctx* c, const uint32_t* entries, co
     uint64_t total = 0;
     HFZ_CUDA(cudaMemcpyAsync(&total, entry_off + n_exec, 8, cudaMemcpyDeviceToHost, c->stream));
     HFZ_CUDA(cudaStreamSynchronize(c->stream));
-    return fold_chunks(c, entries, entry_off, n_exec, n_exec, true, total, virgin_inout, edge_counts_inout,
-                       classed_out, nullptr, admit_out, sig_full_out, sig_simple_out, nnz_out, nullptr);
+    return fold_chunks(c, entries, entry_off, nullptr, nullptr, n_exec, n_exec, true, total, virgin_inout,
+                       edge_counts_inout, classed_out, nullptr, admit_out, sig_full_out, sig_simple_out, nnz_out,
+                       nullptr);
   }
   int rc = ensure_dense(c, n_exec);
   if (rc) return rc;
-  return fold_chunks(c, entries, entry_off, n_exec, c->sp_dense_execs, false, 0, virgin_inout, edge_counts_inout,
-                     classed_out, nullptr, admit_out, sig_full_out, sig_simple_out, nnz_out, nullptr);
+  return fold_chunks(c, entries, entry_off, nullptr, nullptr, n_exec, c->sp_dense_execs, false, 0, virgin_inout,
+                     edge_counts_inout, classed_out, nullptr, admit_out, sig_full_out, sig_simple_out, nnz_out, nullptr);
 }
 
-extern "C" int hfz_feedback_batch_sparse_host(hfz_ctx* c, const uint32_t* entries, const uint64_t* entry_off,
-                                              uint64_t n_exec, uint8_t* virgin, uint64_t* counts,
-                                              uint8_t* classed, uint8_t* admit, uint64_t* sigf,
-                                              uint64_t* sigs, uint32_t* nnz) {
-  if (!c || !virgin || !counts || (n_exec && (!entry_off || !admit || !sigf || !sigs))) {
-    hfz_set_error("hfz_feedback_batch_sparse_host: null argument");
+namespace {
+
+int grow(void** buf, uint64_t* cap, uint64_t want, uint64_t unit) {
+  if (*cap >= want) return HFZ_OK;
+  cudaFree(*buf);
+  *buf = nullptr;
+  *cap = 0;
+  const uint64_t ncap = want + want / 8 + 1024;
+  HFZ_CUDA(cudaMalloc(buf, ncap * unit));
+  *cap = ncap;
+  return HFZ_OK;
+}
+
+int check_offsets(const char* what, const uint64_t* off, uint64_t n_exec) {
+  for (uint64_t e = 0; e < n_exec; ++e)
+    if (off[e + 1] < off[e]) {
+      hfz_set_error("%s: offsets are not non-decreasing at exec %llu", what, (unsigned long long)e);
+      return HFZ_EINVAL;
+    }
+  return HFZ_OK;
+}
+
+// Host lists -> device, chunk by chunk on the copy stream, folded as they arrive.  wide pairs
+// {slot, count} and/or compact pairs (slot | count << 16); either list may be absent.
+int sparse_host_impl(hfz_ctx* c, const uint32_t* entries, const uint64_t* entry_off, const uint32_t* compact,
+                     const uint64_t* compact_off, uint64_t n_exec, uint8_t* virgin, uint64_t* counts,
+                     uint8_t* classed, uint8_t* admit, uint64_t* sigf, uint64_t* sigs, uint32_t* nnz) {
+  const char* who = compact_off ? "hfz_feedback_batch_compact_host" : "hfz_feedback_batch_sparse_host";
+  if (!c || !virgin || !counts || (n_exec && ((!entry_off && !compact_off) || !admit || !sigf || !sigs))) {
+    hfz_set_error("%s: null argument", who);
     return HFZ_EINVAL;
   }
   if (n_exec == 0) return HFZ_OK;
-  // entry_off indexes `entries` absolutely, so a sub-range of a larger batch is folded by
-  // passing entry_off + first_exec; only pairs [entry_off[0], entry_off[n_exec]) are copied
-  const uint64_t first_pair = entry_off[0];
-  const uint64_t total = entry_off[n_exec];
-  if (total > first_pair && !entries) {
-    hfz_set_error("hfz_feedback_batch_sparse_host: entries is null");
+  // offsets index their list absolutely, so a sub-range of a larger batch is folded by passing
+  // off + first_exec; only pairs [off[0], off[n_exec]) are copied
+  const uint64_t total = entry_off ? entry_off[n_exec] : 0;
+  const uint64_t ctotal = compact_off ? compact_off[n_exec] : 0;
+  if ((entry_off && total > entry_off[0] && !entries) || (compact_off && ctotal > compact_off[0] && !compact)) {
+    hfz_set_error("%s: a list has pairs but its pointer is null", who);
     return HFZ_EINVAL;
   }
-  for (uint64_t e = 0; e < n_exec; ++e) {
-    if (entry_off[e + 1] < entry_off[e]) {
-      hfz_set_error("hfz_feedback_batch_sparse_host: entry_off is not non-decreasing at exec %llu",
-                    (unsigned long long)e);
-      return HFZ_EINVAL;
-    }
-  }
+  int rc;
+  if (entry_off && (rc = check_offsets(who, entry_off, n_exec))) return rc;
+  if (compact_off && (rc = check_offsets(who, compact_off, n_exec))) return rc;
   HFZ_CUDA(cudaSetDevice(c->device));
-  int rc = hfz_ensure_host_common(c, n_exec);
+  rc = hfz_ensure_host_common(c, n_exec);
   if (rc) return rc;
   const bool native = hfz_sparse_native_ok(c);
+  if (compact_off && !native) {
+    hfz_set_error("%s: compact lists need the list-native fold (map_slots <= 65536, sparse_native = 1)", who);
+    return HFZ_EINVAL;
+  }
   uint64_t C;
   if (native) {
     // chunks only pace the overlap of the H2D stream with the kernels (measured: 4,096 execs)
@@ -213,21 +240,14 @@ extern "C" int hfz_feedback_batch_sparse_host(hfz_ctx* c, const uint32_t* entrie
   }
   const uint64_t n_chunks = (n_exec + C - 1) / C;
   if (classed && (rc = hfz_ensure_classed_stage(c, n_exec < C ? n_exec : C))) return rc;
-  (void)first_pair;  // the device copy keeps the absolute indexing: pairs below first_pair are never read
-  if (c->sp_entries_cap < total) {
-    cudaFree(c->sp_entries);
-    c->sp_entries = nullptr;
-    c->sp_entries_cap = 0;
-    const uint64_t cap = total + total / 8 + 1024;
-    HFZ_CUDA(cudaMalloc(&c->sp_entries, cap * 8));
-    c->sp_entries_cap = cap;
+  // the device copies keep the absolute indexing: pairs below off[0] are never read
+  if (entry_off) {
+    if ((rc = grow(reinterpret_cast<void**>(&c->sp_entries), &c->sp_entries_cap, total, 8))) return rc;
+    if ((rc = grow(reinterpret_cast<void**>(&c->sp_off), &c->sp_off_cap, n_exec + 1, 8))) return rc;
   }
-  if (c->sp_off_cap < n_exec + 1) {
-    cudaFree(c->sp_off);
-    c->sp_off = nullptr;
-    c->sp_off_cap = 0;
-    HFZ_CUDA(cudaMalloc(&c->sp_off, (n_exec + 1 + 1024) * 8));
-    c->sp_off_cap = n_exec + 1 + 1024;
+  if (compact_off) {
+    if ((rc = grow(reinterpret_cast<void**>(&c->sp_compact), &c->sp_compact_cap, ctotal, 4))) return rc;
+    if ((rc = grow(reinterpret_cast<void**>(&c->sp_coff), &c->sp_coff_cap, n_exec + 1, 8))) return rc;
   }
   while (c->sp_events.size() < n_chunks) {
     cudaEvent_t ev;
@@ -237,21 +257,25 @@ extern "C" int hfz_feedback_batch_sparse_host(hfz_ctx* c, const uint32_t* entrie
   cudaStream_t st = c->stream;
   // small inputs first: the H2D copy engine serves copies in issue order, so queueing them
   // behind the pairs would hold the first chunk's kernels back until every pair has arrived
-  HFZ_CUDA(cudaMemcpyAsync(c->sp_off, entry_off, (n_exec + 1) * 8, cudaMemcpyHostToDevice, st));
+  if (entry_off) HFZ_CUDA(cudaMemcpyAsync(c->sp_off, entry_off, (n_exec + 1) * 8, cudaMemcpyHostToDevice, st));
+  if (compact_off) HFZ_CUDA(cudaMemcpyAsync(c->sp_coff, compact_off, (n_exec + 1) * 8, cudaMemcpyHostToDevice, st));
   HFZ_CUDA(cudaMemcpyAsync(c->d_virgin, virgin, c->S, cudaMemcpyHostToDevice, st));
   HFZ_CUDA(cudaMemcpyAsync(c->d_counts, counts, 16, cudaMemcpyHostToDevice, st));
   HFZ_CUDA(cudaMemsetAsync(c->d_small + kBadSlot, 0, sizeof(unsigned long long), st));
   // the pairs stream in on the copy stream, one event per chunk; everything else on `st`
   for (uint64_t k = 0; k < n_chunks; ++k) {
     const uint64_t e0 = k * C, e1 = e0 + C < n_exec ? e0 + C : n_exec;
-    const uint64_t b = entry_off[e0], t = entry_off[e1];
-    if (t > b)
-      HFZ_CUDA(cudaMemcpyAsync(c->sp_entries + 2 * b, entries + 2 * b, (t - b) * 8, cudaMemcpyHostToDevice,
-                               c->copy_stream));
+    if (entry_off && entry_off[e1] > entry_off[e0])
+      HFZ_CUDA(cudaMemcpyAsync(c->sp_entries + 2 * entry_off[e0], entries + 2 * entry_off[e0],
+                               (entry_off[e1] - entry_off[e0]) * 8, cudaMemcpyHostToDevice, c->copy_stream));
+    if (compact_off && compact_off[e1] > compact_off[e0])
+      HFZ_CUDA(cudaMemcpyAsync(c->sp_compact + compact_off[e0], compact + compact_off[e0],
+                               (compact_off[e1] - compact_off[e0]) * 4, cudaMemcpyHostToDevice, c->copy_stream));
     HFZ_CUDA(cudaEventRecord(c->sp_events[k], c->copy_stream));
   }
-  rc = fold_chunks(c, c->sp_entries, c->sp_off, n_exec, C, native, total, c->d_virgin, c->d_counts, nullptr,
-                   classed, c->d_admit, c->d_sigf, c->d_sigs, c->d_nnz, c->sp_events.data());
+  rc = fold_chunks(c, c->sp_entries, entry_off ? c->sp_off : nullptr, c->sp_compact, compact_off ? c->sp_coff : nullptr,
+                   n_exec, C, native, total + ctotal, c->d_virgin, c->d_counts, nullptr, classed, c->d_admit,
+                   c->d_sigf, c->d_sigs, c->d_nnz, c->sp_events.data());
   if (rc) {
     cudaStreamSynchronize(c->copy_stream);
     cudaStreamSynchronize(st);
@@ -267,10 +291,36 @@ extern "C" int hfz_feedback_batch_sparse_host(hfz_ctx* c, const uint32_t* entrie
   HFZ_CUDA(cudaMemcpyAsync(&bad, c->d_small + kBadSlot, sizeof(bad), cudaMemcpyDeviceToHost, st));
   HFZ_CUDA(cudaStreamSynchronize(st));
   if (bad) {
-    hfz_set_error("hfz_feedback_batch_sparse_host: %llu pairs name a slot >= %u (ignored)", bad, c->S);
+    hfz_set_error("%s: %llu pairs name a slot >= %u (ignored)", who, bad, c->S);
     return HFZ_EINVAL;
   }
   return HFZ_OK;
+}
+
+}  // namespace
+
+extern "C" int hfz_feedback_batch_sparse_host(hfz_ctx* c, const uint32_t* entries, const uint64_t* entry_off,
+                                              uint64_t n_exec, uint8_t* virgin, uint64_t* counts,
+                                              uint8_t* classed, uint8_t* admit, uint64_t* sigf,
+                                              uint64_t* sigs, uint32_t* nnz) {
+  if (n_exec && !entry_off) {
+    hfz_set_error("hfz_feedback_batch_sparse_host: null argument");
+    return HFZ_EINVAL;
+  }
+  return sparse_host_impl(c, entries, entry_off, nullptr, nullptr, n_exec, virgin, counts, classed, admit, sigf, sigs,
+                          nnz);
+}
+
+extern "C" int hfz_feedback_batch_compact_host(hfz_ctx* c, const uint32_t* compact, const uint64_t* compact_off,
+                                               const uint32_t* wide, const uint64_t* wide_off, uint64_t n_exec,
+                                               uint8_t* virgin, uint64_t* counts, uint8_t* classed, uint8_t* admit,
+                                               uint64_t* sigf, uint64_t* sigs, uint32_t* nnz) {
+  if (n_exec && !compact_off) {
+    hfz_set_error("hfz_feedback_batch_compact_host: null argument");
+    return HFZ_EINVAL;
+  }
+  return sparse_host_impl(c, wide, wide_off, compact, compact_off, n_exec, virgin, counts, classed, admit, sigf, sigs,
+                          nnz);
 }
 
 extern "C" int hfz_expand_sparse(hfz_ctx* c, const uint32_t* entries, const uint64_t* entry_off,

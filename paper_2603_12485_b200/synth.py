@@ -186,6 +186,22 @@ def to_sparse(raw: np.ndarray, n_exec: int, S: int = 65536, shuffle_seed: int | 
     return entries, off
 
 
+def to_compact(raw: np.ndarray, n_exec: int, S: int = 65536, shuffle_seed: int | None = 1):
+    """Dense records -> the compact list form (S <= 65,536): (compact uint32 words slot | count << 16,
+    compact_off, wide (M, 2) uint32 pairs for counts >= 65,536, wide_off)."""
+    assert S <= 65536
+    entries, off = to_sparse(raw, n_exec, S, shuffle_seed)
+    rows = np.repeat(np.arange(n_exec), np.diff(off).astype(np.int64))
+    big = entries[:, 1] >= 65536
+    compact = (entries[~big, 0] | (entries[~big, 1] << np.uint32(16))).astype(np.uint32)
+    wide = np.ascontiguousarray(entries[big])
+    coff = np.zeros(n_exec + 1, np.uint64)
+    woff = np.zeros(n_exec + 1, np.uint64)
+    np.cumsum(np.bincount(rows[~big], minlength=n_exec), out=coff[1:])
+    np.cumsum(np.bincount(rows[big], minlength=n_exec), out=woff[1:])
+    return np.ascontiguousarray(compact), coff, wide, woff
+
+
 # ---- havoc seeds (config 4) ---------------------------------------------------
 
 def havoc_inputs(n: int, seed: int = 45, lo: int = 1024, hi: int = 4096):

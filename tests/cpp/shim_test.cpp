@@ -105,6 +105,7 @@ int main() {
     std::vector<CoverageMap> maps(n);
     std::vector<std::uint8_t> raw(std::size_t(n) * kHostSlots * 5);
     b200::SparseBatch batch;
+    b200::CompactBatch cbatch;
     for (int e = 0; e < n; ++e) {
       const int hits = e == 7 ? 0 : 200 + int(rng.below(800));  // exec 7 touches nothing
       for (int i = 0; i < hits; ++i) {
@@ -119,6 +120,7 @@ int main() {
       }
       maps[e].pack(&raw[std::size_t(e) * kHostSlots * 5]);
       batch.append(maps[e]);
+      cbatch.append(maps[e]);
     }
     REQUIRE(batch.size() == std::uint64_t(n));
     VirginMap va, vb;
@@ -130,6 +132,11 @@ int main() {
     REQUIRE(a.nnz == b.nnz);
     REQUIRE(a.classed == b.classed);
     REQUIRE(a.nnz[7] == 0 && a.sig_full[7] == 14695981039346656037ULL);
+    VirginMap vc;
+    b200::FeedbackResult cc = b200::feedback_batch(b200::default_context(), cbatch, vc.data(), vc.edge_counts(), true);
+    REQUIRE(a.admit == cc.admit && a.sig_full == cc.sig_full && a.sig_simple == cc.sig_simple);
+    REQUIRE(a.nnz == cc.nnz && a.classed == cc.classed);
+    REQUIRE(va.host_edges() == vc.host_edges() && va.device_edges() == vc.device_edges());
     REQUIRE(va.host_edges() == vb.host_edges() && va.device_edges() == vb.device_edges());
     bool same = true;
     for (std::uint32_t i = 0; i < kMapSize; ++i) same = same && va.at(i) == vb.at(i);

@@ -236,3 +236,54 @@ def test_sparse_empty_batch_and_all_empty_lists(sctx):
     got = sctx.feedback_batch_sparse_host(np.zeros((0, 2), np.uint32), np.zeros(6, np.uint64), v, c)
     assert got["admit"].tolist() == [0] * 5 and got["nnz"].tolist() == [0] * 5
     assert all(int(x) == 14695981039346656037 for x in got["sig_full"]) and not v.any() and not c.any()
+
+
+@pytest.mark.parametrize("mode", ["campaign", "iid", "edge"])
+def test_compact_lists_equal_oracle(checker, mode):
+    """The 4-byte list form (slot | count << 16, wide pairs for counts >= 65,536)."""
+    c = hfz.Context(0)
+    try:
+        if mode == "edge":
+            raw, n = synth.maps_edge_cases(S)
+        else:
+            n = 500
+            raw = synth.maps_iid(n, S, seed=71) if mode == "iid" else synth.maps_campaign(n, S, seed=72, p_extra=8, p_rare=8)
+        compact, coff, wide, woff = synth.to_compact(raw, n, S, shuffle_seed=11)
+        assert wide.shape[0] > 0  # device counts of 65,536 and more occur in every mode
+        v, cnt = np.zeros(S, np.uint8), np.zeros(2, np.uint64)
+        got = c.feedback_batch_compact_host(compact, coff, wide, woff, v, cnt, want_classed=True)
+        check_host(c, got, v, cnt, cpu(checker, raw, n))
+        # sub-range folds through absolute offsets, compact list only when an exec has no wide pairs
+        v2, cnt2 = np.zeros(S, np.uint8), np.zeros(2, np.uint64)
+        k = n // 3
+        a = c.feedback_batch_compact_host(compact, coff[:k + 1].copy(), wide, woff[:k + 1].copy(), v2, cnt2)
+        b = c.feedback_batch_compact_host(compact, coff[k:].copy(), wide, woff[k:].copy(), v2, cnt2)
+        assert np.array_equal(np.concatenate([a["admit"], b["admit"]]), got["admit"])
+        assert np.array_equal(np.concatenate([a["sig_full"], b["sig_full"]]), got["sig_full"])
+        assert np.array_equal(v2, v) and np.array_equal(cnt2, cnt)
+    finally:
+        c.close()
+
+
+def test_compact_without_wide_list_and_rejections(checker):
+    c = hfz.Context(0)
+    try:
+        n = 64
+        raw = synth.maps_campaign(n, S, seed=73)
+        H = S // 2
+        recs = raw.reshape(n, -1)
+        dev = recs[:, H:].view(np.uint32)
+        dev[dev >= 65536] = 65535                      # no wide pairs needed
+        compact, coff, wide, woff = synth.to_compact(raw, n, S)
+        assert wide.shape[0] == 0
+        v, cnt = np.zeros(S, np.uint8), np.zeros(2, np.uint64)
+        got = c.feedback_batch_compact_host(compact, coff, None, None, v, cnt)
+        wo, wv, wc = cpu(checker, raw, n, want_classed=False)
+        for key in wo:
+            assert np.array_equal(got[key], wo[key]), key
+        assert np.array_equal(v, wv) and np.array_equal(cnt, wc)
+        c.set_option("sparse_native", 0)               # the expand fallback has no compact form
+        with pytest.raises(HfzError):
+            c.feedback_batch_compact_host(compact, coff, None, None, v, cnt)
+    finally:
+        c.close()
