@@ -13,8 +13,9 @@ from ._lib import HfzError, LIB_PATH, lib  # noqa: F401  (loads libhfz.so or rai
 from .api import (Context, SigSet, dispatch_batch, GAMMA, HOST_SLOTS, MAP_SIZE, MAX_INPUT_BYTES, i64_to_u64,  # noqa: F401
                   record_bytes, rng_jump, rng_split, u64_to_i64)
 from .binding import (TargetError, deterministic_mutants, havoc_mutant, splice_mutant,  # noqa: F401
-                      feedback_batch, feedback_batch_sparse, havoc_batch, default_context)
+                      feedback_batch, feedback_batch_sparse, feedback_batch_compact, havoc_batch,
+                      default_context)
 
 __all__ = ["Context", "MAP_SIZE", "HOST_SLOTS", "MAX_INPUT_BYTES", "havoc_mutant", "splice_mutant",
-           "deterministic_mutants", "feedback_batch", "feedback_batch_sparse", "havoc_batch", "default_context",
+           "deterministic_mutants", "feedback_batch", "feedback_batch_sparse", "feedback_batch_compact", "havoc_batch", "default_context",
            "record_bytes", "rng_jump", "rng_split", "HfzError", "TargetError"]

@@ -97,3 +97,11 @@ def feedback_batch_sparse(entries: np.ndarray, entry_off: np.ndarray, virgin: np
     entry_off (n_exec+1) uint64.  ~10 KB per exec over PCIe instead of a 163,840-byte record."""
     return default_context(device, map_slots).feedback_batch_sparse_host(entries, entry_off, virgin,
                                                                          edge_counts, want_classed)
+
+
+def feedback_batch_compact(compact: np.ndarray, compact_off: np.ndarray, wide, wide_off, virgin: np.ndarray,
+                           edge_counts: np.ndarray, device: int = 0, want_classed: bool = False):
+    """Touched-slot lists at 4 bytes per pair (65,536-slot maps): compact uint32 words
+    slot | count << 16, plus (M, 2) wide pairs for counts >= 65,536 (or None, None)."""
+    return default_context(device, api.MAP_SIZE).feedback_batch_compact_host(compact, compact_off, wide, wide_off,
+                                                                             virgin, edge_counts, want_classed)
