@@ -34,6 +34,9 @@ def main():
     ent_t, off_t = bench.sparse_lists_from_device(raw, n, dev)
     ent_np, off_np = ent_t.numpy().view(np.uint32), off_t.numpy().view(np.uint64)
     ent_d, off_d = ent_t.to(dev), off_t.to(dev)
+    comp_t, coff_t, wide_t, woff_t = bench.compact_lists(ent_t, off_t)
+    comp_np, coff_np = comp_t.numpy().view(np.uint32), coff_t.numpy().view(np.uint64)
+    wide_np, woff_np = wide_t.numpy().view(np.uint32), woff_t.numpy().view(np.uint64)
     print(f"{n} execs, {ent_np.shape[0] / n:.1f} pairs/exec, {ent_np.nbytes / 1e6:.1f} MB of pairs")
     ctx0.close()
     for chunk in [int(x) for x in args.chunks.split(",")]:
@@ -47,6 +50,14 @@ def main():
             ctx.feedback_batch_sparse_host(ent_np, off_np, vh, ch)
             ts.append(time.perf_counter() - t)
         host_ms = min(ts[1:]) * 1e3
+        ts = []
+        for i in range(4):
+            vh, ch = v0.copy(), c0.copy()
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            ctx.feedback_batch_compact_host(comp_np, coff_np, wide_np, woff_np, vh, ch)
+            ts.append(time.perf_counter() - t)
+        comp_ms = min(ts[1:]) * 1e3
         vd, cd = torch.from_numpy(v0).to(dev), torch.from_numpy(c0.view(np.int64)).to(dev)
         out = None
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -59,7 +70,8 @@ def main():
             torch.cuda.synchronize()
         dev_ms = e0.elapsed_time(e1)
         print(f"chunk {chunk:6d}: host call {host_ms:7.2f} ms ({n / host_ms / 1e3:.2f} M evals/s, "
-              f"{ent_np.nbytes / host_ms / 1e6:.1f} GB/s of pairs) | device call {dev_ms:6.2f} ms "
+              f"{ent_np.nbytes / host_ms / 1e6:.1f} GB/s of pairs) | compact host call {comp_ms:6.2f} ms "
+              f"({n / comp_ms / 1e3:.2f} M evals/s) | device call {dev_ms:6.2f} ms "
               f"({n / dev_ms / 1e3:.2f} M evals/s)")
         ctx.close()
 
