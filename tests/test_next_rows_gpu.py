@@ -128,3 +128,47 @@ def test_serial_stream_havoc_block(ctx, checker):
             want, st, _ = checker.havoc(entry, st)
             assert ob[oo[j]:oo[j] + ol[j]].tobytes() == want, (ln, j)
         assert int(api.i64_to_u64(stream)[0]) == st
+
+
+def test_nccl_allgather_resolve_through_the_c_abi(ctx, checker):
+    """hfz_feedback_resolve_allgather (what a C/C++ host calls at N > 1): a real ncclAllGather on a
+    single-rank communicator built from torch's bundled libnccl, then the rank-ordered resolve."""
+    import ctypes as C
+    import glob
+    import os
+    from paper_2603_12485_b200._lib import check, lib
+    base = os.path.dirname(os.path.dirname(torch.__file__))
+    cands = glob.glob(os.path.join(base, "nvidia", "nccl", "lib", "libnccl.so*")) + glob.glob("/usr/lib/x86_64-linux-gnu/libnccl.so*")
+    if not cands:
+        pytest.skip("no libnccl found")
+    nccl = C.CDLL(cands[0], mode=C.RTLD_GLOBAL)
+
+    class UniqueId(C.Structure):
+        _fields_ = [("internal", C.c_char * 128)]
+
+    uid = UniqueId()
+    assert nccl.ncclGetUniqueId(C.byref(uid)) == 0
+    comm = C.c_void_p()
+    nccl.ncclCommInitRank.argtypes = [C.POINTER(C.c_void_p), C.c_int, UniqueId, C.c_int]
+    torch.cuda.set_device(0)
+    assert nccl.ncclCommInitRank(C.byref(comm), 1, uid, 0) == 0
+    try:
+        S, n = 65536, 300
+        raw = synth.maps_campaign(n, S, seed=123, p_extra=8, p_rare=8)
+        d_raw = torch.from_numpy(raw).to(ctx.device)
+        virgin, counts = ctx.new_virgin(), ctx.new_edge_counts()
+        scan = ctx.feedback_scan(d_raw, virgin)
+        scratch = torch.empty(S, dtype=torch.uint8, device=ctx.device)
+        admit = torch.empty(n, dtype=torch.uint8, device=ctx.device)
+        p = lambda t: C.c_void_p(t.data_ptr())
+        check(lib.hfz_feedback_resolve_allgather(ctx._h, comm, p(d_raw), n, p(virgin), p(counts), p(scan["delta"]),
+                                                 p(scratch), 1, 0, p(admit)))
+        ctx.synchronize()
+        v, c = np.zeros(S, np.uint8), np.zeros(2, np.uint64)
+        want = checker.feedback_batch(raw, n, S, v, c)
+        assert np.array_equal(admit.cpu().numpy(), want["admit"])
+        assert np.array_equal(virgin.cpu().numpy(), v) and np.array_equal(counts.cpu().numpy().view(np.uint64), c)
+        assert np.array_equal(scratch.cpu().numpy(), scan["delta"].cpu().numpy())
+    finally:
+        nccl.ncclCommDestroy.argtypes = [C.c_void_p]
+        nccl.ncclCommDestroy(comm)
