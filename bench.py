@@ -290,7 +290,7 @@ def run_ours(args):
     ctx.feedback_batch(torch.from_numpy(warm_host).to(dev), virgin, counts)
     v0 = virgin.clone()
     c0 = counts.clone()
-    eng = ShardedFeedback(ctx)
+    eng = ShardedFeedback(ctx, exchange=args.exchange)
 
     def barrier():
         if world > 1:
@@ -514,6 +514,9 @@ def main():
     ap.add_argument("--no-e2e-dense", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--exchange", default="allgather", choices=["allgather", "peers"],
+                    help="N > 1: NCCL allgather of the deltas (default) or peer-memory loads through torch "
+                         "symmetric memory (hfz_feedback_resolve_peers)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -201,6 +201,18 @@ HFZ_API int hfz_feedback_resolve(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t
                                  const uint8_t* deltas, uint32_t n_ranks, uint32_t rank,
                                  uint8_t* admit_out);
 
+/* Peer-memory form of hfz_feedback_resolve: no allgather, no staging copy.  delta_ptrs (HOST
+ * array of n_ranks <= 16 device pointers) names every rank's novelty delta where its scan wrote
+ * it: own memory for this rank, peer memory mapped into this device's address space for the
+ * others (cudaIpcOpenMemHandle, CUDA VMM or torch symmetric memory; NVLink / NVSwitch loads).
+ * The merge kernel reads the R x S bytes straight from their owners in fixed rank order.  The
+ * caller orders the call after every rank's scan (and the next scan after every rank's resolve)
+ * with a device- or host-side barrier. */
+HFZ_API int hfz_feedback_resolve_peers(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec,
+                                       uint8_t* virgin_inout, uint64_t* edge_counts_inout,
+                                       const uint8_t* const* delta_ptrs, uint32_t n_ranks, uint32_t rank,
+                                       uint8_t* admit_out);
+
 /* K4 alone: virgin_inout |= OR_q deltas[q] in rank order, edge counters updated
  * (bitwise OR in reference polarity == AFL's virgin AND-merge). */
 HFZ_API int hfz_virgin_merge(hfz_ctx* ctx, uint8_t* virgin_inout, uint64_t* edge_counts_inout,

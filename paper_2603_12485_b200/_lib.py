@@ -41,6 +41,7 @@ PROTOTYPES = {
     "hfz_host_free": (C.c_int, [_vp]),
     "hfz_feedback_scan": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hfz_feedback_resolve": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _u32, _u32, _vp]),
+    "hfz_feedback_resolve_peers": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _u32, _u32, _vp]),
     "hfz_virgin_merge": (C.c_int, [_vp, _vp, _vp, _vp, _u32]),
     "hfz_feedback_resolve_allgather": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _u32, _u32, _vp]),
     "hfz_edge_record_batch": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _u64, _u64, _vp, _vp]),

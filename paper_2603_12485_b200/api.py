@@ -149,6 +149,18 @@ class Context:
                                        _ptr(deltas), n_ranks, rank, _ptr(admit)))
         return admit
 
+    def feedback_resolve_peers(self, raw, virgin, edge_counts, delta_tensors, rank, admit=None):
+        """feedback_resolve reading every rank's delta in place: delta_tensors[q] is rank q's delta
+        tensor (own or peer-mapped memory visible from this device)."""
+        n = raw.numel() // self.rec
+        if admit is None:
+            admit = torch.empty(n, dtype=torch.uint8, device=self.device)
+        ptrs = (C.c_void_p * len(delta_tensors))(*[t.data_ptr() for t in delta_tensors])
+        self._sync_stream()
+        check(lib.hfz_feedback_resolve_peers(self._h, _ptr(raw), n, _ptr(virgin), _ptr(edge_counts), ptrs,
+                                             len(delta_tensors), rank, _ptr(admit)))
+        return admit
+
     def virgin_merge(self, virgin, edge_counts, deltas, n_ranks):
         self._sync_stream()
         check(lib.hfz_virgin_merge(self._h, _ptr(virgin), _ptr(edge_counts), _ptr(deltas), n_ranks))

@@ -655,6 +655,40 @@ __global__ void hfz_k_merge(uint8_t* __restrict__ virgin, const uint8_t* __restr
   }
 }
 
+// K4 over peer memory: the same ordered merge, but every rank's delta is loaded from where it was
+// produced -- ptrs.p[q] is rank q's delta, own or peer-mapped (NVLink) device memory -- instead
+// of from an allgathered staging copy.  64 KB per rank: one 128-bit load per thread and rank.
+constexpr int kMaxPeers = 16;
+struct PeerPtrs {
+  const uint8_t* p[kMaxPeers];
+};
+
+__global__ void hfz_k_merge_peers(uint8_t* __restrict__ virgin, const PeerPtrs ptrs, uint32_t n_ranks, uint32_t rank,
+                                  uint8_t* __restrict__ prior_out, unsigned long long* __restrict__ edge_counts,
+                                  uint32_t S, uint32_t H) {
+  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;  // 16-byte vector index
+  uint32_t newh = 0, newd = 0;
+  if (v < S / 16) {
+    uint4 acc = reinterpret_cast<uint4*>(virgin)[v];
+    const uint4 old = acc;
+    for (uint32_t q = 0; q < n_ranks; ++q) {
+      if (q == rank) reinterpret_cast<uint4*>(prior_out)[v] = acc;
+      const uint4 d = reinterpret_cast<const uint4*>(ptrs.p[q])[v];
+      acc.x |= d.x; acc.y |= d.y; acc.z |= d.z; acc.w |= d.w;
+    }
+    reinterpret_cast<uint4*>(virgin)[v] = acc;
+    const uint32_t turned = __popc(nz_bytes(acc.x) & ~nz_bytes(old.x)) + __popc(nz_bytes(acc.y) & ~nz_bytes(old.y)) +
+                            __popc(nz_bytes(acc.z) & ~nz_bytes(old.z)) + __popc(nz_bytes(acc.w) & ~nz_bytes(old.w));
+    if (v * 16 < H) newh = turned; else newd = turned;
+  }
+  newh = __reduce_add_sync(0xffffffffu, newh);
+  newd = __reduce_add_sync(0xffffffffu, newd);
+  if ((threadIdx.x & 31) == 0) {
+    if (newh) atomicAdd(edge_counts + 0, (unsigned long long)newh);
+    if (newd) atomicAdd(edge_counts + 1, (unsigned long long)newd);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K2b: exact Admit codes of the candidate execs.  Work item = (candidate, 16 KB piece of its
 // raw record), dealt round-robin to all warps; a piece ORs {1: new class bit on a known slot,
@@ -1509,19 +1543,24 @@ extern "C" int hfz_virgin_merge(hfz_ctx* ctx, uint8_t* virgin_inout, uint64_t* e
   return HFZ_OK;
 }
 
-extern "C" int hfz_feedback_resolve(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec,
-                                    uint8_t* virgin_inout, uint64_t* edge_counts_inout,
-                                    const uint8_t* deltas, uint32_t n_ranks, uint32_t rank,
-                                    uint8_t* admit_out) {
-  if (!ctx || !virgin_inout || !edge_counts_inout || !deltas || n_ranks == 0 || rank >= n_ranks ||
+namespace {
+int resolve_impl(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec, uint8_t* virgin_inout,
+                 uint64_t* edge_counts_inout, const uint8_t* deltas, const PeerPtrs* peers, uint32_t n_ranks,
+                 uint32_t rank, uint8_t* admit_out) {
+  if (!ctx || !virgin_inout || !edge_counts_inout || (!deltas && !peers) || n_ranks == 0 || rank >= n_ranks ||
       (n_exec && ((!raw_maps && !ctx->sc_sparse) || !admit_out))) {
     hfz_set_error("hfz_feedback_resolve: bad argument");
     return HFZ_EINVAL;
   }
   HFZ_CUDA(cudaSetDevice(ctx->device));
-  hfz_k_merge<<<(ctx->S / 16 + 255) / 256, 256, 0, ctx->stream>>>(
-      virgin_inout, deltas, n_ranks, rank, ctx->prior,
-      reinterpret_cast<unsigned long long*>(edge_counts_inout), ctx->S, ctx->H);
+  if (peers)
+    hfz_k_merge_peers<<<(ctx->S / 16 + 255) / 256, 256, 0, ctx->stream>>>(
+        virgin_inout, *peers, n_ranks, rank, ctx->prior, reinterpret_cast<unsigned long long*>(edge_counts_inout),
+        ctx->S, ctx->H);
+  else
+    hfz_k_merge<<<(ctx->S / 16 + 255) / 256, 256, 0, ctx->stream>>>(
+        virgin_inout, deltas, n_ranks, rank, ctx->prior,
+        reinterpret_cast<unsigned long long*>(edge_counts_inout), ctx->S, ctx->H);
   ++ctx->launches;
   HFZ_CUDA(cudaGetLastError());
   if (n_exec) {
@@ -1562,6 +1601,38 @@ extern "C" int hfz_feedback_resolve(hfz_ctx* ctx, const uint8_t* raw_maps, uint6
     HFZ_CUDA(cudaGetLastError());
   }
   return HFZ_OK;
+}
+}  // namespace
+
+extern "C" int hfz_feedback_resolve(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec,
+                                    uint8_t* virgin_inout, uint64_t* edge_counts_inout,
+                                    const uint8_t* deltas, uint32_t n_ranks, uint32_t rank,
+                                    uint8_t* admit_out) {
+  if (!deltas) {
+    hfz_set_error("hfz_feedback_resolve: bad argument");
+    return HFZ_EINVAL;
+  }
+  return resolve_impl(ctx, raw_maps, n_exec, virgin_inout, edge_counts_inout, deltas, nullptr, n_ranks, rank,
+                      admit_out);
+}
+
+extern "C" int hfz_feedback_resolve_peers(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec,
+                                          uint8_t* virgin_inout, uint64_t* edge_counts_inout,
+                                          const uint8_t* const* delta_ptrs, uint32_t n_ranks, uint32_t rank,
+                                          uint8_t* admit_out) {
+  if (!delta_ptrs || n_ranks == 0 || n_ranks > (uint32_t)kMaxPeers) {
+    hfz_set_error("hfz_feedback_resolve_peers: 1..%d delta pointers expected", kMaxPeers);
+    return HFZ_EINVAL;
+  }
+  PeerPtrs peers;
+  for (uint32_t q = 0; q < (uint32_t)kMaxPeers; ++q) peers.p[q] = q < n_ranks ? delta_ptrs[q] : nullptr;
+  for (uint32_t q = 0; q < n_ranks; ++q)
+    if (!peers.p[q] || ((uintptr_t)peers.p[q] & 15)) {
+      hfz_set_error("hfz_feedback_resolve_peers: delta pointer %u is null or not 16-byte aligned", q);
+      return HFZ_EINVAL;
+    }
+  return resolve_impl(ctx, raw_maps, n_exec, virgin_inout, edge_counts_inout, nullptr, &peers, n_ranks, rank,
+                      admit_out);
 }
 
 extern "C" int hfz_feedback_batch(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec,

@@ -34,17 +34,39 @@ def shard_range(n_total: int, world: int, rank: int):
 
 
 class ShardedFeedback:
-    def __init__(self, engine, group=None):
+    """exchange = "allgather" (default): one all_gather_into_tensor of the deltas per step (NCCL).
+    exchange = "peers": every rank's delta lives in torch symmetric memory; the merge kernel of
+    each rank loads the R deltas straight from their owners over NVLink (hfz_feedback_resolve_peers),
+    bracketed by the symmetric-memory barrier -- no collective, no staging copy."""
+
+    def __init__(self, engine, group=None, exchange: str = "allgather"):
         self.engine = engine
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self._deltas = None
+        self.exchange = exchange
+        self._symm = None
+        if exchange == "peers" and self.world > 1:
+            import torch.distributed._symmetric_memory as symm_mem
+            S = engine.S
+            self._delta_buf = symm_mem.empty(S, dtype=torch.uint8, device=engine.device)
+            self._symm = symm_mem.rendezvous(self._delta_buf, group if group is not None else dist.group.WORLD)
+            self._peer_deltas = [self._symm.get_buffer(q, (S,), torch.uint8) for q in range(self.world)]
 
     def step(self, raw_local: torch.Tensor, virgin: torch.Tensor, edge_counts: torch.Tensor,
              out: dict | None = None):
         """One campaign iteration on this rank's shard.  `virgin`/`edge_counts` are the
         replicated campaign state (identical on all ranks before and after)."""
+        if self._symm is not None:
+            out = dict(out or {})
+            out["delta"] = self._delta_buf              # the scan writes this rank's delta in place
+            o = self.engine.feedback_scan(raw_local, virgin, out=out)
+            self._symm.barrier()                        # every rank's delta is complete
+            o["admit"] = self.engine.feedback_resolve_peers(raw_local, virgin, edge_counts, self._peer_deltas,
+                                                            self.rank, admit=o.get("admit"))
+            self._symm.barrier()                        # nobody overwrites a delta that is still being read
+            return o
         o = self.engine.feedback_scan(raw_local, virgin, out=out)
         delta = o["delta"]
         if self.world == 1:

@@ -92,6 +92,15 @@ def test_sharded_fold_equals_single_rank_at_full_size(full_batch):
             assert torch.equal(v, v1) and torch.equal(c, c1), f"rank {r} state differs"
         assert torch.equal(torch.cat(admits), o1["admit"])
         assert torch.equal(torch.cat([s["sig_full"] for s in scans]), o1["sig_full"])
+        # the peer-memory form: each rank's merge reads the four deltas where the scans left them
+        peer_deltas = [s["delta"] for s in scans]
+        admits2 = []
+        for r in range(R):
+            v, c = v0.clone(), c0.clone()
+            admits2.append(ctxs[r].feedback_resolve_peers(shards[r], v, c, peer_deltas, r))
+            ctxs[r].synchronize()
+            assert torch.equal(v, v1) and torch.equal(c, c1), f"rank {r} state differs (peers)"
+        assert torch.equal(torch.cat(admits2), o1["admit"])
     finally:
         for c in ctxs:
             c.close()
