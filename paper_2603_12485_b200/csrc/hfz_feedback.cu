@@ -1336,7 +1336,11 @@ int launch_scan(hfz_ctx* ctx, const ScanParams& p) {
   // measured: 65,536 slots -- wins up to ~3 k maps; 262,144 slots (virgin not in shared memory for the
   // other kernels) -- 1,024 maps 0.82 vs 1.72 ms, 4,096 maps 1.60 vs 1.72 ms
   const uint64_t ts_limit = ctx->scan_two_stage >= 0 ? (uint64_t)ctx->scan_two_stage : (p.S <= 65536u ? 3072 : 4096);
-  if (p.n_exec <= ts_limit && two_stage_fits(ctx, p.n_exec)) return launch_scan_two_stage(ctx, p);
+  if (p.n_exec <= ts_limit && two_stage_fits(ctx, p.n_exec)) {
+    const int rc = launch_scan_two_stage(ctx, p);
+    if (rc != HFZ_ENOMEM) return rc;
+    cudaGetLastError();  // no room for the list scratch: the kernels below need none
+  }
   if (p.n_exec <= small_limit) {
     const bool classed = p.classed != nullptr;
     if (vsmem) return classed ? launch_scan_wpm_t<true, true>(ctx, p) : launch_scan_wpm_t<true, false>(ctx, p);
