@@ -31,7 +31,7 @@
 
 namespace {
 
-constexpr int kEdgeWarps = 16;
+constexpr int kEdgeWarps = 24;
 constexpr uint32_t kRows = 256;        // site table rows
 // One table serves either general-path variant:
 //   transposed replay: keys u64[kRows] + per-row byte matrix [kRows][32]  (2 KB + 8 KB)
@@ -39,7 +39,7 @@ constexpr uint32_t kRows = 256;        // site table rows
 // Only non-coherent simulated warps need one, so the CTA keeps a POOL of kPool tables that its
 // 16 warps borrow (free-mask in shared memory) instead of one table per warp.
 constexpr uint32_t kTabBytes = kRows * (8 + 32) + 64;
-constexpr int kPool = 9;
+constexpr int kPool = 16;
 constexpr uint32_t kSmemSlots = 32768; // device slots whose counters fit in shared memory
 constexpr uint32_t kMaxBlockThreads = 1024;         // hdvm.hpp:167
 constexpr uint64_t kMaxLaunchThreads = 1ull << 22;  // hdvm.hpp:168
@@ -83,6 +83,29 @@ __device__ __forceinline__ void bump(uint32_t* c) {
   if (atomicAdd(c, 1u) == 0xffffffffu) atomicExch(c, 0xffffffffu);
 }
 
+// Where an exec's counters live while it is replayed.
+//   packed  shared memory, TWO 16-bit counters per 32-bit word (64 KB for 32,768 slots instead of
+//           128 KB: room for more warps and tables).  A counter that comes near 16 bits raises
+//           *overflow; the exec is then replayed once more with
+//   wide    saturating u32 counters in the exec's output record (global atomics).
+// kNear leaves more headroom than the CTA has threads, so no concurrent burst of bumps can
+// carry into the neighbouring counter before one of them has seen the flag condition.
+constexpr uint32_t kNear = 0xf000;
+struct Counters {
+  uint32_t* base;
+  bool packed;
+  uint32_t* overflow;
+  __device__ __forceinline__ void bump_slot(uint32_t slot) const {
+    if (packed) {
+      const uint32_t sh = (slot & 1u) * 16u;
+      const uint32_t old = atomicAdd(base + (slot >> 1), 1u << sh);
+      if (((old >> sh) & 0xffffu) >= kNear) *overflow = 1u;
+    } else {
+      bump(base + slot);
+    }
+  }
+};
+
 struct WarpTable {
   unsigned long long* keys;  // [kRows]  0 = empty, else (1<<32 | site)
   uint32_t* m;               // [kRows]  max visit count of this site among LOWER simulated lanes
@@ -114,7 +137,7 @@ __device__ __forceinline__ uint32_t table_insert(WarpTable& t, uint32_t site, ui
 // General path for one simulated warp.  e0/n_ev/prev0 are per real lane = per simulated lane.
 // Returns this real lane's share of the bumps.
 __device__ __forceinline__ uint64_t general_path(WarpTable& tab, const uint32_t* sites, uint64_t e0,
-                                                 uint32_t n_ev, uint32_t prev0, uint32_t* counters,
+                                                 uint32_t n_ev, uint32_t prev0, const Counters& counters,
                                                  uint32_t hmask, int lane) {
   uint64_t bumps = 0;
   const uint32_t lane_le = 0xffffffffu >> (31 - lane);
@@ -193,7 +216,7 @@ __device__ __forceinline__ uint64_t general_path(WarpTable& tab, const uint32_t*
             }
             const uint32_t k = cc + __popc(grp & lane_le);
             if (k > mm) {
-              bump(&counters[(pv ^ s) & hmask]);
+              counters.bump_slot((pv ^ s) & hmask);
               ++bumps;
             }
           }
@@ -228,7 +251,7 @@ constexpr uint32_t kTEmpty = 0xffffffffu;  // key of a free row; the site 0xffff
 static_assert((kTRows + 1) * (4 + 16) <= kTabBytes, "transposed table must fit a pool table");
 
 __device__ __forceinline__ bool transposed_path(uint8_t* tab, const uint32_t* sites, uint64_t e0, uint32_t n_ev,
-                                                uint32_t prev0, uint32_t* counters, uint32_t hmask, int lane,
+                                                uint32_t prev0, const Counters& counters, uint32_t hmask, int lane,
                                                 uint64_t& bumps_out) {
   uint32_t* keys = reinterpret_cast<uint32_t*>(tab);                    // [kTRows + 1]
   uint32_t* cnt = reinterpret_cast<uint32_t*>(tab + (kTRows + 4) * 4);  // [kTRows + 1][4], 16-byte aligned
@@ -314,7 +337,7 @@ __device__ __forceinline__ bool transposed_path(uint8_t* tab, const uint32_t* si
       if ((*reinterpret_cast<volatile uint32_t*>(c) >> shift) & 15u) {  // only this lane changes its nibble
         atomicSub(c, 1u << shift);
         const uint32_t pv = i ? (sites[e0 + i - 1] >> 1) : prev0;
-        bump(&counters[(pv ^ s) & hmask]);
+        counters.bump_slot((pv ^ s) & hmask);
         ++bumps;
       }
     }
@@ -336,21 +359,30 @@ __device__ __forceinline__ uint32_t div_small(uint32_t a, uint32_t b, float rb) 
 template <bool SMEM_HIST>
 __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const EdgeParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
-  uint32_t* hist = SMEM_HIST ? reinterpret_cast<uint32_t*>(smem) : nullptr;
-  uint8_t* pool = smem + (SMEM_HIST ? (size_t)p.H * 4 : 0);
+  uint32_t* hist = SMEM_HIST ? reinterpret_cast<uint32_t*>(smem) : nullptr;  // H / 2 words: two u16 counters each
+  uint8_t* pool = smem + (SMEM_HIST ? (size_t)p.H * 2 : 0);
   const int lane = threadIdx.x & 31;
   __shared__ unsigned long long s_events;
   __shared__ uint32_t s_next;
-  __shared__ uint32_t s_free;  // bit t set = pool table t is free
+  __shared__ uint32_t s_free;      // bit t set = pool table t is free
+  __shared__ uint32_t s_overflow;  // a packed counter came near 16 bits: replay the exec with wide counters
   if (threadIdx.x == 0) s_free = (1u << kPool) - 1u;
   uint32_t* prev_tab = p.prev_scratch + (size_t)blockIdx.x * p.prev_stride;
   const uint32_t hmask = p.H - 1;
 
   for (uint64_t e = blockIdx.x; e < p.n_exec; e += gridDim.x) {
-    uint32_t* ghist = reinterpret_cast<uint32_t*>(p.raw + e * p.rec_bytes + p.H);
-    uint32_t* counters = SMEM_HIST ? hist : ghist;
-    for (uint32_t i = threadIdx.x; i < p.H; i += blockDim.x) counters[i] = 0;
-    if (threadIdx.x == 0) s_events = 0;
+   uint32_t* ghist = reinterpret_cast<uint32_t*>(p.raw + e * p.rec_bytes + p.H);
+   for (int attempt = 0; attempt < 2; ++attempt) {
+    const bool packed = SMEM_HIST && attempt == 0;
+    Counters counters;
+    counters.base = packed ? hist : ghist;
+    counters.packed = packed;
+    counters.overflow = &s_overflow;
+    for (uint32_t i = threadIdx.x; i < (packed ? p.H / 2 : p.H); i += blockDim.x) counters.base[i] = 0;
+    if (threadIdx.x == 0) {
+      s_events = 0;
+      s_overflow = 0;
+    }
     const uint64_t l0 = p.launch_off[e], l1 = p.launch_off[e + 1];
     // prev is carried across launches per flattened gtid (hdvm.cpp:376,426-430): only needed
     // when the exec has more than one launch
@@ -486,7 +518,7 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
             for (uint32_t i = lane; i < n_lead; i += 32) {
               const uint32_t s = sl[i];
               const uint32_t pv = i ? (sl[i - 1] >> 1) : prev_lead;
-              bump(&counters[(pv ^ s) & hmask]);
+              counters.bump_slot((pv ^ s) & hmask);
             }
             if (lane == 0) my_events += n_lead;
             if (use_tab && active && n_ev) prev_tab[gtid] = sm[n_ev - 1] >> 1;
@@ -534,13 +566,18 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
     // block-reduce the event tally, flush the counters (copy, merge_device_into_map)
     if (my_events) atomicAdd(&s_events, (unsigned long long)my_events);
     __syncthreads();
-    if (SMEM_HIST) {
-      uint4* dst = reinterpret_cast<uint4*>(ghist);
-      const uint4* src = reinterpret_cast<const uint4*>(hist);
-      for (uint32_t i = threadIdx.x; i < p.H / 4; i += blockDim.x) dst[i] = src[i];
+    const bool redo = packed && s_overflow != 0;
+    if (packed && !redo) {  // unpack: two counters per word -> the record's u32 device half
+      uint2* dst = reinterpret_cast<uint2*>(ghist);
+      for (uint32_t i = threadIdx.x; i < p.H / 2; i += blockDim.x) {
+        const uint32_t w = hist[i];
+        dst[i] = make_uint2(w & 0xffffu, w >> 16);
+      }
     }
-    if (threadIdx.x == 0 && p.warp_events) p.warp_events[e] = s_events;
+    if (!redo && threadIdx.x == 0 && p.warp_events) p.warp_events[e] = s_events;
     __syncthreads();
+    if (!redo) break;
+   }
   }
 }
 
@@ -647,7 +684,7 @@ extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, c
   p.prev_stride = stride;
   const size_t wsmem = (size_t)kPool * kTabBytes;
   const bool smem_hist = ctx->H <= kSmemSlots;
-  const size_t smem = wsmem + (smem_hist ? (size_t)ctx->H * 4 : 0);
+  const size_t smem = wsmem + (smem_hist ? (size_t)ctx->H * 2 : 0);  // packed u16 counters
   if (smem_hist) {
     e = cudaFuncSetAttribute(hfz_k_edge_record<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) hfz_k_edge_record<true><<<grid, kEdgeWarps * 32, smem, ctx->stream>>>(p);

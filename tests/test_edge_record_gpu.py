@@ -155,6 +155,25 @@ def test_divergent_warps_small_tables(ctx, port):
     check(ctx, port, pack(execs), len(execs))
 
 
+def test_counts_beyond_16_bits_replay_with_wide_counters(ctx, port):
+    """The shared-memory counters are 16-bit pairs; an exec whose counter comes near 65,536 is
+    replayed with u32 counters in its output record.  One thread looping 70,000 times on a site,
+    a warp of 32 coherent threads looping 66,000 times, next to ordinary execs."""
+    dims = np.array([[1, 1, 1, 1, 1, 1]], np.uint32)
+    loop1 = ([dims, [0, 70000], [4242] * 70000])
+    d32 = np.array([[1, 1, 1, 32, 1, 1]], np.uint32)
+    sites, ev = [], [0]
+    for t in range(32):
+        sites += [77, 78] * 33000
+        ev.append(len(sites))
+    loop32 = (d32, ev, sites)
+    execs = [chain((64, 1, 1), [[1, 2, 3]]), loop1, chain((33, 1, 1), [[9, 9, 9, 10]]), loop32, chain((8, 1, 1), [[5, 6], [6, 5, 6]])]
+    raw = check(ctx, port, pack(execs), len(execs))
+    dev = raw.reshape(len(execs), synth.record_bytes(S))[:, H:].view(np.uint32)
+    assert dev[1][4242] == 1 and dev[1][(4242 >> 1) ^ 4242] == 69999
+    assert int(dev[3].max()) >= 32999
+
+
 def test_many_distinct_sites_forces_partitioning(ctx, port):
     """Fully divergent warps with far more distinct sites than the per-warp table holds."""
     rng = np.random.default_rng(12)
