@@ -104,3 +104,37 @@ def test_product_does_not_import_oracle():
         p = os.path.join(ROOT, "include", f)
         if os.path.isfile(p):
             assert "hfz_oracle" not in open(p).read()
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/hfz.h is a C header (no C++ needed): a C99 program that includes it, takes the
+    address of every declared entry point and calls the host-only ones links against libhfz.so."""
+    import re
+    import subprocess
+    hdr = open(os.path.join(ROOT, "include", "hfz.h")).read()
+    names = re.findall(r"HFZ_API\s+[\w\s\*]+?\b(hfz_\w+)\s*\(", hdr)
+    assert len(names) > 40
+    src = tmp_path / "abi.c"
+    body = "\n".join(f"  p[{i}] = (fn)&{n};" for i, n in enumerate(names))
+    src.write_text(f'''#include <stdio.h>
+#include "hfz.h"
+typedef void (*fn)(void);
+int main(void) {{
+  fn p[{len(names)}];
+{body}
+  unsigned long long s = 1;
+  if (hfz_version() != HFZ_VERSION) return 2;
+  if (hfz_rng_jump(5, 3) != 5 + 3 * 0x9e3779b97f4a7c15ULL) return 3;
+  (void)hfz_rng_next((uint64_t*)&s);
+  if (hfz_record_bytes(65536) != 163840) return 4;
+  if (hfz_havoc_max_out(100) != 1124) return 5;
+  printf("%d symbols\\n", (int)(sizeof p / sizeof p[0]));
+  return p[0] ? 0 : 1;
+}}
+''')
+    exe = str(tmp_path / "abi")
+    lib_dir = os.path.join(ROOT, "paper_2603_12485_b200")
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-Werror", "-pedantic", "-I", os.path.join(ROOT, "include"),
+                    str(src), "-o", exe, "-L", lib_dir, "-l:libhfz.so", f"-Wl,-rpath,{lib_dir}"], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
