@@ -139,3 +139,23 @@ def test_edge_record_conserves_bumps(ctx):
     dev_half = raw1.view(n, REC)[:, S // 2:].contiguous().view(torch.int32).to(torch.int64)
     assert torch.equal(dev_half.sum(dim=1), ev1)
     assert int(ev1.min()) > 0
+
+
+def test_one_large_fold_equals_two_half_folds(full_batch):
+    """A batch larger than configs[1] (2 x 65,536 execs = 21 GB: every warp of the throughput kernel
+    walks several groups) folded in ONE call equals folding its halves one after the other."""
+    ctx, raw, v0, c0 = full_batch
+    dev = raw.device
+    second = torch.empty_like(raw)
+    for i in range(0, N_FULL, 4096):
+        second[i * REC:(i + 4096) * REC] = torch.from_numpy(
+            synth.maps_campaign(4096, S, first=N_FULL + i, p_extra=64, p_rare=64)).to(dev)
+    both = torch.cat([raw, second])
+    o_all, v_all, c_all = fold(ctx, both, v0, c0)
+    o1, v1, c1 = fold(ctx, raw, v0, c0)
+    o2, v2, c2 = fold(ctx, second, v1, c1)
+    assert torch.equal(v_all, v2) and torch.equal(c_all, c2)
+    for k in ("admit", "sig_full", "sig_simple", "nnz"):
+        assert torch.equal(o_all[k], torch.cat([o1[k], o2[k]])), k
+    assert int((o2["admit"] != 0).sum()) > 0
+    del both, second
