@@ -287,3 +287,36 @@ def test_compact_without_wide_list_and_rejections(checker):
             c.feedback_batch_compact_host(compact, coff, None, None, v, cnt)
     finally:
         c.close()
+
+
+def test_calls_on_a_non_default_stream(checker):
+    """Everything is enqueued on the context's stream (here a non-default torch stream): dense,
+    sparse and compact folds interleaved with torch work on the same stream stay ordered."""
+    c = hfz.Context(0)
+    try:
+        n = 200
+        raw = synth.maps_campaign(n, S, seed=81, p_extra=8, p_rare=8)
+        wo, wv, wc = cpu(checker, raw, n, want_classed=False)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            d_raw = torch.from_numpy(raw).to(c.device, non_blocking=True)
+            virgin, counts = c.new_virgin(), c.new_edge_counts()
+            o = c.feedback_batch(d_raw, virgin, counts)
+            admit_sum = o["admit"].sum()              # torch op queued behind the fold on the same stream
+            entries, off = synth.to_sparse(raw, n, S, shuffle_seed=5)
+            d_ent = torch.from_numpy(entries.view(np.int32)).to(c.device, non_blocking=True)
+            d_off = torch.from_numpy(off.view(np.int64)).to(c.device, non_blocking=True)
+            v2, c2 = c.new_virgin(), c.new_edge_counts()
+            o2 = c.feedback_batch_sparse(d_ent, d_off, v2, c2)
+        s.synchronize()
+        assert int(admit_sum) == int(wo["admit"].sum())
+        assert np.array_equal(o["admit"].cpu().numpy(), wo["admit"]) and np.array_equal(virgin.cpu().numpy(), wv)
+        assert np.array_equal(o2["sig_full"].cpu().numpy().view(np.uint64), wo["sig_full"])
+        assert np.array_equal(v2.cpu().numpy(), wv) and np.array_equal(c2.cpu().numpy().view(np.uint64), wc)
+        with torch.cuda.stream(s):
+            vh, ch = np.zeros(S, np.uint8), np.zeros(2, np.uint64)
+            comp, coff, wide, woff = synth.to_compact(raw, n, S)
+            o3 = c.feedback_batch_compact_host(comp, coff, wide, woff, vh, ch)
+        assert np.array_equal(o3["admit"], wo["admit"]) and np.array_equal(vh, wv)
+    finally:
+        c.close()
