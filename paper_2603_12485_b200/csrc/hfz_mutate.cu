@@ -278,11 +278,15 @@ __global__ void __launch_bounds__(kHavocWarps * 32) hfz_k_havoc(
     const uint8_t* __restrict__ in_bytes, const uint64_t* __restrict__ in_off, uint64_t n,
     uint64_t* __restrict__ state, uint8_t* __restrict__ out_bytes,
     const uint64_t* __restrict__ out_off, uint64_t* __restrict__ out_len,
-    uint32_t* __restrict__ draws_out) {
+    uint32_t* __restrict__ draws_out, unsigned long long* __restrict__ next_slot) {
   __shared__ __align__(16) uint8_t s_buf[kHavocWarps][kSmemCap];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (uint64_t j = (uint64_t)blockIdx.x * kHavocWarps + warp; j < n;
-       j += (uint64_t)gridDim.x * kHavocWarps) {
+  // slots are handed out dynamically: a mutant stacks 1..64 edits, so their costs differ widely
+  for (;;) {
+    unsigned long long jj = 0;
+    if (lane == 0) jj = atomicAdd(next_slot, 1ull);
+    const uint64_t j = __shfl_sync(0xffffffffu, jj, 0);
+    if (j >= n) break;
     const uint64_t i0 = in_off[j];
     uint64_t len = in_off[j + 1] - i0;
     uint8_t* out = out_bytes + out_off[j];
@@ -439,10 +443,12 @@ extern "C" int hfz_havoc_batch(hfz_ctx* ctx, const uint8_t* in_bytes, const uint
   if (n == 0) return HFZ_OK;
   HFZ_CUDA(cudaSetDevice(ctx->device));
   uint64_t blocks = (n + kHavocWarps - 1) / kHavocWarps;
-  const uint64_t maxb = (uint64_t)ctx->num_sms * 8;
+  const uint64_t maxb = (uint64_t)ctx->num_sms * 4;  // at most 4 CTAs of 48 KB fit an SM
   if (blocks > maxb) blocks = maxb;
+  unsigned long long* next_slot = ctx->d_small + 5;
+  HFZ_CUDA(cudaMemsetAsync(next_slot, 0, sizeof(unsigned long long), ctx->stream));
   hfz_k_havoc<<<(uint32_t)blocks, kHavocWarps * 32, 0, ctx->stream>>>(
-      in_bytes, in_off, n, rng_state_inout, out_bytes, out_off, out_len, draws_out);
+      in_bytes, in_off, n, rng_state_inout, out_bytes, out_off, out_len, draws_out, next_slot);
   ++ctx->launches;
   HFZ_CUDA(cudaGetLastError());
   return HFZ_OK;
