@@ -46,7 +46,7 @@ extern "C" {
 #define HFZ_API __attribute__((visibility("default")))
 #endif
 
-#define HFZ_VERSION 100 /* 0.1.0 */
+#define HFZ_VERSION 110 /* 0.1.1: + sparse / compact list ingest, peer-memory resolve, serial-stream havoc with host buffers */
 
 enum {
   HFZ_OK = 0,
