@@ -21,7 +21,7 @@
 namespace {
 
 constexpr uint32_t kNone = 0xffffffffu;
-constexpr uint32_t kNovMax = 8;  // novel entries kept per map; more -> resolve re-reads the map
+constexpr uint32_t kNovMax = 32;  // novel entries kept per map (128 B of scratch each); more -> resolve re-reads the map
 constexpr int kPad = 16;  // per-lane slot padding: makes 128-bit shared loads conflict-free
 
 struct ScanParams {
