@@ -25,7 +25,8 @@ def test_small_bench_line_has_every_key():
     assert r.returncode == 0, r.stderr[-3000:]
     d = last_json(r.stdout)
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
-              "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "e2e_pairs", "e2e_dense", "gpu_launches",
+              "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "e2e_pairs", "e2e_dense", "stress_mode",
+              "gpu_launches",
               "clocks"):
         assert k in d, k
     assert d["gpu_launches"] > 0 and d["config"]["parity_checked"] is True
