@@ -68,7 +68,31 @@ class _FeedbackMixin:
         return out
 
 
-class Port(_FeedbackMixin):
+class _BatchMixin:
+    """Range calls for the CPU legs of bench.py and full-size checks: ctypes releases the GIL, so one
+    call per host thread runs in parallel."""
+
+    def havoc_range(self, in_bytes, in_off, first, count, state, out, out_off, out_len):
+        """Slots [first, first+count): state (u64[n]) advanced in place, out/out_len filled."""
+        f = self.lib.orc_havoc_batch if self.kind == "port" else self.lib.ref_havoc_batch
+        rc = f(_p(in_bytes, _u8p), _p(in_off, _u64p), first, count, _p(state, _u64p), _p(out, _u8p),
+               _p(out_off, _u64p), _p(out_len, _u64p))
+        assert rc == 0, rc
+
+    def edge_record_range(self, tr, first, count, S, raw, ev):
+        """Execs [first, first+count) of trace batch `tr` (dict of contiguous arrays in
+        hfz_edge_record_batch layout) -> device halves of raw (records) and warp events."""
+        args = [_p(tr["launch_off"], _u64p), _p(tr["dims"], _u32p), _p(tr["thread_off"], _u64p),
+                _p(tr["ev_off"], _u64p), _p(tr["sites"], _u32p), first, count]
+        if self.kind == "port":
+            rc = self.lib.orc_edge_record_range(*args, S, _p(raw, _u8p), _p(ev, _u64p))
+        else:
+            assert S == self.S
+            rc = self.lib.ref_edge_record_range(*args, _p(raw, _u8p), _p(ev, _u64p))
+        assert rc == 0, rc
+
+
+class Port(_FeedbackMixin, _BatchMixin):
     """Plain-C restatement (kind "port")."""
 
     kind = "port"
@@ -107,6 +131,11 @@ class Port(_FeedbackMixin):
         L.orc_edge_record_exec.argtypes = [_u32p, C.c_uint32, _u64p, _u32p, C.c_uint32, _u32p, _u64p]
         L.orc_edge_record_batch.restype = C.c_int
         L.orc_edge_record_batch.argtypes = [_u64p, _u32p, _u64p, _u64p, _u32p, C.c_uint64,
+                                            C.c_uint32, _u8p, _u64p]
+        L.orc_havoc_batch.restype = C.c_int
+        L.orc_havoc_batch.argtypes = [_u8p, _u64p, C.c_uint64, C.c_uint64, _u64p, _u8p, _u64p, _u64p]
+        L.orc_edge_record_range.restype = C.c_int
+        L.orc_edge_record_range.argtypes = [_u64p, _u32p, _u64p, _u64p, _u32p, C.c_uint64, C.c_uint64,
                                             C.c_uint32, _u8p, _u64p]
         L.orc_rank_delta.restype = C.c_int
         L.orc_rank_delta.argtypes = [_u8p, C.c_uint64, C.c_uint32, _u8p, _u8p]
@@ -225,7 +254,7 @@ class Port(_FeedbackMixin):
         return raw, ev
 
 
-class Ref(_FeedbackMixin):
+class Ref(_FeedbackMixin, _BatchMixin):
     """The compiled, unmodified reference (kind "reference")."""
 
     kind = "reference"
@@ -266,8 +295,12 @@ class Ref(_FeedbackMixin):
         L.ref_host_edge_record.argtypes = [_u16p, C.c_uint64, _u8p, _u64p]
         L.ref_edge_record_exec.restype = C.c_int
         L.ref_edge_record_exec.argtypes = [_u32p, C.c_uint32, _u64p, _u32p, _u32p, _u64p]
+        L.ref_edge_record_range.restype = C.c_int
+        L.ref_edge_record_range.argtypes = [_u64p, _u32p, _u64p, _u64p, _u32p, C.c_uint64, C.c_uint64, _u8p, _u64p]
         self.has_engine = hasattr(L, "ref_havoc")
         if self.has_engine:
+            L.ref_havoc_batch.restype = C.c_int
+            L.ref_havoc_batch.argtypes = [_u8p, _u64p, C.c_uint64, C.c_uint64, _u64p, _u8p, _u64p, _u64p]
             L.ref_havoc.restype = C.c_int
             L.ref_havoc.argtypes = [_u8p, C.c_uint64, _u64p, _u8p, _u64p]
             L.ref_splice.restype = C.c_int

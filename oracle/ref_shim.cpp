@@ -190,6 +190,26 @@ REF_API int ref_edge_record_exec(const std::uint32_t* dims, std::uint32_t n_laun
   return 0;
 }
 
+// execs [first, first+count) of a trace batch in hfz_edge_record_batch layout, each through
+// hdvm::execute as above; raw (records of S/2*5 bytes: the device half is written) and
+// warp_events are indexed by exec.  One call per host thread = the CPU baseline leg of bench.py.
+REF_API int ref_edge_record_range(const std::uint64_t* launch_off, const std::uint32_t* dims,
+                                  const std::uint64_t* thread_off, const std::uint64_t* ev_off,
+                                  const std::uint32_t* sites, std::uint64_t first, std::uint64_t count,
+                                  std::uint8_t* raw, std::uint64_t* warp_events) {
+  const std::uint64_t rec = std::uint64_t(kHostSlots) * 5;
+  for (std::uint64_t e = first; e < first + count; ++e) {
+    const std::uint64_t l0 = launch_off[e], l1 = launch_off[e + 1];
+    std::uint64_t ev = 0;
+    int rc = ref_edge_record_exec(dims + l0 * 6, static_cast<std::uint32_t>(l1 - l0),
+                                  ev_off + (l1 > l0 ? thread_off[l0] : 0), sites,
+                                  reinterpret_cast<std::uint32_t*>(raw + e * rec + kHostSlots), &ev);
+    if (rc) return rc;
+    if (warp_events) warp_events[e] = ev;
+  }
+  return 0;
+}
+
 // ---- mutators ------------------------------------------------------------------
 #ifndef REF_NO_ENGINE
 
@@ -201,6 +221,21 @@ REF_API int ref_havoc(const std::uint8_t* in, std::uint64_t in_len, std::uint64_
   *state = rng_state(rng);
   if (!r.empty()) std::memcpy(out, r.data(), r.size());
   *out_len = r.size();
+  return 0;
+}
+
+// slots [first, first+count): slot j reads in[in_off[j] .. in_off[j+1]), writes at out + out_off[j]
+REF_API int ref_havoc_batch(const std::uint8_t* in, const std::uint64_t* in_off, std::uint64_t first,
+                            std::uint64_t count, std::uint64_t* state_inout, std::uint8_t* out,
+                            const std::uint64_t* out_off, std::uint64_t* out_len) {
+  for (std::uint64_t j = first; j < first + count; ++j) {
+    Rng rng(state_inout[j]);
+    std::vector<std::uint8_t> v(in + in_off[j], in + in_off[j + 1]);
+    std::vector<std::uint8_t> r = havoc_mutant(v, rng);
+    state_inout[j] = rng_state(rng);
+    if (!r.empty()) std::memcpy(out + out_off[j], r.data(), r.size());
+    out_len[j] = r.size();
+  }
   return 0;
 }
 

@@ -13,9 +13,11 @@
 // visit of s by L in this launch) bumps a counter iff k > max_{L' < L, same warp} count_{L'}(s),
 // at slot (prev_L ^ s) % H with lane L's own running prev (= previous site >> 1, carried
 // across launches per flattened gtid).  That rule is separable per site, so here:
-//   * one CTA owns one execution; its 32,768 x u32 counter table lives in SHARED memory
-//     (warp bumps are shared-memory atomics, flushed to HBM once per exec -- no global atomic
-//     per hit); maps with more than 32,768 device slots fall back to global atomics;
+//   * one CTA owns one execution; its counters live in SHARED memory (warp bumps are
+//     shared-memory atomics, flushed to HBM once per exec -- no global atomic per hit): a dense
+//     table of packed 16-bit counters for up to 32,768 device slots, a hashed dirty-slot table
+//     (slot -> u32 count, the reference's own dirty list of src/hdvm.cpp:356-366 as an open-
+//     addressing table) for larger maps such as the 131,072 device slots of a 262,144-slot map;
 //   * a real warp replays one simulated warp, real lane L <-> simulated lane L:
 //       fast path   all active lanes walk the same site sequence (the SIMT common case):
 //                   only the lowest lane can ever bump, every event of it does;
@@ -86,20 +88,49 @@ __device__ __forceinline__ void bump(uint32_t* c) {
 // Where an exec's counters live while it is replayed.
 //   packed  shared memory, TWO 16-bit counters per 32-bit word (64 KB for 32,768 slots instead of
 //           128 KB: room for more warps and tables).  A counter that comes near 16 bits raises
-//           *overflow; the exec is then replayed once more with
-//   wide    saturating u32 counters in the exec's output record (global atomics).
+//           *overflow; the exec is then replayed once more with wide counters.
+//   hashed  shared memory, open-addressing table slot -> saturating u32 count (kHashCap rows,
+//           64 KB) for maps whose device half does not fit shared memory even packed: an exec
+//           touches a few thousand distinct slots (~2 % of the map), so the table holds the
+//           dirty slots only and the flush is zero-fill + scatter.  More than kHashLimit
+//           distinct slots raise *overflow; the exec is then replayed with wide counters.
+//   wide    saturating u32 counters in the exec's output record (global atomics): the replay
+//           after an overflow, nothing else.
 // kNear leaves more headroom than the CTA has threads, so no concurrent burst of bumps can
 // carry into the neighbouring counter before one of them has seen the flag condition.
 constexpr uint32_t kNear = 0xf000;
+constexpr uint32_t kHashBits = 13, kHashCap = 1u << kHashBits;  // 8,192 rows x (u32 key + u32 count) = 64 KB
+constexpr uint32_t kHashLimit = kHashCap * 3 / 4;               // distinct slots before the exec is replayed wide
+constexpr uint32_t kHashEmpty = 0xffffffffu;                     // slot ids are < 2^23
+enum { kCntWide = 0, kCntPacked = 1, kCntHashed = 2 };
 struct Counters {
-  uint32_t* base;
-  bool packed;
+  uint32_t* base;      // packed: H/2 words; hashed: keys[kHashCap] then counts[kHashCap]; wide: the record's device half
+  int mode;
   uint32_t* overflow;
+  uint32_t* used;      // hashed: rows taken
   __device__ __forceinline__ void bump_slot(uint32_t slot) const {
-    if (packed) {
+    if (mode == kCntPacked) {
       const uint32_t sh = (slot & 1u) * 16u;
       const uint32_t old = atomicAdd(base + (slot >> 1), 1u << sh);
       if (((old >> sh) & 0xffffu) >= kNear) *overflow = 1u;
+    } else if (mode == kCntHashed) {
+      if (*reinterpret_cast<volatile uint32_t*>(overflow)) return;  // the exec is replayed anyway; keeps the table from filling up
+      volatile uint32_t* keys = base;
+      uint32_t r = (slot * 0x9e3779b1u) >> (32 - kHashBits);
+      for (;;) {
+        const uint32_t cur = keys[r];
+        if (cur == slot) break;
+        if (cur == kHashEmpty) {
+          const uint32_t old = atomicCAS(base + r, kHashEmpty, slot);
+          if (old == kHashEmpty) {
+            if (atomicAdd(used, 1u) >= kHashLimit) *overflow = 1u;
+            break;
+          }
+          if (old == slot) break;
+        }
+        r = (r + 1) & (kHashCap - 1);
+      }
+      bump(base + kHashCap + r);
     } else {
       bump(base + slot);
     }
@@ -356,16 +387,22 @@ __device__ __forceinline__ uint32_t div_small(uint32_t a, uint32_t b, float rb) 
   return q;
 }
 
-template <bool SMEM_HIST>
+// bytes of shared memory the exec's counters take in mode MODE
+__host__ __device__ constexpr size_t counters_smem(int mode, uint32_t H) {
+  return mode == kCntPacked ? (size_t)H * 2 : (mode == kCntHashed ? (size_t)kHashCap * 8 : 0);
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const EdgeParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
-  uint32_t* hist = SMEM_HIST ? reinterpret_cast<uint32_t*>(smem) : nullptr;  // H / 2 words: two u16 counters each
-  uint8_t* pool = smem + (SMEM_HIST ? (size_t)p.H * 2 : 0);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);  // packed: H / 2 words; hashed: keys + counts
+  uint8_t* pool = smem + counters_smem(MODE, p.H);
   const int lane = threadIdx.x & 31;
   __shared__ unsigned long long s_events;
   __shared__ uint32_t s_next;
   __shared__ uint32_t s_free;      // bit t set = pool table t is free
-  __shared__ uint32_t s_overflow;  // a packed counter came near 16 bits: replay the exec with wide counters
+  __shared__ uint32_t s_overflow;  // a packed counter came near 16 bits / the hashed table is nearly full: replay with wide counters
+  __shared__ uint32_t s_used;      // rows of the hashed table in use
   if (threadIdx.x == 0) s_free = (1u << kPool) - 1u;
   uint32_t* prev_tab = p.prev_scratch + (size_t)blockIdx.x * p.prev_stride;
   const uint32_t hmask = p.H - 1;
@@ -373,15 +410,28 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
   for (uint64_t e = blockIdx.x; e < p.n_exec; e += gridDim.x) {
    uint32_t* ghist = reinterpret_cast<uint32_t*>(p.raw + e * p.rec_bytes + p.H);
    for (int attempt = 0; attempt < 2; ++attempt) {
-    const bool packed = SMEM_HIST && attempt == 0;
+    const bool packed = attempt == 0;  // first attempt: counters in shared memory (mode MODE)
     Counters counters;
     counters.base = packed ? hist : ghist;
-    counters.packed = packed;
+    counters.mode = packed ? MODE : kCntWide;
     counters.overflow = &s_overflow;
-    for (uint32_t i = threadIdx.x; i < (packed ? p.H / 2 : p.H); i += blockDim.x) counters.base[i] = 0;
+    counters.used = &s_used;
+    if (packed && MODE == kCntHashed) {
+      for (uint32_t i = threadIdx.x; i < kHashCap; i += blockDim.x) {
+        hist[i] = kHashEmpty;
+        hist[kHashCap + i] = 0;
+      }
+      // the record's device half: zero-fill now (fire-and-forget stores under the replay), scatter the
+      // dirty slots at the end
+      uint4* z = reinterpret_cast<uint4*>(ghist);
+      for (uint32_t i = threadIdx.x; i < p.H / 4; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    } else {
+      for (uint32_t i = threadIdx.x; i < (packed ? p.H / 2 : p.H); i += blockDim.x) counters.base[i] = 0;
+    }
     if (threadIdx.x == 0) {
       s_events = 0;
       s_overflow = 0;
+      s_used = 0;
     }
     const uint64_t l0 = p.launch_off[e], l1 = p.launch_off[e + 1];
     // prev is carried across launches per flattened gtid (hdvm.cpp:376,426-430): only needed
@@ -567,11 +617,18 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
     if (my_events) atomicAdd(&s_events, (unsigned long long)my_events);
     __syncthreads();
     const bool redo = packed && s_overflow != 0;
-    if (packed && !redo) {  // unpack: two counters per word -> the record's u32 device half
-      uint2* dst = reinterpret_cast<uint2*>(ghist);
-      for (uint32_t i = threadIdx.x; i < p.H / 2; i += blockDim.x) {
-        const uint32_t w = hist[i];
-        dst[i] = make_uint2(w & 0xffffu, w >> 16);
+    if (packed && !redo) {
+      if (MODE == kCntHashed) {  // scatter the dirty slots over the zero-filled device half
+        for (uint32_t i = threadIdx.x; i < kHashCap; i += blockDim.x) {
+          const uint32_t k = hist[i];
+          if (k != kHashEmpty) ghist[k] = hist[kHashCap + i];
+        }
+      } else {  // unpack: two counters per word -> the record's u32 device half
+        uint2* dst = reinterpret_cast<uint2*>(ghist);
+        for (uint32_t i = threadIdx.x; i < p.H / 2; i += blockDim.x) {
+          const uint32_t w = hist[i];
+          dst[i] = make_uint2(w & 0xffffu, w >> 16);
+        }
       }
     }
     if (!redo && threadIdx.x == 0 && p.warp_events) p.warp_events[e] = s_events;
@@ -683,14 +740,16 @@ extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, c
   p.prev_scratch = d_prev;
   p.prev_stride = stride;
   const size_t wsmem = (size_t)kPool * kTabBytes;
-  const bool smem_hist = ctx->H <= kSmemSlots;
-  const size_t smem = wsmem + (smem_hist ? (size_t)ctx->H * 2 : 0);  // packed u16 counters
-  if (smem_hist) {
-    e = cudaFuncSetAttribute(hfz_k_edge_record<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) hfz_k_edge_record<true><<<grid, kEdgeWarps * 32, smem, ctx->stream>>>(p);
+  // counters in shared memory either way: packed 16-bit pairs when the device half fits, else the
+  // hashed dirty-slot table (both 64 KB at most)
+  const int mode = ctx->H <= kSmemSlots ? kCntPacked : kCntHashed;
+  const size_t smem = wsmem + counters_smem(mode, ctx->H);
+  if (mode == kCntPacked) {
+    e = cudaFuncSetAttribute(hfz_k_edge_record<kCntPacked>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) hfz_k_edge_record<kCntPacked><<<grid, kEdgeWarps * 32, smem, ctx->stream>>>(p);
   } else {
-    e = cudaFuncSetAttribute(hfz_k_edge_record<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) hfz_k_edge_record<false><<<grid, kEdgeWarps * 32, smem, ctx->stream>>>(p);
+    e = cudaFuncSetAttribute(hfz_k_edge_record<kCntHashed>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) hfz_k_edge_record<kCntHashed><<<grid, kEdgeWarps * 32, smem, ctx->stream>>>(p);
   }
   ++ctx->launches;
   if (e == cudaSuccess) e = cudaGetLastError();

@@ -218,14 +218,29 @@ def havoc_inputs(n: int, seed: int = 45, lo: int = 1024, hi: int = 4096):
 
 # ---- device basic-block traces (config 3) ---------------------------------------
 
+def _bb_paths(S0, keys, ids, succ, n_sites, max_len):
+    """Path of every key: (lens int64, steps (len(keys), max_len) int16 site indices)."""
+    ks = sm64(S0 ^ np.uint64(0x77), keys)
+    lens = (np.uint64(1) + below32(sm64(ks, 0), max_len)).astype(np.int64)
+    cur = below32(sm64(ks, 1), n_sites).astype(np.int64)
+    steps = np.zeros((keys.size, max_len), np.int16)
+    for s in range(max_len):
+        steps[:, s] = cur
+        cur = succ[cur, below32(sm64(ks, 2 + s), 2).astype(np.int64)]
+    return lens, steps
+
+
 def bb_traces(n_exec: int, seed: int = 44, n_launch: int = 4, grid=(16, 1, 1), block=(256, 1, 1),
-              n_sites: int = 512, max_len: int = 24, divergent_den: int = 16):
+              n_sites: int = 512, max_len: int = 24, divergent_den: int = 16, chunk_execs: int = 64):
     """Per exec `n_launch` launches of grid x block threads.  Each thread walks a random
     CFG over `n_sites` site ids (ids = 32-bit truncations of splitmix64 draws): a warp
     shares one path (coherent) unless it is one of the 1/divergent_den fully divergent
     warps, in which case every lane has its own path.  A path of length 1+below(max_len)
     follows succ[site][below(2)] from a start site, so loops revisit sites.
-    Returns dict(launch_off, dims, thread_off, ev_off, sites) in hfz_edge_record_batch layout."""
+    Returns dict(launch_off, dims, thread_off, ev_off, sites) in hfz_edge_record_batch layout.
+    (Paths are a function of a per-warp or per-thread key, so they are computed once per
+    coherent warp and expanded to its lanes; execs are generated `chunk_execs` at a time.)"""
+    assert n_sites < 32768
     tpb = block[0] * block[1] * block[2]
     blocks = grid[0] * grid[1] * grid[2]
     wpb = (tpb + 31) // 32
@@ -239,27 +254,38 @@ def bb_traces(n_exec: int, seed: int = 44, n_launch: int = 4, grid=(16, 1, 1), b
 
     n_l = n_exec * n_launch
     tl = np.arange(tpb)
-    warp_in_block = tl // 32
-    # path key per (launch, block, thread): warp-shared unless divergent
-    L = np.arange(n_l, dtype=np.uint64)[:, None, None]
-    B = np.arange(blocks, dtype=np.uint64)[None, :, None]
-    W = warp_in_block.astype(np.uint64)[None, None, :]
-    T = tl.astype(np.uint64)[None, None, :]
-    wkey = (L * np.uint64(blocks) + B) * np.uint64(wpb) + W
-    div = below32(sm64(S0 ^ np.uint64(0xD1), wkey), divergent_den) == 0
-    key = np.where(div, (wkey << np.uint64(10)) ^ T ^ np.uint64(1 << 40), wkey)
-    key = key.reshape(-1)                                    # (n_l*threads,)
-    ks = sm64(S0 ^ np.uint64(0x77), key)
-    lens = (np.uint64(1) + below32(sm64(ks, 0), max_len)).astype(np.int64)
-    cur = below32(sm64(ks, 1), n_sites).astype(np.int64)
-    steps = np.zeros((key.size, max_len), np.int64)
-    for s in range(max_len):
-        steps[:, s] = cur
-        cur = succ[cur, below32(sm64(ks, 2 + s), 2).astype(np.int64)]
-    ev_off = np.zeros(key.size + 1, np.uint64)
+    warp_of_tl = tl // 32
+    cols = np.arange(max_len)[None, :]
+    site_chunks, len_chunks = [], []
+    l_step = max(1, chunk_execs * n_launch)
+    for l0 in range(0, n_l, l_step):
+        l1 = min(n_l, l0 + l_step)
+        L = np.arange(l0, l1, dtype=np.uint64)[:, None, None]
+        B = np.arange(blocks, dtype=np.uint64)[None, :, None]
+        W = np.arange(wpb, dtype=np.uint64)[None, None, :]
+        wkey = ((L * np.uint64(blocks) + B) * np.uint64(wpb) + W).reshape(-1)      # one per simulated warp
+        div = below32(sm64(S0 ^ np.uint64(0xD1), wkey), divergent_den) == 0
+        wlens, wsteps = _bb_paths(S0, wkey, ids, succ, n_sites, max_len)
+        # thread -> row of the path table: its warp's row unless the warp is divergent
+        n_w = wkey.size
+        warp_of_thread = (np.arange(n_w // wpb)[:, None] * wpb + warp_of_tl[None, :]).reshape(-1)
+        row = warp_of_thread.copy()
+        tdiv = div[warp_of_thread]
+        if tdiv.any():
+            T = np.broadcast_to(tl.astype(np.uint64)[None, :], (n_w // wpb, tpb)).reshape(-1)[tdiv]
+            tkey = (wkey[warp_of_thread[tdiv]] << np.uint64(10)) ^ T ^ np.uint64(1 << 40)
+            tlens, tsteps = _bb_paths(S0, tkey, ids, succ, n_sites, max_len)
+            row[tdiv] = n_w + np.arange(tkey.size)
+            wlens = np.concatenate([wlens, tlens])
+            wsteps = np.concatenate([wsteps, tsteps])
+        lens = wlens[row]
+        keep = cols < lens[:, None]
+        site_chunks.append(ids[wsteps[row][keep]])
+        len_chunks.append(lens)
+    lens = np.concatenate(len_chunks) if len_chunks else np.zeros(0, np.int64)
+    ev_off = np.zeros(lens.size + 1, np.uint64)
     np.cumsum(lens.astype(np.uint64), out=ev_off[1:])
-    keep = np.arange(max_len)[None, :] < lens[:, None]
-    sites = ids[steps[keep]]
+    sites = np.concatenate(site_chunks) if site_chunks else np.zeros(0, np.uint32)
     dims = np.tile(np.array([*grid, *block], np.uint32), (n_l, 1))
     launch_off = (np.arange(n_exec + 1, dtype=np.uint64) * np.uint64(n_launch))
     thread_off = (np.arange(n_l + 1, dtype=np.uint64) * np.uint64(threads))

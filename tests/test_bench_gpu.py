@@ -20,16 +20,20 @@ def last_json(stdout):
 
 def test_small_bench_line_has_every_key():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3", "--execs", "2048",
-                        "--cpu-seconds", "1", "--cpu-sample", "256", "--e2e-steps", "1"],
+                        "--cpu-seconds", "1", "--cpu-sample", "256", "--e2e-steps", "1", "--edge-execs", "160", "--large-execs", "96",
+                        "--harness-execs", "2048", "--harness-steps", "1"],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     d = last_json(r.stdout)
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "e2e_pairs", "e2e_dense", "stress_mode",
-              "gpu_launches",
-              "clocks"):
+              "gpu_launches", "clocks", "parity", "config0_small_batch", "k1_edge_record", "config2_large_map", "k3_havoc",
+              "e2e_from_coveragemap"):
         assert k in d, k
-    assert d["gpu_launches"] > 0 and d["config"]["parity_checked"] is True
+    assert d["gpu_launches"] > 0 and d["parity_checked"] is True and d["parity"]["execs"] == 2048
+    for k in ("config0_small_batch", "k1_edge_record", "config2_large_map", "k3_havoc"):
+        assert d[k]["value"] > 0 and d[k]["parity_checked"] and d[k]["cpu_baseline"]["cores"] >= 1, k
+        assert 0 < d[k]["frac"] < 1.2, k
     assert d["e2e"]["equals_device_fold"] is True and d["e2e"]["h2d_bytes_per_step"] > 0
     assert d["roofline"]["bound"] == "hbm" and d["cpu_baseline"]["cores"] >= 1
 
@@ -43,4 +47,4 @@ def test_two_rank_bench_path_over_gloo():
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     d = last_json(r.stdout)
     assert d["n_gpus"] == 2 and d["config"]["global_execs_per_step"] == 2048
-    assert d["config"]["parity_checked"] is True and d["e2e"]["equals_device_fold"] is True
+    assert d["parity_checked"] is True and d["e2e"]["equals_device_fold"] is True
