@@ -9,19 +9,29 @@
 
 #include "../hfz.h"
 
-namespace hetfuzz {
+// Built against the reference's own tree (its include directory AFTER this one on the include
+// path, so that hdvm.hpp / sanitizers.hpp / targets.hpp / engine.hpp are the reference's)?
+#if defined(__has_include)
+#if __has_include("hetfuzz/hdvm.hpp")
+#define HETFUZZ_B200_WITH_REFERENCE 1
+#endif
+#endif
 
-// Same role as the reference's InternalError (include/hetfuzz/hdvm.hpp:16-18): a failure of
-// the library itself (CUDA error, missing GPU), mapped to exit code 3 by the reference CLI.
-struct InternalError : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
+namespace hetfuzz {
 
 namespace b200 {
 
+// A failure of the library itself (CUDA error, missing GPU): the role of the reference's
+// InternalError (include/hetfuzz/hdvm.hpp:16-18), which its CLI maps to exit code 3.  It is its own
+// type so that this header never collides with the reference's definition when both are in one
+// translation unit; without the reference on the include path hetfuzz::InternalError names it.
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
 inline void check(int rc, const char* what) {
   if (rc != HFZ_OK)
-    throw InternalError(std::string(what) + ": " + hfz_last_error() + " (hfz error " + std::to_string(rc) + ")");
+    throw Error(std::string(what) + ": " + hfz_last_error() + " (hfz error " + std::to_string(rc) + ")");
 }
 
 class Context {
@@ -42,7 +52,7 @@ class Context {
 // One lazily created context per host thread for the reference-named single-item calls.
 inline Context& default_context(std::uint32_t map_slots = 65536) {
   thread_local Context ctx(0, map_slots);
-  if (ctx.map_slots() != map_slots) throw InternalError("default_context: map size differs from the first use");
+  if (ctx.map_slots() != map_slots) throw Error("default_context: map size differs from the first use");
   return ctx;
 }
 
@@ -71,4 +81,9 @@ inline FeedbackResult feedback_batch(Context& ctx, const std::uint8_t* raw, std:
 }
 
 }  // namespace b200
+
+#ifndef HETFUZZ_B200_WITH_REFERENCE
+using InternalError = b200::Error;
+#endif
+
 }  // namespace hetfuzz

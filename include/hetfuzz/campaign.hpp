@@ -67,6 +67,13 @@ struct ShadowOutcome {                      // of one shadow execution + run_all
   bool violates_invariants = false;
 };
 
+// CONTRACT: execute() must be a PURE function of its input -- same map, cost and outcome whatever
+// was executed before (the reference's fresh-process mode, hdvm::execute).  BatchCampaign executes a
+// whole mutation stage before it folds the coverage, so after a splice cut or a virtual-time stop
+// inside a fold a few inputs have been executed that the serial campaign never runs; with a pure
+// executor those surplus executions are invisible.  A stateful executor (the reference's
+// PersistentSession: start-up cost charged once per process, iterations counted, runtime dropped
+// on a crash) would see its later virtual costs shift, so CampaignConfig::persistent is rejected.
 class Executor {
  public:
   virtual ~Executor() = default;
@@ -162,7 +169,10 @@ class BatchCampaign {
  public:
   BatchCampaign(const CampaignConfig& cfg, Executor& exec, Context& ctx)
       : cfg_(cfg), exec_(exec), ctx_(ctx), rng_(cfg.rng_seed), next_stats_(cfg.stats_every) {
-    if (ctx.map_slots() != kMapSize) throw InternalError("BatchCampaign: context map size != kMapSize");
+    if (ctx.map_slots() != kMapSize) throw Error("BatchCampaign: context map size != kMapSize");
+    if (cfg.persistent)
+      throw Error("BatchCampaign: persistent mode is not supported -- stages are executed speculatively, which is "
+                          "only exact for an executor that is a pure function of its input (see Executor)");
   }
 
   CampaignResult run() {  // engine.cpp:569-584
@@ -481,7 +491,7 @@ class BatchCampaign {
                                 state.data(), out.data(), out_off.data(), out_len.data()),
           "hfz_splice_batch_host");
     for (int j = 0; j < n; ++j)
-      if (state[j] != state_after[j]) throw InternalError("splice_stage: draw count differs from the device's");
+      if (state[j] != state_after[j]) throw Error("splice_stage: draw count differs from the device's");
     res_.gpu_mutants += n;
     std::vector<Bytes> res(n);
     for (int j = 0; j < n; ++j) res[j].assign(out.begin() + out_off[j], out.begin() + out_off[j] + out_len[j]);

@@ -9,7 +9,9 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
+#include <string>
 #include <unordered_map>
 #include <vector>
 
@@ -315,25 +317,48 @@ enum class Admit : std::uint8_t { None = 0, NewCounts = 1, NewEdges = 2 };
 enum class SignatureMode : std::uint8_t { Full, Simple };
 
 namespace detail {
-// A raw record that classifies to exactly the given class bytes (lowest count of each rung):
-// has_new_bits / trace_signature take a ClassedTrace, the device path takes raw maps.
-inline void record_from_classed(const ClassedTrace& t, std::vector<std::uint8_t>& rec) {
+// The touched-slot list of a map that classifies to exactly the given class bytes (lowest count of
+// each rung): has_new_bits / trace_signature take a ClassedTrace, the device path takes counts.
+// ~1,300 pairs (10 KB) cross PCIe per call instead of a dense 163,840-byte record.  A class byte
+// that is not one rung of its half's ladder cannot come from classify_trace: refused, not guessed.
+inline void pairs_from_classed(const ClassedTrace& t, b200::SparseBatch& out) {
   static const std::uint32_t host_lo[8] = {1, 2, 3, 4, 8, 16, 32, 128};
-  static const std::uint32_t dev_lo[8] = {1, 2, 3, 512, 4096, 16384, 65536, 65536};
-  rec.assign(std::size_t(kHostSlots) * 5, 0);
+  static const std::uint32_t dev_lo[7] = {1, 2, 3, 512, 4096, 16384, 65536};
+  CoverageMap m;
   for (std::uint32_t idx : t.nonzero) {
+    if (idx >= kMapSize) throw b200::Error("ClassedTrace: slot index out of range");
     const std::uint8_t k = t.classed[idx];
     int rung = 0;
-    while (rung < 7 && !(k >> rung & 1)) ++rung;
-    if (idx < kHostSlots) {
-      rec[idx] = static_cast<std::uint8_t>(host_lo[rung]);
-    } else {
-      const std::uint32_t c = dev_lo[rung];
-      std::memcpy(&rec[kHostSlots + std::size_t(idx - kHostSlots) * 4], &c, 4);
-    }
+    while (rung < 8 && !(k >> rung & 1)) ++rung;
+    if (k == 0 || (k & (k - 1)) != 0 || (idx >= kHostSlots && rung > 6))
+      throw b200::Error("ClassedTrace: class byte " + std::to_string(k) + " of slot " + std::to_string(idx) +
+                        " is not a rung of the bucket ladder");
+    if (idx < kHostSlots)
+      m.host_assign(idx, static_cast<std::uint8_t>(host_lo[rung]));
+    else
+      m.device_store(idx, dev_lo[rung]);
   }
+  out.append(m);
 }
 }  // namespace detail
+
+namespace b200 {
+// Everything Campaign::run_one needs from one execution's map (src/engine.cpp:471-478) in ONE device
+// call: classes are implied, both signatures, the Admit code, virgin folded in place.  The
+// reference-named functions below cost one call each; a host loop that adopts this library
+// should call this (or, better, feedback_batch over many executions).
+struct FeedbackOne {
+  Admit admit;
+  std::uint64_t sig_full, sig_simple;
+  std::uint32_t nonzero_slots;
+};
+inline FeedbackOne feedback_one(const CoverageMap& map, VirginMap& virgin) {
+  SparseBatch one;
+  one.append(map);
+  FeedbackResult r = feedback_batch(default_context(), one, virgin.data(), virgin.edge_counts());
+  return FeedbackOne{static_cast<Admit>(r.admit[0]), r.sig_full[0], r.sig_simple[0], r.nnz[0]};
+}
+}  // namespace b200
 
 inline ClassedTrace classify_trace(const CoverageMap& map) {
   b200::SparseBatch one;
@@ -345,26 +370,29 @@ inline ClassedTrace classify_trace(const CoverageMap& map) {
   ClassedTrace out;
   out.classed = std::move(r.classed);
   out.nonzero.reserve(r.nnz[0]);
-  for (std::uint32_t i = 0; i < kMapSize; ++i)
-    if (out.classed[i]) out.nonzero.push_back(i);
+  // the touched list names every candidate slot: no scan of the 65,536 class bytes
+  for (std::uint32_t s : map.touched())
+    if (out.classed[s]) out.nonzero.push_back(s);
+  std::sort(out.nonzero.begin(), out.nonzero.end());
+  out.nonzero.erase(std::unique(out.nonzero.begin(), out.nonzero.end()), out.nonzero.end());  // a slot zeroed and hit again is listed twice
   return out;
 }
 
 inline Admit has_new_bits(const ClassedTrace& trace, VirginMap& virgin) {
-  std::vector<std::uint8_t> rec;
-  detail::record_from_classed(trace, rec);
+  b200::SparseBatch one;
+  detail::pairs_from_classed(trace, one);
   b200::FeedbackResult r =
-      b200::feedback_batch(b200::default_context(), rec.data(), 1, virgin.data(), virgin.edge_counts());
+      b200::feedback_batch(b200::default_context(), one, virgin.data(), virgin.edge_counts());
   return static_cast<Admit>(r.admit[0]);
 }
 
 inline std::uint64_t trace_signature(const ClassedTrace& trace, SignatureMode mode) {
-  std::vector<std::uint8_t> rec;
-  detail::record_from_classed(trace, rec);
+  b200::SparseBatch one;
+  detail::pairs_from_classed(trace, one);
   std::vector<std::uint8_t> scratch_virgin(kMapSize, 0);
   std::uint64_t counts[2] = {0, 0};
   b200::FeedbackResult r =
-      b200::feedback_batch(b200::default_context(), rec.data(), 1, scratch_virgin.data(), counts);
+      b200::feedback_batch(b200::default_context(), one, scratch_virgin.data(), counts);
   return mode == SignatureMode::Full ? r.sig_full[0] : r.sig_simple[0];
 }
 

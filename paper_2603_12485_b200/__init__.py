@@ -14,8 +14,8 @@ from .api import (Context, SigSet, dispatch_batch, GAMMA, HOST_SLOTS, MAP_SIZE, 
                   record_bytes, rng_jump, rng_split, u64_to_i64)
 from .binding import (TargetError, deterministic_mutants, havoc_mutant, splice_mutant,  # noqa: F401
                       feedback_batch, feedback_batch_sparse, feedback_batch_compact, havoc_batch,
-                      default_context)
+                      default_context, signatures, replay_signatures)
 
 __all__ = ["Context", "MAP_SIZE", "HOST_SLOTS", "MAX_INPUT_BYTES", "havoc_mutant", "splice_mutant",
-           "deterministic_mutants", "feedback_batch", "feedback_batch_sparse", "feedback_batch_compact", "havoc_batch", "default_context",
+           "deterministic_mutants", "feedback_batch", "feedback_batch_sparse", "feedback_batch_compact", "havoc_batch", "default_context", "signatures", "replay_signatures",
            "record_bytes", "rng_jump", "rng_split", "HfzError", "TargetError"]

@@ -105,3 +105,52 @@ def feedback_batch_compact(compact: np.ndarray, compact_off: np.ndarray, wide, w
     slot | count << 16, plus (M, 2) wide pairs for counts >= 65,536 (or None, None)."""
     return default_context(device, api.MAP_SIZE).feedback_batch_compact_host(compact, compact_off, wide, wide_off,
                                                                              virgin, edge_counts, want_classed)
+
+
+def _as_pairs(m, map_slots):
+    """One execution's map in any of the accepted forms -> (entries (N, 2) uint32 of (slot, count))."""
+    if isinstance(m, (bytes, bytearray, memoryview)):
+        m = np.frombuffer(bytes(m), np.uint8)
+    a = np.asarray(m)
+    H = map_slots // 2
+    if a.dtype == np.uint8 and a.size == api.record_bytes(map_slots):      # dense raw record
+        host = a[:H]
+        dev = a[H:].view(np.uint32)
+        hs = np.nonzero(host)[0]
+        ds = np.nonzero(dev)[0]
+        out = np.empty((hs.size + ds.size, 2), np.uint32)
+        out[:hs.size, 0] = hs
+        out[:hs.size, 1] = host[hs]
+        out[hs.size:, 0] = ds + H
+        out[hs.size:, 1] = dev[ds]
+        return out
+    a = np.ascontiguousarray(a, dtype=np.uint32)
+    if a.ndim == 2 and a.shape[1] == 2:                                  # (slot, count) pairs, any order
+        return a
+    raise TypeError("a map is a dense raw record (bytes / uint8 array of map_slots/2*5 bytes) or an (N, 2) array "
+                    "of (slot, count) pairs")
+
+
+def replay_signatures(maps, device: int = 0, map_slots: int = api.MAP_SIZE):
+    """The hot-path part of the reference's ``replay_sequence`` (bindings.cpp:268-286, which returns
+    ``full_sigs`` / ``simple_sigs`` of the executed inputs): the same two lists for maps the caller
+    already holds -- the simulator that produces them is out of scope here.  Each map is a dense raw
+    record or an (N, 2) array of (slot, count) pairs.  Also returns ``nonzero_slots`` per map."""
+    pairs = [_as_pairs(m, map_slots) for m in maps]
+    off = np.zeros(len(pairs) + 1, np.uint64)
+    np.cumsum([p.shape[0] for p in pairs], out=off[1:])
+    ent = np.concatenate(pairs) if pairs else np.zeros((0, 2), np.uint32)
+    if ent.shape[0] == 0:
+        ent = np.zeros((1, 2), np.uint32)
+    o = default_context(device, map_slots).feedback_batch_sparse_host(
+        np.ascontiguousarray(ent), off, np.zeros(map_slots, np.uint8), np.zeros(2, np.uint64))
+    return {"full_sigs": [int(x) for x in o["sig_full"]], "simple_sigs": [int(x) for x in o["sig_simple"]],
+            "nonzero_slots": [int(x) for x in o["nnz"]]}
+
+
+def signatures(m, device: int = 0, map_slots: int = api.MAP_SIZE):
+    """The hot-path outputs of the reference's ``run_input`` (bindings.cpp:199-202) for a map the caller
+    already holds: ``{"nonzero_slots", "full_sig", "simple_sig"}`` -- classify_trace + both trace_signature
+    calls on the GPU."""
+    r = replay_signatures([m], device, map_slots)
+    return {"nonzero_slots": r["nonzero_slots"][0], "full_sig": r["full_sigs"][0], "simple_sig": r["simple_sigs"][0]}

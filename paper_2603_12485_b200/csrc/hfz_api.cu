@@ -48,7 +48,7 @@ extern "C" int hfz_ctx_create(hfz_ctx** out, int device, uint32_t map_slots, voi
   HFZ_CUDA(cudaSetDevice(device));
   cudaDeviceProp prop;
   HFZ_CUDA(cudaGetDeviceProperties(&prop, device));
-  if (prop.major < 10) {
+  if (prop.major != 10 || prop.minor != 0) {
     hfz_set_error("device %d is sm_%d%d; the kernels are built for sm_100a only", device,
                   prop.major, prop.minor);
     return HFZ_ECUDA;
@@ -66,7 +66,7 @@ extern "C" int hfz_ctx_create(hfz_ctx** out, int device, uint32_t map_slots, voi
   if (a == cudaSuccess) a = cudaMalloc(&c->prior, map_slots);
   if (a == cudaSuccess) a = cudaMalloc(&c->delta, map_slots);
   if (a == cudaSuccess) a = cudaMalloc(&c->v0, map_slots);
-  if (a == cudaSuccess) a = cudaMalloc(&c->d_small, 8 * sizeof(unsigned long long));
+  if (a == cudaSuccess) a = cudaMalloc(&c->d_small, 32 * sizeof(unsigned long long));
   if (a != cudaSuccess) {
     hfz_ctx_destroy(c);
     hfz_set_error("hfz_ctx_create: scratch allocation failed (%s)", cudaGetErrorString(a));
@@ -97,6 +97,7 @@ extern "C" int hfz_ctx_destroy(hfz_ctx* c) {
     cudaEventDestroy(ev.second);
   }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->ev_stream) cudaEventDestroy(c->ev_stream);
   cudaFree(c->d_virgin);
   cudaFree(c->d_counts);
   cudaFree(c->d_admit);
@@ -113,6 +114,11 @@ extern "C" int hfz_ctx_destroy(hfz_ctx* c) {
   cudaFree(c->ts_sorted);
   cudaFree(c->ts_cnt);
   cudaFree(c->sp_cnt);
+  cudaFree(c->ss_first[0]);
+  cudaFree(c->ss_first[1]);
+  cudaFree(c->ss_counts);
+  cudaFree(c->ss_nov);
+  cudaFree(c->ss_deltas);
   for (cudaEvent_t ev : c->sp_events) cudaEventDestroy(ev);
   delete c;
   return HFZ_OK;
@@ -120,6 +126,13 @@ extern "C" int hfz_ctx_destroy(hfz_ctx* c) {
 
 extern "C" int hfz_ctx_set_stream(hfz_ctx* c, void* stream) {
   if (!c) return HFZ_EINVAL;
+  if (c->stream == (cudaStream_t)stream) return HFZ_OK;
+  // The context's scratch (first-occurrence tables, candidate lists, prior, piece lists) is shared by
+  // all calls: work already enqueued on the old stream must finish before the new stream touches it.
+  HFZ_CUDA(cudaSetDevice(c->device));
+  if (!c->ev_stream) HFZ_CUDA(cudaEventCreateWithFlags(&c->ev_stream, cudaEventDisableTiming));
+  HFZ_CUDA(cudaEventRecord(c->ev_stream, c->stream));
+  HFZ_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, c->ev_stream, 0));
   c->stream = (cudaStream_t)stream;
   return HFZ_OK;
 }
@@ -152,6 +165,10 @@ extern "C" int hfz_ctx_set_option(hfz_ctx* c, const char* key, int64_t value) {
     c->scan_pipe = value;
   } else if (!strcmp(key, "scan_two_stage")) {
     c->scan_two_stage = value;
+  } else if (!strcmp(key, "small_fused")) {
+    c->small_fused = value != 0;
+  } else if (!strcmp(key, "step_probe")) {
+    c->ss_dbg = value != 0;
   } else if (!strcmp(key, "time_scan")) {
     c->time_scan = value != 0;
   } else if (!strcmp(key, "sparse_native")) {
@@ -190,6 +207,28 @@ extern "C" int hfz_ctx_get_stat(hfz_ctx* c, const char* key, double* out) {
     *out = total;
     return HFZ_OK;
   }
+  if (!strcmp(key, "ignored_pairs")) {  // pairs with slot >= S seen by the last sparse fold (device or host call)
+    unsigned long long bad = 0;
+    HFZ_CUDA(cudaStreamSynchronize(c->stream));
+    HFZ_CUDA(cudaMemcpy(&bad, c->d_small + 4, sizeof(bad), cudaMemcpyDeviceToHost));
+    *out = (double)bad;
+    return HFZ_OK;
+  }
+  if (!strncmp(key, "step_c", 6) && key[6] >= '0' && key[6] <= '7' && !key[7]) {  // dev probe: raw counters
+    unsigned long long t[8];
+    HFZ_CUDA(cudaStreamSynchronize(c->stream));
+    HFZ_CUDA(cudaMemcpy(t, c->d_small + 16, sizeof(t), cudaMemcpyDeviceToHost));
+    *out = (double)t[key[6] - '0'];
+    return HFZ_OK;
+  }
+  if (!strncmp(key, "step_t", 6) && key[6] >= '1' && key[6] <= '6' && !key[7]) {
+    // dev probe: microseconds from the fused step's first CTA start to the LAST CTA passing boundary k
+    unsigned long long t[8];
+    HFZ_CUDA(cudaStreamSynchronize(c->stream));
+    HFZ_CUDA(cudaMemcpy(t, c->d_small + 8, sizeof(t), cudaMemcpyDeviceToHost));
+    *out = t[key[6] - '0'] >= t[0] ? (double)(t[key[6] - '0'] - t[0]) / 1e3 : -1.0;
+    return HFZ_OK;
+  }
   hfz_set_error("hfz_ctx_get_stat: unknown key %s", key);
   return HFZ_EINVAL;
 }
@@ -199,11 +238,11 @@ extern "C" int hfz_ctx_get_stat(hfz_ctx* c, const char* key, double* out) {
 
 // copy stream, device copies of virgin / counters and per-exec outputs shared by the _host calls
 int hfz_ensure_host_common(hfz_ctx* c, uint64_t n_exec) {
-  if (!c->copy_stream) {
-    HFZ_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
-    HFZ_CUDA(cudaMalloc(&c->d_virgin, c->S));
-    HFZ_CUDA(cudaMalloc(&c->d_counts, 2 * sizeof(uint64_t)));
-  }
+  // each resource on its own: a failed allocation is retried by the next call instead of leaving a
+  // null pointer behind an "already initialised" flag
+  if (!c->copy_stream) HFZ_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  if (!c->d_virgin) HFZ_CUDA(cudaMalloc(&c->d_virgin, c->S));
+  if (!c->d_counts) HFZ_CUDA(cudaMalloc(&c->d_counts, 2 * sizeof(uint64_t)));
   if (c->d_out_cap < n_exec) {
     cudaFree(c->d_admit);
     cudaFree(c->d_sigf);

@@ -44,6 +44,7 @@ struct hfz_ctx {
   uint8_t* stage_raw[2] = {nullptr, nullptr};
   uint64_t stage_execs = 0;
   cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_stream = nullptr;  // orders a new stream after the old one (hfz_ctx_set_stream)
   cudaEvent_t ev_copied[2] = {nullptr, nullptr};
   cudaEvent_t ev_done[2] = {nullptr, nullptr};
   uint8_t* d_virgin = nullptr;
@@ -99,6 +100,19 @@ struct hfz_ctx {
   uint32_t* ts_cnt = nullptr;     // [n_exec][pieces] entries per piece, then [n_exec] novel-slot counters
   uint64_t ts_cnt_cap = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> scan_events;
+
+  // fused small step (hfz_k_small_step, hfz_feedback.cu; owned, lazily allocated)
+  int small_fused = 1;            // small dense batches: the whole fold as one cooperative launch
+  int coop_grid = -1;             // co-resident grid of the fused step (-1 = not probed, 0 = unsupported)
+  uint32_t* ss_first[2] = {nullptr, nullptr};  // double-buffered first-occurrence tables, all-ones between calls
+  int ss_pp = 0;                  // table / candidate counter the last call used
+  uint32_t* ss_counts = nullptr;  // [2] candidate counters, zero between calls
+  uint32_t* ss_nov = nullptr;     // [n_exec] novel-slot counters, zero between calls
+  uint64_t ss_nov_cap = 0;
+  uint8_t* ss_deltas = nullptr;   // staging for peer deltas (resolve_peers after a fused scan)
+  int ss_dbg = 0;                 // dev probe: phase timestamps of the fused step in d_small[8..16)
+  bool sc_small = false;          // last scan was the scan half of the fused step
+  std::vector<uint8_t> sc_step;   // its parameters, for the resolve half
 };
 
 void hfz_set_error(const char* fmt, ...);

@@ -13,10 +13,15 @@
 //    Admit code then only depends on whether it is that first exec (resolve kernel, runs on
 //    the few candidate maps only).  Final virgin = V0 | OR of the novelty deltas (merge).
 #include <stdio.h>
+#include <string.h>
+
+#include <cooperative_groups.h>
 
 #include <type_traits>
 
 #include "hfz_common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -710,15 +715,16 @@ struct ResolveParams {
 
 __device__ __forceinline__ uint32_t first_any(const uint32_t* first, uint32_t idx) {
   const uint4* f = reinterpret_cast<const uint4*>(first + (size_t)idx * 8);
-  const uint4 a = f[0], b = f[1];
+  const uint4 a = __ldcg(f), b = __ldcg(f + 1);
   return min(min(min(a.x, a.y), min(a.z, a.w)), min(min(b.x, b.y), min(b.z, b.w)));
 }
 
 __device__ __forceinline__ uint32_t resolve_entry(const ResolveParams& p, uint32_t idx,
                                                   uint32_t klass, uint32_t e) {
-  const uint32_t pr = __ldg(p.prior + idx);
+  // (L2 loads: in the fused step these tables were written earlier in the SAME launch by other SMs)
+  const uint32_t pr = __ldcg(p.prior + idx);
   if (!(klass & ~pr)) return 0;
-  if (p.first[(size_t)idx * 8 + (31 - __clz(klass))] != e) return 0;  // an earlier exec had it
+  if (__ldcg(p.first + (size_t)idx * 8 + (31 - __clz(klass))) != e) return 0;  // an earlier exec had it
   if (pr == 0 && first_any(p.first, idx) == e) return 2;              // slot never seen before e
   return 1;
 }
@@ -1025,14 +1031,11 @@ struct CompactParams {
   uint8_t* classed;
 };
 
-__global__ void __launch_bounds__(256) hfz_k_compact(const CompactParams p) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const uint64_t items = p.n_exec * p.pieces;
-  const uint32_t lane_lt = (1u << lane) - 1u;
-  (void)lane_lt;
-  for (uint64_t it = warp; it < items; it += nwarps) {
+// one work item of the compact stage: (map, piece) by one warp.  `staged` = the piece already in
+// shared memory (fused step: TMA bulk copy), or null = stream it from global memory.
+__device__ __forceinline__ void compact_item(const CompactParams& p, uint64_t it, uint32_t lane,
+                                             const uint4* staged = nullptr) {
+  {
     const uint64_t e64 = it / p.pieces;
     const uint32_t pc = (uint32_t)(it - e64 * p.pieces), e = (uint32_t)e64;
     const bool host = pc < p.host_pieces;
@@ -1047,7 +1050,7 @@ __global__ void __launch_bounds__(256) hfz_k_compact(const CompactParams p) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const uint32_t v = v0 + j * 32 + lane;
-        x[j] = v < vecs ? hfz_ldg_stream(src + v) : make_uint4(0, 0, 0, 0);
+        x[j] = v < vecs ? (staged ? staged[v] : hfz_ldg_stream(src + v)) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -1097,6 +1100,14 @@ __global__ void __launch_bounds__(256) hfz_k_compact(const CompactParams p) {
     }
     if (lane == 0) p.cnt[it] = fill;
   }
+}
+
+__global__ void __launch_bounds__(256) hfz_k_compact(const CompactParams p) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t items = p.n_exec * p.pieces;
+  for (uint64_t it = warp; it < items; it += nwarps) compact_item(p, it, lane);
 }
 
 // one lane per map: chains over the map's piece lists, nnz, candidate bookkeeping
@@ -1181,6 +1192,569 @@ __global__ void __launch_bounds__(256) hfz_k_resolve_pieces(const ResolveParams 
 }
 
 // ---------------------------------------------------------------------------
+// Small batches as ONE cooperative launch ("fused step").  The two-stage path above is latency-
+// bound by its launches: 7 kernels + 4 memsets for 26 us of HBM time at 1,024 maps.  Here the
+// whole fold -- compact, chains, candidate list, delta, ordered merge, resolve, Admit codes -- is
+// one persistent kernel (one 1,024-thread CTA per SM, cooperative launch) with two grid-wide
+// barriers, and nothing is memset between calls:
+//   * the first-occurrence table is double-buffered: a call uses one table (all-ones on entry)
+//     and scrubs the OTHER one, which the previous call left dirty, while it streams the maps;
+//   * the per-map novel counters are zeroed again by the warp that reads them; the candidate
+//     counter alternates between two words, each call zeroing the one the next call will use;
+//   * Admit codes of non-candidates are written (0) by the candidate pass, those of candidates by
+//     the resolve pass: one warp per candidate, no flag array, no separate admit kernel.
+//   phase 1   all warps: (map, piece) items -> ordered piece lists + first-occurrence updates
+//   --- grid barrier ---
+//   phase 2   by role: one lane per map runs both FNV chains over its piece lists (32 maps per
+//             warp, the warps spread one per SM) | candidate list | delta + merge (4 slots per
+//             thread: delta word from the table, virgin |= delta, prior, edge counters)
+//   --- grid barrier ---
+//   phase 3   one warp per candidate: exact Admit code from the first-occurrence table
+// The scan and resolve halves can also be launched separately (multi-rank: the deltas of all ranks
+// are exchanged in between); the resolve half then starts with the rank-ordered merge.
+struct StepParams {
+  CompactParams c;           // phase 1 (c.first = this call's table)
+  uint32_t* first_prev;      // the other table, scrubbed to all-ones (scan half)
+  uint64_t* sig_full;
+  uint64_t* sig_simple;
+  uint32_t* nnz;
+  uint8_t* delta_out;        // this rank's novelty delta (S bytes)
+  uint32_t* cand_list;
+  uint32_t* cand_nov;
+  uint32_t* cand_count;      // [1] candidates of this call (zero on entry)
+  uint32_t* cand_count_next; // [1] zeroed for the next call
+  uint8_t* virgin;           // resolve half: virgin_inout
+  uint8_t* prior;            // P_r
+  unsigned long long* edge_counts;
+  const uint8_t* deltas;     // n_ranks x S (== delta_out when fused)
+  uint32_t n_ranks, rank;
+  uint8_t* admit;
+  int do_scan, do_resolve;
+  unsigned long long* dbg;   // optional: [8] latest %globaltimer at each phase boundary (dev probe)
+};
+
+__device__ __forceinline__ void dbg_mark(const StepParams& p, int k) {
+  if (p.dbg && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (k == 0) atomicMin(p.dbg + 0, t); else atomicMax(p.dbg + k, t);
+  }
+}
+
+__device__ __forceinline__ uint32_t piece_slot0(const CompactParams& c, uint32_t pc) {
+  return pc < c.host_pieces ? pc * c.piece : c.H + (pc - c.host_pieces) * (c.piece / 4);
+}
+
+constexpr int kStepWarps = 24;
+constexpr uint32_t kStepBuf = 8192;                 // shared memory per warp: two staging buffers of one piece (phase 1),
+constexpr uint32_t kStepPiece = kStepBuf / 2;       //   then one list buffer of kStepCap entries (phase 2)
+constexpr uint32_t kStepCap = kStepBuf / 4;
+
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(hfz_smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+constexpr uint32_t kDescCap = 256;  // element descriptors buffered per warp between two lane-parallel passes
+
+constexpr size_t kStepSmem = (size_t)kStepWarps * (kStepBuf + kDescCap * 4 + 16);  // staging + descriptors + 2 mbarriers per warp
+
+// Compaction of one staged piece, in two loops so that the expensive per-element work runs with
+// all lanes busy: loop 1 (per 512-byte row: element masks, one warp scan) only drops a 4-byte
+// descriptor `local slot | count << 12` per non-zero element into a shared buffer at its rank;
+// loop 2 walks the buffer one element per lane: classification, virgin test, first-occurrence
+// update, and the ordered list entries go out as coalesced stores.  (A 2 %-dense row has ~10
+// non-zero elements spread over 32 lanes: doing the per-element work in loop 1 kept 5 of 32 lanes
+// busy.)  Device counts are clipped at 65,536, the last rung boundary, to fit the descriptor.
+__device__ __noinline__ void compact_staged_rows(const CompactParams& p, uint64_t it, uint32_t lane, const uint4* src,
+                                                uint32_t* desc) {
+  const uint64_t e64 = it / p.pieces;
+  const uint32_t pc = (uint32_t)(it - e64 * p.pieces), e = (uint32_t)e64;
+  const bool host = pc < p.host_pieces;
+  const uint32_t slot0 = host ? pc * p.piece : p.H + (pc - p.host_pieces) * (p.piece / 4);
+  uint32_t* out = p.sorted + e64 * p.S + slot0;
+  uint8_t* classed_row = p.classed ? p.classed + e64 * p.S : nullptr;
+  uint32_t fill = 0, nbuf = 0;
+  const uint32_t vecs = p.piece / 16;
+  auto element = [&](uint32_t idx, uint32_t cnt, uint32_t pos) {
+    const uint32_t klass = host ? hfz_class_host(cnt) : hfz_class_device(cnt);
+    const uint32_t rung = 31 - __clz(klass);
+    const uint32_t en = idx | (rung << 24);
+    out[pos] = en;
+    if (klass & ~(uint32_t)__ldg(p.v0 + idx)) {
+      const uint32_t k = atomicAdd(p.nov_cnt + e64, 1u);
+      if (k < kNovMax) p.novel_ent[e64 * kNovMax + k] = en;
+      atomicMin(p.first + (size_t)idx * 8 + rung, e);
+    }
+    if (classed_row) classed_row[idx] = (uint8_t)klass;
+  };
+  auto flush = [&]() {
+    __syncwarp();
+    for (uint32_t t = lane; t < nbuf; t += 32) {
+      const uint32_t d = desc[t];
+      element(slot0 + (d & 0xfffu), d >> 12, fill + t);
+    }
+    fill += nbuf;
+    nbuf = 0;
+    __syncwarp();
+  };
+  for (uint32_t v0 = 0; v0 < vecs; v0 += 32) {
+    const uint32_t v = v0 + lane;
+    const uint4 x = v < vecs ? src[v] : make_uint4(0, 0, 0, 0);
+    uint32_t m;
+    if (host)
+      m = nz_bytes(x.x) | (nz_bytes(x.y) << 4) | (nz_bytes(x.z) << 8) | (nz_bytes(x.w) << 12);
+    else
+      m = (x.x != 0u) | ((x.y != 0u) << 1) | ((x.z != 0u) << 2) | ((x.w != 0u) << 3);
+    if (!__any_sync(0xffffffffu, m != 0u)) continue;
+    const uint32_t cn = __popc(m);
+    uint32_t inc = cn;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += o;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+    if (nbuf + total > kDescCap) flush();
+    const bool direct = total > kDescCap;  // a dense row: per-lane element work, no buffering
+    uint32_t pos = (direct ? fill : nbuf) + inc - cn;
+    while (m) {
+      const uint32_t b = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t wi = host ? (b >> 2) : b;
+      const uint32_t word = wi == 0 ? x.x : (wi == 1 ? x.y : (wi == 2 ? x.z : x.w));
+      const uint32_t local = host ? v * 16 + b : v * 4 + b;
+      const uint32_t cnt = host ? ((word >> (8 * (b & 3))) & 0xffu) : min(word, 65536u);
+      if (direct)
+        element(slot0 + local, cnt, pos++);
+      else
+        desc[pos++] = local | (cnt << 12);
+    }
+    if (direct) fill += total; else nbuf += total;
+  }
+  flush();
+  if (lane == 0) p.cnt[it] = fill;
+}
+
+// The usual (sparse) piece: every lane owns a CONTIGUOUS span of the piece (8 vectors = 128 bytes of
+// a 4 KB piece), so ascending slot order is lane-major and ONE warp scan of the per-lane element
+// counts ranks the whole piece (the row-wise version above needs one scan per 512-byte row, and the
+// dependent shuffles were what a piece cost).  The lane's vectors are read in a rotated order
+// (vector (j + lane) mod 8 at step j: the 8 lanes of a quarter-warp then touch 8 different bank
+// groups, no conflicts for the 128-byte lane stride) and their element masks are merged into one
+// bitset in true order, which the lane then walks: descriptor = local slot | count << 12, the
+// count read back from the staged bytes.  Loop 2 is the lane-parallel element pass as above.
+__device__ __forceinline__ void compact_staged(const CompactParams& p, uint32_t it, uint32_t lane, const uint4* src,
+                                               uint32_t* desc) {
+  const uint32_t e = it / p.pieces;
+  const uint32_t pc = it - e * p.pieces;
+  const bool host = pc < p.host_pieces;
+  const uint32_t vpl = p.piece / 512;  // vectors per lane: 8 for the 4 KB piece (1, 2, 4 for tiny maps)
+  if (vpl == 0) {                      // pieces below 512 bytes (maps of fewer than 1,024 slots): row-wise path
+    compact_staged_rows(p, it, lane, src, desc);
+    return;
+  }
+  uint64_t w0 = 0, w1 = 0;             // element bitset of the lane's span, true order (host: 1 bit per byte, 128 bits;
+  const uint4* mine = src + lane * vpl;  // device: 1 bit per u32, 32 bits)
+#pragma unroll
+  for (uint32_t j = 0; j < 8; ++j) {
+    if (j < vpl) {
+      const uint32_t t = (j + lane) & (vpl - 1);
+      const uint4 x = mine[t];
+      if (host) {
+        const uint64_t m = nz_bytes(x.x) | (nz_bytes(x.y) << 4) | (nz_bytes(x.z) << 8) | (nz_bytes(x.w) << 12);
+        if (t < 4) w0 |= m << (16 * t); else w1 |= m << (16 * (t - 4));
+      } else {
+        const uint32_t m = (x.x != 0u) | ((x.y != 0u) << 1) | ((x.z != 0u) << 2) | ((x.w != 0u) << 3);
+        w0 |= (uint64_t)m << (4 * t);
+      }
+    }
+  }
+  const uint32_t cn = __popcll(w0) + __popcll(w1);
+  uint32_t inc = cn;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+  if (total == 0) {
+    if (lane == 0) p.cnt[it] = 0;
+    return;
+  }
+  if (total > kDescCap) {  // a dense piece: the row-wise path handles any density
+    compact_staged_rows(p, it, lane, src, desc);
+    return;
+  }
+  // loop 1: descriptors at their rank
+  uint32_t pos = inc - cn;
+  const uint8_t* bytes = reinterpret_cast<const uint8_t*>(mine);
+  const uint32_t span0 = host ? lane * vpl * 16 : lane * vpl * 4;  // first local slot of the lane's span
+  if (host) {
+    while (w0) {
+      const uint32_t g = __ffsll((long long)w0) - 1;
+      w0 &= w0 - 1;
+      desc[pos++] = (span0 + g) | ((uint32_t)bytes[g] << 12);
+    }
+    while (w1) {
+      const uint32_t g = 64 + __ffsll((long long)w1) - 1;
+      w1 &= w1 - 1;
+      desc[pos++] = (span0 + g) | ((uint32_t)bytes[g] << 12);
+    }
+  } else {
+    uint32_t w = (uint32_t)w0;
+    while (w) {
+      const uint32_t g = __ffs(w) - 1;
+      w &= w - 1;
+      desc[pos++] = (span0 + g) | (min(reinterpret_cast<const uint32_t*>(mine)[g], 65536u) << 12);
+    }
+  }
+  __syncwarp();
+  // loop 2: one element per lane
+  const uint32_t slot0 = host ? pc * p.piece : p.H + (pc - p.host_pieces) * (p.piece / 4);
+  uint32_t* out = p.sorted + (uint64_t)e * p.S + slot0;
+  uint8_t* classed_row = p.classed ? p.classed + (uint64_t)e * p.S : nullptr;
+  for (uint32_t t = lane; t < total; t += 32) {
+    const uint32_t d = desc[t];
+    const uint32_t idx = slot0 + (d & 0xfffu), cnt = d >> 12;
+    const uint32_t klass = host ? hfz_class_host(cnt) : hfz_class_device(cnt);
+    const uint32_t rung = 31 - __clz(klass);
+    const uint32_t en = idx | (rung << 24);
+    out[t] = en;
+    const bool novel = (klass & ~(uint32_t)__ldg(p.v0 + idx)) != 0u;
+    // one counter update per warp and pass, not per element (cold start: every element is novel)
+    const uint32_t act = __activemask();
+    const uint32_t nm = __ballot_sync(act, novel);
+    if (nm) {
+      uint32_t k0 = 0;
+      const uint32_t leader = __ffs(nm) - 1;
+      if (lane == leader) k0 = atomicAdd(p.nov_cnt + e, __popc(nm));
+      k0 = __shfl_sync(act, k0, leader);
+      if (novel) {
+        const uint32_t k = k0 + __popc(nm & ((1u << lane) - 1u));
+        if (k < kNovMax) p.novel_ent[(uint64_t)e * kNovMax + k] = en;
+        atomicMin(p.first + (size_t)idx * 8 + rung, e);
+      }
+    }
+    if (classed_row) classed_row[idx] = (uint8_t)klass;
+  }
+  if (lane == 0) p.cnt[it] = total;
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kStepWarps * 32, 1) hfz_k_small_step(const StepParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  cg::grid_group grid = cg::this_grid();
+  const CompactParams& c = p.c;
+  const uint32_t lane = threadIdx.x & 31, wic = threadIdx.x >> 5;
+  const uint64_t W = (uint64_t)gridDim.x * kStepWarps;
+  const uint64_t gw = (uint64_t)wic * gridDim.x + blockIdx.x;  // consecutive warps sit on different SMs
+  const uint64_t gthread = gw * 32 + lane, nthreads = W * 32;
+  const bool fused = p.do_scan && p.do_resolve;
+  const uint4 ones = make_uint4(kNone, kNone, kNone, kNone);
+  uint8_t* wbuf = smem + (size_t)wic * kStepBuf;
+  uint32_t* desc = reinterpret_cast<uint32_t*>(smem + (size_t)kStepWarps * kStepBuf) + wic * kDescCap;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kStepWarps * (kStepBuf + kDescCap * 4)) + wic * 2;
+
+  dbg_mark(p, 0);
+  if (p.do_scan) {
+    if (gthread == 0) *p.cand_count_next = 0;
+    // ---- phase 1: compact.  (map, piece) items dealt round-robin over all warps of the grid; the
+    // piece is staged in shared memory by ONE TMA bulk copy per item (SASS: UBLKCP), double-buffered:
+    // item k + 1 is in flight while item k is compacted.
+    if (lane == 0) {
+      hfz_mbar_init(bars + 0, 1);
+      hfz_mbar_init(bars + 1, 1);
+      hfz_fence_barrier_init();
+    }
+    __syncwarp();
+    const uint64_t items = c.n_exec * c.pieces;
+    const uint64_t pol = hfz_policy_evict_first();
+    auto issue = [&](uint64_t it, uint32_t b) {
+      if (lane == 0) {
+        const uint64_t e64 = it / c.pieces;
+        const uint32_t pc = (uint32_t)(it - e64 * c.pieces);
+        hfz_fence_proxy_async();  // the buffer's last readers (generic proxy) are done: ordered before the async write
+        hfz_mbar_expect_tx(bars + b, c.piece);
+        hfz_bulk_g2s_stream(wbuf + b * kStepPiece, c.raw + e64 * c.rec_bytes + (uint64_t)pc * c.piece, c.piece, bars + b, pol);
+      }
+    };
+    if (gw < items) issue(gw, 0);
+    uint32_t k = 0;
+    long long t_wait = 0, t_work = 0;
+    for (uint64_t it = gw; it < items; it += W, ++k) {
+      const uint32_t b = k & 1;
+      if (it + W < items) issue(it + W, b ^ 1);
+      const long long t0 = clock64();
+      hfz_mbar_wait(bars + b, (k >> 1) & 1);
+      const long long t1 = clock64();
+      compact_staged(c, (uint32_t)it, lane, reinterpret_cast<const uint4*>(wbuf + b * kStepPiece), desc);
+      __syncwarp();
+      t_wait += t1 - t0;
+      t_work += clock64() - t1;
+    }
+    if (p.dbg && gw == 0 && lane == 0) {
+      p.dbg[11] = (unsigned long long)t_wait;
+      p.dbg[12] = (unsigned long long)t_work;
+      p.dbg[13] = k;
+    }
+    dbg_mark(p, 1);
+    // scrub the previous call's table (nobody reads it in this launch)
+    for (uint64_t s = gthread; s < c.S; s += nthreads) {
+      uint4* f = reinterpret_cast<uint4*>(p.first_prev + s * 8);
+      const uint4 a = f[0], b = f[1];
+      if ((a.x & a.y & a.z & a.w & b.x & b.y & b.z & b.w) != kNone) {
+        f[0] = ones;
+        f[1] = ones;
+      }
+    }
+    dbg_mark(p, 2);
+    __threadfence();
+    grid.sync();
+    dbg_mark(p, 3);
+
+    // ---- phase 2, by role: [0, D) delta (+ merge), [D, D + G) candidate list, then one warp per two maps: chains
+    const uint64_t D = c.S / 128;  // warps: 4 slots per thread
+    const uint64_t G = (c.n_exec + 31) / 32;
+    uint32_t newh = 0, newd = 0;
+    for (uint64_t role = gw; role < D + G + (c.n_exec + 1) / 2; role += W) {
+      if (role < D) {
+        // delta word of 4 slots from the table; fused: the single-rank merge right here
+        const uint64_t t = role * 32 + lane;  // word index, < S / 4
+        const uint4* f = reinterpret_cast<const uint4*>(c.first + t * 32);
+        uint32_t d = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint4 a = __ldcg(f + 2 * q), b = __ldcg(f + 2 * q + 1);
+          const uint32_t byte = (a.x != kNone) | ((a.y != kNone) << 1) | ((a.z != kNone) << 2) | ((a.w != kNone) << 3) |
+                                ((b.x != kNone) << 4) | ((b.y != kNone) << 5) | ((b.z != kNone) << 6) | ((b.w != kNone) << 7);
+          d |= byte << (8 * q);
+        }
+        reinterpret_cast<uint32_t*>(p.delta_out)[t] = d;
+        if (fused) {
+          uint32_t* vw = reinterpret_cast<uint32_t*>(p.virgin) + t;
+          const uint32_t old = *vw, nw = old | d;
+          reinterpret_cast<uint32_t*>(p.prior)[t] = old;
+          if (nw != old) *vw = nw;
+          const uint32_t turned = __popc(nz_bytes(nw) & ~nz_bytes(old));
+          if (t * 4 < c.H) newh += turned; else newd += turned;
+        }
+      } else if (role < D + G) {
+        // candidate list: maps with any novelty versus V0; the counters are left zeroed
+        const uint64_t e = (role - D) * 32 + lane;
+        const uint32_t novel = e < c.n_exec ? __ldcg(c.nov_cnt + e) : 0u;
+        const uint32_t cm = __ballot_sync(0xffffffffu, novel != 0u);
+        if (cm) {
+          uint32_t basei = 0;
+          if (lane == 0) basei = atomicAdd(p.cand_count, __popc(cm));
+          basei = __shfl_sync(0xffffffffu, basei, 0);
+          if (novel) {
+            const uint32_t ci = basei + __popc(cm & ((1u << lane) - 1u));
+            p.cand_list[ci] = (uint32_t)e;
+            p.cand_nov[ci] = novel <= kNovMax ? novel : kNovMax + 1;
+            c.nov_cnt[e] = 0;
+          }
+        }
+        if (fused && e < c.n_exec && !novel) p.admit[e] = 0;
+      } else {
+        // chains of TWO maps per warp.  The warp gathers the maps' ordered piece lists into shared
+        // memory (cp.async; one piece per lane, every copy in flight at once), then lanes 0/1 run the
+        // Full/Simple chains of the first map and lanes 2/3 those of the second over the buffers --
+        // one instruction stream for the four chains.  A chain is serial (3 dependent multiply
+        // steps per entry), so what matters is that nothing else sits on its critical path and
+        // that a scheduler has at most one such warp to issue for.
+        const uint64_t ea = (role - D - G) * 2;
+        uint32_t* buf = reinterpret_cast<uint32_t*>(wbuf);
+        constexpr uint32_t kHalf = kStepCap / 2;  // entries per map per round
+        // per-lane chain state (lanes 0..3)
+        uint32_t lo = (uint32_t)HFZ_FNV_OFFSET, hi = (uint32_t)(HFZ_FNV_OFFSET >> 32);
+        const bool full_lane = (lane & 1) == 0;
+        const uint32_t cmask = full_lane ? 0xffu : 0u, p3lo = full_lane ? 0x1b3u : 1u, p3hi = full_lane ? 0x100u : 0u;
+        uint32_t cur_pc[2] = {0, 0}, cur_i[2] = {0, 0}, nnz[2] = {0, 0};
+        const long long tg0 = clock64();
+        for (;;) {
+          uint32_t got[2] = {0, 0};
+#pragma unroll
+          for (int m = 0; m < 2; ++m) {
+            const uint64_t e = ea + m;
+            if (e >= c.n_exec) continue;
+            uint32_t* dst = buf + m * kHalf;
+            const uint32_t* base = c.sorted + e * c.S;
+            const uint32_t* cnt = c.cnt + e * c.pieces;
+            uint32_t pos = 0;
+            while (cur_pc[m] < c.pieces && pos < kHalf) {
+              if (cur_i[m] == 0) {
+                // whole pieces, one per lane: as many leading pieces of this batch as still fit
+                const uint32_t pcl = cur_pc[m] + lane;
+                const uint32_t my_n = pcl < c.pieces ? __ldcg(cnt + pcl) : 0u;
+                uint32_t inc = my_n;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                  const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+                  if (lane >= d) inc += o;
+                }
+                const uint32_t fits = __ballot_sync(0xffffffffu, inc <= kHalf - pos);
+                uint32_t k = fits == 0xffffffffu ? 32u : (uint32_t)__ffs(~fits) - 1u;  // leading lanes whose pieces fit
+                k = min(k, c.pieces - cur_pc[m]);
+                if (k) {
+                  if (lane < k) {
+                    const uint32_t* list = base + piece_slot0(c, pcl);
+                    uint32_t* d0 = dst + pos + inc - my_n;
+                    for (uint32_t i = 0; i < my_n; ++i) cp_async4(d0 + i, list + i);
+                  }
+                  pos += __shfl_sync(0xffffffffu, inc, k - 1);
+                  cur_pc[m] += k;
+                  continue;
+                }
+              }
+              // a piece that does not fit the rest of the buffer: part of it, coalesced
+              const uint32_t n_pc = __ldcg(cnt + cur_pc[m]);
+              const uint32_t take = min(n_pc - cur_i[m], kHalf - pos);
+              const uint32_t* list = base + piece_slot0(c, cur_pc[m]) + cur_i[m];
+              for (uint32_t i = lane; i < take; i += 32) cp_async4(dst + pos + i, list + i);
+              pos += take;
+              cur_i[m] += take;
+              if (cur_i[m] == n_pc) {
+                ++cur_pc[m];
+                cur_i[m] = 0;
+              }
+            }
+            got[m] = pos;
+            nnz[m] += pos;
+          }
+          if (got[0] == 0 && got[1] == 0) break;
+          cp_async_wait_all();
+          __syncwarp();
+          const long long tc0 = clock64();
+          if (p.dbg && ea == 0 && lane == 0) p.dbg[8] = (unsigned long long)(tc0 - tg0);
+          if (lane < 4) {
+            const uint32_t* mybuf = buf + (lane >> 1) * kHalf;
+            const uint32_t n_my = (lane >> 1) ? got[1] : got[0];
+            // h = (h ^ byte) * P, P = 2^40 + 0x1b3, in 32-bit halves: lo' depends on lo alone and
+            // hi' = hi * 0x1b3 + t with t off the lo chain.  The class byte step is the same code on all
+            // four lanes: the Simple lanes multiply by 1.  Measured 53-64 cycles per entry: a lone warp
+            // owns its scheduler, but every IMAD occupies the 16-lane pipe for two cycles whether 4 or
+            // 32 lanes are active, so the ~20 instructions per entry are what bounds it (splitting the
+            // 64-bit product into IMAD + IMAD.HI to shorten the dependency made it slower: 72 cycles).
+            auto fnv32 = [&](uint32_t byte, uint32_t plo, uint32_t phi) {
+              const uint32_t x = lo ^ byte;
+              const uint64_t w = (uint64_t)x * plo;
+              const uint32_t t = (uint32_t)(w >> 32) + x * phi;
+              hi = hi * plo + t;
+              lo = (uint32_t)w;
+            };
+            auto step = [&](uint32_t en) {
+              fnv32(en & 0xffu, 0x1b3u, 0x100u);
+              fnv32((en >> 8) & 0xffu, 0x1b3u, 0x100u);
+              fnv32((1u << (en >> 24)) & cmask, p3lo, p3hi);
+            };
+            uint32_t i = 0;
+            if (n_my >= 4) {
+              uint4 cur = *reinterpret_cast<const uint4*>(mybuf);
+              for (; i + 8 <= n_my; i += 4) {
+                const uint4 nxt = *reinterpret_cast<const uint4*>(mybuf + i + 4);
+                step(cur.x); step(cur.y); step(cur.z); step(cur.w);
+                cur = nxt;
+              }
+              step(cur.x); step(cur.y); step(cur.z); step(cur.w);
+              i += 4;
+            }
+            for (; i < n_my; ++i) step(mybuf[i]);
+          }
+          if (p.dbg && ea == 0 && lane == 0) {
+            p.dbg[9] = (unsigned long long)(clock64() - tc0);
+            p.dbg[10] = got[0];
+          }
+          __syncwarp();
+        }
+        if (lane < 4) {
+          const uint64_t e = ea + (lane >> 1);
+          if (e < c.n_exec) {
+            const uint64_t h = ((uint64_t)hi << 32) | lo;
+            if (full_lane) {
+              p.sig_full[e] = h;
+              if (p.nnz) p.nnz[e] = (lane >> 1) ? nnz[1] : nnz[0];
+            } else {
+              p.sig_simple[e] = h;
+            }
+          }
+        }
+      }
+    }
+    if (fused) {
+      newh = __reduce_add_sync(0xffffffffu, newh);
+      newd = __reduce_add_sync(0xffffffffu, newd);
+      if (lane == 0) {
+        if (newh) atomicAdd(p.edge_counts + 0, (unsigned long long)newh);
+        if (newd) atomicAdd(p.edge_counts + 1, (unsigned long long)newd);
+      }
+    }
+    dbg_mark(p, 4);
+    if (!p.do_resolve) return;
+    __threadfence();
+    grid.sync();
+    dbg_mark(p, 5);
+  }
+
+  if (!fused) {
+    // resolve half on its own: rank-ordered merge first (prior = virgin before D_rank), Admit codes zeroed
+    uint32_t newh = 0, newd = 0;
+    for (uint64_t v = gthread; v < c.S / 16; v += nthreads) {
+      uint4 acc = reinterpret_cast<uint4*>(p.virgin)[v];
+      const uint4 old = acc;
+      for (uint32_t q = 0; q < p.n_ranks; ++q) {
+        if (q == p.rank) reinterpret_cast<uint4*>(p.prior)[v] = acc;
+        const uint4 d = reinterpret_cast<const uint4*>(p.deltas + (size_t)q * c.S)[v];
+        acc.x |= d.x; acc.y |= d.y; acc.z |= d.z; acc.w |= d.w;
+      }
+      reinterpret_cast<uint4*>(p.virgin)[v] = acc;
+      const uint32_t turned = __popc(nz_bytes(acc.x) & ~nz_bytes(old.x)) + __popc(nz_bytes(acc.y) & ~nz_bytes(old.y)) +
+                              __popc(nz_bytes(acc.z) & ~nz_bytes(old.z)) + __popc(nz_bytes(acc.w) & ~nz_bytes(old.w));
+      if (v * 16 < c.H) newh += turned; else newd += turned;
+    }
+    newh = __reduce_add_sync(0xffffffffu, newh);
+    newd = __reduce_add_sync(0xffffffffu, newd);
+    if (lane == 0) {
+      if (newh) atomicAdd(p.edge_counts + 0, (unsigned long long)newh);
+      if (newd) atomicAdd(p.edge_counts + 1, (unsigned long long)newd);
+    }
+    for (uint64_t e = gthread; e < c.n_exec; e += nthreads) p.admit[e] = 0;
+    __threadfence();
+    grid.sync();
+  }
+
+  // ---- phase 3: one warp per candidate
+  ResolveParams r;
+  r.S = c.S;
+  r.H = c.H;
+  r.prior = p.prior;
+  r.first = c.first;
+  const uint32_t n_cand = __ldcg(p.cand_count);
+  for (uint64_t ci = gw; ci < n_cand; ci += W) {
+    const uint32_t e = __ldcg(p.cand_list + ci), nov = __ldcg(p.cand_nov + ci);
+    uint32_t flags = 0;
+    if (nov <= kNovMax) {
+      if (lane < nov) {
+        const uint32_t en = __ldcg(c.novel_ent + (size_t)e * kNovMax + lane);
+        flags = resolve_entry(r, en & 0xffffffu, 1u << (en >> 24), e);
+      }
+    } else {  // more novel slots than were recorded: walk the map's ordered piece lists
+      for (uint32_t pc = 0; pc < c.pieces; ++pc) {
+        const uint32_t* list = c.sorted + (uint64_t)e * c.S + piece_slot0(c, pc);
+        const uint32_t n = __ldcg(c.cnt + (uint64_t)e * c.pieces + pc);
+        for (uint32_t i = lane; i < n; i += 32) {
+          const uint32_t en = __ldcg(list + i);
+          flags |= resolve_entry(r, en & 0xffffffu, 1u << (en >> 24), e);
+        }
+      }
+    }
+    flags = __reduce_or_sync(0xffffffffu, flags);
+    if (lane == 0) p.admit[e] = (flags & 2u) ? 2 : ((flags & 1u) ? 1 : 0);
+  }
+  dbg_mark(p, 6);
+}
+
+// ---------------------------------------------------------------------------
 // launch plumbing
 
 template <int ROW>
@@ -1262,6 +1836,29 @@ int launch_scan_pipe_r(hfz_ctx* ctx, const ScanParams& p, int row) {
                  : launch_scan_pipe_t<REC_CT, 512, VSMEM, false>(ctx, p);
 }
 
+// grow-only scratch with geometric slack (no cudaFree + cudaMalloc per slightly larger batch)
+template <typename T>
+int grow(T*& ptr, uint64_t& cap, uint64_t need, const char* what) {
+  if (cap >= need) return HFZ_OK;
+  uint64_t want = cap * 2 > need ? cap * 2 : need;
+  cudaFree(ptr);
+  ptr = nullptr;
+  cap = 0;
+  cudaError_t e = cudaMalloc(&ptr, want * sizeof(T));
+  if (e != cudaSuccess && want > need) {
+    cudaGetLastError();
+    want = need;
+    e = cudaMalloc(&ptr, want * sizeof(T));
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    hfz_set_error("%s: cudaMalloc of %llu bytes failed (%s)", what, (unsigned long long)(want * sizeof(T)), cudaGetErrorString(e));
+    return HFZ_ENOMEM;
+  }
+  cap = want;
+  return HFZ_OK;
+}
+
 // compact + chain for a dense batch; false when the scratch it would need is not allowed
 bool two_stage_fits(const hfz_ctx* ctx, uint64_t n_exec) {
   return n_exec * (uint64_t)ctx->S <= (1ull << 30);  // <= 4 GB of u32 entries
@@ -1283,27 +1880,10 @@ int launch_scan_two_stage(hfz_ctx* ctx, const ScanParams& sp) {
   p.first = sp.first;
   p.novel_ent = sp.novel_ent;
   p.classed = sp.classed;
-  const uint64_t need = sp.n_exec * (uint64_t)sp.S;
-  if (ctx->ts_sorted_cap < need) {
-    cudaFree(ctx->ts_sorted);
-    ctx->ts_sorted = nullptr;
-    ctx->ts_sorted_cap = 0;
-    cudaError_t e = cudaMalloc(&ctx->ts_sorted, need * 4);
-    if (e != cudaSuccess) {
-      hfz_set_error("two-stage scan: cudaMalloc of %llu scratch bytes failed (%s)", (unsigned long long)need * 4,
-                    cudaGetErrorString(e));
-      return HFZ_ENOMEM;
-    }
-    ctx->ts_sorted_cap = need;
-  }
-  const uint64_t need_cnt = sp.n_exec * (uint64_t)(p.pieces + 1);
-  if (ctx->ts_cnt_cap < need_cnt) {
-    cudaFree(ctx->ts_cnt);
-    ctx->ts_cnt = nullptr;
-    ctx->ts_cnt_cap = 0;
-    HFZ_CUDA(cudaMalloc(&ctx->ts_cnt, (need_cnt + 1024) * 4));
-    ctx->ts_cnt_cap = need_cnt + 1024;
-  }
+  // grow-only scratch with geometric slack (hfz.h documents the footprint: 4 x S bytes per exec)
+  int rc = grow(ctx->ts_sorted, ctx->ts_sorted_cap, sp.n_exec * (uint64_t)sp.S, "two-stage scan: piece lists");
+  if (rc) return rc;
+  if ((rc = grow(ctx->ts_cnt, ctx->ts_cnt_cap, sp.n_exec * (uint64_t)(p.pieces + 1), "two-stage scan: piece counts"))) return rc;
   p.sorted = ctx->ts_sorted;
   p.cnt = ctx->ts_cnt;
   p.nov_cnt = ctx->ts_cnt + sp.n_exec * (uint64_t)p.pieces;
@@ -1324,6 +1904,156 @@ int launch_scan_two_stage(hfz_ctx* ctx, const ScanParams& sp) {
   ctx->sc_host_pieces = p.host_pieces;
   ctx->sc_npieces = p.pieces;
   return HFZ_OK;
+}
+
+// ---- fused small step: host side
+int ensure_cand(hfz_ctx* ctx, uint64_t n_exec);
+bool small_step_ok(hfz_ctx* ctx, uint64_t n_exec) {
+  if (!ctx->small_fused || n_exec == 0) return false;
+  // measured on B200 (65,536 slots, warm): 4,096 maps 0.27 ms fused vs 0.36 ms pipelined; 8,192 maps 0.51 vs 0.41 ms
+  const uint64_t limit = ctx->scan_two_stage >= 0 ? (uint64_t)ctx->scan_two_stage : 4096;
+  if (n_exec > limit || !two_stage_fits(ctx, n_exec)) return false;
+  if (ctx->coop_grid < 0) {  // once: cooperative launch support and the co-resident grid size
+    int coop = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, ctx->device);
+    const size_t smem = kStepSmem;
+    if (coop && cudaFuncSetAttribute(hfz_k_small_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hfz_k_small_step, kStepWarps * 32, smem) == cudaSuccess && per_sm >= 1)
+      ctx->coop_grid = ctx->num_sms;
+    else
+      ctx->coop_grid = 0;
+    cudaGetLastError();
+  }
+  return ctx->coop_grid > 0;
+}
+
+int small_step_scratch(hfz_ctx* ctx, uint64_t n_exec, uint32_t pieces) {
+  int rc = ensure_cand(ctx, n_exec);
+  if (rc) return rc;
+  if ((rc = grow(ctx->ts_sorted, ctx->ts_sorted_cap, n_exec * (uint64_t)ctx->S, "small step: piece lists"))) return rc;
+  if ((rc = grow(ctx->ts_cnt, ctx->ts_cnt_cap, n_exec * (uint64_t)pieces, "small step: piece counts"))) return rc;
+  if (ctx->ss_nov_cap < n_exec) {  // per-map novel counters: zero between calls (the kernel re-zeroes what it reads)
+    const uint64_t old = ctx->ss_nov_cap;
+    if ((rc = grow(ctx->ss_nov, ctx->ss_nov_cap, n_exec, "small step: novel counters"))) return rc;
+    (void)old;
+    HFZ_CUDA(cudaMemsetAsync(ctx->ss_nov, 0, ctx->ss_nov_cap * 4, ctx->stream));
+  }
+  if (!ctx->ss_first[0]) {  // two first-occurrence tables (all-ones between calls) + the two candidate counters
+    const size_t bytes = (size_t)ctx->S * 8 * sizeof(uint32_t);
+    for (int i = 0; i < 2; ++i) {
+      HFZ_CUDA(cudaMalloc(&ctx->ss_first[i], bytes));
+      HFZ_CUDA(cudaMemsetAsync(ctx->ss_first[i], 0xff, bytes, ctx->stream));
+    }
+    HFZ_CUDA(cudaMalloc(&ctx->ss_counts, 2 * sizeof(uint32_t)));
+    HFZ_CUDA(cudaMemsetAsync(ctx->ss_counts, 0, 2 * sizeof(uint32_t), ctx->stream));
+  }
+  return HFZ_OK;
+}
+
+int launch_small_step(hfz_ctx* ctx, StepParams& p) {
+  void* args[] = {&p};
+  HFZ_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(hfz_k_small_step), dim3((unsigned)ctx->coop_grid),
+                                       dim3(kStepWarps * 32), args, kStepSmem, ctx->stream));
+  ++ctx->launches;
+  return HFZ_OK;
+}
+
+// scan half (and, with virgin_inout, the whole single-rank step) of a small dense batch
+int small_step_scan(hfz_ctx* ctx, const uint8_t* raw, uint64_t n_exec, const uint8_t* v0, uint8_t* classed,
+                    uint64_t* sig_full, uint64_t* sig_simple, uint32_t* nnz, uint8_t* delta_out,
+                    uint8_t* virgin_inout, uint64_t* edge_counts, uint8_t* admit) {
+  HFZ_CUDA(cudaSetDevice(ctx->device));
+  StepParams p;
+  CompactParams& c = p.c;
+  c.raw = raw;
+  c.n_exec = n_exec;
+  c.rec_bytes = ctx->rec_bytes;
+  c.S = ctx->S;
+  c.H = ctx->H;
+  // piece = what one TMA bulk copy stages for a warp (4 KB, or the whole host half of a tiny map)
+  uint32_t piece = kStepPiece;
+  while (ctx->H % piece) piece >>= 1;
+  c.piece = piece;
+  c.host_pieces = ctx->H / piece;
+  c.pieces = (uint32_t)(ctx->rec_bytes / piece);
+  int rc = small_step_scratch(ctx, n_exec, c.pieces);
+  if (rc) return rc;
+  if (classed) HFZ_CUDA(cudaMemsetAsync(classed, 0, n_exec * (size_t)ctx->S, ctx->stream));
+  ctx->ss_pp ^= 1;
+  c.v0 = v0;
+  c.first = ctx->ss_first[ctx->ss_pp];
+  c.novel_ent = ctx->cand_list + 4 * ctx->cand_cap;
+  c.sorted = ctx->ts_sorted;
+  c.cnt = ctx->ts_cnt;
+  c.nov_cnt = ctx->ss_nov;
+  c.classed = classed;
+  p.first_prev = ctx->ss_first[ctx->ss_pp ^ 1];
+  p.sig_full = sig_full;
+  p.sig_simple = sig_simple;
+  p.nnz = nnz;
+  p.delta_out = delta_out;
+  p.cand_list = ctx->cand_list;
+  p.cand_nov = ctx->cand_list + 2 * ctx->cand_cap;
+  p.cand_count = ctx->ss_counts + ctx->ss_pp;
+  p.cand_count_next = ctx->ss_counts + (ctx->ss_pp ^ 1);
+  p.virgin = virgin_inout;
+  p.prior = ctx->prior;
+  p.edge_counts = reinterpret_cast<unsigned long long*>(edge_counts);
+  p.deltas = delta_out;
+  p.n_ranks = 1;
+  p.rank = 0;
+  p.admit = admit;
+  p.do_scan = 1;
+  p.do_resolve = virgin_inout != nullptr;
+  p.dbg = ctx->ss_dbg ? ctx->d_small + 8 : nullptr;
+  if (p.dbg) {
+    HFZ_CUDA(cudaMemsetAsync(p.dbg, 0, 16 * 8, ctx->stream));
+    HFZ_CUDA(cudaMemsetAsync(p.dbg, 0xff, 8, ctx->stream));
+  }
+  ctx->sc_sparse = false;
+  ctx->sc_pieces = false;
+  ctx->sc_small = !p.do_resolve;  // a resolve-only launch follows (hfz_feedback_resolve)
+  if (ctx->sc_small) {
+    ctx->sc_step.resize(sizeof(StepParams));
+    memcpy(ctx->sc_step.data(), &p, sizeof(StepParams));
+  }
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (ctx->time_scan) {
+    HFZ_CUDA(cudaEventCreate(&ev0));
+    HFZ_CUDA(cudaEventCreate(&ev1));
+    HFZ_CUDA(cudaEventRecord(ev0, ctx->stream));
+  }
+  rc = launch_small_step(ctx, p);
+  if (ctx->time_scan) {
+    HFZ_CUDA(cudaEventRecord(ev1, ctx->stream));
+    ctx->scan_events.emplace_back(ev0, ev1);
+  }
+  return rc;
+}
+
+// resolve half after small_step_scan(virgin_inout = nullptr): merge in rank order + Admit codes
+int small_step_resolve(hfz_ctx* ctx, uint64_t n_exec, uint8_t* virgin_inout, uint64_t* edge_counts,
+                       const uint8_t* deltas, uint32_t n_ranks, uint32_t rank, uint8_t* admit) {
+  StepParams p;
+  if (ctx->sc_step.size() != sizeof(StepParams)) {
+    hfz_set_error("hfz_feedback_resolve: no scan to resolve");
+    return HFZ_EINVAL;
+  }
+  memcpy(&p, ctx->sc_step.data(), sizeof(StepParams));
+  if (p.c.n_exec != n_exec) {
+    hfz_set_error("hfz_feedback_resolve: n_exec differs from the scan's");
+    return HFZ_EINVAL;
+  }
+  HFZ_CUDA(cudaSetDevice(ctx->device));
+  p.virgin = virgin_inout;
+  p.edge_counts = reinterpret_cast<unsigned long long*>(edge_counts);
+  p.deltas = deltas;
+  p.n_ranks = n_ranks;
+  p.rank = rank;
+  p.admit = admit;
+  p.do_scan = 0;
+  p.do_resolve = 1;
+  return launch_small_step(ctx, p);
 }
 
 int launch_scan(hfz_ctx* ctx, const ScanParams& p) {
@@ -1403,6 +2133,10 @@ extern "C" int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t
     return HFZ_EINVAL;
   }
   HFZ_CUDA(cudaSetDevice(ctx->device));
+  if (small_step_ok(ctx, n_exec))  // small batch: the scan half of the fused step, one launch
+    return small_step_scan(ctx, raw_maps, n_exec, virgin_v0, classed_out, sig_full_out, sig_simple_out, nnz_out,
+                           delta_out, nullptr, nullptr, nullptr);
+  ctx->sc_small = false;
   int rc = ensure_cand(ctx, n_exec);
   if (rc) return rc;
   ctx->sc_sparse = false;  // the resolve step re-reads candidates from their dense records ...
@@ -1557,6 +2291,16 @@ int resolve_impl(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec, uint8_t
     return HFZ_EINVAL;
   }
   HFZ_CUDA(cudaSetDevice(ctx->device));
+  if (ctx->sc_small && n_exec) {  // the scan was the fused small step: its resolve half, one launch
+    if (peers) {  // gather the peers' deltas (64 KB each) into the context's staging first
+      if (!ctx->ss_deltas) HFZ_CUDA(cudaMalloc(&ctx->ss_deltas, (size_t)kMaxPeers * ctx->S));
+      for (uint32_t q = 0; q < n_ranks; ++q)
+        HFZ_CUDA(cudaMemcpyAsync(ctx->ss_deltas + (size_t)q * ctx->S, peers->p[q], ctx->S, cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+      deltas = ctx->ss_deltas;
+    }
+    return small_step_resolve(ctx, n_exec, virgin_inout, edge_counts_inout, deltas, n_ranks, rank, admit_out);
+  }
   if (peers)
     hfz_k_merge_peers<<<(ctx->S / 16 + 255) / 256, 256, 0, ctx->stream>>>(
         virgin_inout, *peers, n_ranks, rank, ctx->prior, reinterpret_cast<unsigned long long*>(edge_counts_inout),
@@ -1647,6 +2391,18 @@ extern "C" int hfz_feedback_batch(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_
   if (!ctx) {
     hfz_set_error("hfz_feedback_batch: null context");
     return HFZ_EINVAL;
+  }
+  if (small_step_ok(ctx, n_exec)) {  // small batch: scan + resolve as ONE cooperative launch
+    if (!raw_maps || !virgin_inout || !edge_counts_inout || !admit_out || !sig_full_out || !sig_simple_out) {
+      hfz_set_error("hfz_feedback_batch: null argument");
+      return HFZ_EINVAL;
+    }
+    if (((uintptr_t)raw_maps | (uintptr_t)virgin_inout) & 15) {
+      hfz_set_error("hfz_feedback_batch: raw_maps/virgin must be 16-byte aligned");
+      return HFZ_EINVAL;
+    }
+    return small_step_scan(ctx, raw_maps, n_exec, virgin_inout, classed_out, sig_full_out, sig_simple_out, nnz_out,
+                           ctx->delta, virgin_inout, edge_counts_inout, admit_out);
   }
   int rc = hfz_feedback_scan(ctx, raw_maps, n_exec, virgin_inout, classed_out, sig_full_out,
                              sig_simple_out, nnz_out, ctx->delta);

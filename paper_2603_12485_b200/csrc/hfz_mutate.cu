@@ -289,6 +289,10 @@ __global__ void __launch_bounds__(kHavocWarps * 32) hfz_k_havoc(
     if (j >= n) break;
     const uint64_t i0 = in_off[j];
     uint64_t len = in_off[j + 1] - i0;
+    // Inputs longer than kMaxInputBytes are rejected by the host-buffer entry points (hfz.h); a
+    // device-buffer caller that passes one anyway gets a memory-safe result: the slot's capacity is
+    // hfz_havoc_max_out(len) = 1 MiB, so only the first 1 MiB is mutated.
+    if (len > kMaxInput) len = kMaxInput;
     uint8_t* out = out_bytes + out_off[j];
     const bool in_smem = havoc_cap(len) <= kSmemCap;
     uint8_t* v = in_smem ? s_buf[warp] : out;
@@ -341,7 +345,7 @@ __global__ void __launch_bounds__(256) hfz_k_splice(
     WarpRng rng;
     rng.init(state[j], lane);
     const uint64_t ca = rng.below(alen + 1);
-    const uint64_t cb = rng.below(blen + 1);
+    const uint64_t cb = rng.below(blen + 1);  // (draws use the true lengths; the copies below are clamped to 1 MiB)
     const uint64_t total = ca + (blen - cb);
     const uint64_t keep = total > kMaxInput ? kMaxInput : total;
     const uint64_t head = ca < keep ? ca : keep;
@@ -541,6 +545,22 @@ struct DevBuf {
   } while (0)
 }  // namespace
 
+
+namespace {
+// host-side validation of packed inputs: lengths up to kMaxInputBytes, offsets non-decreasing
+int check_lengths(const char* who, const uint64_t* in_off, uint64_t n) {
+  for (uint64_t j = 0; j < n; ++j) {
+    if (in_off[j + 1] < in_off[j] || in_off[j + 1] - in_off[j] > kMaxInput) {
+      hfz_set_error("%s: input %llu is longer than HFZ_MAX_INPUT_BYTES (or its offsets decrease); the reference accepts "
+                    "such inputs and truncates after the first edit (src/engine.cpp:190), this library rejects them",
+                    who, (unsigned long long)j);
+      return HFZ_EINVAL;
+    }
+  }
+  return HFZ_OK;
+}
+}  // namespace
+
 extern "C" int hfz_havoc_batch_host(hfz_ctx* ctx, const uint8_t* in_bytes, const uint64_t* in_off,
                                     uint64_t n, uint64_t* rng_state_inout, uint8_t* out_bytes,
                                     const uint64_t* out_off, uint64_t* out_len, uint32_t* draws_out) {
@@ -549,6 +569,7 @@ extern "C" int hfz_havoc_batch_host(hfz_ctx* ctx, const uint8_t* in_bytes, const
     return HFZ_EINVAL;
   }
   if (n == 0) return HFZ_OK;
+  if (int rc = check_lengths("hfz_havoc_batch_host", in_off, n)) return rc;
   HFZ_TRY(cudaSetDevice(ctx->device));
   const uint64_t in_total = in_off[n], out_total = out_off[n];
   DevBuf d_in, d_ioff, d_state, d_out, d_ooff, d_olen, d_draws;
@@ -584,6 +605,7 @@ extern "C" int hfz_havoc_serial_host(hfz_ctx* ctx, const uint8_t* in_bytes, cons
     return HFZ_EINVAL;
   }
   if (n == 0) return HFZ_OK;
+  if (int rc = check_lengths("hfz_havoc_serial_host", in_off, n)) return rc;
   HFZ_TRY(cudaSetDevice(ctx->device));
   const uint64_t in_total = in_off[n], out_total = out_off[n];
   DevBuf d_in, d_ioff, d_stream, d_state, d_out, d_ooff, d_olen;
@@ -625,6 +647,7 @@ extern "C" int hfz_splice_batch_host(hfz_ctx* ctx, const uint8_t* in_bytes, cons
       hfz_set_error("hfz_splice_batch_host: input index out of range");
       return HFZ_EINVAL;
     }
+  if (int rc = check_lengths("hfz_splice_batch_host", in_off, n_inputs)) return rc;
   HFZ_TRY(cudaSetDevice(ctx->device));
   const uint64_t in_total = in_off[n_inputs], out_total = out_off[n];
   DevBuf d_in, d_ioff, d_a, d_b, d_state, d_out, d_ooff, d_olen;

@@ -287,6 +287,21 @@ int main(int argc, char** argv) {
   };
   const int n_cases = static_cast<int>(sizeof(cases) / sizeof(cases[0]));
   const int only = argc > 3 ? std::atoi(argv[3]) : -1;
+  if (only < 0) {  // the Executor contract: a persistent (stateful) campaign is refused, not run inexactly
+    struct Dummy : Executor {
+      ExecOutcome execute(const Bytes&, CoverageMap&) override { return {}; }
+      ShadowOutcome shadow(const Bytes&) override { return {}; }
+    } dummy;
+    CampaignConfig pc;
+    pc.persistent = true;
+    bool refused = false;
+    try {
+      BatchCampaign bc(pc, dummy, ctx);
+    } catch (const hetfuzz::InternalError&) {
+      refused = true;
+    }
+    REQUIRE(refused);
+  }
   for (int i = 0; i < n_cases; ++i)
     if (only < 0 || only == i) run_case(lib, ctx, cases[i], argv[2], i);
   if (g_fail) {

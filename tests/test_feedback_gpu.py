@@ -14,30 +14,34 @@ pytestmark = pytest.mark.gpu
 S = 65536
 
 
-KERNEL_OPTS = {  # (scan_small, scan_pipe, scan_two_stage): force one of the four scan kernels
-    "lane_per_map": (0, 0, 0),
-    "warp_per_map": (1 << 40, 0, 0),
-    "pipelined": (0, 1 << 20, 0),
-    "two_stage": (0, 0, 1 << 40),
+KERNEL_OPTS = {  # (scan_small, scan_pipe, scan_two_stage, small_fused): force one of the five dense paths
+    "lane_per_map": (0, 0, 0, 0),
+    "warp_per_map": (1 << 40, 0, 0, 0),
+    "pipelined": (0, 1 << 20, 0, 0),
+    "two_stage": (0, 0, 1 << 40, 0),
+    "fused_step": (0, 0, 1 << 40, 1),   # the two-stage fold as ONE cooperative launch (the small-batch default)
 }
 
 
 def force_kernel(c, name):
-    small, pipe, two = KERNEL_OPTS[name]
+    small, pipe, two, fused = KERNEL_OPTS[name]
     c.set_option("scan_small", small)
     c.set_option("scan_pipe", pipe)
     c.set_option("scan_two_stage", two)
+    c.set_option("small_fused", fused)
 
 
 @pytest.fixture(autouse=True, params=list(KERNEL_OPTS))
 def scan_kernel(request, ctx):
-    """Every test runs against all four scan kernels: the throughput kernel (32 maps per warp),
-    the warp-per-map kernel, the pipelined kernel (producer warps + one consumer warp per 32 maps)
-    and the two-stage path (compact + chain); by default the library picks by batch size."""
+    """Every test runs against all five dense paths: the throughput kernel (32 maps per warp),
+    the warp-per-map kernel, the pipelined kernel (producer warps + one consumer warp per 32 maps),
+    the two-stage path (compact + chain) and the fused step (the same fold as one cooperative
+    launch); by default the library picks by batch size."""
     force_kernel(ctx, request.param)
     yield request.param
     for k in ("scan_small", "scan_pipe", "scan_two_stage"):
         ctx.set_option(k, -1)
+    ctx.set_option("small_fused", 1)
 
 
 def run_gpu(ctx, raw, virgin0=None, counts0=None, want_classed=True):

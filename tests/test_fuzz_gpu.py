@@ -13,8 +13,8 @@ pytestmark = pytest.mark.gpu
 
 HOST_VALUES = np.array([1, 2, 3, 4, 7, 8, 15, 16, 31, 32, 127, 128, 255], np.uint8)
 DEV_VALUES = np.array([1, 2, 3, 511, 512, 4095, 4096, 16383, 16384, 65535, 65536, 0x7FFFFFFF, 0xFFFFFFFF], np.uint32)
-KERNELS = {"lane_per_map": (0, 0, 0), "warp_per_map": (1 << 40, 0, 0), "pipelined": (0, 1 << 20, 0),
-           "two_stage": (0, 0, 1 << 40), "auto": (-1, -1, -1)}
+KERNELS = {"lane_per_map": (0, 0, 0, 0), "warp_per_map": (1 << 40, 0, 0, 0), "pipelined": (0, 1 << 20, 0, 0),
+           "two_stage": (0, 0, 1 << 40, 0), "fused_step": (0, 0, 1 << 40, 1), "auto": (-1, -1, -1, 1)}
 
 
 def random_batch(rng, n, S):
@@ -57,7 +57,7 @@ def test_random_batches_against_the_oracle(seed, port):
     ctx = hfz.Context(0, S)
     try:
         kname = list(KERNELS)[seed % len(KERNELS)]
-        for key, val in zip(("scan_small", "scan_pipe", "scan_two_stage"), KERNELS[kname]):
+        for key, val in zip(("scan_small", "scan_pipe", "scan_two_stage", "small_fused"), KERNELS[kname]):
             ctx.set_option(key, val)
         ctx.set_option("sparse_native", seed % 2)
         # dense, device buffers
