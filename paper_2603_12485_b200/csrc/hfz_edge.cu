@@ -33,15 +33,19 @@
 
 namespace {
 
-constexpr int kEdgeWarps = 24;
+constexpr int kEdgeWarps = 32;
 constexpr uint32_t kRows = 256;        // site table rows
 // One table serves either general-path variant:
 //   transposed replay: keys u64[kRows] + per-row byte matrix [kRows][32]  (2 KB + 8 KB)
 //   partitioned replay (fallback): keys u64, m u32, c u32, stamp u32       (5 KB)
-// Only non-coherent simulated warps need one, so the CTA keeps a POOL of kPool tables that its
-// 16 warps borrow (free-mask in shared memory) instead of one table per warp.
+// Only non-coherent simulated warps need one, and 24 tables do not fit beside the counters: the
+// first kPool warps of the CTA each OWN a table for the whole kernel; the other warps hand a
+// non-coherent simulated warp they popped over to the owners through a small queue in shared memory
+// (atomics only).  No table ever changes hands, so there is no lock for compute-sanitizer's
+// racecheck to misread (the pool of borrowed tables this replaces was a spin lock on a free-mask).
 constexpr uint32_t kTabBytes = kRows * (8 + 32) + 64;
 constexpr int kPool = 16;
+constexpr uint32_t kDeferCap = 64;  // queue slots (simulated warp index + 1; 0 = empty)
 constexpr uint32_t kSmemSlots = 32768; // device slots whose counters fit in shared memory
 constexpr uint32_t kMaxBlockThreads = 1024;         // hdvm.hpp:167
 constexpr uint64_t kMaxLaunchThreads = 1ull << 22;  // hdvm.hpp:168
@@ -295,7 +299,8 @@ __device__ __forceinline__ bool transposed_path(uint8_t* tab, const uint32_t* si
   const uint32_t max_n = __reduce_max_sync(0xffffffffu, n_ev);
   auto find = [&](uint32_t s, bool insert) -> uint32_t {
     if (s == kTEmpty) return kTRows;
-    uint32_t r = mix32(s) & (kTRows - 1);
+    uint32_t r = (s * 0x9e3779b1u) >> (32 - 9);  // multiplicative hash: the top 9 bits index the 512 rows
+    static_assert(kTRows == 512, "hash shift assumes 512 rows");
     for (uint32_t probe = 0; probe < kTRows; ++probe) {
       const uint32_t cur = keys[r];
       if (cur == s) return r;
@@ -338,6 +343,26 @@ __device__ __forceinline__ bool transposed_path(uint8_t* tab, const uint32_t* si
     // non-zero nibble flags of each word, then: exactly one visiting lane?
     auto nzn = [](uint32_t v) { return (v | (v >> 1) | (v >> 2) | (v >> 3)) & 0x11111111u; };
     if (__popc(nzn(x.x)) + __popc(nzn(x.y)) + __popc(nzn(x.z)) + __popc(nzn(x.w)) == 1) continue;
+    if (((x.x | x.y | x.z | x.w) & 0xeeeeeeeeu) == 0u) {
+      // every visiting lane visited once (the usual row of a divergent warp): only the LOWEST visiting
+      // lane owes a bump.  Lane order: low nibbles of words 0..3, then the high nibbles.
+      const uint32_t lo[4] = {x.x & 0x0f0f0f0fu, x.y & 0x0f0f0f0fu, x.z & 0x0f0f0f0fu, x.w & 0x0f0f0f0fu};
+      uint4 d4 = make_uint4(0, 0, 0, 0);
+      if (lo[0] | lo[1] | lo[2] | lo[3]) {
+        if (lo[0]) d4.x = lo[0] & (0u - lo[0]);
+        else if (lo[1]) d4.y = lo[1] & (0u - lo[1]);
+        else if (lo[2]) d4.z = lo[2] & (0u - lo[2]);
+        else d4.w = lo[3] & (0u - lo[3]);
+      } else {
+        const uint32_t hi4[4] = {x.x & 0xf0f0f0f0u, x.y & 0xf0f0f0f0u, x.z & 0xf0f0f0f0u, x.w & 0xf0f0f0f0u};
+        if (hi4[0]) d4.x = hi4[0] & (0u - hi4[0]);
+        else if (hi4[1]) d4.y = hi4[1] & (0u - hi4[1]);
+        else if (hi4[2]) d4.z = hi4[2] & (0u - hi4[2]);
+        else d4.w = hi4[3] & (0u - hi4[3]);
+      }
+      reinterpret_cast<uint4*>(cnt)[r] = d4;
+      continue;
+    }
     const uint32_t w[4] = {x.x, x.y, x.z, x.w};
     uint32_t d[4] = {0, 0, 0, 0};
     uint32_t carry = 0;  // max count among the lanes seen so far
@@ -400,10 +425,14 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
   const int lane = threadIdx.x & 31;
   __shared__ unsigned long long s_events;
   __shared__ uint32_t s_next;
-  __shared__ uint32_t s_free;      // bit t set = pool table t is free
+  __shared__ uint32_t s_defer[kDeferCap];  // non-coherent simulated warps waiting for a table-owning warp
+  __shared__ uint32_t s_dhead, s_dtail;    // tickets taken by consumers / producers
+  __shared__ uint32_t s_left;              // non-owner warps that have left the pop loop of this pass
   __shared__ uint32_t s_overflow;  // a packed counter came near 16 bits / the hashed table is nearly full: replay with wide counters
   __shared__ uint32_t s_used;      // rows of the hashed table in use
-  if (threadIdx.x == 0) s_free = (1u << kPool) - 1u;
+  const bool owner = (threadIdx.x >> 5) < (uint32_t)kPool;
+  const uint32_t n_nonowners = kEdgeWarps - kPool;
+  if (threadIdx.x < kDeferCap) s_defer[threadIdx.x] = 0;
   uint32_t* prev_tab = p.prev_scratch + (size_t)blockIdx.x * p.prev_stride;
   const uint32_t hmask = p.H - 1;
 
@@ -475,7 +504,12 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
     const uint64_t l_step = uniform ? (l1 - l0) : 1;
     for (uint64_t l = l0; l < l1; l += l_step) {
       const uint32_t* d = p.dims + l * 6;
-      if (threadIdx.x == 0) s_next = 0;
+      if (threadIdx.x == 0) {
+        s_next = 0;
+        s_dhead = 0;
+        s_dtail = 0;
+        s_left = 0;
+      }
       __syncthreads();
       if (launch_valid(d)) {
         // all of these fit 32 bits: blocks * tpb <= 2^22, tpb <= 1024 (launch_valid)
@@ -489,9 +523,43 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
         // simulated warps are handed out dynamically: divergent ones take far longer
         for (;;) {
           uint32_t q = 0;
-          if (lane == 0) q = atomicAdd(&s_next, 1u);
-          q = __shfl_sync(0xffffffffu, q, 0);
-          if (q >= n_q) break;  // n_q < 2^31 (checked where `uniform` is set; n_sw <= 2^22 otherwise)
+          bool deferred = false;
+          if (owner) {  // table-owning warps serve the queue of handed-over simulated warps first
+            uint32_t got = 0;
+            if (lane == 0) {
+              uint32_t h = atomicAdd(&s_dhead, 0u);
+              while (h < atomicAdd(&s_dtail, 0u)) {
+                const uint32_t seen = atomicCAS(&s_dhead, h, h + 1);
+                if (seen == h) {  // ticket h is ours: its slot is filled by a producer that already holds a ticket
+                  uint32_t* slot = &s_defer[h % kDeferCap];
+                  while ((got = atomicExch(slot, 0u)) == 0u) {
+                  }
+                  break;
+                }
+                h = seen;
+              }
+            }
+            got = __shfl_sync(0xffffffffu, got, 0);
+            if (got) {
+              q = got - 1;
+              deferred = true;
+            }
+          }
+          if (!deferred) {
+            uint32_t done = 0;
+            if (lane == 0) {
+              q = atomicAdd(&s_next, 0u) < n_q ? atomicAdd(&s_next, 1u) : (uint32_t)n_q;  // n_q < 2^31
+              if (q >= n_q && owner)  // an owner leaves once no warp can hand over any more work
+                done = atomicAdd(&s_left, 0u) == n_nonowners && atomicAdd(&s_dhead, 0u) == atomicAdd(&s_dtail, 0u);
+            }
+            q = __shfl_sync(0xffffffffu, q, 0);
+            if (q >= n_q) {
+              if (!owner) break;
+              if (__shfl_sync(0xffffffffu, done, 0)) break;
+              __nanosleep(200);
+              continue;
+            }
+          }
           const uint32_t lq = uniform ? q / n_sw : 0u;  // launch within the exec (uniform pass only)
           const uint32_t sw = q - lq * n_sw;
           const uint64_t t0 = p.thread_off[l + lq];
@@ -557,7 +625,7 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
           bool same_l = !active || n_ev == n_lead;
           if (same_l && active) {
             uint32_t diff = 0;
-#pragma unroll 4
+#pragma unroll 8
             for (uint32_t i = 0; i < n_lead; ++i) diff |= sl[i] ^ sm[i];
             same_l = diff == 0;
           }
@@ -575,25 +643,18 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
             continue;
           }
 
-          // ---- general path: borrow a table from the CTA's pool.  Hand-over = shared-memory
-          // atomic on the free-mask, release after __syncwarp() + __threadfence_block().
-          // (compute-sanitizer racecheck does not model lock-style synchronisation and reports
-          // the previous owner's last reads against the next owner's clear as WAR hazards;
-          // one private table per warp instead -- 9 warps -- is race-report-free but 30 % slower.)
-          uint32_t t = 0;
-          if (lane == 0) {
-            for (;;) {
-              const uint32_t m = *reinterpret_cast<volatile uint32_t*>(&s_free);
-              if (m == 0) {
-                __nanosleep(400);
-                continue;
+          // ---- general path: needs a site table.  A warp without one hands the simulated warp over.
+          if (!owner) {
+            if (lane == 0) {
+              const uint32_t ticket = atomicAdd(&s_dtail, 1u);
+              uint32_t* slot = &s_defer[ticket % kDeferCap];
+              while (atomicCAS(slot, 0u, q + 1) != 0u) {  // queue full: the owners drain it with priority
+                __nanosleep(100);
               }
-              t = __ffs(m) - 1;
-              if (atomicAnd(&s_free, ~(1u << t)) & (1u << t)) break;
             }
+            continue;
           }
-          t = __shfl_sync(0xffffffffu, t, 0);
-          uint8_t* tmem = pool + (size_t)t * kTabBytes;
+          uint8_t* tmem = pool + (size_t)(threadIdx.x >> 5) * kTabBytes;
           if (!transposed_path(tmem, p.sites, e0, n_ev, prev0, counters, hmask, lane, my_events)) {
             WarpTable tab;
             tab.keys = reinterpret_cast<unsigned long long*>(tmem);
@@ -604,17 +665,29 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
             my_events += general_path(tab, p.sites, e0, n_ev, prev0, counters, hmask, lane);
           }
           __syncwarp();
-          if (lane == 0) {
-            __threadfence_block();
-            atomicOr(&s_free, 1u << t);
-          }
           if (use_tab && active && n_ev) prev_tab[gtid] = p.sites[e1 - 1] >> 1;
         }
+        if (!owner && lane == 0) atomicAdd(&s_left, 1u);
       }
       __syncthreads();  // prev table and counters are launch-ordered
     }
     // block-reduce the event tally, flush the counters (copy, merge_device_into_map)
-    if (my_events) atomicAdd(&s_events, (unsigned long long)my_events);
+    // one 64-bit shared-memory atomic per WARP: 64-bit adds on shared memory are CAS loops, and 768
+    // threads retrying on one word at the end of every exec were 13 % of the kernel's instructions
+    {
+      uint32_t lo = (uint32_t)my_events, hi = (uint32_t)(my_events >> 32);
+      const uint32_t lo_sum = __reduce_add_sync(0xffffffffu, lo);           // low words: carries recovered below
+      uint32_t carry = 0;
+      if (__any_sync(0xffffffffu, hi != 0u) || __reduce_max_sync(0xffffffffu, lo) > 0x07ffffffu) {
+        // rare: exact 64-bit warp sum by shuffles
+        uint64_t v = my_events;
+        for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+        if (lane == 0 && v) atomicAdd(&s_events, (unsigned long long)v);
+      } else if (lane == 0 && lo_sum) {
+        (void)carry;
+        atomicAdd(&s_events, (unsigned long long)lo_sum);  // 32 lanes x < 2^27 cannot wrap 32 bits
+      }
+    }
     __syncthreads();
     const bool redo = packed && s_overflow != 0;
     if (packed && !redo) {

@@ -21,7 +21,7 @@ namespace {
 
 constexpr uint32_t kMaxInput = HFZ_MAX_INPUT_BYTES;
 constexpr int kHavocWarps = 8;
-constexpr uint32_t kSmemCap = 6144;  // working buffer bytes per warp (>= 4096 + 1024)
+constexpr uint32_t kSmemCap = 6128;  // working buffer bytes per warp (>= 4096 + 1024); + 16 bytes of padding = 6 KB per warp, 48 KB static per CTA
 
 __constant__ int16_t c_interesting16[10] = {-32768, -129, 128, 255, 256, 512, 1000, 1024, 4096, 32767};
 __constant__ int32_t c_interesting32[8] = {(-2147483647 - 1), -100663046, -32769, 32768,
@@ -55,10 +55,14 @@ struct WarpRng {
     ++draws;
     return r;
   }
-  // below(n): n <= 1 returns 0 WITHOUT drawing (rng.hpp:24-28)
-  __device__ __forceinline__ uint64_t below(uint64_t n) {
+  // below(n): n <= 1 returns 0 WITHOUT drawing (rng.hpp:24-28); (u128(next()) * n) >> 64 otherwise.
+  // Every bound on this path fits 32 bits (the largest is 8 x kMaxInputBytes = 2^23 bit positions), so
+  // the 64 x 64 -> high-64 product is two 32 x 32 -> 64 multiplies: hi32(r) * n + (lo32(r) * n >> 32).
+  __device__ __forceinline__ uint32_t below(uint32_t n) {
     if (n <= 1) return 0;
-    return __umul64hi(next(), n);
+    const uint64_t r = next();
+    const uint64_t t = (uint64_t)(uint32_t)(r >> 32) * n + (((uint64_t)(uint32_t)r * n) >> 32);
+    return (uint32_t)(t >> 32);
   }
 };
 
@@ -168,6 +172,98 @@ __device__ __forceinline__ void warp_move_up(uint8_t* buf, uint64_t dst, uint64_
   }
 }
 
+// The same two overlapping moves for a working buffer in SHARED memory, 16 bytes per lane and step
+// instead of 4 single bytes: destination block k (16-byte aligned) is assembled from five aligned
+// source words with funnel shifts -- the byte distance between source and destination is the same
+// for the whole move, so one shift serves every word -- and stored with one 128-bit store; the two
+// partial blocks at the ends of the range keep the bytes outside it.  buf must be 16-byte aligned
+// and readable for 16 bytes beyond the data (the working buffers are padded).  A quarter of the
+// kernel's instructions used to be the byte-granular version of these loops.
+__device__ __forceinline__ uint32_t block_mask(uint64_t blk_lo, uint64_t lo, uint64_t hi) {
+  // 16-bit mask of the bytes of block [blk_lo, blk_lo + 16) that lie inside [lo, hi)
+  const uint64_t a = lo > blk_lo ? lo - blk_lo : 0, b = hi < blk_lo + 16 ? (hi > blk_lo ? hi - blk_lo : 0) : 16;
+  return a >= b ? 0u : ((0xffffu >> (16 - (uint32_t)(b - a))) << (uint32_t)a);
+}
+__device__ __forceinline__ uint32_t bytes_of(uint32_t m4) {  // 4-bit byte mask -> 32-bit lane mask
+  return ((m4 & 1u) * 0xffu) | (((m4 >> 1) & 1u) * 0xff00u) | (((m4 >> 2) & 1u) * 0xff0000u) | (((m4 >> 3) & 1u) * 0xff000000u);
+}
+// one step: blocks [k0, k0 + 32) of the destination (block k = bytes [16k, 16k + 16)); delta = src - dst (signed)
+__device__ __forceinline__ void move_blocks(uint8_t* buf, uint64_t k0, uint64_t k_end, int64_t delta, uint64_t dlo, uint64_t dhi,
+                                            int lane) {
+  const uint64_t k = k0 + lane;
+  const bool on = k < k_end;
+  uint4 out = make_uint4(0, 0, 0, 0);
+  uint32_t m = 0;
+  if (on) {
+    const int64_t sb = (int64_t)(k * 16) + delta;          // source byte of the block's first byte (may be < 0 only for masked bytes)
+    const int64_t sw = sb >> 2;                              // aligned source word (floor)
+    const uint32_t sh = (uint32_t)(sb & 3) * 8;
+    const uint32_t* w32 = reinterpret_cast<const uint32_t*>(buf);
+    uint32_t w[5];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) w[j] = sw + j >= 0 ? w32[sw + j] : 0u;
+    out.x = __funnelshift_r(w[0], w[1], sh);
+    out.y = __funnelshift_r(w[1], w[2], sh);
+    out.z = __funnelshift_r(w[2], w[3], sh);
+    out.w = __funnelshift_r(w[3], w[4], sh);
+    m = block_mask(k * 16, dlo, dhi);
+    if (m != 0xffffu) {  // a partial block at either end of the range: keep the bytes outside it
+      const uint4 old = reinterpret_cast<const uint4*>(buf)[k];
+      const uint32_t m0 = bytes_of(m), m1 = bytes_of(m >> 4), m2 = bytes_of(m >> 8), m3 = bytes_of(m >> 12);
+      out.x = (out.x & m0) | (old.x & ~m0);
+      out.y = (out.y & m1) | (old.y & ~m1);
+      out.z = (out.z & m2) | (old.z & ~m2);
+      out.w = (out.w & m3) | (old.w & ~m3);
+    }
+  }
+  __syncwarp();  // every block of this step is read before any is written
+  if (on && m) reinterpret_cast<uint4*>(buf)[k] = out;
+  __syncwarp();
+}
+// buf[dst + i] = buf[src + i], i ascending (dst < src)
+__device__ __forceinline__ void smem_move_down(uint8_t* buf, uint64_t dst, uint64_t src, uint64_t n, int lane) {
+  if (n == 0) return;
+  const uint64_t k_first = dst / 16, k_end = (dst + n + 15) / 16;
+  for (uint64_t k0 = k_first; k0 < k_end; k0 += 32) move_blocks(buf, k0, k_end, (int64_t)(src - dst), dst, dst + n, lane);
+}
+// buf[dst + i] = buf[src + i], i descending (dst > src)
+__device__ __forceinline__ void smem_move_up(uint8_t* buf, uint64_t dst, uint64_t src, uint64_t n, int lane) {
+  if (n == 0) return;
+  const uint64_t k_first = dst / 16, k_end = (dst + n + 15) / 16;
+  uint64_t k0 = k_first + ((k_end - k_first - 1) / 32) * 32;  // the highest step first
+  for (;;) {
+    move_blocks(buf, k0, k_end, -(int64_t)(dst - src), dst, dst + n, lane);
+    if (k0 == k_first) break;
+    k0 -= 32;
+  }
+}
+
+// global (any alignment) -> shared (16-byte aligned dst): aligned 32-bit loads + one funnel shift per word
+__device__ __forceinline__ void copy_in_smem(uint8_t* dst, const uint8_t* src, uint64_t n, int lane) {
+  const uint32_t a = (uint32_t)((uintptr_t)src & 3);
+  const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src - a);  // aligned down: the first word may start before src
+  const uint32_t sh = a * 8;
+  uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+  const uint64_t words = (n + 3) / 4;
+  // the last source word read is s32[words] when a != 0: it holds bytes of the input itself or, for the batch's
+  // last input, of the 16 bytes of slack callers keep behind the packed inputs (hfz.h); guard it anyway
+  const uint64_t last_word = ((uint64_t)a + n + 3) / 4;  // exclusive bound of words that hold input bytes
+  for (uint64_t w0 = 0; w0 < words; w0 += 32 * 4) {
+    uint32_t lo[4], hi[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t w = w0 + k * 32 + lane;
+      lo[k] = w < words ? __ldg(s32 + w) : 0u;
+      hi[k] = (w < words && w + 1 < last_word) ? __ldg(s32 + w + 1) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t w = w0 + k * 32 + lane;
+      if (w < words) d32[w] = __funnelshift_r(lo[k], hi[k], sh);
+    }
+  }
+}
+
 __device__ __forceinline__ uint64_t havoc_cap(uint64_t len) {
   const uint64_t m = len + 64 * 16;
   return m > kMaxInput ? kMaxInput : m;
@@ -176,7 +272,7 @@ __device__ __forceinline__ uint64_t havoc_cap(uint64_t len) {
 // The stacked-havoc edit loop of one slot (src/engine.cpp:120-191).  DRY = true runs only the
 // Rng draws and the length bookkeeping -- every below() bound depends on the current length
 // alone, never on the bytes -- which is what a serial-stream plan needs (hfz_havoc_serial_plan).
-template <bool DRY>
+template <bool DRY, bool SMEM = false>
 __device__ __forceinline__ uint64_t havoc_edit(uint8_t* v, uint64_t len, WarpRng& rng, int lane) {
   const uint64_t ops = 1 + rng.below(64);
   for (uint64_t op = 0; op < ops; ++op) {
@@ -192,7 +288,7 @@ __device__ __forceinline__ uint64_t havoc_edit(uint8_t* v, uint64_t len, WarpRng
     }
     switch ((uint32_t)rng.below(9)) {
       case 0: {  // flip one bit, MSB-first numbering
-        const uint64_t pos = rng.below(len * 8);
+        const uint64_t pos = rng.below((uint32_t)(len * 8));
         if (!DRY && lane == 0) v[pos / 8] ^= (uint8_t)(0x80u >> (pos % 8));
         break;
       }
@@ -230,7 +326,10 @@ __device__ __forceinline__ uint64_t havoc_edit(uint8_t* v, uint64_t len, WarpRng
         const uint64_t max_n = len - off < q ? len - off : q;
         const uint64_t cnt = 1 + rng.below(max_n);
         if (!DRY) __syncwarp();
-        if (!DRY) warp_move_down(v, off, off + cnt, len - off - cnt, lane);
+        if (!DRY) {
+          if (SMEM) smem_move_down(v, off, off + cnt, len - off - cnt, lane);
+          else warp_move_down(v, off, off + cnt, len - off - cnt, lane);
+        }
         len -= cnt;
         break;
       }
@@ -244,7 +343,10 @@ __device__ __forceinline__ uint64_t havoc_edit(uint8_t* v, uint64_t len, WarpRng
         // insert with the 1 MiB clamp folded in: bytes that would land past the cap are dropped
         const uint64_t new_len = len + cnt > kMaxInput ? kMaxInput : len + cnt;
         if (!DRY) __syncwarp();
-        if (!DRY && new_len > dst + cnt) warp_move_up(v, dst + cnt, dst, new_len - dst - cnt, lane);
+        if (!DRY && new_len > dst + cnt) {
+          if (SMEM) smem_move_up(v, dst + cnt, dst, new_len - dst - cnt, lane);
+          else warp_move_up(v, dst + cnt, dst, new_len - dst - cnt, lane);
+        }
         if (!DRY && (uint64_t)lane < cnt && dst + lane < new_len) v[dst + lane] = blk;
         len = new_len;
         break;
@@ -279,7 +381,7 @@ __global__ void __launch_bounds__(kHavocWarps * 32) hfz_k_havoc(
     uint64_t* __restrict__ state, uint8_t* __restrict__ out_bytes,
     const uint64_t* __restrict__ out_off, uint64_t* __restrict__ out_len,
     uint32_t* __restrict__ draws_out, unsigned long long* __restrict__ next_slot) {
-  __shared__ __align__(16) uint8_t s_buf[kHavocWarps][kSmemCap];
+  __shared__ __align__(16) uint8_t s_buf[kHavocWarps][kSmemCap + 16];  // + 16: the block moves read one block past the data
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // slots are handed out dynamically: a mutant stacks 1..64 edits, so their costs differ widely
   for (;;) {
@@ -296,12 +398,13 @@ __global__ void __launch_bounds__(kHavocWarps * 32) hfz_k_havoc(
     uint8_t* out = out_bytes + out_off[j];
     const bool in_smem = havoc_cap(len) <= kSmemCap;
     uint8_t* v = in_smem ? s_buf[warp] : out;
-    warp_copy(v, in_bytes + i0, len, lane);
+    if (in_smem) copy_in_smem(v, in_bytes + i0, len, lane);
+    else warp_copy(v, in_bytes + i0, len, lane);
     __syncwarp();
 
     WarpRng rng;
     rng.init(state[j], lane);
-    len = havoc_edit<false>(v, len, rng, lane);
+    len = in_smem ? havoc_edit<false, true>(v, len, rng, lane) : havoc_edit<false, false>(v, len, rng, lane);
     if (in_smem) {
       warp_copy(out, v, len, lane);
       __syncwarp();

@@ -138,3 +138,21 @@ int main(void) {{
                     str(src), "-o", exe, "-L", lib_dir, "-l:libhfz.so", f"-Wl,-rpath,{lib_dir}"], check=True)
     r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_cpp_harness_generates_the_same_maps_as_the_python_recipe():
+    """bench/e2e_coveragemap.cpp restates synth.maps_campaign in C++ (it builds hetfuzz::CoverageMap
+    objects directly): the first 8 records must be byte-identical."""
+    import json
+    import subprocess
+    import numpy as np
+    from paper_2603_12485_b200 import synth
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "bench", "e2e_coveragemap")
+    if not os.path.exists(exe):
+        pytest.skip("bench/e2e_coveragemap not built")
+    got = json.loads(subprocess.run([exe, "--gen-only"], capture_output=True, text=True, check=True).stdout)["first8_fnv"]
+    h, P, M = 14695981039346656037, 1099511628211, (1 << 64) - 1
+    for b in synth.maps_campaign(8, 65536).tobytes():
+        h = ((h ^ b) * P) & M
+    assert got == "%016x" % h
