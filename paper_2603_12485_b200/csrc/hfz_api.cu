@@ -87,6 +87,7 @@ extern "C" int hfz_ctx_destroy(hfz_ctx* c) {
   cudaFree(c->v0);
   cudaFree(c->d_small);
   cudaFree(c->edge_prev);
+  cudaFree(c->hv_ops);
   for (int i = 0; i < 2; ++i) {
     cudaFree(c->stage_raw[i]);
     if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);

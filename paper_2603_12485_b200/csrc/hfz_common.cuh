@@ -38,7 +38,11 @@ struct hfz_ctx {
   // K1 scratch (owned, grow-only)
   uint32_t* edge_prev = nullptr;
   uint64_t edge_prev_words = 0;
-  unsigned long long* d_small = nullptr;  // [8] small device scalars
+  unsigned long long* d_small = nullptr;  // [32] small device scalars
+
+  // K3 scratch (owned, grow-only): edit lists of one chunk of slots, 528 bytes per slot (hfz_mutate.cu)
+  uint64_t* hv_ops = nullptr;
+  uint64_t hv_ops_cap = 0;  // slots
 
   // host-buffer path staging (owned, lazily allocated)
   uint8_t* stage_raw[2] = {nullptr, nullptr};

@@ -6,11 +6,20 @@
 //   for_each_deterministic  src/engine.cpp:53-105
 //   Rng                     include/hetfuzz/rng.hpp:11-46
 //
-// One warp owns one slot.  The splitmix64 stream is warp-uniform (every lane advances the
-// same state), single-byte edits are done by lane 0 and block moves (erase / insert / copy)
-// by the whole warp on a working buffer that lives in shared memory when the slot's maximum
-// output fits (inputs up to ~5 KB: BASELINE.json configs[3]) and directly in the slot's
-// output region in global memory otherwise (inputs up to kMaxInputBytes = 1 MiB).
+// Havoc runs as PLAN then APPLY.  Every Rng bound of the edit loop depends on the current LENGTH
+// alone, never on the bytes, so the whole draw sequence of a slot can be walked without touching
+// its data:
+//   hfz_k_havoc_plan_ops   one THREAD per slot: scalar splitmix64, branch-light walk of the 1..64
+//                          stacked edits; writes the slot's edit list (one 64-bit word per edit),
+//                          its final length, end Rng state and draw count;
+//   hfz_k_havoc_apply      one WARP per slot (dynamic hand-out): reads the edit list with one
+//                          coalesced load, applies it -- single-byte edits by lane 0, block moves
+//                          (erase / insert) by the whole warp, 16 bytes per lane and step -- on a
+//                          working buffer in shared memory when the slot's maximum output fits
+//                          (inputs up to ~5 KB: BASELINE.json configs[3]) and directly in the
+//                          slot's output region in global memory otherwise (up to 1 MiB).
+// (One warp per slot doing both, with a warp-uniform Rng, spent 3/4 of its instructions on the
+// scalar control flow that 32 lanes executed redundantly: 8.8 k warp-instructions per mutant.)
 #include <string.h>
 
 #include <vector>
@@ -21,6 +30,7 @@ namespace {
 
 constexpr uint32_t kMaxInput = HFZ_MAX_INPUT_BYTES;
 constexpr int kHavocWarps = 8;
+constexpr uint64_t kHavocChunk = 1ull << 17;  // slots planned and applied per launch pair
 constexpr uint32_t kSmemCap = 6128;  // working buffer bytes per warp (>= 4096 + 1024); + 16 bytes of padding = 6 KB per warp, 48 KB static per CTA
 
 __constant__ int16_t c_interesting16[10] = {-32768, -129, 128, 255, 256, 512, 1000, 1024, 4096, 32767};
@@ -64,6 +74,10 @@ struct WarpRng {
     const uint64_t t = (uint64_t)(uint32_t)(r >> 32) * n + (((uint64_t)(uint32_t)r * n) >> 32);
     return (uint32_t)(t >> 32);
   }
+  // the per-edit interface of the planner (LaneRng below draws ahead here; this stream is warp-uniform already)
+  __device__ __forceinline__ void edit_begin() {}
+  __device__ __forceinline__ uint32_t take(uint32_t n) { return below(n); }
+  __device__ __forceinline__ void edit_end() {}
 };
 
 // non-overlapping copy by one warp; loads are issued in batches of 8 per lane so that a
@@ -175,28 +189,21 @@ __device__ __forceinline__ void warp_move_up(uint8_t* buf, uint64_t dst, uint64_
 // The same two overlapping moves for a working buffer in SHARED memory, 16 bytes per lane and step
 // instead of 4 single bytes: destination block k (16-byte aligned) is assembled from five aligned
 // source words with funnel shifts -- the byte distance between source and destination is the same
-// for the whole move, so one shift serves every word -- and stored with one 128-bit store; the two
-// partial blocks at the ends of the range keep the bytes outside it.  buf must be 16-byte aligned
-// and readable for 16 bytes beyond the data (the working buffers are padded).  A quarter of the
-// kernel's instructions used to be the byte-granular version of these loops.
-__device__ __forceinline__ uint32_t block_mask(uint64_t blk_lo, uint64_t lo, uint64_t hi) {
-  // 16-bit mask of the bytes of block [blk_lo, blk_lo + 16) that lie inside [lo, hi)
-  const uint64_t a = lo > blk_lo ? lo - blk_lo : 0, b = hi < blk_lo + 16 ? (hi > blk_lo ? hi - blk_lo : 0) : 16;
-  return a >= b ? 0u : ((0xffffu >> (16 - (uint32_t)(b - a))) << (uint32_t)a);
-}
-__device__ __forceinline__ uint32_t bytes_of(uint32_t m4) {  // 4-bit byte mask -> 32-bit lane mask
-  return ((m4 & 1u) * 0xffu) | (((m4 >> 1) & 1u) * 0xff00u) | (((m4 >> 2) & 1u) * 0xff0000u) | (((m4 >> 3) & 1u) * 0xff000000u);
-}
-// one step: blocks [k0, k0 + 32) of the destination (block k = bytes [16k, 16k + 16)); delta = src - dst (signed)
-__device__ __forceinline__ void move_blocks(uint8_t* buf, uint64_t k0, uint64_t k_end, int64_t delta, uint64_t dlo, uint64_t dhi,
+// for the whole move, so one shift serves every word -- and stored with one 128-bit store.  The
+// partial block at the START of the range keeps the bytes below it.  The block at the END is
+// written whole: both moves of the edit loop end exactly at the buffer's new length (erase: len -
+// count, insert: the new length), so the bytes behind the range are dead.  buf must be 16-byte
+// aligned and padded to a whole block beyond the largest length.
+// one step: blocks [k0, k0 + 32) of the destination (block k = bytes [16k, 16k + 16)); delta = src - dst (signed);
+// the destination range starts at dlo
+__device__ __forceinline__ void move_blocks(uint8_t* buf, uint32_t k0, uint32_t k_end, int32_t delta, uint32_t dlo,
                                             int lane) {
-  const uint64_t k = k0 + lane;
+  const uint32_t k = k0 + lane;
   const bool on = k < k_end;
   uint4 out = make_uint4(0, 0, 0, 0);
-  uint32_t m = 0;
   if (on) {
-    const int64_t sb = (int64_t)(k * 16) + delta;          // source byte of the block's first byte (may be < 0 only for masked bytes)
-    const int64_t sw = sb >> 2;                              // aligned source word (floor)
+    const int32_t sb = (int32_t)(k * 16) + delta;  // source byte of the block's first byte (< 0 only for bytes outside the range)
+    const int32_t sw = sb >> 2;                    // aligned source word (floor)
     const uint32_t sh = (uint32_t)(sb & 3) * 8;
     const uint32_t* w32 = reinterpret_cast<const uint32_t*>(buf);
     uint32_t w[5];
@@ -206,10 +213,15 @@ __device__ __forceinline__ void move_blocks(uint8_t* buf, uint64_t k0, uint64_t 
     out.y = __funnelshift_r(w[1], w[2], sh);
     out.z = __funnelshift_r(w[2], w[3], sh);
     out.w = __funnelshift_r(w[3], w[4], sh);
-    m = block_mask(k * 16, dlo, dhi);
-    if (m != 0xffffu) {  // a partial block at either end of the range: keep the bytes outside it
+    const uint32_t b0 = k * 16;
+    if (b0 < dlo) {  // the range's first block: keep the bytes below dlo (at most one lane of one step gets here)
+      const uint32_t lo8 = (dlo - b0) * 8;  // 8 .. 120 bits to keep
       const uint4 old = reinterpret_cast<const uint4*>(buf)[k];
-      const uint32_t m0 = bytes_of(m), m1 = bytes_of(m >> 4), m2 = bytes_of(m >> 8), m3 = bytes_of(m >> 12);
+      // word j keeps its low clamp(lo8 - 32 j, 0, 32) bits: a clamping funnel shift of (ones : zeros)
+      const uint32_t m0 = __funnelshift_lc(0u, ~0u, lo8 < 32u ? lo8 : 32u);
+      const uint32_t m1 = lo8 <= 32u ? ~0u : __funnelshift_lc(0u, ~0u, lo8 - 32u < 32u ? lo8 - 32u : 32u);
+      const uint32_t m2 = lo8 <= 64u ? ~0u : __funnelshift_lc(0u, ~0u, lo8 - 64u < 32u ? lo8 - 64u : 32u);
+      const uint32_t m3 = lo8 <= 96u ? ~0u : __funnelshift_lc(0u, ~0u, lo8 - 96u);
       out.x = (out.x & m0) | (old.x & ~m0);
       out.y = (out.y & m1) | (old.y & ~m1);
       out.z = (out.z & m2) | (old.z & ~m2);
@@ -217,51 +229,77 @@ __device__ __forceinline__ void move_blocks(uint8_t* buf, uint64_t k0, uint64_t 
     }
   }
   __syncwarp();  // every block of this step is read before any is written
-  if (on && m) reinterpret_cast<uint4*>(buf)[k] = out;
+  if (on) reinterpret_cast<uint4*>(buf)[k] = out;
   __syncwarp();
 }
 // buf[dst + i] = buf[src + i], i ascending (dst < src)
-__device__ __forceinline__ void smem_move_down(uint8_t* buf, uint64_t dst, uint64_t src, uint64_t n, int lane) {
+__device__ __forceinline__ void smem_move_down(uint8_t* buf, uint32_t dst, uint32_t src, uint32_t n, int lane) {
   if (n == 0) return;
-  const uint64_t k_first = dst / 16, k_end = (dst + n + 15) / 16;
-  for (uint64_t k0 = k_first; k0 < k_end; k0 += 32) move_blocks(buf, k0, k_end, (int64_t)(src - dst), dst, dst + n, lane);
+  const uint32_t k_first = dst / 16, k_end = (dst + n + 15) / 16;
+  for (uint32_t k0 = k_first; k0 < k_end; k0 += 32) move_blocks(buf, k0, k_end, (int32_t)(src - dst), dst, lane);
 }
 // buf[dst + i] = buf[src + i], i descending (dst > src)
-__device__ __forceinline__ void smem_move_up(uint8_t* buf, uint64_t dst, uint64_t src, uint64_t n, int lane) {
+__device__ __forceinline__ void smem_move_up(uint8_t* buf, uint32_t dst, uint32_t src, uint32_t n, int lane) {
   if (n == 0) return;
-  const uint64_t k_first = dst / 16, k_end = (dst + n + 15) / 16;
-  uint64_t k0 = k_first + ((k_end - k_first - 1) / 32) * 32;  // the highest step first
+  const uint32_t k_first = dst / 16, k_end = (dst + n + 15) / 16;
+  uint32_t k0 = k_first + ((k_end - k_first - 1) / 32) * 32;  // the highest step first
   for (;;) {
-    move_blocks(buf, k0, k_end, -(int64_t)(dst - src), dst, dst + n, lane);
+    move_blocks(buf, k0, k_end, -(int32_t)(dst - src), dst, lane);
     if (k0 == k_first) break;
     k0 -= 32;
   }
 }
 
-// global (any alignment) -> shared (16-byte aligned dst): aligned 32-bit loads + one funnel shift per word
-__device__ __forceinline__ void copy_in_smem(uint8_t* dst, const uint8_t* src, uint64_t n, int lane) {
-  const uint32_t a = (uint32_t)((uintptr_t)src & 3);
-  const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src - a);  // aligned down: the first word may start before src
-  const uint32_t sh = a * 8;
-  uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
-  const uint64_t words = (n + 3) / 4;
-  // the last source word read is s32[words] when a != 0: it holds bytes of the input itself or, for the batch's
-  // last input, of the 16 bytes of slack callers keep behind the packed inputs (hfz.h); guard it anyway
-  const uint64_t last_word = ((uint64_t)a + n + 3) / 4;  // exclusive bound of words that hold input bytes
-  for (uint64_t w0 = 0; w0 < words; w0 += 32 * 4) {
-    uint32_t lo[4], hi[4];
+// global (any alignment) -> shared (16-byte aligned dst), 16 bytes per lane: two aligned 128-bit loads
+// (the second one is the next lane's first: an L1 hit) + one funnel shift per word + one 128-bit store.
+// Reads only 16-byte blocks that hold at least one byte of [src, src + n): no slack needed around the input.
+__device__ __forceinline__ void copy_in_smem(uint8_t* dst, const uint8_t* src, uint32_t n, int lane) {
+  const uint32_t a = (uint32_t)((uintptr_t)src & 15);
+  const uint4* s4 = reinterpret_cast<const uint4*>(src - a);
+  const uint32_t sh = (a & 3) * 8, wsel = a >> 2;
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  const uint32_t blocks = (n + 15) / 16;
+  const uint32_t src_blocks = (a + n + 15) / 16;  // aligned source blocks that hold input bytes
+  for (uint32_t b0 = 0; b0 < blocks; b0 += 32 * 2) {
+    uint4 lo[2], hi[2];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint64_t w = w0 + k * 32 + lane;
-      lo[k] = w < words ? __ldg(s32 + w) : 0u;
-      hi[k] = (w < words && w + 1 < last_word) ? __ldg(s32 + w + 1) : 0u;
+    for (int k = 0; k < 2; ++k) {
+      const uint32_t b = b0 + k * 32 + lane;
+      lo[k] = b < blocks ? __ldg(s4 + b) : make_uint4(0, 0, 0, 0);
+      hi[k] = (b < blocks && b + 1 < src_blocks) ? __ldg(s4 + b + 1) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint64_t w = w0 + k * 32 + lane;
-      if (w < words) d32[w] = __funnelshift_r(lo[k], hi[k], sh);
+    for (int k = 0; k < 2; ++k) {
+      const uint32_t b = b0 + k * 32 + lane;
+      if (b >= blocks) continue;
+      const uint32_t w[8] = {lo[k].x, lo[k].y, lo[k].z, lo[k].w, hi[k].x, hi[k].y, hi[k].z, hi[k].w};
+      uint32_t v[5];
+#pragma unroll
+      for (int j = 0; j < 5; ++j)  // words wsel .. wsel + 4 of the 8: a 4-way select, wsel is warp-uniform
+        v[j] = wsel == 0 ? w[j] : (wsel == 1 ? w[j + 1] : (wsel == 2 ? w[j + 2] : w[j + 3]));
+      d4[b] = make_uint4(__funnelshift_r(v[0], v[1], sh), __funnelshift_r(v[1], v[2], sh),
+                         __funnelshift_r(v[2], v[3], sh), __funnelshift_r(v[3], v[4], sh));
     }
   }
+}
+// shared (16-byte aligned src) -> global (any alignment): byte stores up to the first 16-byte boundary of dst,
+// 128-bit stores for the body (five aligned shared words + funnel shifts per block), byte stores for the tail
+__device__ __forceinline__ void copy_out_smem(uint8_t* dst, const uint8_t* src, uint32_t n, int lane) {
+  uint32_t head = (16u - (uint32_t)((uintptr_t)dst & 15)) & 15u;
+  if (head > n) head = n;
+  if ((uint32_t)lane < head) dst[lane] = src[lane];
+  const uint32_t blocks = (n - head) / 16;
+  const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src) + (head >> 2);
+  const uint32_t sh = (head & 3) * 8;
+  uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+  for (uint32_t b = lane; b < blocks; b += 32) {
+    const uint32_t* w = s32 + b * 4;
+    const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];  // w[4]: inside the padded buffer
+    d4[b] = make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
+                       __funnelshift_r(w3, w4, sh));
+  }
+  const uint32_t done = head + blocks * 16;
+  if (done + lane < n) dst[done + lane] = src[done + lane];
 }
 
 __device__ __forceinline__ uint64_t havoc_cap(uint64_t len) {
@@ -269,118 +307,239 @@ __device__ __forceinline__ uint64_t havoc_cap(uint64_t len) {
   return m > kMaxInput ? kMaxInput : m;
 }
 
-// The stacked-havoc edit loop of one slot (src/engine.cpp:120-191).  DRY = true runs only the
-// Rng draws and the length bookkeeping -- every below() bound depends on the current length
-// alone, never on the bytes -- which is what a serial-stream plan needs (hfz_havoc_serial_plan).
-template <bool DRY, bool SMEM = false>
-__device__ __forceinline__ uint64_t havoc_edit(uint8_t* v, uint64_t len, WarpRng& rng, int lane) {
-  const uint64_t ops = 1 + rng.below(64);
-  for (uint64_t op = 0; op < ops; ++op) {
-    if (len == 0) {  // engine.cpp:124-129 (no 1 MiB clamp on this branch)
-      const uint64_t cnt = 1 + rng.below(8);
-      for (uint64_t i = 0; i < cnt; ++i) {
-        const uint8_t b = (uint8_t)rng.below(256);
-        if (!DRY && lane == 0) v[len] = b;
-        ++len;
+// ---- edit lists.  One 64-bit word per edit: kind (4 bits) | A (23) | B (21) | C (16).
+//   0 flip bit        A = bit position (MSB-first inside the byte)
+//   1 set byte        A = index, C = value
+//   2 byte +/- delta  A = index, B = delta, C = 1 add / 0 subtract
+//   3 interesting 16  A = offset, C = table index
+//   4 interesting 32  A = offset, C = table index
+//   5 delete block    A = offset, B = count
+//   6 duplicate block A = source, B = destination, C = count
+//   7 constant fill   A = offset, B = count, C = value
+//   8 swap bytes      A = i, B = k
+//   9 append to an EMPTY input: bits 4-7 = count (1..8), bits 8-63 = bytes 0..6;  10: bits 8-15 = byte 7
+// Word 0 of a slot's list is the number of edit words that follow (<= 65).
+constexpr uint32_t kOpWords = 66;
+__device__ __forceinline__ uint64_t op_word(uint32_t kind, uint32_t a, uint32_t b, uint32_t c) {
+  return (uint64_t)kind | ((uint64_t)a << 4) | ((uint64_t)b << 27) | ((uint64_t)c << 48);
+}
+
+// scalar splitmix64 of one slot (rng.hpp:15-28).  The state after k draws is seed + k * gamma, so the
+// raw outputs of the next draws do not depend on the bounds they will be reduced by: edit_begin()
+// mixes the next four at once (independent multiply chains the scheduler overlaps) and take() hands
+// them out in order; only "was a draw consumed" (bound > 1) stays on the dependent path.
+struct LaneRng {
+  uint64_t s;
+  uint32_t draws;
+  uint64_t r0, r1, r2, r3;
+  uint32_t used;
+  __device__ __forceinline__ void init(uint64_t state, int) {
+    s = state;
+    draws = 0;
+  }
+  static __device__ __forceinline__ uint32_t reduce(uint64_t r, uint32_t n) {  // (u128(r) * n) >> 64 for n < 2^32
+    const uint64_t t = (uint64_t)(uint32_t)(r >> 32) * n + (((uint64_t)(uint32_t)r * n) >> 32);
+    return (uint32_t)(t >> 32);
+  }
+  __device__ __forceinline__ uint32_t below(uint32_t n) {
+    if (n <= 1) return 0;
+    s += HFZ_GAMMA;
+    ++draws;
+    return reduce(hfz_sm64_mix(s), n);
+  }
+  __device__ __forceinline__ void edit_begin() {
+    r0 = hfz_sm64_mix(s + HFZ_GAMMA);
+    r1 = hfz_sm64_mix(s + 2 * HFZ_GAMMA);
+    r2 = hfz_sm64_mix(s + 3 * HFZ_GAMMA);
+    r3 = hfz_sm64_mix(s + 4 * HFZ_GAMMA);
+    used = 0;
+  }
+  __device__ __forceinline__ uint32_t take(uint32_t n) {  // at most four per edit
+    const uint64_t r = used == 0 ? r0 : (used == 1 ? r1 : (used == 2 ? r2 : r3));
+    const bool drawn = n > 1;
+    used += drawn;
+    return drawn ? reduce(r, n) : 0u;
+  }
+  __device__ __forceinline__ void edit_end() {
+    s += (uint64_t)used * HFZ_GAMMA;
+    draws += used;
+  }
+};
+
+// The draw sequence of the stacked-havoc edit loop of one slot (src/engine.cpp:120-191) and, with
+// EMIT, its edit list.  Every edit kind is "up to three draws whose bounds depend on the kind, the
+// current length and the earlier draws" -- a bound of 0 or 1 draws nothing (rng.hpp:24-28) -- so
+// the walk is one straight-line body per edit with selects instead of a nine-way branch: 32
+// slots of a warp stay converged whatever kinds they drew.  Returns the final length.
+template <class R, bool EMIT>
+__device__ __forceinline__ uint32_t havoc_plan(R& rng, uint32_t len, uint64_t* __restrict__ ops) {
+  const uint32_t n_edits = 1 + rng.below(64);
+  uint32_t n_words = 0;
+  for (uint32_t e = 0; e < n_edits; ++e) {
+    if (len == 0) {  // engine.cpp:124-129: only an empty INPUT gets here (a delete leaves >= 1 byte)
+      const uint32_t cnt = 1 + rng.below(8);
+      uint64_t w9 = 9u | ((uint64_t)cnt << 4), w10 = 10u;
+      for (uint32_t i = 0; i < cnt; ++i) {
+        const uint64_t b = rng.below(256);
+        if (i < 7) w9 |= b << (8 + 8 * i);
+        else w10 |= b << 8;
       }
-      if (!DRY) __syncwarp();
+      if (EMIT) {
+        ops[1 + n_words++] = w9;
+        if (cnt == 8) ops[1 + n_words++] = w10;
+      }
+      len = cnt;
       continue;
     }
-    switch ((uint32_t)rng.below(9)) {
-      case 0: {  // flip one bit, MSB-first numbering
-        const uint64_t pos = rng.below((uint32_t)(len * 8));
-        if (!DRY && lane == 0) v[pos / 8] ^= (uint8_t)(0x80u >> (pos % 8));
+    rng.edit_begin();
+    const uint32_t kind = rng.take(9);
+    // kinds 3 / 4 / 5 are no-ops without draws below 2 / 4 / 2 bytes
+    const bool skip = (kind == 3 && len < 2) || (kind == 4 && len < 4) || (kind == 5 && len < 2);
+    uint32_t b1 = len;                       // 5, 6, 7, 8: a position
+    b1 = kind == 0 ? len * 8 : b1;           // bit position (len <= 2^20)
+    b1 = kind == 1 ? 256u : b1;              // the VALUE is drawn before the index (C++17 sequencing of '=')
+    b1 = kind == 2 ? 35u : b1;
+    b1 = kind == 3 ? len - 1 : b1;
+    b1 = kind == 4 ? len - 3 : b1;
+    b1 = skip ? 0u : b1;
+    const uint32_t r1 = rng.take(b1);
+    const uint32_t rest = len - r1;          // kinds 5, 6, 7: bytes from the drawn position to the end
+    const uint32_t quarter = len / 4 ? len / 4 : 1u;
+    uint32_t b2 = len;                       // 1, 2, 8: an index
+    b2 = kind == 0 ? 0u : b2;
+    b2 = kind == 3 ? 10u : b2;
+    b2 = kind == 4 ? 8u : b2;
+    b2 = kind == 5 ? (rest < quarter ? rest : quarter) : b2;
+    b2 = (kind == 6 || kind == 7) ? (rest < 16u ? rest : 16u) : b2;
+    b2 = skip ? 0u : b2;
+    const uint32_t r2 = rng.take(b2);
+    uint32_t b3 = 0;
+    b3 = kind == 2 ? 2u : b3;
+    b3 = kind == 6 ? len + 1 : b3;
+    b3 = kind == 7 ? 256u : b3;
+    const uint32_t r3 = rng.take(b3);
+    rng.edit_end();
+    if (EMIT && !skip) {
+      uint32_t a = r1, b = r2, c = r3;
+      if (kind == 1) a = r2, b = 0, c = r1;
+      if (kind == 2) a = r2, b = 1 + r1, c = r3 < 1;
+      if (kind == 3 || kind == 4) b = 0, c = r2;
+      if (kind == 5) b = 1 + r2, c = 0;
+      if (kind == 6) b = r3, c = 1 + r2;
+      if (kind == 7) b = 1 + r2;
+      ops[1 + n_words++] = op_word(kind, a, b, c);
+    }
+    if (kind == 5 && !skip) len -= 1 + r2;
+    if (kind == 6) {
+      len += 1 + r2;
+      if (len > kMaxInput) len = kMaxInput;  // the insert is clamped to 1 MiB (engine.cpp:190)
+    }
+  }
+  if (EMIT) ops[0] = n_words;
+  return len;
+}
+
+// PLAN: one thread per slot of the chunk.
+__global__ void __launch_bounds__(64) hfz_k_havoc_plan_ops(const uint64_t* __restrict__ in_off, uint64_t n,
+                                                          uint64_t* __restrict__ state, uint64_t* __restrict__ ops,
+                                                          uint64_t* __restrict__ out_len, uint32_t* __restrict__ draws_out,
+                                                          unsigned long long* __restrict__ next_slot) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j == 0) *next_slot = 0;  // the apply kernel's hand-out counter
+  if (j >= n) return;
+  uint64_t len64 = in_off[j + 1] - in_off[j];
+  // Inputs longer than kMaxInputBytes are rejected by the host-buffer entry points (hfz.h); a
+  // device-buffer caller that passes one anyway gets a memory-safe result: the slot's capacity is
+  // hfz_havoc_max_out(len) = 1 MiB, so only the first 1 MiB is mutated.
+  if (len64 > kMaxInput) len64 = kMaxInput;
+  LaneRng rng;
+  rng.init(state[j], 0);
+  const uint32_t len = havoc_plan<LaneRng, true>(rng, (uint32_t)len64, ops + j * kOpWords);
+  out_len[j] = len;
+  state[j] = rng.s;
+  if (draws_out) draws_out[j] = rng.draws;
+}
+
+// APPLY: one warp per slot.  v = the working buffer (SMEM: shared, 16-byte aligned, padded).
+template <bool SMEM>
+__device__ __forceinline__ uint32_t havoc_apply(uint8_t* v, uint32_t len, const uint64_t* __restrict__ ops, int lane) {
+  // the whole list with one coalesced load: lane l holds words l, 32 + l and (lanes 0, 1) 64 + l
+  const uint64_t w_a = ops[lane];
+  const uint32_t n_words = (uint32_t)__shfl_sync(0xffffffffu, w_a, 0);
+  const uint64_t w_b = 32u + lane <= n_words ? ops[32 + lane] : 0ull;
+  const uint64_t w_c = 64u + lane <= n_words ? ops[64 + lane] : 0ull;
+  for (uint32_t i = 1; i <= n_words; ++i) {
+    // (the word's holder changes every 32 edits: selecting it per edit is cheaper than three copies of the switch)
+    const uint64_t held = i < 32 ? w_a : (i < 64 ? w_b : w_c);
+    const uint64_t w = __shfl_sync(0xffffffffu, held, (int)(i & 31));
+    const uint32_t kind = (uint32_t)w & 15u, a = (uint32_t)(w >> 4) & 0x7fffffu, b = (uint32_t)(w >> 27) & 0x1fffffu,
+                   c = (uint32_t)(w >> 48);
+    switch (kind) {
+      case 0:
+        if (lane == 0) v[a / 8] ^= (uint8_t)(0x80u >> (a % 8));
+        break;
+      case 1:
+        if (lane == 0) v[a] = (uint8_t)c;
+        break;
+      case 2:
+        if (lane == 0) v[a] = (uint8_t)(c ? v[a] + b : v[a] - b);
+        break;
+      case 3: {  // little endian (write_le, engine.cpp:46-49)
+        const uint32_t val = (uint16_t)c_interesting16[c];
+        if (lane < 2) v[a + lane] = (uint8_t)(val >> (8 * lane));
         break;
       }
-      case 1: {  // random byte: the VALUE is drawn before the index (C++17 sequencing of '=')
-        const uint8_t val = (uint8_t)rng.below(256);
-        const uint64_t i = rng.below(len);
-        if (!DRY && lane == 0) v[i] = val;
+      case 4: {
+        const uint32_t val = (uint32_t)c_interesting32[c];
+        if (lane < 4) v[a + lane] = (uint8_t)(val >> (8 * lane));
         break;
       }
-      case 2: {  // byte +/- delta
-        const uint8_t d = (uint8_t)(1 + rng.below(35));
-        const uint64_t i = rng.below(len);
-        const bool add = rng.below(2) < 1;
-        if (!DRY && lane == 0) v[i] = (uint8_t)(add ? v[i] + d : v[i] - d);
+      case 5:
+        if (SMEM) smem_move_down(v, a, a + b, len - a - b, lane);
+        else warp_move_down(v, a, a + b, len - a - b, lane);
+        len -= b;
         break;
-      }
-      case 3: {  // interesting 16-bit, little endian
-        if (len < 2) break;
-        const uint64_t off = rng.below(len - 1);
-        const uint16_t val = (uint16_t)c_interesting16[rng.below(10)];
-        if (!DRY && lane < 2) v[off + lane] = (uint8_t)(val >> (8 * lane));
-        break;
-      }
-      case 4: {  // interesting 32-bit, little endian
-        if (len < 4) break;
-        const uint64_t off = rng.below(len - 3);
-        const uint32_t val = (uint32_t)c_interesting32[rng.below(8)];
-        if (!DRY && lane < 4) v[off + lane] = (uint8_t)(val >> (8 * lane));
-        break;
-      }
-      case 5: {  // delete a block
-        if (len < 2) break;
-        const uint64_t off = rng.below(len);
-        const uint64_t q = len / 4 ? len / 4 : 1;
-        const uint64_t max_n = len - off < q ? len - off : q;
-        const uint64_t cnt = 1 + rng.below(max_n);
-        if (!DRY) __syncwarp();
-        if (!DRY) {
-          if (SMEM) smem_move_down(v, off, off + cnt, len - off - cnt, lane);
-          else warp_move_down(v, off, off + cnt, len - off - cnt, lane);
+      case 6: {  // copy the block first, then insert it (the 1 MiB clamp folded in: bytes past the cap are dropped)
+        const uint8_t blk = (uint32_t)lane < c ? v[a + lane] : 0;
+        const uint32_t new_len = len + c > kMaxInput ? kMaxInput : len + c;
+        __syncwarp();
+        if (new_len > b + c) {
+          if (SMEM) smem_move_up(v, b + c, b, new_len - b - c, lane);
+          else warp_move_up(v, b + c, b, new_len - b - c, lane);
         }
-        len -= cnt;
-        break;
-      }
-      case 6: {  // duplicate a block elsewhere (copy first, then insert)
-        const uint64_t src = rng.below(len);
-        const uint64_t lim = len - src < 16 ? len - src : 16;
-        const uint64_t cnt = 1 + rng.below(lim);
-        const uint64_t dst = rng.below(len + 1);
-        if (!DRY) __syncwarp();
-        const uint8_t blk = (!DRY && (uint64_t)lane < cnt) ? v[src + lane] : 0;
-        // insert with the 1 MiB clamp folded in: bytes that would land past the cap are dropped
-        const uint64_t new_len = len + cnt > kMaxInput ? kMaxInput : len + cnt;
-        if (!DRY) __syncwarp();
-        if (!DRY && new_len > dst + cnt) {
-          if (SMEM) smem_move_up(v, dst + cnt, dst, new_len - dst - cnt, lane);
-          else warp_move_up(v, dst + cnt, dst, new_len - dst - cnt, lane);
-        }
-        if (!DRY && (uint64_t)lane < cnt && dst + lane < new_len) v[dst + lane] = blk;
+        if ((uint32_t)lane < c && b + lane < new_len) v[b + lane] = blk;
         len = new_len;
         break;
       }
-      case 7: {  // constant fill
-        const uint64_t off = rng.below(len);
-        const uint64_t lim = len - off < 16 ? len - off : 16;
-        const uint64_t cnt = 1 + rng.below(lim);
-        const uint8_t b = (uint8_t)rng.below(256);
-        if (!DRY && (uint64_t)lane < cnt) v[off + lane] = b;
+      case 7:
+        if ((uint32_t)lane < b) v[a + lane] = (uint8_t)c;
         break;
-      }
-      default: {  // 8: swap two bytes
-        const uint64_t i = rng.below(len);
-        const uint64_t k = rng.below(len);
-        if (!DRY && lane == 0) {
-          const uint8_t t = v[i];
-          v[i] = v[k];
-          v[k] = t;
+      case 8:
+        if (lane == 0) {
+          const uint8_t t = v[a];
+          v[a] = v[b];
+          v[b] = t;
         }
         break;
+      case 9: {
+        const uint32_t cnt = (uint32_t)(w >> 4) & 15u;
+        if ((uint32_t)lane < cnt && lane < 7) v[lane] = (uint8_t)(w >> (8 + 8 * lane));
+        len = cnt;
+        break;
       }
+      default:  // 10: the eighth appended byte
+        if (lane == 0) v[7] = (uint8_t)(w >> 8);
+        break;
     }
-    if (!DRY) __syncwarp();
-    if (len > kMaxInput) len = kMaxInput;
+    __syncwarp();  // edits are ordered; successive ones may be done by different lanes
   }
   return len;
 }
 
-__global__ void __launch_bounds__(kHavocWarps * 32) hfz_k_havoc(
+__global__ void __launch_bounds__(kHavocWarps * 32, 4) hfz_k_havoc_apply(
     const uint8_t* __restrict__ in_bytes, const uint64_t* __restrict__ in_off, uint64_t n,
-    uint64_t* __restrict__ state, uint8_t* __restrict__ out_bytes,
-    const uint64_t* __restrict__ out_off, uint64_t* __restrict__ out_len,
-    uint32_t* __restrict__ draws_out, unsigned long long* __restrict__ next_slot) {
+    const uint64_t* __restrict__ ops, uint8_t* __restrict__ out_bytes, const uint64_t* __restrict__ out_off,
+    unsigned long long* __restrict__ next_slot) {
   __shared__ __align__(16) uint8_t s_buf[kHavocWarps][kSmemCap + 16];  // + 16: the block moves read one block past the data
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // slots are handed out dynamically: a mutant stacks 1..64 edits, so their costs differ widely
@@ -390,29 +549,22 @@ __global__ void __launch_bounds__(kHavocWarps * 32) hfz_k_havoc(
     const uint64_t j = __shfl_sync(0xffffffffu, jj, 0);
     if (j >= n) break;
     const uint64_t i0 = in_off[j];
-    uint64_t len = in_off[j + 1] - i0;
-    // Inputs longer than kMaxInputBytes are rejected by the host-buffer entry points (hfz.h); a
-    // device-buffer caller that passes one anyway gets a memory-safe result: the slot's capacity is
-    // hfz_havoc_max_out(len) = 1 MiB, so only the first 1 MiB is mutated.
-    if (len > kMaxInput) len = kMaxInput;
+    uint64_t len64 = in_off[j + 1] - i0;
+    if (len64 > kMaxInput) len64 = kMaxInput;
+    const uint32_t len = (uint32_t)len64;
     uint8_t* out = out_bytes + out_off[j];
-    const bool in_smem = havoc_cap(len) <= kSmemCap;
-    uint8_t* v = in_smem ? s_buf[warp] : out;
-    if (in_smem) copy_in_smem(v, in_bytes + i0, len, lane);
-    else warp_copy(v, in_bytes + i0, len, lane);
-    __syncwarp();
-
-    WarpRng rng;
-    rng.init(state[j], lane);
-    len = in_smem ? havoc_edit<false, true>(v, len, rng, lane) : havoc_edit<false, false>(v, len, rng, lane);
-    if (in_smem) {
-      warp_copy(out, v, len, lane);
+    const uint64_t* my_ops = ops + j * kOpWords;
+    if (havoc_cap(len) <= kSmemCap) {
+      uint8_t* v = s_buf[warp];
+      copy_in_smem(v, in_bytes + i0, len, lane);
       __syncwarp();
-    }
-    if (lane == 0) {
-      out_len[j] = len;
-      state[j] = rng.s;
-      if (draws_out) draws_out[j] = rng.draws;
+      const uint32_t out_n = havoc_apply<true>(v, len, my_ops, lane);
+      copy_out_smem(out, v, out_n, lane);
+      __syncwarp();  // the buffer is reused for the warp's next slot
+    } else {
+      warp_copy(out, in_bytes + i0, len, lane);
+      __syncwarp();
+      havoc_apply<false>(out, len, my_ops, lane);
     }
   }
 }
@@ -428,7 +580,9 @@ __global__ void hfz_k_havoc_plan(const uint64_t* __restrict__ in_off, uint64_t n
   __syncwarp();
   for (uint64_t j = 0; j < n; ++j) {
     if (lane == 0) slot_states[j] = rng.s;
-    havoc_edit<true>(nullptr, in_off[j + 1] - in_off[j], rng, lane);
+    uint64_t len = in_off[j + 1] - in_off[j];
+    if (len > kMaxInput) len = kMaxInput;
+    havoc_plan<WarpRng, false>(rng, (uint32_t)len, nullptr);
   }
   __syncwarp();
   if (lane == 0) *stream_state = rng.s;
@@ -549,14 +703,33 @@ extern "C" int hfz_havoc_batch(hfz_ctx* ctx, const uint8_t* in_bytes, const uint
   }
   if (n == 0) return HFZ_OK;
   HFZ_CUDA(cudaSetDevice(ctx->device));
-  uint64_t blocks = (n + kHavocWarps - 1) / kHavocWarps;
-  const uint64_t maxb = (uint64_t)ctx->num_sms * 4;  // at most 4 CTAs of 48 KB fit an SM
-  if (blocks > maxb) blocks = maxb;
+  // plan + apply per chunk of slots: the edit lists of a chunk live in context scratch (528 bytes per
+  // slot, at most kHavocChunk slots = 69 MB, grown geometrically and kept for the context's lifetime)
+  const uint64_t chunk = n < kHavocChunk ? n : kHavocChunk;
+  if (ctx->hv_ops_cap < chunk) {
+    uint64_t want = ctx->hv_ops_cap * 2 > chunk ? ctx->hv_ops_cap * 2 : chunk;
+    if (want > kHavocChunk) want = kHavocChunk;
+    HFZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    cudaFree(ctx->hv_ops);
+    ctx->hv_ops = nullptr;
+    ctx->hv_ops_cap = 0;
+    HFZ_CUDA(cudaMalloc(&ctx->hv_ops, want * kOpWords * sizeof(uint64_t)));
+    ctx->hv_ops_cap = want;
+  }
   unsigned long long* next_slot = ctx->d_small + 5;
-  HFZ_CUDA(cudaMemsetAsync(next_slot, 0, sizeof(unsigned long long), ctx->stream));
-  hfz_k_havoc<<<(uint32_t)blocks, kHavocWarps * 32, 0, ctx->stream>>>(
-      in_bytes, in_off, n, rng_state_inout, out_bytes, out_off, out_len, draws_out, next_slot);
-  ++ctx->launches;
+  // four CTAs' working buffers (4 x 48 KB) need the large shared-memory carve-out
+  HFZ_CUDA(cudaFuncSetAttribute(hfz_k_havoc_apply, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
+  for (uint64_t j0 = 0; j0 < n; j0 += chunk) {
+    const uint64_t m = n - j0 < chunk ? n - j0 : chunk;
+    hfz_k_havoc_plan_ops<<<(uint32_t)((m + 63) / 64), 64, 0, ctx->stream>>>(
+        in_off + j0, m, rng_state_inout + j0, ctx->hv_ops, out_len + j0, draws_out ? draws_out + j0 : nullptr, next_slot);
+    uint64_t blocks = (m + kHavocWarps - 1) / kHavocWarps;
+    const uint64_t maxb = (uint64_t)ctx->num_sms * 4;  // 4 CTAs of 48 KB and 256 threads x 64 registers fit an SM
+    if (blocks > maxb) blocks = maxb;
+    hfz_k_havoc_apply<<<(uint32_t)blocks, kHavocWarps * 32, 0, ctx->stream>>>(in_bytes, in_off + j0, m, ctx->hv_ops, out_bytes,
+                                                                               out_off + j0, next_slot);
+    ctx->launches += 2;
+  }
   HFZ_CUDA(cudaGetLastError());
   return HFZ_OK;
 }
