@@ -29,7 +29,25 @@
 //                   more distinct sites than the table holds, the site space is partitioned by
 //                   hash prefix (the rule is separable per site) and the replay repeats per
 //                   partition, splitting on overflow.
+#include <stdio.h>
+
 #include "hfz_common.cuh"
+
+// Dev diagnostic (make EXTRA=-DHFZ_EDGE_PROF): cycles per phase, summed over the lane 0s of the table-owning
+// (row 0) and the other (row 1) warps; read back with hfz_dbg_edge_prof (scripts/probe_k1k3.py edge).
+#ifdef HFZ_EDGE_PROF
+__device__ unsigned long long g_edge_prof[2][16];
+#define PROF_DECL long long _pt = clock64()
+#define PROF(prof, cat)                                                                \
+  do {                                                                                 \
+    const long long _pn = clock64();                                                   \
+    if (lane == 0 && (prof)) atomicAdd((prof) + (cat), (unsigned long long)(_pn - _pt)); \
+    _pt = _pn;                                                                         \
+  } while (0)
+#else
+#define PROF_DECL
+#define PROF(prof, cat)
+#endif
 
 namespace {
 
@@ -269,137 +287,240 @@ __device__ __forceinline__ uint64_t general_path(WarpTable& tab, const uint32_t*
   return bumps;
 }
 
-// Transposed general path: real lane L plays simulated lane L.
-//   phase 1  every lane walks its own events and counts its visits per site in a nibble matrix
-//            cnt[row(site)][L] (shared-memory atomics on the 32-bit word that holds the nibble);
+// Transposed general path for one simulated warp.
+//   phase 1  the warp's events (contiguous in the trace: lane 0's, then lane 1's, ...) are dealt out
+//            32 at a time, one per REAL lane -- coalesced loads, and a warp whose lanes walked paths
+//            of different lengths still keeps every real lane busy.  The simulated lane L of an event
+//            is found by a 5-step shuffle search over the lanes' end offsets; the event is counted in
+//            a nibble matrix cnt[row(site)][L] (shared-memory atomics on the word that holds the nibble);
 //   row pass c_L(s) -> d_L(s) = max(0, c_L(s) - max_{L' < L} c_{L'}(s)): the number of bumps lane L
 //            owes for site s (its visits k = M_L(s)+1 .. c_L(s)); exclusive prefix max over the 32
 //            lanes of a row with SIMD byte ops, saturating byte subtract;
-//   phase 2  every lane walks its events BACKWARDS and hands out its d_L(s) bumps to the last
-//            d_L(s) visits of s -- exactly the visits with k > M_L(s); slot uses that visit's own
-//            prev.  Bumps commute (saturating adds), so their order is free.
-// Table: kTRows x {u32 site key, 16 bytes of nibbles}; byte b holds lane b (low nibble) and lane
-// b + 16 (high nibble).  Returns false (nothing bumped) when the table fills up or a lane visits a
-// site more than 15 times: the caller then runs the partitioned replay, which has neither limit.
+//   phase 2  the events are dealt out again, from the END of the warp's range backwards, and the
+//            d_L(s) bumps go to the last d_L(s) visits of s by L -- exactly the visits with
+//            k > M_L(s): inside a round __match_any groups the visits of one (L, s), the j-th from the
+//            end bumps iff j < d, and the group's first lane takes min(d, size) off the nibble before
+//            the next (earlier) round reads it.  The slot uses that visit's own prev.  Bumps commute
+//            (saturating adds), so their order is free.
+// Table: 128 buckets x 4 site keys, then (kTRows + 1) rows of 16 bytes of nibbles; byte b of a row
+// holds lane b (low nibble) and lane b + 16 (high nibble).  A lookup reads a whole bucket with one
+// 128-bit load (1.2 probes on average at the ~55 % load of a fully divergent warp; linear probing
+// over single keys needed ~8 warp-level steps until the slowest lane had found its row).
+// Returns false (nothing bumped) when the table fills up, a lane visits a site more than 15 times
+// or the warp has 2^31 events or more: the caller then runs the partitioned replay, which has none
+// of these limits.
 constexpr uint32_t kTRows = 512;
+constexpr uint32_t kTBuckets = kTRows / 4;
 constexpr uint32_t kTEmpty = 0xffffffffu;  // key of a free row; the site 0xffffffff gets row kTRows
 static_assert((kTRows + 1) * (4 + 16) <= kTabBytes, "transposed table must fit a pool table");
 
 __device__ __forceinline__ bool transposed_path(uint8_t* tab, const uint32_t* sites, uint64_t e0, uint32_t n_ev,
-                                                uint32_t prev0, const Counters& counters, uint32_t hmask, int lane,
-                                                uint64_t& bumps_out) {
-  uint32_t* keys = reinterpret_cast<uint32_t*>(tab);                    // [kTRows + 1]
+                                                bool active, uint32_t prev0, const Counters& counters, uint32_t hmask,
+                                                int lane, uint64_t& bumps_out, unsigned long long* prof = nullptr) {
+  PROF_DECL;
+  uint32_t* keys = reinterpret_cast<uint32_t*>(tab);                    // [kTRows + 1], buckets of 4
   uint32_t* cnt = reinterpret_cast<uint32_t*>(tab + (kTRows + 4) * 4);  // [kTRows + 1][4], 16-byte aligned
   for (uint32_t i = lane; i < kTRows + 1; i += 32) keys[i] = kTEmpty;
   uint4* clr = reinterpret_cast<uint4*>(cnt);
   for (uint32_t i = lane; i < kTRows + 1; i += 32) clr[i] = make_uint4(0, 0, 0, 0);
+  // the warp's event range [first, first + N); rel_end = end of this lane's events inside it
+  // (non-decreasing over the lanes: the inactive lanes of a partial warp are its last ones)
+  const uint64_t first = __shfl_sync(0xffffffffu, e0, 0);
+  const uint64_t my_end = active ? e0 + n_ev - first : 0;
+  uint64_t n64 = my_end;
+  for (int d = 16; d; d >>= 1) {
+    const uint64_t o = __shfl_xor_sync(0xffffffffu, n64, d);
+    n64 = o > n64 ? o : n64;
+  }
   __syncwarp();
-  const uint32_t b = lane & 15;
-  const uint32_t word = b >> 2, shift = (b & 3) * 8 + (lane >> 4) * 4;
-  const uint32_t max_n = __reduce_max_sync(0xffffffffu, n_ev);
-  auto find = [&](uint32_t s, bool insert) -> uint32_t {
-    if (s == kTEmpty) return kTRows;
-    uint32_t r = (s * 0x9e3779b1u) >> (32 - 9);  // multiplicative hash: the top 9 bits index the 512 rows
-    static_assert(kTRows == 512, "hash shift assumes 512 rows");
-    for (uint32_t probe = 0; probe < kTRows; ++probe) {
-      const uint32_t cur = keys[r];
-      if (cur == s) return r;
-      if (insert && cur == kTEmpty) {
-        const uint32_t old = atomicCAS(&keys[r], kTEmpty, s);
-        if (old == kTEmpty || old == s) return r;
-      }
-      r = (r + 1) & (kTRows - 1);
+  if (n64 >= (1ull << 31)) return false;
+  const uint32_t N = (uint32_t)n64;
+  const uint32_t rel_end = active ? (uint32_t)my_end : N;
+  const uint32_t* ev = sites + first;
+  PROF(prof, 5);
+  auto sim_lane = [&](uint32_t g) -> uint32_t {  // lanes whose events end at or before g
+    uint32_t L = 0;
+#pragma unroll
+    for (uint32_t step = 16; step; step >>= 1) {
+      const uint32_t pe = __shfl_sync(0xffffffffu, rel_end, (int)(L + step - 1));
+      L += pe <= g ? step : 0u;
     }
-    return kTRows + 1;  // full
+    return L & 31u;  // (a lane past the range computes 32: it is off anyway)
+  };
+  auto cell_word = [](uint32_t L) { return (L & 15u) >> 2; };
+  auto cell_shift = [](uint32_t L) { return (L & 3u) * 8u + (L >> 4) * 4u; };
+  // find (insert = false) or find-or-insert, called by the WHOLE warp (on = this lane has a site to
+  // look up): the probe loop is warp-synchronous -- it runs until no lane is pending, so the lanes
+  // leave it together (a per-lane loop with early returns left the warp split for everything after it).
+  // Returns the row, kTRows for the site 0xffffffff, kTRows + 1 when the table is full / the key absent.
+  const uint4* keys4 = reinterpret_cast<const uint4*>(keys);
+  auto find = [&](uint32_t s, bool on, bool insert) -> uint32_t {
+    uint32_t b = (s * 0x9e3779b1u) >> (32 - 7);  // multiplicative hash: the top 7 bits pick one of 128 buckets
+    static_assert(kTBuckets == 128, "hash shift assumes 128 buckets");
+    uint32_t res = kTRows + 1, probes = 0;
+    bool pending = on;
+    if (on && s == kTEmpty) {
+      res = kTRows;
+      pending = false;
+    }
+    while (__any_sync(0xffffffffu, pending)) {
+      if (pending) {
+        uint4 k;  // (volatile: other lanes insert between two looks at a bucket)
+        asm volatile("ld.volatile.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(k.x), "=r"(k.y), "=r"(k.z), "=r"(k.w)
+                     : "r"(hfz_smem_u32(keys4 + b)));
+        int j = k.x == s ? 0 : (k.y == s ? 1 : (k.z == s ? 2 : (k.w == s ? 3 : -1)));
+        bool advance = false;
+        if (j < 0) {
+          if (insert) {
+            const int f = k.x == kTEmpty ? 0 : (k.y == kTEmpty ? 1 : (k.z == kTEmpty ? 2 : (k.w == kTEmpty ? 3 : -1)));
+            if (f < 0) {
+              advance = true;  // bucket full of other keys
+            } else {
+              const uint32_t old = atomicCAS(&keys[b * 4 + f], kTEmpty, s);
+              if (old == kTEmpty || old == s) j = f;  // else: another key took the slot -- read the bucket again
+            }
+          } else {
+            advance = true;  // lookups are for keys phase 1 inserted: the key sits in a later bucket
+          }
+        }
+        if (j >= 0) {
+          res = b * 4 + (uint32_t)j;
+          pending = false;
+        } else if (advance) {
+          b = (b + 1) & (kTBuckets - 1);
+          pending = ++probes < kTBuckets;
+        }
+      }
+    }
+    return res;
   };
   bool bad = false;
-  for (uint32_t i = 0; i < max_n; ++i) {
-    if (i < n_ev && !bad) {
-      const uint32_t r = find(sites[e0 + i], true);
+  for (uint32_t g0 = 0; g0 < N; g0 += 32) {
+    const uint32_t g = g0 + lane;
+    const bool on = g < N && !bad;
+    const uint32_t s = g < N ? ev[g] : 0u;
+    const uint32_t L = sim_lane(g);
+    const uint32_t r = find(s, on, true);
+    if (on) {
       if (r > kTRows) {
         bad = true;
       } else {
-        const uint32_t old = atomicAdd(&cnt[r * 4 + word], 1u << shift);
-        bad = ((old >> shift) & 15u) == 15u;  // nibble overflow: the table is abandoned
+        const uint32_t sh = cell_shift(L);
+        const uint32_t old = atomicAdd(&cnt[r * 4 + cell_word(L)], 1u << sh);
+        bad = ((old >> sh) & 15u) == 15u;  // nibble overflow: the table is abandoned
       }
     }
+    __syncwarp();
   }
   const bool any_bad = __any_sync(0xffffffffu, bad);
   __syncwarp();  // table reads above are ordered before whatever reuses the table next
+  PROF(prof, 6);
   if (any_bad) return false;
-  // rows -> owed bumps.  Lane order inside a row: low nibbles of words 0..3, then high nibbles.
-  // Most rows of a divergent warp were visited by ONE lane only (d = c, nothing to do); the
-  // byte-wise max / saturating subtract are plain SWAR arithmetic (values <= 15 leave bit 7 of
-  // every byte free as a borrow guard; the video intrinsics are emulated on sm_100).
-  auto max4 = [](uint32_t a, uint32_t b2) {
-    const uint32_t ge = (((a | 0x80808080u) - b2) >> 7) & 0x01010101u;  // 1 where a >= b
-    const uint32_t m = ge * 0xffu;
-    return (a & m) | (b2 & ~m);
-  };
-  for (uint32_t r = lane; r < kTRows + 1; r += 32) {
-    const uint4 x = reinterpret_cast<uint4*>(cnt)[r];
-    const uint32_t any = x.x | x.y | x.z | x.w;
-    if (any == 0u) continue;
-    // non-zero nibble flags of each word, then: exactly one visiting lane?
-    auto nzn = [](uint32_t v) { return (v | (v >> 1) | (v >> 2) | (v >> 3)) & 0x11111111u; };
-    if (__popc(nzn(x.x)) + __popc(nzn(x.y)) + __popc(nzn(x.z)) + __popc(nzn(x.w)) == 1) continue;
-    if (((x.x | x.y | x.z | x.w) & 0xeeeeeeeeu) == 0u) {
-      // every visiting lane visited once (the usual row of a divergent warp): only the LOWEST visiting
-      // lane owes a bump.  Lane order: low nibbles of words 0..3, then the high nibbles.
-      const uint32_t lo[4] = {x.x & 0x0f0f0f0fu, x.y & 0x0f0f0f0fu, x.z & 0x0f0f0f0fu, x.w & 0x0f0f0f0fu};
-      uint4 d4 = make_uint4(0, 0, 0, 0);
-      if (lo[0] | lo[1] | lo[2] | lo[3]) {
-        if (lo[0]) d4.x = lo[0] & (0u - lo[0]);
-        else if (lo[1]) d4.y = lo[1] & (0u - lo[1]);
-        else if (lo[2]) d4.z = lo[2] & (0u - lo[2]);
-        else d4.w = lo[3] & (0u - lo[3]);
-      } else {
-        const uint32_t hi4[4] = {x.x & 0xf0f0f0f0u, x.y & 0xf0f0f0f0u, x.z & 0xf0f0f0f0u, x.w & 0xf0f0f0f0u};
-        if (hi4[0]) d4.x = hi4[0] & (0u - hi4[0]);
-        else if (hi4[1]) d4.y = hi4[1] & (0u - hi4[1]);
-        else if (hi4[2]) d4.z = hi4[2] & (0u - hi4[2]);
-        else d4.w = hi4[3] & (0u - hi4[3]);
-      }
-      reinterpret_cast<uint4*>(cnt)[r] = d4;
-      continue;
-    }
-    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-    uint32_t d[4] = {0, 0, 0, 0};
-    uint32_t carry = 0;  // max count among the lanes seen so far
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint32_t v = (w[k] >> (4 * half)) & 0x0f0f0f0fu;
-        uint32_t pm = max4(v, v << 8);
-        pm = max4(pm, pm << 16);                          // inclusive prefix max inside the word
-        pm = max4(pm, carry * 0x01010101u);               // ... including the earlier lanes
-        const uint32_t ex = (pm << 8) | carry;            // exclusive prefix max per lane
-        const uint32_t t = (v | 0x80808080u) - ex;        // per byte: v - ex with a borrow guard
-        const uint32_t ge = (t >> 7) & 0x01010101u;       // 1 where v >= ex
-        d[k] |= (t & 0x0f0f0f0fu & (ge * 0xffu)) << (4 * half);
-        carry = pm >> 24;
+  // rows -> owed bumps.  Lane order inside a row: low nibbles of words 0..3 (lanes 0..15), then the
+  // high nibbles (lanes 16..31).  Each real lane takes every 32nd row.  Nearly every visited row of a
+  // divergent warp is one of two cheap kinds -- ONE visiting lane (d = c: nothing to do), or all
+  // visiting lanes with the SAME count c (only the lowest of them owes bumps, c of them) -- and is
+  // rewritten in place by its lane.  Rows whose visitors differ in their counts are rare; taking
+  // them on inside the per-lane loop made every lane of the warp step through the 240-instruction
+  // prefix-max each time one lane needed it (a quarter of the kernel's instructions), so they
+  // are flagged by ballot and done by the WHOLE warp: lane L holds c_L, five shuffle steps give the
+  // exclusive prefix max, and the new nibbles are gathered with four warp-wide ORs.
+  auto nzn = [](uint32_t v) { return (v | (v >> 1) | (v >> 2) | (v >> 3)) & 0x11111111u; };
+  const uint32_t my_word = cell_word((uint32_t)lane), my_shift = cell_shift((uint32_t)lane);
+  for (uint32_t r0 = 0; r0 < kTRows + 1; r0 += 32) {
+    const uint32_t r = r0 + lane;
+    bool general = false;
+    if (r < kTRows + 1) {
+      const uint4 x = reinterpret_cast<uint4*>(cnt)[r];
+      const uint32_t any = x.x | x.y | x.z | x.w;
+      const uint32_t n0 = nzn(x.x), n1 = nzn(x.y), n2 = nzn(x.z), n3 = nzn(x.w);
+      if (any != 0u && __popc(n0) + __popc(n1) + __popc(n2) + __popc(n3) > 1) {
+        // the lowest visiting lane's nibble: low nibbles of words 0..3 first, then the high ones
+        const uint32_t l0 = n0 & 0x01010101u, l1 = n1 & 0x01010101u, l2 = n2 & 0x01010101u, l3 = n3 & 0x01010101u;
+        const bool low = (l0 | l1 | l2 | l3) != 0u;
+        const uint32_t c0 = low ? l0 : n0, c1 = low ? l1 : n1, c2 = low ? l2 : n2, c3 = low ? l3 : n3;  // candidates (flag bits)
+        const int wsel = c0 ? 0 : (c1 ? 1 : (c2 ? 2 : 3));
+        const uint32_t cw = wsel == 0 ? c0 : (wsel == 1 ? c1 : (wsel == 2 ? c2 : c3));
+        const uint32_t xw = wsel == 0 ? x.x : (wsel == 1 ? x.y : (wsel == 2 ? x.z : x.w));
+        const uint32_t pos = (uint32_t)__ffs(cw) - 1u;  // bit 0 of the lowest visiting lane's nibble
+        const uint32_t c = (xw >> pos) & 15u;           // its count
+        // same count everywhere?  every visited nibble equals c <=> x == flags * c
+        if (x.x == n0 * c && x.y == n1 * c && x.z == n2 * c && x.w == n3 * c) {
+          uint4 d4 = make_uint4(0, 0, 0, 0);
+          const uint32_t keep = c << pos;
+          d4.x = wsel == 0 ? keep : 0u;
+          d4.y = wsel == 1 ? keep : 0u;
+          d4.z = wsel == 2 ? keep : 0u;
+          d4.w = wsel == 3 ? keep : 0u;
+          reinterpret_cast<uint4*>(cnt)[r] = d4;
+        } else {
+          general = true;
+        }
       }
     }
-    reinterpret_cast<uint4*>(cnt)[r] = make_uint4(d[0], d[1], d[2], d[3]);
+    uint32_t todo = __ballot_sync(0xffffffffu, general);
+    while (todo) {  // warp-uniform
+      const uint32_t rr = r0 + (uint32_t)__ffs(todo) - 1;
+      todo &= todo - 1;
+      uint32_t* row = &cnt[rr * 4];
+      const uint32_t c = (row[my_word] >> my_shift) & 15u;  // c_L of this lane
+      uint32_t pm = c;  // inclusive prefix max over the lanes
+#pragma unroll
+      for (int dd = 1; dd < 32; dd <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, pm, dd);
+        if (lane >= dd) pm = max(pm, o);
+      }
+      uint32_t ex = __shfl_up_sync(0xffffffffu, pm, 1);
+      if (lane == 0) ex = 0;
+      const uint32_t dv = c > ex ? c - ex : 0u;
+      const uint32_t mine = dv << my_shift;
+      __syncwarp();  // every lane has read its nibble
+      const uint32_t w0 = __reduce_or_sync(0xffffffffu, my_word == 0 ? mine : 0u);
+      const uint32_t w1 = __reduce_or_sync(0xffffffffu, my_word == 1 ? mine : 0u);
+      const uint32_t w2 = __reduce_or_sync(0xffffffffu, my_word == 2 ? mine : 0u);
+      const uint32_t w3 = __reduce_or_sync(0xffffffffu, my_word == 3 ? mine : 0u);
+      if (lane == 0) *reinterpret_cast<uint4*>(row) = make_uint4(w0, w1, w2, w3);
+    }
   }
   __syncwarp();
+  PROF(prof, 7);
   uint32_t bumps = 0;
-  for (uint32_t i = max_n; i-- > 0;) {
-    if (i < n_ev) {
-      const uint32_t s = sites[e0 + i];
-      const uint32_t r = find(s, false);  // present since phase 1
-      uint32_t* c = &cnt[r * 4 + word];
-      if ((*reinterpret_cast<volatile uint32_t*>(c) >> shift) & 15u) {  // only this lane changes its nibble
-        atomicSub(c, 1u << shift);
-        const uint32_t pv = i ? (sites[e0 + i - 1] >> 1) : prev0;
+  const uint32_t lanes_above = lane == 31 ? 0u : (0xffffffffu << (lane + 1));
+  for (uint32_t hi = N; hi > 0; hi = hi > 32 ? hi - 32 : 0) {
+    const int32_t g = (int32_t)hi - 32 + lane;  // higher lane = later event
+    const bool on = g >= 0;
+    const uint32_t s = on ? ev[g] : 0u;
+    const uint32_t L = sim_lane(on ? (uint32_t)g : 0u);
+    const uint32_t r = find(s, on, false);  // present since phase 1
+#ifdef HFZ_EDGE_DEBUG
+    if (on && r > kTRows) printf("phase 2: site %08x not found (blk %d)\n", s, blockIdx.x);
+#endif
+    const uint32_t end_below = __shfl_sync(0xffffffffu, rel_end, (int)((L - 1) & 31u));  // (every lane shuffles)
+    const uint32_t lane_start = L ? end_below : 0u;
+    const uint32_t lane_prev0 = __shfl_sync(0xffffffffu, prev0, (int)L);
+    const unsigned long long key = on ? (((unsigned long long)L << 32) | s) : (0xffffffff00000000ull | (uint32_t)lane);
+    const uint32_t grp = __match_any_sync(0xffffffffu, key);
+    uint32_t* c = &cnt[(on ? r : kTRows) * 4 + cell_word(L)];
+    const uint32_t sh = cell_shift(L);
+    const uint32_t d = on ? ((*reinterpret_cast<volatile uint32_t*>(c) >> sh) & 15u) : 0u;
+    __syncwarp();  // every nibble of this round is read before any is lowered
+    if (on && d) {
+      if ((uint32_t)__popc(grp & lanes_above) < d) {  // one of the last d visits of s by L still open
+        const uint32_t pv = (uint32_t)g > lane_start ? (ev[g - 1] >> 1) : lane_prev0;
         counters.bump_slot((pv ^ s) & hmask);
         ++bumps;
       }
+      if ((grp & (0u - grp)) == (1u << lane)) {  // the group's first lane lowers the nibble for the earlier rounds
+        const uint32_t m = (uint32_t)__popc(grp);
+        atomicSub(c, (m < d ? m : d) << sh);
+      }
     }
+    __syncwarp();
   }
   bumps_out += bumps;
   __syncwarp();
+  PROF(prof, 8);
   return true;
 }
 
@@ -432,6 +553,17 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
   __shared__ uint32_t s_used;      // rows of the hashed table in use
   const bool owner = (threadIdx.x >> 5) < (uint32_t)kPool;
   const uint32_t n_nonowners = kEdgeWarps - kPool;
+#ifdef HFZ_EDGE_PROF
+  __shared__ unsigned long long s_prof[2][16];
+  if (threadIdx.x < 32) s_prof[threadIdx.x >> 4][threadIdx.x & 15] = 0;
+  unsigned long long* prof = s_prof[owner ? 0 : 1];
+  const long long t_kernel = clock64();
+  __syncthreads();
+#else
+  unsigned long long* prof = nullptr;
+  (void)prof;
+#endif
+  PROF_DECL;
   if (threadIdx.x < kDeferCap) s_defer[threadIdx.x] = 0;
   uint32_t* prev_tab = p.prev_scratch + (size_t)blockIdx.x * p.prev_stride;
   const uint32_t hmask = p.H - 1;
@@ -498,6 +630,7 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
       for (uint64_t i = threadIdx.x; i < mx; i += blockDim.x) prev_tab[i] = 0;
     }
     __syncthreads();
+    PROF(prof, 12);
 
     uint64_t my_events = 0;
     // uniform: one pass over all launches (sw runs over launch-major simulated warps)
@@ -511,6 +644,7 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
         s_left = 0;
       }
       __syncthreads();
+      PROF(prof, 12);
       if (launch_valid(d)) {
         // all of these fit 32 bits: blocks * tpb <= 2^22, tpb <= 1024 (launch_valid)
         const uint32_t gx = d[0], gy = d[1], bdx = d[3], bdy = d[4], bdz = d[5];
@@ -543,6 +677,9 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
             if (got) {
               q = got - 1;
               deferred = true;
+#ifdef HFZ_EDGE_DEBUG
+              if (q >= n_q && lane == 0) printf("bad deferred q %u n_q %llu blk %d warp %d\n", q, (unsigned long long)n_q, blockIdx.x, threadIdx.x >> 5);
+#endif
             }
           }
           if (!deferred) {
@@ -557,9 +694,14 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
               if (!owner) break;
               if (__shfl_sync(0xffffffffu, done, 0)) break;
               __nanosleep(200);
+              PROF(prof, 10);
               continue;
             }
           }
+          PROF(prof, 0);
+#ifdef HFZ_EDGE_DEBUG
+          if (q >= n_q && lane == 0) printf("bad q %u n_q %llu blk %d warp %d deferred %d\n", q, (unsigned long long)n_q, blockIdx.x, threadIdx.x >> 5, (int)deferred);
+#endif
           const uint32_t lq = uniform ? q / n_sw : 0u;  // launch within the exec (uniform pass only)
           const uint32_t sw = q - lq * n_sw;
           const uint64_t t0 = p.thread_off[l + lq];
@@ -610,6 +752,7 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
               asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint8_t*>(
                   p.ev_off + t0 + (uint64_t)bl * tpb + (uint64_t)(sw - bl * wpb) * 32 + (uint64_t)kEdgeWarps * 32) + lane * 128));
           }
+          PROF(prof, 1);
           const bool use_tab = multi && !uniform;
           uint32_t prev0 = uniform ? prev_u : ((use_tab && active) ? prev_tab[gtid] : 0);
           const uint32_t amask = __ballot_sync(0xffffffffu, active);
@@ -629,7 +772,9 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
             for (uint32_t i = 0; i < n_lead; ++i) diff |= sl[i] ^ sm[i];
             same_l = diff == 0;
           }
-          if (__all_sync(0xffffffffu, same_l)) {
+          const bool coherent = __all_sync(0xffffffffu, same_l);
+          PROF(prof, 2);
+          if (coherent) {
             // only the lead lane can bump, on every event; event i is independent of the
             // others (prev_i = site_{i-1} >> 1), so the lanes share the bumps
             const uint32_t prev_lead = __shfl_sync(0xffffffffu, prev0, lead);
@@ -640,6 +785,7 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
             }
             if (lane == 0) my_events += n_lead;
             if (use_tab && active && n_ev) prev_tab[gtid] = sm[n_ev - 1] >> 1;
+            PROF(prof, 3);
             continue;
           }
 
@@ -652,10 +798,12 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
                 __nanosleep(100);
               }
             }
+            PROF(prof, 4);
             continue;
           }
           uint8_t* tmem = pool + (size_t)(threadIdx.x >> 5) * kTabBytes;
-          if (!transposed_path(tmem, p.sites, e0, n_ev, prev0, counters, hmask, lane, my_events)) {
+          PROF(prof, 1);
+          if (!transposed_path(tmem, p.sites, e0, n_ev, active, prev0, counters, hmask, lane, my_events, prof)) {
             WarpTable tab;
             tab.keys = reinterpret_cast<unsigned long long*>(tmem);
             tab.m = reinterpret_cast<uint32_t*>(tab.keys + kRows);
@@ -666,10 +814,15 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
           }
           __syncwarp();
           if (use_tab && active && n_ev) prev_tab[gtid] = p.sites[e1 - 1] >> 1;
+#ifdef HFZ_EDGE_PROF
+          _pt = clock64();  // (the table path accounts for itself)
+#endif
         }
         if (!owner && lane == 0) atomicAdd(&s_left, 1u);
       }
+      PROF(prof, 0);
       __syncthreads();  // prev table and counters are launch-ordered
+      PROF(prof, 11);
     }
     // block-reduce the event tally, flush the counters (copy, merge_device_into_map)
     // one 64-bit shared-memory atomic per WARP: 64-bit adds on shared memory are CAS loops, and 768
@@ -706,9 +859,15 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
     }
     if (!redo && threadIdx.x == 0 && p.warp_events) p.warp_events[e] = s_events;
     __syncthreads();
+    PROF(prof, 12);
     if (!redo) break;
    }
   }
+#ifdef HFZ_EDGE_PROF
+  __syncthreads();
+  if (threadIdx.x < 32) atomicAdd(&g_edge_prof[threadIdx.x >> 4][threadIdx.x & 15], s_prof[threadIdx.x >> 4][threadIdx.x & 15]);
+  if (threadIdx.x == 0) atomicAdd(&g_edge_prof[0][15], (unsigned long long)(clock64() - t_kernel));
+#endif
 }
 
 // max simulated threads of any valid launch (sizes the per-CTA prev table)
@@ -761,6 +920,17 @@ __global__ void __launch_bounds__(256, 1) hfz_k_host_edge_record(const uint64_t*
 }
 
 }  // namespace
+
+#ifdef HFZ_EDGE_PROF
+extern "C" __attribute__((visibility("default"))) int hfz_dbg_edge_prof(unsigned long long* out32, int reset) {
+  if (cudaMemcpyFromSymbol(out32, g_edge_prof, sizeof(unsigned long long) * 32) != cudaSuccess) return -1;
+  if (reset) {
+    unsigned long long z[32] = {0};
+    if (cudaMemcpyToSymbol(g_edge_prof, z, sizeof(z)) != cudaSuccess) return -1;
+  }
+  return 0;
+}
+#endif
 
 extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, const uint32_t* dims,
                                      const uint64_t* thread_off, const uint64_t* ev_off,

@@ -49,6 +49,17 @@ if what in ("all", "edge"):
         ev = tr["sites"].size
         threads = int(tr["thread_off"][-1])
         byts = 4 * ev + 8 * threads + 4 * 32768 * n_exec
+        import ctypes
+        from paper_2603_12485_b200 import _lib
+        L = _lib.lib if hasattr(_lib, "lib") else None
+        if L is not None and hasattr(L, "hfz_dbg_edge_prof"):
+            buf = (ctypes.c_ulonglong * 32)()
+            L.hfz_dbg_edge_prof(buf, 1); run(); torch.cuda.synchronize(); L.hfz_dbg_edge_prof(buf, 1)
+            names = ["pop", "setup", "coherent", "fast", "handover", "t.clear", "t.phase1", "t.rows", "t.phase2", "-", "owner idle", "barrier", "zero/flush", "-", "-", "kernel(cta)"]
+            tot = buf[15] / 1.0
+            for role in (0, 1):
+                print(("owners    " if role == 0 else "non-owners") + " (16 warps, % of CTA time each warp): " + ", ".join(
+                    f"{names[c]} {buf[role * 16 + c] / 16 / tot * 100:.1f}" for c in range(13) if names[c] != "-"))
         print(f"K1 edge record: {n_exec} execs, {ms:.3f} ms -> {n_exec/ms*1e3:.0f} execs/s, {ev/ms/1e6:.2f} G events/s, {byts/ms/1e6:.1f} GB/s algorithmic, bumps/exec {res['o'][1].float().mean().item():.0f}")
 if what in ("all", "k2"):
     S = 65536
