@@ -87,6 +87,18 @@ extern "C" int hfz_ctx_destroy(hfz_ctx* c) {
   cudaFree(c->v0);
   cudaFree(c->d_small);
   cudaFree(c->edge_prev);
+  cudaFree(c->fl_nsw);
+  cudaFree(c->fl_sw_off);
+  cudaFree(c->fl_l_exec);
+  cudaFree(c->fl_elig);
+  cudaFree(c->fl_exec_ev0);
+  cudaFree(c->fl_exec_sw0);
+  cudaFree(c->fl_inelig);
+  cudaFree(c->fl_scratch);
+  cudaFree(c->fl_rec_first);
+  cudaFree(c->fl_rec_cnt);
+  cudaFree(c->fl_div);
+  cudaFree(c->fl_lines);
   cudaFree(c->hv_ops);
   for (int i = 0; i < 2; ++i) {
     cudaFree(c->stage_raw[i]);
@@ -170,6 +182,11 @@ extern "C" int hfz_ctx_set_option(hfz_ctx* c, const char* key, int64_t value) {
     c->small_fused = value != 0;
   } else if (!strcmp(key, "step_probe")) {
     c->ss_dbg = value != 0;
+  } else if (!strcmp(key, "edge_flat")) {
+    c->edge_flat = value != 0;
+  } else if (!strcmp(key, "edge_scratch_mb")) {
+    if (value < 1 || value > (1 << 20)) return HFZ_EINVAL;
+    c->edge_scratch_mb = value;
   } else if (!strcmp(key, "time_scan")) {
     c->time_scan = value != 0;
   } else if (!strcmp(key, "sparse_native")) {

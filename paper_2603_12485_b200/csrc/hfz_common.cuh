@@ -39,6 +39,21 @@ struct hfz_ctx {
   uint32_t* edge_prev = nullptr;
   uint64_t edge_prev_words = 0;
   unsigned long long* d_small = nullptr;  // [32] small device scalars
+  // K1 flat path (hfz_edge.cu: decide + count; owned, grow-only)
+  int edge_flat = 1;               // 0 = every exec through the per-exec kernel
+  int64_t edge_scratch_mb = 2048;  // bump-list scratch per chunk of execs (4 bytes per trace event of the chunk)
+  uint32_t* fl_nsw = nullptr;      uint64_t fl_nsw_cap = 0;
+  uint64_t* fl_sw_off = nullptr;   uint64_t fl_sw_off_cap = 0;
+  uint32_t* fl_l_exec = nullptr;   uint64_t fl_l_exec_cap = 0;
+  uint8_t* fl_elig = nullptr;      uint64_t fl_elig_cap = 0;
+  uint64_t* fl_exec_ev0 = nullptr; uint64_t fl_exec_ev0_cap = 0;
+  uint64_t* fl_exec_sw0 = nullptr; uint64_t fl_exec_sw0_cap = 0;
+  uint32_t* fl_inelig = nullptr;   uint64_t fl_inelig_cap = 0;
+  uint32_t* fl_scratch = nullptr;  uint64_t fl_scratch_cap = 0;
+  uint64_t* fl_rec_first = nullptr; uint64_t fl_rec_first_cap = 0;
+  uint32_t* fl_rec_cnt = nullptr;  uint64_t fl_rec_cnt_cap = 0;
+  uint32_t* fl_div = nullptr;      uint64_t fl_div_cap = 0;
+  uint32_t* fl_lines = nullptr;    uint64_t fl_lines_cap = 0;
 
   // K3 scratch (owned, grow-only): edit lists of one chunk of slots, 528 bytes per slot (hfz_mutate.cu)
   uint64_t* hv_ops = nullptr;

@@ -30,6 +30,7 @@
 //                   hash prefix (the rule is separable per site) and the replay repeats per
 //                   partition, splitting on overflow.
 #include <stdio.h>
+#include <string.h>
 
 #include "hfz_common.cuh"
 
@@ -81,6 +82,7 @@ struct EdgeParams {
   uint64_t* warp_events;
   uint32_t* prev_scratch;    // [gridDim.x][prev_stride]
   uint64_t prev_stride;
+  const uint32_t* exec_list; // NULL: execs 0 .. n_exec - 1; else the n_exec execs listed (any order)
 };
 
 // bijective 32-bit mixer: distinct sites have distinct hashes, so a partition of depth 32 holds one site
@@ -159,6 +161,30 @@ struct Counters {
   }
 };
 
+// Where the replay paths put a bump.  emit() is called by all 32 lanes together (f = this lane bumps).
+//   CounterSink  the per-exec kernel: straight into the exec's counters (n = this lane's bumps)
+//   ListSink     the flat kernel: appended to the simulated warp's bump list in global scratch, one
+//                ballot per call instead of an atomic per bump (n = bumps of the warp so far, warp-uniform)
+struct CounterSink {
+  Counters c;
+  uint32_t n;
+  __device__ __forceinline__ void emit(bool f, uint32_t slot, int) {
+    if (f) {
+      c.bump_slot(slot);
+      ++n;
+    }
+  }
+};
+struct ListSink {
+  uint32_t* out;
+  uint32_t n;
+  __device__ __forceinline__ void emit(bool f, uint32_t slot, int lane) {
+    const uint32_t m = __ballot_sync(0xffffffffu, f);
+    if (f) out[n + __popc(m & ((1u << lane) - 1u))] = slot;
+    n += __popc(m);
+  }
+};
+
 struct WarpTable {
   unsigned long long* keys;  // [kRows]  0 = empty, else (1<<32 | site)
   uint32_t* m;               // [kRows]  max visit count of this site among LOWER simulated lanes
@@ -188,11 +214,11 @@ __device__ __forceinline__ uint32_t table_insert(WarpTable& t, uint32_t site, ui
 }
 
 // General path for one simulated warp.  e0/n_ev/prev0 are per real lane = per simulated lane.
-// Returns this real lane's share of the bumps.
-__device__ __forceinline__ uint64_t general_path(WarpTable& tab, const uint32_t* sites, uint64_t e0,
-                                                 uint32_t n_ev, uint32_t prev0, const Counters& counters,
-                                                 uint32_t hmask, int lane) {
-  uint64_t bumps = 0;
+// Bumps go to the sink.
+template <class Sink>
+__device__ __forceinline__ void general_path(WarpTable& tab, const uint32_t* sites, uint64_t e0,
+                                             uint32_t n_ev, uint32_t prev0, Sink& sink,
+                                             uint32_t hmask, int lane) {
   const uint32_t lane_le = 0xffffffffu >> (31 - lane);
   const uint32_t ev_total = __reduce_add_sync(0xffffffffu, n_ev);
   // initial depth: the expected events per partition fit the table even if all were distinct
@@ -258,6 +284,7 @@ __device__ __forceinline__ uint64_t general_path(WarpTable& tab, const uint32_t*
           const unsigned long long key = mine ? ((1ull << 32) | s) : (unsigned long long)lane;
           const uint32_t grp = __match_any_sync(0xffffffffu, key);
           uint32_t row = 0, mm = 0, cc = 0;
+          bool bf = false;
           if (mine) {
             row = table_insert(tab, s, h);  // cannot fail: checked by the dry run / event bound
             const uint32_t owner = tab.stamp[row];
@@ -267,12 +294,9 @@ __device__ __forceinline__ uint64_t general_path(WarpTable& tab, const uint32_t*
             } else if (owner != 0xffffffffu) {  // counts of an earlier lane: fold into the max
               mm = max(tab.m[row], tab.c[row]);
             }
-            const uint32_t k = cc + __popc(grp & lane_le);
-            if (k > mm) {
-              counters.bump_slot((pv ^ s) & hmask);
-              ++bumps;
-            }
+            bf = cc + __popc(grp & lane_le) > mm;
           }
+          sink.emit(bf, (pv ^ s) & hmask, lane);
           __syncwarp();
           if (mine && (grp & (0u - grp)) == (1u << lane)) {  // one writer per site
             tab.m[row] = mm;
@@ -284,7 +308,6 @@ __device__ __forceinline__ uint64_t general_path(WarpTable& tab, const uint32_t*
       }
     }
   }
-  return bumps;
 }
 
 // Transposed general path for one simulated warp.
@@ -314,9 +337,10 @@ constexpr uint32_t kTBuckets = kTRows / 4;
 constexpr uint32_t kTEmpty = 0xffffffffu;  // key of a free row; the site 0xffffffff gets row kTRows
 static_assert((kTRows + 1) * (4 + 16) <= kTabBytes, "transposed table must fit a pool table");
 
+template <class Sink>
 __device__ __forceinline__ bool transposed_path(uint8_t* tab, const uint32_t* sites, uint64_t e0, uint32_t n_ev,
-                                                bool active, uint32_t prev0, const Counters& counters, uint32_t hmask,
-                                                int lane, uint64_t& bumps_out, unsigned long long* prof = nullptr) {
+                                                bool active, uint32_t prev0, Sink& sink, uint32_t hmask,
+                                                int lane, unsigned long long* prof = nullptr) {
   PROF_DECL;
   uint32_t* keys = reinterpret_cast<uint32_t*>(tab);                    // [kTRows + 1], buckets of 4
   uint32_t* cnt = reinterpret_cast<uint32_t*>(tab + (kTRows + 4) * 4);  // [kTRows + 1][4], 16-byte aligned
@@ -485,7 +509,6 @@ __device__ __forceinline__ bool transposed_path(uint8_t* tab, const uint32_t* si
   }
   __syncwarp();
   PROF(prof, 7);
-  uint32_t bumps = 0;
   const uint32_t lanes_above = lane == 31 ? 0u : (0xffffffffu << (lane + 1));
   for (uint32_t hi = N; hi > 0; hi = hi > 32 ? hi - 32 : 0) {
     const int32_t g = (int32_t)hi - 32 + lane;  // higher lane = later event
@@ -505,22 +528,100 @@ __device__ __forceinline__ bool transposed_path(uint8_t* tab, const uint32_t* si
     const uint32_t sh = cell_shift(L);
     const uint32_t d = on ? ((*reinterpret_cast<volatile uint32_t*>(c) >> sh) & 15u) : 0u;
     __syncwarp();  // every nibble of this round is read before any is lowered
+    bool bf = false;
+    uint32_t bslot = 0;
     if (on && d) {
       if ((uint32_t)__popc(grp & lanes_above) < d) {  // one of the last d visits of s by L still open
         const uint32_t pv = (uint32_t)g > lane_start ? (ev[g - 1] >> 1) : lane_prev0;
-        counters.bump_slot((pv ^ s) & hmask);
-        ++bumps;
+        bslot = (pv ^ s) & hmask;
+        bf = true;
       }
       if ((grp & (0u - grp)) == (1u << lane)) {  // the group's first lane lowers the nibble for the earlier rounds
         const uint32_t m = (uint32_t)__popc(grp);
         atomicSub(c, (m < d ? m : d) << sh);
       }
     }
+    sink.emit(bf, bslot, lane);
     __syncwarp();
   }
-  bumps_out += bumps;
   __syncwarp();
   PROF(prof, 8);
+  return true;
+}
+
+
+// Divergent warps with SHORT paths (every lane at most kShortPath events -- the usual basic-block
+// trace of one kernel launch): real lane L keeps simulated lane L's events in registers.
+// Visit (L, s, k) bumps iff no lower lane reaches a k-th visit of s, i.e. iff L is the LOWEST lane
+// holding the pair (s, k) -- a first-occurrence test:
+//   pass 1  step i of every lane at once: k = 1 + earlier events of the lane at the same site
+//           (register compares), then find-or-insert (s, k) in an open-addressing table of 1,024
+//           64-bit entries {site, k << 8 | lowest lane} (claimed by one 64-bit CAS, lane by atomicMin);
+//   pass 2  the visit bumps iff the entry's lane is its own; slot from its own prev (the event before).
+// One table operation per event, no per-site count matrix, no row pass, no second lookup (the row
+// found in pass 1 is kept, 10 bits per event).  Returns false without bumping when a lane has more
+// than kShortPath events: the caller then takes the transposed replay, which has no such limit.
+constexpr int kShortPath = 24;
+constexpr uint32_t kShortRows = 1024;  // >= 32 x kShortPath distinct (s, k) pairs at 75 % load
+static_assert(kShortRows * 8 <= kTabBytes, "short-path table must fit a site table");
+
+template <class Sink>
+__device__ __forceinline__ bool short_divergent_path(uint8_t* tab, const uint32_t* sites, uint64_t e0, uint32_t n_ev,
+                                                     uint32_t prev0, Sink& sink, uint32_t hmask, int lane) {
+  const uint32_t n_max = __reduce_max_sync(0xffffffffu, n_ev);
+  if (n_max > (uint32_t)kShortPath) return false;
+  unsigned long long* ent = reinterpret_cast<unsigned long long*>(tab);
+  constexpr unsigned long long kFree = ~0ull;
+  {
+    uint4* clr = reinterpret_cast<uint4*>(tab);
+#pragma unroll
+    for (uint32_t i = 0; i < kShortRows * 8 / 16 / 32; ++i) clr[i * 32 + lane] = make_uint4(~0u, ~0u, ~0u, ~0u);
+  }
+  uint32_t ev[kShortPath];
+  const uint32_t* mine = sites + e0;
+#pragma unroll
+  for (int i = 0; i < kShortPath; ++i) ev[i] = (uint32_t)i < n_ev ? mine[i] : 0u;
+  uint32_t rows[kShortPath / 3];  // three 10-bit rows per word
+#pragma unroll
+  for (int i = 0; i < kShortPath / 3; ++i) rows[i] = 0;
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < kShortPath; ++i) {
+    if ((uint32_t)i < n_max) {  // warp-uniform
+      const bool on = (uint32_t)i < n_ev;
+      const uint32_t s = ev[i];
+      uint32_t k = 1;
+#pragma unroll
+      for (int j = 0; j < i; ++j) k += ev[j] == s ? 1u : 0u;
+      uint32_t r = (s * 0x9e3779b1u + k * 0x85ebca6bu) >> 22;
+      static_assert(kShortRows == 1024, "hash shift assumes 1,024 rows");
+      const unsigned long long want = ((unsigned long long)((k << 8) | 0xffu) << 32) | s;  // a claim: lane field open
+      bool pending = on;
+      while (__any_sync(0xffffffffu, pending)) {  // warp-synchronous probes: the lanes leave together
+        if (pending) {
+          unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(ent + r);
+          if (cur == kFree) cur = atomicCAS(ent + r, kFree, want);
+          // ours if the row was free (now claimed) or holds (s, k) already; the lane byte is ignored
+          if (cur == kFree || ((cur ^ want) & 0xffffff00ffffffffull) == 0ull) pending = false;
+          else r = (r + 1) & (kShortRows - 1);
+        }
+      }
+      if (on) atomicMin(reinterpret_cast<uint32_t*>(ent + r) + 1, (k << 8) | (uint32_t)lane);
+      rows[i / 3] |= r << (10 * (i % 3));
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < kShortPath; ++i) {
+    if ((uint32_t)i < n_max) {
+      const bool on = (uint32_t)i < n_ev;
+      const uint32_t r = (rows[i / 3] >> (10 * (i % 3))) & 1023u;
+      const uint32_t y = reinterpret_cast<const uint32_t*>(ent + r)[1];
+      const uint32_t pv = i ? ev[i > 0 ? i - 1 : 0] >> 1 : prev0;
+      sink.emit(on && (y & 0xffu) == (uint32_t)lane, (pv ^ ev[i]) & hmask, lane);
+    }
+  }
+  __syncwarp();
   return true;
 }
 
@@ -568,7 +669,8 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
   uint32_t* prev_tab = p.prev_scratch + (size_t)blockIdx.x * p.prev_stride;
   const uint32_t hmask = p.H - 1;
 
-  for (uint64_t e = blockIdx.x; e < p.n_exec; e += gridDim.x) {
+  for (uint64_t ei = blockIdx.x; ei < p.n_exec; ei += gridDim.x) {
+   const uint64_t e = p.exec_list ? p.exec_list[ei] : ei;
    uint32_t* ghist = reinterpret_cast<uint32_t*>(p.raw + e * p.rec_bytes + p.H);
    for (int attempt = 0; attempt < 2; ++attempt) {
     const bool packed = attempt == 0;  // first attempt: counters in shared memory (mode MODE)
@@ -803,15 +905,17 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
           }
           uint8_t* tmem = pool + (size_t)(threadIdx.x >> 5) * kTabBytes;
           PROF(prof, 1);
-          if (!transposed_path(tmem, p.sites, e0, n_ev, active, prev0, counters, hmask, lane, my_events, prof)) {
+          CounterSink sink{counters, 0u};
+          if (!transposed_path(tmem, p.sites, e0, n_ev, active, prev0, sink, hmask, lane, prof)) {
             WarpTable tab;
             tab.keys = reinterpret_cast<unsigned long long*>(tmem);
             tab.m = reinterpret_cast<uint32_t*>(tab.keys + kRows);
             tab.c = tab.m + kRows;
             tab.stamp = tab.c + kRows;
             tab.used = tab.stamp + kRows;
-            my_events += general_path(tab, p.sites, e0, n_ev, prev0, counters, hmask, lane);
+            general_path(tab, p.sites, e0, n_ev, prev0, sink, hmask, lane);
           }
+          my_events += sink.n;
           __syncwarp();
           if (use_tab && active && n_ev) prev_tab[gtid] = p.sites[e1 - 1] >> 1;
 #ifdef HFZ_EDGE_PROF
@@ -868,6 +972,499 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
   if (threadIdx.x < 32) atomicAdd(&g_edge_prof[threadIdx.x >> 4][threadIdx.x & 15], s_prof[threadIdx.x >> 4][threadIdx.x & 15]);
   if (threadIdx.x == 0) atomicAdd(&g_edge_prof[0][15], (unsigned long long)(clock64() - t_kernel));
 #endif
+}
+
+
+// ---------------------------------------------------------------------------
+// Flat path (the default): decide, then count.
+//
+// Which events bump is a question about ONE simulated warp (its site table, the lanes' carried prev);
+// only the counting is per exec.  The per-exec kernel above does both under one CTA: the counters
+// take 64 KB of the CTA's shared memory, so only half of its warps can own a site table, and every
+// exec ends at a CTA-wide barrier behind its slowest divergent warp (a quarter of the warp-time).
+// Here the two halves are separate launches:
+//   hfz_k_edge_classify   ALL simulated warps of a chunk of execs are one flat queue (a global counter,
+//                      kPop warps per pop); no shared memory, no barrier.  A coherent warp (every lane
+//                      walked the lead lane's sequence -- the SIMT common case) is recognised straight
+//                      from the trace: its events are contiguous, so they are dealt out 32 per coalesced
+//                      load and event g is compared with event g - n (the same position one lane down).
+//                      Only its lead lane bumps, on every event.  The slots to bump go to the simulated
+//                      warp's own region of a scratch list (indexed like the trace: a warp never bumps
+//                      more often than it has events) -- one ballot per round, no atomics.  The other
+//                      (divergent) warps are appended to a list;
+//   hfz_k_edge_divergent  the listed warps, a flat queue again; shared memory holds nothing but one site
+//                      table per real warp (22 per SM), so every warp can take one and none waits;
+//   hfz_k_edge_count      one CTA per exec streams the exec's bump lists into u32 counters in SHARED
+//                      memory (shared-memory atomics; 16,384 slots = 64 KB per pass over the lists, so
+//                      three execs are in flight per SM and one's zero / flush phases hide behind the
+//                      others' list reads) and flushes them to the record: still no global atomic per
+//                      hit, and the counters are full-width, so there is no overflow replay.
+// Launches of an exec that differ in geometry carry prev per flattened gtid IN LAUNCH ORDER
+// (hdvm.cpp:376,426-430), which a flat queue cannot honour: those execs (and execs whose thread
+// offsets are not a CSR of their launch sizes) are left to the per-exec kernel.
+constexpr int kFlatWarps = 22;       // divergent kernel: 22 site tables = 226,688 bytes of shared memory
+constexpr int kClassifyWarps = 16;   // classify kernel: no shared memory, two CTAs per SM
+constexpr uint32_t kPop = 16;        // simulated warps per pop
+constexpr uint32_t kCountSlots = 16384;  // u32 counters per pass of the count kernel: 64 KB, three CTAs (execs) in flight per SM
+constexpr int kCountWarps = 16;
+
+struct FlatParams {
+  const uint64_t* launch_off;
+  const uint32_t* dims;
+  const uint64_t* thread_off;
+  const uint64_t* ev_off;
+  const uint32_t* sites;
+  uint64_t n_exec, n_launch;
+  uint32_t H;
+  uint64_t rec_bytes;
+  uint8_t* raw;
+  uint64_t* warp_events;
+  // written by hfz_k_edge_prep / hfz_k_edge_scan
+  uint32_t* nsw;        // [n_launch] simulated warps of a launch; 0 = invalid launch or exec left to the per-exec kernel
+  uint64_t* sw_off;     // [n_launch + 1] exclusive prefix of nsw: the flat queue
+  uint32_t* l_exec;     // [n_launch] exec of a launch
+  uint8_t* elig;        // [n_exec] 1 = flat path
+  uint64_t* exec_ev0;   // [n_exec + 1] first event of an exec (index into sites)
+  uint64_t* exec_sw0;   // [n_exec + 1] first flat simulated warp of an exec
+  uint32_t* inelig;     // [n_exec] execs left to the per-exec kernel
+  unsigned long long* small;  // [0] their number, [1] max threads of their launches, [2] pop counter, [3]/[4] min/max nsw
+  // one chunk of execs
+  uint64_t e_lo, e_hi;  // execs
+  uint64_t q_lo, q_hi;  // flat simulated warps
+  uint64_t l_lo, l_hi;  // launches
+  uint64_t ev_lo;       // first event
+  uint32_t uni_nsw;     // every launch of the batch has this many simulated warps (0 = they differ)
+  uint32_t* scratch;    // bump slots; a simulated warp's list starts at (its first event - ev_lo)
+  uint64_t* rec_first;  // [q_hi - q_lo] first event of the simulated warp (list items only)
+  uint32_t* rec_cnt;    // [q_hi - q_lo] its bumps; | kSegFlag: listed in scratch, else in its line
+  uint32_t* div_list;   // [q_hi - q_lo] simulated warps (chunk-relative) that need a site table; small[5] of them
+  uint32_t* lines;      // [q_hi - q_lo][32] a coherent warp's bump slots: one 128-byte line per simulated warp
+};
+constexpr uint32_t kSegFlag = 0x80000000u;  // rec_cnt: the bumps are a list in scratch (rec_first), not a line
+
+// one thread per exec: eligibility, simulated warps per launch, the exec's first event
+__global__ void __launch_bounds__(256) hfz_k_edge_prep(const FlatParams p) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= p.n_exec; e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t l0 = p.launch_off[e];
+    p.exec_ev0[e] = p.n_launch ? p.ev_off[p.thread_off[l0]] : 0;
+    if (e == p.n_exec) break;
+    const uint64_t l1 = p.launch_off[e + 1];
+    bool ok = true;
+    unsigned long long mx = 0;
+    for (uint64_t l = l0; l < l1; ++l) {
+      const uint32_t* d = p.dims + l * 6;
+      if (l > l0) {
+        const uint32_t* d0 = p.dims + l0 * 6;
+        ok = ok && d[0] == d0[0] && d[1] == d0[1] && d[2] == d0[2] && d[3] == d0[3] && d[4] == d0[4] && d[5] == d0[5];
+      }
+      const uint64_t ta = p.thread_off[l], tb = p.thread_off[l + 1];
+      if (launch_valid(d)) {
+        const unsigned long long tt = (unsigned long long)d[0] * d[1] * d[2] * d[3] * d[4] * d[5];
+        mx = tt > mx ? tt : mx;
+        ok = ok && tb >= ta && tb - ta >= tt;
+      } else {
+        ok = ok && tb >= ta;
+      }
+    }
+    for (uint64_t l = l0; l < l1; ++l) {
+      const uint32_t* d = p.dims + l * 6;
+      uint32_t n = 0;
+      if (ok && launch_valid(d)) n = d[0] * d[1] * d[2] * ((d[3] * d[4] * d[5] + 31) / 32);  // <= 2^22
+      p.nsw[l] = n;
+      p.l_exec[l] = (uint32_t)e;
+      if (ok) {
+        atomicMax(p.small + 3, ~(unsigned long long)n);  // (zero-initialised: the complement's max is the min)
+        atomicMax(p.small + 4, (unsigned long long)n);
+      }
+    }
+    p.elig[e] = ok ? 1 : 0;
+    if (!ok) {
+      p.inelig[atomicAdd(p.small + 0, 1ull)] = (uint32_t)e;
+      atomicMax(p.small + 1, mx);
+    }
+  }
+}
+
+// one CTA: sw_off = exclusive prefix sum of nsw; then the flat start of every exec
+__global__ void __launch_bounds__(1024, 1) hfz_k_edge_scan(const FlatParams p) {
+  __shared__ unsigned long long wsum[32];
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long carry = 0;
+  if (threadIdx.x == 0) p.sw_off[0] = 0;
+  for (uint64_t base = 0; base < p.n_launch; base += 1024) {
+    const uint64_t i = base + threadIdx.x;
+    unsigned long long x = i < p.n_launch ? p.nsw[i] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long o = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= (uint32_t)d) x += o;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      unsigned long long y = wsum[lane];
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long o = __shfl_up_sync(0xffffffffu, y, d);
+        if (lane >= (uint32_t)d) y += o;
+      }
+      wsum[lane] = y;
+    }
+    __syncthreads();
+    const unsigned long long incl = x + (w ? wsum[w - 1] : 0) + carry;
+    if (i < p.n_launch) p.sw_off[i + 1] = incl;
+    carry += wsum[31];
+    __syncthreads();
+  }
+  __syncthreads();  // (the CTA's own global writes are visible to it after the barrier)
+  for (uint64_t e = threadIdx.x; e <= p.n_exec; e += 1024) p.exec_sw0[e] = p.sw_off[p.launch_off[e]];
+}
+
+// The launch a flat simulated-warp index belongs to, cached between consecutive items.
+struct LaunchCtx {
+  uint64_t sw0 = 1, sw1 = 0;  // flat range of the launch (empty: forces a lookup)
+  uint64_t t0 = 0, tprev = 0; // first thread of the launch / of the launch before it in the same exec
+  uint64_t l = 0, l0 = 0;     // the launch, the first launch of its exec
+  uint32_t tpb = 1, wpb = 1;
+};
+__device__ __forceinline__ void flat_locate(const FlatParams& p, uint64_t q, LaunchCtx& c) {
+  uint64_t l;
+  if (p.uni_nsw) {
+    l = q < (1ull << 32) ? (uint64_t)((uint32_t)q / p.uni_nsw) : q / p.uni_nsw;
+    c.sw0 = l * p.uni_nsw;
+    c.sw1 = c.sw0 + p.uni_nsw;
+  } else {  // last launch with sw_off[l] <= q
+    uint64_t lo = p.l_lo, hi = p.l_hi;
+    while (hi - lo > 1) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (p.sw_off[mid] <= q) lo = mid; else hi = mid;
+    }
+    l = lo;
+    c.sw0 = p.sw_off[l];
+    c.sw1 = p.sw_off[l + 1];
+  }
+  const uint32_t* d = p.dims + l * 6;
+  c.tpb = d[3] * d[4] * d[5];
+  c.wpb = (c.tpb + 31) / 32;
+  c.l = l;
+  c.l0 = p.launch_off[p.l_exec[l]];
+  c.t0 = p.thread_off[l];
+  c.tprev = l > c.l0 ? p.thread_off[l - 1] : 0;
+}
+// nearest launch below lb_from (within the exec) where thread j ran events: prev is carried per gtid
+// (hdvm.cpp:376,426-430), and with one geometry per exec thread j has the same gtid in every launch
+__device__ __forceinline__ uint32_t flat_prev_walk(const FlatParams& p, const LaunchCtx& c, uint64_t j, uint32_t lb_from) {
+  for (uint32_t lb = lb_from; lb > 0;) {
+    --lb;
+    const uint64_t tb = p.thread_off[c.l0 + lb] + j;
+    const uint64_t b1 = p.ev_off[tb + 1];
+    if (b1 > p.ev_off[tb]) return p.sites[b1 - 1] >> 1;
+  }
+  return 0u;
+}
+
+__global__ void __launch_bounds__(kClassifyWarps * 32, 2) hfz_k_edge_classify(const FlatParams p) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t hmask = p.H - 1;
+  const uint64_t n_items = p.q_hi - p.q_lo;
+  // the launch the last simulated warp belonged to (a pop is kPop consecutive warps: usually one launch)
+  LaunchCtx c;
+  for (;;) {
+    unsigned long long qb = 0;
+    if (lane == 0) qb = atomicAdd(p.small + 2, (unsigned long long)kPop);
+    qb = __shfl_sync(0xffffffffu, qb, 0);
+    if (qb >= n_items) break;
+    const uint64_t qe = qb + kPop < n_items ? qb + kPop : n_items;
+    // software pipeline over the pop's items: while item i is worked on, the event offsets of item
+    // i + 1 are in flight, and once they have landed its events are pulled into L2
+    bool have_next = false;
+    uint64_t nx_e0 = 0, nx_e1 = 0, nx_pa = 0, nx_pb = 0;  // (nx_pa / nx_pb / nx_ps: lane 0 only)
+    uint32_t nx_ps = 0;
+    for (uint64_t qi = qb; qi < qe; ++qi) {
+      const uint64_t q = p.q_lo + qi;
+      if (q < c.sw0 || q >= c.sw1) {
+        have_next = false;
+        flat_locate(p, q, c);
+      }
+      const uint32_t tpb = c.tpb, wpb = c.wpb;
+      const uint32_t sw = (uint32_t)(q - c.sw0);
+      const uint32_t lq = (uint32_t)(c.l - c.l0);  // launch within its exec: every earlier one has this geometry
+      const uint32_t bl = sw / wpb, tl = (sw - bl * wpb) * 32 + lane;
+      const bool active = tl < tpb;
+      const uint64_t j = (uint64_t)bl * tpb + tl;  // thread within its launch
+      uint64_t e0 = 0, e1 = 0, pa = 0, pb = 0;
+      uint32_t ps = 0;  // the site that ends the lead lane's events one launch back
+      const bool piped = have_next;
+      if (piped) {
+        e0 = nx_e0;
+        e1 = nx_e1;
+        pa = nx_pa;
+        pb = nx_pb;
+        ps = nx_ps;
+      } else if (active) {
+        e0 = p.ev_off[c.t0 + j];
+        e1 = p.ev_off[c.t0 + j + 1];
+      }
+      have_next = qi + 1 < qe && q + 1 < c.sw1;
+      bool nx_active = false;
+      if (have_next) {
+        const uint32_t wi2 = sw + 1 - bl * wpb;  // warp within its block: the next warp, or the first one of the next block
+        const uint32_t bl2 = wi2 == wpb ? bl + 1 : bl, tl2 = (wi2 == wpb ? 0u : wi2) * 32 + lane;
+        nx_active = tl2 < tpb;
+        nx_e0 = nx_e1 = 0;
+        const uint64_t j2 = (uint64_t)bl2 * tpb + tl2;
+        if (nx_active) {
+          nx_e0 = p.ev_off[c.t0 + j2];
+          nx_e1 = p.ev_off[c.t0 + j2 + 1];
+        }
+        if (lq && lane == 0) {
+          nx_pa = p.ev_off[c.tprev + j2];
+          nx_pb = p.ev_off[c.tprev + j2 + 1];
+        }
+      }
+      if (lq && lane == 0 && !piped) {  // the lead lane's carried prev: usually the end of its events one launch back
+        pa = p.ev_off[c.tprev + j];
+        pb = p.ev_off[c.tprev + j + 1];
+      }
+      const uint32_t n_ev = (uint32_t)(e1 - e0);
+      const uint64_t first = __shfl_sync(0xffffffffu, e0, 0);
+      const uint32_t n_lead = __shfl_sync(0xffffffffu, n_ev, 0);
+      const uint32_t n_act = (uint32_t)__popc(__ballot_sync(0xffffffffu, active));
+      const bool same_n = __all_sync(0xffffffffu, !active || n_ev == n_lead);
+      const uint32_t* ev = p.sites + first;
+      uint32_t prev_lead = 0;
+      if (lq && lane == 0) {
+        if (pb > pa) prev_lead = (piped ? ps : p.sites[pb - 1]) >> 1;
+        else prev_lead = flat_prev_walk(p, c, j, lq - 1);
+      }
+      // ---- coherent?  every active lane walked the lead lane's sequence
+      bool coherent = false;
+      uint32_t r0 = 0;
+      if (same_n && n_lead <= 32u) {
+        // the warp's events are contiguous: dealt 32 per load; the lead's events are lanes 0 .. n_lead - 1
+        // of the first round
+        const uint32_t N = n_act * n_lead;  // <= 1,024
+        uint32_t diff = 0;
+        if (n_lead) {
+          // lane t's i-th event equals lane t - 1's: event g against event g - n_lead, both streams coalesced
+          // (blocks of 8 rounds = 16 loads in flight, all predicated: a remainder loop would take its
+          // rounds one memory latency at a time)
+          const uint32_t* evb = ev - n_lead;
+          r0 = (uint32_t)lane < N ? ev[lane] : 0u;
+          {
+            uint32_t a[7], b[8];
+            b[0] = ((uint32_t)lane >= n_lead && (uint32_t)lane < N) ? evb[lane] : r0;
+#pragma unroll
+            for (int u = 1; u < 8; ++u) {
+              const uint32_t g = 32u * u + lane;
+              a[u - 1] = g < N ? ev[g] : 0u;
+              b[u] = g < N ? evb[g] : 0u;
+            }
+            diff = r0 ^ b[0];
+#pragma unroll
+            for (int u = 1; u < 8; ++u) diff |= a[u - 1] ^ b[u];
+          }
+          for (uint32_t g0 = 256; g0 < N; g0 += 256) {  // warp-uniform
+            uint32_t a[8], b[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const uint32_t g = g0 + 32u * u + lane;
+              a[u] = g < N ? ev[g] : 0u;
+              b[u] = g < N ? evb[g] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) diff |= a[u] ^ b[u];
+          }
+        }
+        coherent = __all_sync(0xffffffffu, diff == 0u);
+      } else if (same_n) {  // long paths: each lane against the lead's, read as a broadcast load
+        uint32_t diff = 0;
+        if (active) {
+          const uint32_t* mine = p.sites + e0;
+#pragma unroll 8
+          for (uint32_t i = 0; i < n_lead; ++i) diff |= ev[i] ^ mine[i];
+        }
+        coherent = __all_sync(0xffffffffu, diff == 0u);
+      }
+      if (have_next) {  // the next item's events into L2, one 128-byte line per lane (4 KB covers the usual warp)
+        const uint32_t am2 = __ballot_sync(0xffffffffu, nx_active);
+        const uint64_t f2 = __shfl_sync(0xffffffffu, nx_e0, 0);
+        const uint64_t l2 = __shfl_sync(0xffffffffu, nx_e1, 31 - __clz((int)am2));
+        const uint8_t* a2 = reinterpret_cast<const uint8_t*>(p.sites + f2) + (uint64_t)lane * 128;
+        if (a2 < reinterpret_cast<const uint8_t*>(p.sites + l2)) asm volatile("prefetch.global.L2 [%0];" ::"l"(a2));
+        if (lq && lane == 0 && nx_pb > nx_pa) nx_ps = p.sites[nx_pb - 1];
+      }
+      if (coherent) {
+        // only the lead lane can bump, on every event; event i needs site i - 1 only
+        if (n_lead <= 32u) {  // the usual case: the bumps fill (part of) the warp's own 128-byte line
+          const uint32_t up = __shfl_up_sync(0xffffffffu, r0, 1);
+          if ((uint32_t)lane < n_lead) p.lines[qi * 32 + lane] = ((lane ? up >> 1 : prev_lead) ^ r0) & hmask;
+          if (lane == 0) p.rec_cnt[qi] = n_lead;
+        } else {
+          ListSink sink{p.scratch + (first - p.ev_lo), 0u};
+          for (uint32_t i0 = 0; i0 < n_lead; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const bool f = i < n_lead;
+            const uint32_t s = f ? ev[i] : 0u;
+            const uint32_t pv = (f && i) ? ev[i - 1] >> 1 : prev_lead;
+            sink.emit(f, (pv ^ s) & hmask, lane);
+          }
+          if (lane == 0) {
+            p.rec_first[qi] = first;
+            p.rec_cnt[qi] = sink.n | kSegFlag;
+          }
+        }
+      } else if (lane == 0) {  // needs a site table: left to hfz_k_edge_divergent
+        p.div_list[atomicAdd(p.small + 5, 1ull)] = (uint32_t)qi;
+      }
+    }
+  }
+}
+
+
+// The simulated warps hfz_k_edge_classify set aside: replayed lane by lane with a site table per real warp.
+__global__ void __launch_bounds__(kFlatWarps * 32, 1) hfz_k_edge_divergent(const FlatParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  uint8_t* tmem = smem + (size_t)(threadIdx.x >> 5) * kTabBytes;
+  const uint32_t hmask = p.H - 1;
+  const unsigned long long n_div = p.small[5];
+  LaunchCtx c;
+  for (;;) {
+    unsigned long long di = 0;
+    if (lane == 0) di = atomicAdd(p.small + 6, 1ull);
+    di = __shfl_sync(0xffffffffu, di, 0);
+    if (di >= n_div) break;
+    const uint64_t qi = p.div_list[di];
+    const uint64_t q = p.q_lo + qi;
+    if (q < c.sw0 || q >= c.sw1) flat_locate(p, q, c);
+    const uint32_t sw = (uint32_t)(q - c.sw0), lq = (uint32_t)(c.l - c.l0);
+    const uint32_t bl = sw / c.wpb, tl = (sw - bl * c.wpb) * 32 + lane;
+    const bool active = tl < c.tpb;
+    const uint64_t j = (uint64_t)bl * c.tpb + tl;
+    uint64_t e0 = 0, e1 = 0;
+    uint32_t prev0 = 0;
+    if (active) {
+      e0 = p.ev_off[c.t0 + j];
+      e1 = p.ev_off[c.t0 + j + 1];
+      if (lq) prev0 = flat_prev_walk(p, c, j, lq);
+    }
+    const uint32_t n_ev = (uint32_t)(e1 - e0);
+    const uint64_t first = __shfl_sync(0xffffffffu, e0, 0);
+    ListSink sink{p.scratch + (first - p.ev_lo), 0u};
+    __syncwarp();
+    if (!short_divergent_path(tmem, p.sites, e0, n_ev, prev0, sink, hmask, lane) &&
+        !transposed_path(tmem, p.sites, e0, n_ev, active, prev0, sink, hmask, lane)) {
+      WarpTable tab;
+      tab.keys = reinterpret_cast<unsigned long long*>(tmem);
+      tab.m = reinterpret_cast<uint32_t*>(tab.keys + kRows);
+      tab.c = tab.m + kRows;
+      tab.stamp = tab.c + kRows;
+      tab.used = tab.stamp + kRows;
+      general_path(tab, p.sites, e0, n_ev, prev0, sink, hmask, lane);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      p.rec_first[qi] = first;
+      p.rec_cnt[qi] = sink.n | kSegFlag;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kCountWarps * 32, 3) hfz_k_edge_count(const FlatParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
+  constexpr uint32_t kBigCap = 512;
+  __shared__ unsigned long long s_total;
+  __shared__ unsigned long long s_big_f[kBigCap];
+  __shared__ uint32_t s_big_c[kBigCap];
+  __shared__ uint32_t s_nbig;
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t R = p.H < kCountSlots ? p.H : kCountSlots;  // (both multiples of 4)
+  for (uint64_t e = p.e_lo + blockIdx.x; e < p.e_hi; e += gridDim.x) {
+    if (!p.elig[e]) continue;  // the per-exec kernel writes this record
+    const uint64_t q0 = p.exec_sw0[e] - p.q_lo, q1 = p.exec_sw0[e + 1] - p.q_lo;
+    uint32_t* ghist = reinterpret_cast<uint32_t*>(p.raw + e * p.rec_bytes + p.H);
+    if (threadIdx.x == 0) s_total = 0;
+    unsigned long long total = 0;
+    for (uint32_t r0 = 0; r0 < p.H; r0 += R) {
+      const uint32_t n = p.H - r0 < R ? p.H - r0 : R;
+      uint4* z = reinterpret_cast<uint4*>(hist);
+      for (uint32_t i = threadIdx.x; i < n / 4; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+      if (threadIdx.x == 0) s_nbig = 0;
+      __syncthreads();
+      // a warp takes 32 consecutive simulated warps: the coherent ones' lines are 32 independent coalesced
+      // loads (no load depends on another); the listed ones (divergent warps) are set aside and then dealt
+      // out over ALL warps of the CTA (they sit unevenly in the queue, and the CTA waits for its slowest warp)
+      for (uint64_t qb = q0 + (uint64_t)w * 32; qb < q1; qb += kCountWarps * 32) {
+        const uint64_t q = qb + lane;
+        const uint32_t cnt = q < q1 ? p.rec_cnt[q] : 0u;
+        const uint4* lines4 = reinterpret_cast<const uint4*>(p.lines + qb * 32) + lane;
+        bool seg = (cnt & kSegFlag) != 0u;
+        uint64_t f = 0;
+        if (seg) {
+          f = p.rec_first[q] - p.ev_lo;
+          const uint32_t at = atomicAdd(&s_nbig, 1u);
+          if (at < kBigCap) {
+            s_big_f[at] = f;
+            s_big_c[at] = cnt & ~kSegFlag;
+            seg = false;
+          }
+        }
+        // the group's 32 lines = 4 KB contiguous: eight 128-bit loads per lane, all in flight at once
+        // (lane L, load k: line 4k + L / 8, elements 4 (L % 8) .. + 3)
+        uint4 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = lines4[k * 32];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          uint32_t ck = __shfl_sync(0xffffffffu, cnt, 4 * k + (lane >> 3));
+          ck = (ck & kSegFlag) ? 0u : ck;  // a listed or absent warp: nothing of its line counts
+          const uint32_t i0 = (lane & 7u) * 4u;
+          const uint32_t x[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint32_t rel = x[c] - r0;
+            if (i0 + c < ck && rel < n) bump(hist + rel);
+          }
+        }
+        uint32_t left = __ballot_sync(0xffffffffu, seg);  // more lists than the side list holds: here and now
+        while (left) {
+          const int k = __ffs(left) - 1;
+          left &= left - 1;
+          const uint32_t cc = __shfl_sync(0xffffffffu, cnt, k) & ~kSegFlag;
+          const uint32_t* list = p.scratch + __shfl_sync(0xffffffffu, f, k);
+          for (uint32_t i = lane; i < cc; i += 32) {
+            const uint32_t rel = list[i] - r0;
+            if (rel < n) bump(hist + rel);
+          }
+        }
+        if (r0 == 0) total += cnt & ~kSegFlag;
+      }
+      __syncthreads();
+      {
+        const uint32_t nb = s_nbig < kBigCap ? s_nbig : kBigCap;
+        for (uint32_t b = w; b < nb; b += kCountWarps) {
+          const uint32_t cc = s_big_c[b];
+          const uint32_t* list = p.scratch + s_big_f[b];
+#pragma unroll 12
+          for (uint32_t i = lane; i < cc; i += 32) {
+            const uint32_t rel = list[i] - r0;
+            if (rel < n) bump(hist + rel);
+          }
+        }
+      }
+      __syncthreads();
+      uint4* dst = reinterpret_cast<uint4*>(ghist + r0);
+      for (uint32_t i = threadIdx.x; i < n / 4; i += blockDim.x) dst[i] = z[i];
+      __syncthreads();
+    }
+    for (int d = 16; d; d >>= 1) total += __shfl_xor_sync(0xffffffffu, total, d);
+    if (lane == 0 && total) atomicAdd(&s_total, total);
+    __syncthreads();
+    if (threadIdx.x == 0 && p.warp_events) p.warp_events[e] = s_total;
+    __syncthreads();
+  }
 }
 
 // max simulated threads of any valid launch (sizes the per-CTA prev table)
@@ -932,28 +1529,12 @@ extern "C" __attribute__((visibility("default"))) int hfz_dbg_edge_prof(unsigned
 }
 #endif
 
-extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, const uint32_t* dims,
-                                     const uint64_t* thread_off, const uint64_t* ev_off,
-                                     const uint32_t* sites, uint64_t n_exec, uint64_t n_launch,
-                                     uint8_t* raw_maps, uint64_t* warp_events_out) {
-  if (!ctx || (n_exec && (!launch_off || !raw_maps)) ||
-      (n_launch && (!dims || !thread_off || !ev_off))) {
-    hfz_set_error("hfz_edge_record_batch: null argument");
-    return HFZ_EINVAL;
-  }
-  if (n_exec == 0) return HFZ_OK;
-  HFZ_CUDA(cudaSetDevice(ctx->device));
-  // size the per-CTA prev table from the launch geometry (one 8-byte D2H read)
-  unsigned long long mx = 0;
-  HFZ_CUDA(cudaMemsetAsync(ctx->d_small, 0, sizeof(unsigned long long), ctx->stream));
-  if (n_launch) {
-    hfz_k_edge_max_threads<<<64, 256, 0, ctx->stream>>>(dims, n_launch, ctx->d_small);
-    ++ctx->launches;
-    HFZ_CUDA(cudaGetLastError());
-  }
-  HFZ_CUDA(cudaMemcpyAsync(&mx, ctx->d_small, sizeof(mx), cudaMemcpyDeviceToHost, ctx->stream));
-  HFZ_CUDA(cudaStreamSynchronize(ctx->stream));
-
+// The per-exec kernel over all execs (exec_list = NULL) or the listed ones; mx = most threads of any of
+// their valid launches (sizes the per-CTA prev table).
+static int edge_record_per_exec(hfz_ctx* ctx, const uint64_t* launch_off, const uint32_t* dims,
+                                const uint64_t* thread_off, const uint64_t* ev_off, const uint32_t* sites,
+                                uint64_t n_exec, const uint32_t* exec_list, unsigned long long mx,
+                                uint8_t* raw_maps, uint64_t* warp_events_out) {
   uint32_t grid = (uint32_t)(n_exec < (uint64_t)ctx->num_sms ? n_exec : (uint64_t)ctx->num_sms);
   const uint64_t stride = mx ? mx : 1;
   if (ctx->edge_prev_words < (uint64_t)grid * stride) {
@@ -982,6 +1563,7 @@ extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, c
   p.warp_events = warp_events_out;
   p.prev_scratch = d_prev;
   p.prev_stride = stride;
+  p.exec_list = exec_list;
   const size_t wsmem = (size_t)kPool * kTabBytes;
   // counters in shared memory either way: packed 16-bit pairs when the device half fits, else the
   // hashed dirty-slot table (both 64 KB at most)
@@ -997,6 +1579,148 @@ extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, c
   ++ctx->launches;
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return hfz_cuda_fail(e, "hfz_edge_record_batch");
+  return HFZ_OK;
+}
+
+// grow-only device buffer of the context
+template <class T>
+static bool edge_grow(T** buf, uint64_t* cap, uint64_t want) {
+  if (*cap >= want) return true;
+  cudaFree(*buf);
+  *buf = nullptr;
+  *cap = 0;
+  const uint64_t n = want + want / 4 + 64;
+  if (cudaMalloc(buf, (size_t)n * sizeof(T)) != cudaSuccess) {
+    hfz_set_error("hfz_edge_record_batch: scratch allocation failed (%llu bytes)", (unsigned long long)(n * sizeof(T)));
+    return false;
+  }
+  *cap = n;
+  return true;
+}
+
+extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, const uint32_t* dims,
+                                     const uint64_t* thread_off, const uint64_t* ev_off,
+                                     const uint32_t* sites, uint64_t n_exec, uint64_t n_launch,
+                                     uint8_t* raw_maps, uint64_t* warp_events_out) {
+  if (!ctx || (n_exec && (!launch_off || !raw_maps)) ||
+      (n_launch && (!dims || !thread_off || !ev_off))) {
+    hfz_set_error("hfz_edge_record_batch: null argument");
+    return HFZ_EINVAL;
+  }
+  if (n_exec == 0) return HFZ_OK;
+  HFZ_CUDA(cudaSetDevice(ctx->device));
+  if (n_exec >= (1ull << 32) || n_launch >= (1ull << 32)) {
+    hfz_set_error("hfz_edge_record_batch: more than 2^32 - 1 execs or launches in one call");
+    return HFZ_EINVAL;
+  }
+  if (!ctx->edge_flat) {  // everything through the per-exec kernel (one 8-byte D2H read sizes its prev table)
+    unsigned long long mx = 0;
+    HFZ_CUDA(cudaMemsetAsync(ctx->d_small, 0, sizeof(unsigned long long), ctx->stream));
+    if (n_launch) {
+      hfz_k_edge_max_threads<<<64, 256, 0, ctx->stream>>>(dims, n_launch, ctx->d_small);
+      ++ctx->launches;
+      HFZ_CUDA(cudaGetLastError());
+    }
+    HFZ_CUDA(cudaMemcpyAsync(&mx, ctx->d_small, sizeof(mx), cudaMemcpyDeviceToHost, ctx->stream));
+    HFZ_CUDA(cudaStreamSynchronize(ctx->stream));
+    return edge_record_per_exec(ctx, launch_off, dims, thread_off, ev_off, sites, n_exec, nullptr, mx, raw_maps,
+                                warp_events_out);
+  }
+
+  // ---- flat path: prep (eligibility, flat queue) -> per chunk of execs: decide, count
+  if (!edge_grow(&ctx->fl_nsw, &ctx->fl_nsw_cap, n_launch + 1) || !edge_grow(&ctx->fl_sw_off, &ctx->fl_sw_off_cap, n_launch + 1) ||
+      !edge_grow(&ctx->fl_l_exec, &ctx->fl_l_exec_cap, n_launch + 1) || !edge_grow(&ctx->fl_elig, &ctx->fl_elig_cap, n_exec) ||
+      !edge_grow(&ctx->fl_exec_ev0, &ctx->fl_exec_ev0_cap, n_exec + 1) ||
+      !edge_grow(&ctx->fl_exec_sw0, &ctx->fl_exec_sw0_cap, n_exec + 1) || !edge_grow(&ctx->fl_inelig, &ctx->fl_inelig_cap, n_exec))
+    return HFZ_ENOMEM;
+  FlatParams p;
+  memset(&p, 0, sizeof(p));
+  p.launch_off = launch_off;
+  p.dims = dims;
+  p.thread_off = thread_off;
+  p.ev_off = ev_off;
+  p.sites = sites;
+  p.n_exec = n_exec;
+  p.n_launch = n_launch;
+  p.H = ctx->H;
+  p.rec_bytes = ctx->rec_bytes;
+  p.raw = raw_maps;
+  p.warp_events = warp_events_out;
+  p.nsw = ctx->fl_nsw;
+  p.sw_off = ctx->fl_sw_off;
+  p.l_exec = ctx->fl_l_exec;
+  p.elig = ctx->fl_elig;
+  p.exec_ev0 = ctx->fl_exec_ev0;
+  p.exec_sw0 = ctx->fl_exec_sw0;
+  p.inelig = ctx->fl_inelig;
+  p.small = ctx->d_small;
+  HFZ_CUDA(cudaMemsetAsync(ctx->d_small, 0, 5 * sizeof(unsigned long long), ctx->stream));
+  {
+    const uint64_t blocks = (n_exec + 1 + 255) / 256;
+    hfz_k_edge_prep<<<(uint32_t)(blocks < 1024 ? blocks : 1024), 256, 0, ctx->stream>>>(p);
+    hfz_k_edge_scan<<<1, 1024, 0, ctx->stream>>>(p);
+    ctx->launches += 2;
+    HFZ_CUDA(cudaGetLastError());
+  }
+  unsigned long long h_small[5] = {0, 0, 0, 0, 0};
+  std::vector<uint64_t> h_ev0(n_exec + 1), h_sw0(n_exec + 1);
+  HFZ_CUDA(cudaMemcpyAsync(h_small, ctx->d_small, sizeof(h_small), cudaMemcpyDeviceToHost, ctx->stream));
+  HFZ_CUDA(cudaMemcpyAsync(h_ev0.data(), ctx->fl_exec_ev0, (n_exec + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  HFZ_CUDA(cudaMemcpyAsync(h_sw0.data(), ctx->fl_exec_sw0, (n_exec + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  HFZ_CUDA(cudaStreamSynchronize(ctx->stream));
+  const uint64_t n_inelig = h_small[0];
+  if (n_inelig) {  // execs whose launches differ in geometry (prev is launch-ordered there)
+    const int rc = edge_record_per_exec(ctx, launch_off, dims, thread_off, ev_off, sites, n_inelig, ctx->fl_inelig,
+                                        h_small[1], raw_maps, warp_events_out);
+    if (rc != HFZ_OK) return rc;
+  }
+  // small[3] holds the max of ~nsw, i.e. ~min
+  p.uni_nsw = (n_inelig == 0 && h_small[4] > 0 && ~h_small[3] == h_small[4]) ? (uint32_t)h_small[4] : 0u;
+  p.l_lo = 0;
+  p.l_hi = n_launch;
+  const uint64_t cap_events = (uint64_t)ctx->edge_scratch_mb << 18;  // u32 entries
+  const uint64_t cap_items = 1ull << 24;
+  const size_t tab_smem = (size_t)kFlatWarps * kTabBytes;
+  const uint32_t cslots = ctx->H < kCountSlots ? ctx->H : kCountSlots;
+  HFZ_CUDA(cudaFuncSetAttribute(hfz_k_edge_divergent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab_smem));
+  HFZ_CUDA(cudaFuncSetAttribute(hfz_k_edge_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(cslots * 4)));
+  for (uint64_t e_lo = 0; e_lo < n_exec;) {
+    uint64_t e_hi = e_lo + 1;
+    while (e_hi < n_exec && h_ev0[e_hi + 1] - h_ev0[e_lo] <= cap_events && h_sw0[e_hi + 1] - h_sw0[e_lo] <= cap_items) ++e_hi;
+    const uint64_t n_ev = h_ev0[e_hi] - h_ev0[e_lo], n_items = h_sw0[e_hi] - h_sw0[e_lo];
+    if (!edge_grow(&ctx->fl_scratch, &ctx->fl_scratch_cap, n_ev + 1) ||
+        !edge_grow(&ctx->fl_rec_first, &ctx->fl_rec_first_cap, n_items + 1) ||
+        !edge_grow(&ctx->fl_rec_cnt, &ctx->fl_rec_cnt_cap, n_items + 1) ||
+        !edge_grow(&ctx->fl_div, &ctx->fl_div_cap, n_items + 1) ||
+        !edge_grow(&ctx->fl_lines, &ctx->fl_lines_cap, (n_items + 32) * 32))
+      return HFZ_ENOMEM;
+    p.e_lo = e_lo;
+    p.e_hi = e_hi;
+    p.q_lo = h_sw0[e_lo];
+    p.q_hi = h_sw0[e_hi];
+    p.ev_lo = h_ev0[e_lo];
+    p.scratch = ctx->fl_scratch;
+    p.rec_first = ctx->fl_rec_first;
+    p.rec_cnt = ctx->fl_rec_cnt;
+    p.div_list = ctx->fl_div;
+    p.lines = ctx->fl_lines;
+    if (n_items) {
+      HFZ_CUDA(cudaMemsetAsync(ctx->d_small + 2, 0, 5 * sizeof(unsigned long long), ctx->stream));  // pop counters, divergent count
+      const uint64_t want = (n_items + kPop * kClassifyWarps - 1) / (kPop * kClassifyWarps);
+      const uint64_t full = (uint64_t)ctx->num_sms * 2;
+      hfz_k_edge_classify<<<(uint32_t)(want < full ? want : full), kClassifyWarps * 32, 0, ctx->stream>>>(p);
+      const uint64_t wantd = (n_items + kFlatWarps - 1) / kFlatWarps;  // (the divergent count is known on the device only)
+      hfz_k_edge_divergent<<<(uint32_t)(wantd < (uint64_t)ctx->num_sms ? wantd : (uint64_t)ctx->num_sms), kFlatWarps * 32, tab_smem,
+                             ctx->stream>>>(p);
+      ctx->launches += 2;
+    }
+    const uint64_t ne = e_hi - e_lo;
+    const uint64_t cgrid = (uint64_t)ctx->num_sms * 3;
+    hfz_k_edge_count<<<(uint32_t)(ne < cgrid ? ne : cgrid), kCountWarps * 32, cslots * 4, ctx->stream>>>(p);
+    ++ctx->launches;
+    HFZ_CUDA(cudaGetLastError());
+    e_lo = e_hi;
+  }
   return HFZ_OK;
 }
 

@@ -13,7 +13,8 @@ def timeit(fn, reps=5):
         ts.append(e0.elapsed_time(e1))
     return min(ts[1:])
 
-ctx = hfz.Context(0)
+ctx = hfz.Context(0, int(os.environ.get("EDGE_S", "65536")))
+ctx.set_option("edge_flat", int(os.environ.get("EDGE_FLAT", "1")))
 dev = ctx.device
 what = sys.argv[1] if len(sys.argv) > 1 else "all"
 if what in ("all", "havoc"):
@@ -48,7 +49,7 @@ if what in ("all", "edge"):
         ms = timeit(run, reps=3)
         ev = tr["sites"].size
         threads = int(tr["thread_off"][-1])
-        byts = 4 * ev + 8 * threads + 4 * 32768 * n_exec
+        byts = 4 * ev + 8 * threads + 4 * (ctx.S // 2) * n_exec
         import ctypes
         from paper_2603_12485_b200 import _lib
         L = _lib.lib if hasattr(_lib, "lib") else None

@@ -11,6 +11,15 @@ pytestmark = pytest.mark.gpu
 S, H = 65536, 32768
 
 
+@pytest.fixture(autouse=True, params=["flat", "per_exec"])
+def edge_path(request, ctx):
+    """Every case runs through both K1 paths: the flat decide + count kernels (default; execs whose
+    launches differ in geometry still go to the per-exec kernel) and the per-exec kernel alone."""
+    ctx.set_option("edge_flat", 1 if request.param == "flat" else 0)
+    yield request.param
+    ctx.set_option("edge_flat", 1)
+
+
 def to_dev(ctx, tr):
     i64 = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.uint64).view(np.int64)).to(ctx.device)
     sites = np.ascontiguousarray(tr["sites"], np.uint32)
@@ -213,10 +222,41 @@ def test_synthetic_config3_shape(ctx, port):
     assert np.array_equal(o["sig_full"].cpu().numpy().view(np.uint64), want["sig_full"])
 
 
-def test_large_map_262144_edges(port):
-    """262,144-slot map: 131,072 device slots do not fit shared memory -> global-atomic path."""
+def test_flat_path_in_chunks(ctx, port, edge_path):
+    """A 1 MB bump-list scratch (262,144 events) cuts the batch into chunks of one exec each."""
+    if edge_path != "flat":
+        pytest.skip("flat path only")
+    tr = synth.bb_traces(5, seed=21)
+    ctx.set_option("edge_scratch_mb", 1)
+    try:
+        check(ctx, port, tr, 5)
+    finally:
+        ctx.set_option("edge_scratch_mb", 2048)
+
+
+def test_flat_path_mixed_batch(ctx, port):
+    """Execs the flat path takes (one launch, or equal geometries) interleaved with execs it leaves to
+    the per-exec kernel (launches of differing geometry), plus launches of differing sizes so the
+    flat queue is searched rather than divided."""
+    from tests.test_oracle_vs_ref import random_exec
+    rng = np.random.default_rng(23)
+    execs = []
+    for i in range(40):
+        if i % 3 == 0:
+            execs.append(random_exec(rng, int(rng.integers(2, 4)), three_d=bool(i % 2)))
+        elif i % 3 == 1:
+            execs.append(chain((int(rng.integers(1, 200)), 1, 1), [[3, 4, 5, 3], [9, 3]], grid=(int(rng.integers(1, 4)), 1, 1)))
+        else:
+            execs.append(chain((int(rng.integers(1, 70)), 2, 1), [[1, 2, 1]]))
+    check(ctx, port, pack(execs), len(execs))
+
+
+def test_large_map_262144_edges(port, edge_path):
+    """262,144-slot map: the 131,072 device counters do not fit shared memory at once -> the count kernel
+    takes them in ranges (flat path) / hashed dirty-slot table (per-exec kernel)."""
     S2 = 262144
     c2 = hfz.Context(0, S2)
+    c2.set_option("edge_flat", 1 if edge_path == "flat" else 0)
     try:
         tr = synth.bb_traces(3, seed=5, grid=(4, 1, 1), block=(128, 1, 1), n_launch=2)
         check(c2, port, tr, 3, S_=S2)
