@@ -995,10 +995,12 @@ __global__ void __launch_bounds__(kEdgeWarps * 32, 1) hfz_k_edge_record(const Ed
 //   hfz_k_edge_divergent  the listed warps, a flat queue again; shared memory holds nothing but one site
 //                      table per real warp (22 per SM), so every warp can take one and none waits;
 //   hfz_k_edge_count      one CTA per exec streams the exec's bump lists into u32 counters in SHARED
-//                      memory (shared-memory atomics; 16,384 slots = 64 KB per pass over the lists, so
-//                      three execs are in flight per SM and one's zero / flush phases hide behind the
-//                      others' list reads) and flushes them to the record: still no global atomic per
-//                      hit, and the counters are full-width, so there is no overflow replay.
+//                      memory (shared-memory atomics; 64 KB per CTA, so three execs are in flight per SM
+//                      and one's zero / flush phases hide behind the others' list reads) and flushes
+//                      them to the record: still no global atomic per hit.  An exec with fewer than 65,536
+//                      bumps in all (summed first) packs two 16-bit counters per word -- 32,768 slots per
+//                      pass; any other exec counts in full u32 words, 16,384 slots per pass, saturating.
+//                      Either way a counter cannot overflow, so nothing is ever replayed.
 // Launches of an exec that differ in geometry carry prev per flattened gtid IN LAUNCH ORDER
 // (hdvm.cpp:376,426-430), which a flat queue cannot honour: those execs (and execs whose thread
 // offsets are not a CSR of their launch sizes) are left to the per-exec kernel.
@@ -1380,17 +1382,32 @@ __global__ void __launch_bounds__(kCountWarps * 32, 3) hfz_k_edge_count(const Fl
   __shared__ uint32_t s_big_c[kBigCap];
   __shared__ uint32_t s_nbig;
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t R = p.H < kCountSlots ? p.H : kCountSlots;  // (both multiples of 4)
+  __shared__ uint32_t s_wsum[kCountWarps];
   for (uint64_t e = p.e_lo + blockIdx.x; e < p.e_hi; e += gridDim.x) {
     if (!p.elig[e]) continue;  // the per-exec kernel writes this record
     const uint64_t q0 = p.exec_sw0[e] - p.q_lo, q1 = p.exec_sw0[e + 1] - p.q_lo;
     uint32_t* ghist = reinterpret_cast<uint32_t*>(p.raw + e * p.rec_bytes + p.H);
-    if (threadIdx.x == 0) s_total = 0;
+    // the exec's bumps in all: fewer than 65,536 (the rule) cannot overflow a 16-bit counter, so two
+    // counters share a word and a pass covers twice the slots (the whole device half of a 65,536-slot map)
     unsigned long long total = 0;
+    for (uint64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) total += p.rec_cnt[q] & ~kSegFlag;
+    for (int d = 16; d; d >>= 1) total += __shfl_xor_sync(0xffffffffu, total, d);
+    if (lane == 0) s_wsum[w] = (uint32_t)(total < 0xffffffffull ? total : 0xffffffffull);
+    if (threadIdx.x == 0) s_total = 0;
+    __syncthreads();
+    if (lane == 0 && total) atomicAdd(&s_total, total);
+    uint64_t bound = 0;  // (saturating per-warp sums: only "below 65,536 or not" matters here)
+    for (int i = 0; i < kCountWarps; ++i) bound += s_wsum[i];
+    const bool packed = bound < 65536u;
+    const uint32_t R = packed ? (p.H < 2 * kCountSlots ? p.H : 2 * kCountSlots) : (p.H < kCountSlots ? p.H : kCountSlots);
+    auto add = [&](uint32_t rel) {
+      if (packed) atomicAdd(hist + (rel >> 1), 1u << ((rel & 1u) * 16u));
+      else bump(hist + rel);
+    };
     for (uint32_t r0 = 0; r0 < p.H; r0 += R) {
       const uint32_t n = p.H - r0 < R ? p.H - r0 : R;
       uint4* z = reinterpret_cast<uint4*>(hist);
-      for (uint32_t i = threadIdx.x; i < n / 4; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+      for (uint32_t i = threadIdx.x; i < (packed ? n / 8 : n / 4); i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
       if (threadIdx.x == 0) s_nbig = 0;
       __syncthreads();
       // a warp takes 32 consecutive simulated warps: the coherent ones' lines are 32 independent coalesced
@@ -1425,7 +1442,7 @@ __global__ void __launch_bounds__(kCountWarps * 32, 3) hfz_k_edge_count(const Fl
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const uint32_t rel = x[c] - r0;
-            if (i0 + c < ck && rel < n) bump(hist + rel);
+            if (i0 + c < ck && rel < n) add(rel);
           }
         }
         uint32_t left = __ballot_sync(0xffffffffu, seg);  // more lists than the side list holds: here and now
@@ -1436,10 +1453,9 @@ __global__ void __launch_bounds__(kCountWarps * 32, 3) hfz_k_edge_count(const Fl
           const uint32_t* list = p.scratch + __shfl_sync(0xffffffffu, f, k);
           for (uint32_t i = lane; i < cc; i += 32) {
             const uint32_t rel = list[i] - r0;
-            if (rel < n) bump(hist + rel);
+            if (rel < n) add(rel);
           }
         }
-        if (r0 == 0) total += cnt & ~kSegFlag;
       }
       __syncthreads();
       {
@@ -1450,18 +1466,23 @@ __global__ void __launch_bounds__(kCountWarps * 32, 3) hfz_k_edge_count(const Fl
 #pragma unroll 12
           for (uint32_t i = lane; i < cc; i += 32) {
             const uint32_t rel = list[i] - r0;
-            if (rel < n) bump(hist + rel);
+            if (rel < n) add(rel);
           }
         }
       }
       __syncthreads();
       uint4* dst = reinterpret_cast<uint4*>(ghist + r0);
-      for (uint32_t i = threadIdx.x; i < n / 4; i += blockDim.x) dst[i] = z[i];
+      if (packed) {
+        const uint2* z2 = reinterpret_cast<const uint2*>(hist);
+        for (uint32_t i = threadIdx.x; i < n / 4; i += blockDim.x) {
+          const uint2 t = z2[i];
+          dst[i] = make_uint4(t.x & 0xffffu, t.x >> 16, t.y & 0xffffu, t.y >> 16);
+        }
+      } else {
+        for (uint32_t i = threadIdx.x; i < n / 4; i += blockDim.x) dst[i] = z[i];
+      }
       __syncthreads();
     }
-    for (int d = 16; d; d >>= 1) total += __shfl_xor_sync(0xffffffffu, total, d);
-    if (lane == 0 && total) atomicAdd(&s_total, total);
-    __syncthreads();
     if (threadIdx.x == 0 && p.warp_events) p.warp_events[e] = s_total;
     __syncthreads();
   }
