@@ -602,8 +602,9 @@ def bench_edge_and_large_map(hfz, dev, timer, peak, peak_src, args, threads):
                     f"{events / n1:.0f} thread events per exec, 65,536-slot maps",
           "value": n1 / (t_k1["mean"] / 1e3), "unit": "execs/s", "kernel_ms": t_k1["mean"], "kernel_ms_min": t_k1["min"],
           "iters": t_k1["iters"], "events_per_sec": events / (t_k1["mean"] / 1e3),
-          "roofline": roof(k1_bytes(n1, S // 2), t_k1["mean"], peak, peak_src, "hfz_k_edge_record<packed>",
-                           "bytes = 4 x events + 8 x (threads + launches) read + 4 x H written per exec; issue/latency-bound"),
+          "roofline": roof(k1_bytes(n1, S // 2), t_k1["mean"], peak, peak_src, "hfz_edge_record_batch: hfz_k_edge_classify + hfz_k_edge_divergent + hfz_k_edge_count (whole call)",
+                           "bytes = 4 x events + 8 x (threads + launches) read + 4 x H written per exec; the time is the whole "
+                           "C-ABI call (prep + scan launches, one D2H read of the queue sizes, then the three kernels); latency-bound"),
           "cpu_baseline": cpu_k1,
           "parity_checked": f"first {n_par} execs: device half of every record and warp_edge_events vs the reference runtime",
           "l2_policy": f"traces of {events * 4 / 1e6:.0f} MB + {n_threads * 8 / 1e6:.0f} MB of offsets per launch exceed L2",
@@ -667,8 +668,8 @@ def bench_edge_and_large_map(hfz, dev, timer, peak, peak_src, args, threads):
                      f"{n2} execs, K1 -> K2 chained on the device",
            "value": n2 / (ms_chain / 1e3), "unit": "execs/s", "ms_per_step": ms_chain, "iters": 10,
            "edge_record": {"value": n2 / (t_k1l["mean"] / 1e3), "unit": "execs/s", "kernel_ms": t_k1l["mean"], "kernel_ms_min": t_k1l["min"],
-                           "counters": "hashed dirty-slot table in shared memory (no global atomic per hit)",
-                           "roofline": roof(k1_bytes(n2, S_LARGE // 2), t_k1l["mean"], peak, peak_src, "hfz_k_edge_record<hashed>")},
+                           "counters": "per-exec shared-memory histogram in the count kernel, ranges of 32,768 slots per pass (no global atomic per hit)",
+                           "roofline": roof(k1_bytes(n2, S_LARGE // 2), t_k1l["mean"], peak, peak_src, "hfz_edge_record_batch: classify + divergent + count (whole call)")},
            "fold": {"value": n2 / (t_k2["mean"] / 1e3), "unit": UNIT, "ms_per_step": t_k2["mean"], "ms_per_step_min": t_k2["min"],
                     "state": "empty virgin", "admits_per_step": admits,
                     "roofline": roof(n2 * REC_LARGE, t_k2["mean"], peak, peak_src, "whole step (scan + resolve + merge launches)")},

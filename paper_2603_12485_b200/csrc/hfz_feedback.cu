@@ -20,6 +20,7 @@
 #include <type_traits>
 
 #include "hfz_common.cuh"
+#include "hfz_fnv.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -1249,6 +1250,7 @@ constexpr int kStepWarps = 24;
 constexpr uint32_t kStepBuf = 8192;                 // shared memory per warp: two staging buffers of one piece (phase 1),
 constexpr uint32_t kStepPiece = kStepBuf / 2;       //   then one list buffer of kStepCap entries (phase 2)
 constexpr uint32_t kStepCap = kStepBuf / 4;
+constexpr uint32_t kChainRound = 1024;              // entries per round of the signature chains (phase 2)
 
 __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(hfz_smem_u32(smem_dst)), "l"(gsrc) : "memory");
@@ -1517,7 +1519,7 @@ __global__ void __launch_bounds__(kStepWarps * 32, 1) hfz_k_small_step(const Ste
     const uint64_t D = c.S / 128;  // warps: 4 slots per thread
     const uint64_t G = (c.n_exec + 31) / 32;
     uint32_t newh = 0, newd = 0;
-    for (uint64_t role = gw; role < D + G + (c.n_exec + 1) / 2; role += W) {
+    for (uint64_t role = gw; role < D + G + c.n_exec; role += W) {
       if (role < D) {
         // delta word of 4 slots from the table; fused: the single-rank merge right here
         const uint64_t t = role * 32 + lane;  // word index, < S / 4
@@ -1557,127 +1559,78 @@ __global__ void __launch_bounds__(kStepWarps * 32, 1) hfz_k_small_step(const Ste
         }
         if (fused && e < c.n_exec && !novel) p.admit[e] = 0;
       } else {
-        // chains of TWO maps per warp.  The warp gathers the maps' ordered piece lists into shared
-        // memory (cp.async; one piece per lane, every copy in flight at once), then lanes 0/1 run the
-        // Full/Simple chains of the first map and lanes 2/3 those of the second over the buffers --
-        // one instruction stream for the four chains.  A chain is serial (3 dependent multiply
-        // steps per entry), so what matters is that nothing else sits on its critical path and
-        // that a scheduler has at most one such warp to issue for.
-        const uint64_t ea = (role - D - G) * 2;
+        // signatures: ONE map per warp, the whole warp on its two chains (hfz_fnv.cuh).  The warp gathers the
+        // map's ordered piece lists into shared memory (cp.async; one piece per lane, every copy in flight
+        // at once), 1,024 entries per round, then runs the Full and the Simple chain over the buffer
+        // bit-sliced, 32 steps per lane.  (Until round 2 of the build, lanes 0..3 ran the four chains of two
+        // maps serially: 53-64 cycles per entry, ~78 k cycles for two maps at 2 % density; a scheduler had
+        // one such warp to issue for and nothing could shorten the dependency.)
+        const uint64_t e = role - D - G;
         uint32_t* buf = reinterpret_cast<uint32_t*>(wbuf);
-        constexpr uint32_t kHalf = kStepCap / 2;  // entries per map per round
-        // per-lane chain state (lanes 0..3)
-        uint32_t lo = (uint32_t)HFZ_FNV_OFFSET, hi = (uint32_t)(HFZ_FNV_OFFSET >> 32);
-        const bool full_lane = (lane & 1) == 0;
-        const uint32_t cmask = full_lane ? 0xffu : 0u, p3lo = full_lane ? 0x1b3u : 1u, p3hi = full_lane ? 0x100u : 0u;
-        uint32_t cur_pc[2] = {0, 0}, cur_i[2] = {0, 0}, nnz[2] = {0, 0};
+        uint8_t* stream = wbuf + kChainRound * 4;  // 3,072 bytes of byte stream + slack (the buffer is 8 KB)
+        static_assert(kChainRound * 4 + 3072 + 16 <= kStepBuf, "entry buffer + byte stream must fit the warp's staging buffer");
+        uint64_t hf = HFZ_FNV_OFFSET, hs = HFZ_FNV_OFFSET;
+        uint32_t cur_pc = 0, cur_i = 0, nnz = 0;
+        const uint32_t* base = c.sorted + e * c.S;
+        const uint32_t* cnt = c.cnt + e * c.pieces;
         const long long tg0 = clock64();
         for (;;) {
-          uint32_t got[2] = {0, 0};
+          uint32_t pos = 0;
+          while (cur_pc < c.pieces && pos < kChainRound) {
+            if (cur_i == 0) {
+              // whole pieces, one per lane: as many leading pieces of this batch as still fit
+              const uint32_t pcl = cur_pc + lane;
+              const uint32_t my_n = pcl < c.pieces ? __ldcg(cnt + pcl) : 0u;
+              uint32_t inc = my_n;
 #pragma unroll
-          for (int m = 0; m < 2; ++m) {
-            const uint64_t e = ea + m;
-            if (e >= c.n_exec) continue;
-            uint32_t* dst = buf + m * kHalf;
-            const uint32_t* base = c.sorted + e * c.S;
-            const uint32_t* cnt = c.cnt + e * c.pieces;
-            uint32_t pos = 0;
-            while (cur_pc[m] < c.pieces && pos < kHalf) {
-              if (cur_i[m] == 0) {
-                // whole pieces, one per lane: as many leading pieces of this batch as still fit
-                const uint32_t pcl = cur_pc[m] + lane;
-                const uint32_t my_n = pcl < c.pieces ? __ldcg(cnt + pcl) : 0u;
-                uint32_t inc = my_n;
-#pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                  const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
-                  if (lane >= d) inc += o;
-                }
-                const uint32_t fits = __ballot_sync(0xffffffffu, inc <= kHalf - pos);
-                uint32_t k = fits == 0xffffffffu ? 32u : (uint32_t)__ffs(~fits) - 1u;  // leading lanes whose pieces fit
-                k = min(k, c.pieces - cur_pc[m]);
-                if (k) {
-                  if (lane < k) {
-                    const uint32_t* list = base + piece_slot0(c, pcl);
-                    uint32_t* d0 = dst + pos + inc - my_n;
-                    for (uint32_t i = 0; i < my_n; ++i) cp_async4(d0 + i, list + i);
-                  }
-                  pos += __shfl_sync(0xffffffffu, inc, k - 1);
-                  cur_pc[m] += k;
-                  continue;
-                }
+              for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += o;
               }
-              // a piece that does not fit the rest of the buffer: part of it, coalesced
-              const uint32_t n_pc = __ldcg(cnt + cur_pc[m]);
-              const uint32_t take = min(n_pc - cur_i[m], kHalf - pos);
-              const uint32_t* list = base + piece_slot0(c, cur_pc[m]) + cur_i[m];
-              for (uint32_t i = lane; i < take; i += 32) cp_async4(dst + pos + i, list + i);
-              pos += take;
-              cur_i[m] += take;
-              if (cur_i[m] == n_pc) {
-                ++cur_pc[m];
-                cur_i[m] = 0;
+              const uint32_t fits = __ballot_sync(0xffffffffu, inc <= kChainRound - pos);
+              uint32_t k = fits == 0xffffffffu ? 32u : (uint32_t)__ffs(~fits) - 1u;  // leading lanes whose pieces fit
+              k = min(k, c.pieces - cur_pc);
+              if (k) {
+                if (lane < k) {
+                  const uint32_t* list = base + piece_slot0(c, pcl);
+                  uint32_t* d0 = buf + pos + inc - my_n;
+                  for (uint32_t i = 0; i < my_n; ++i) cp_async4(d0 + i, list + i);
+                }
+                pos += __shfl_sync(0xffffffffu, inc, k - 1);
+                cur_pc += k;
+                continue;
               }
             }
-            got[m] = pos;
-            nnz[m] += pos;
+            // a piece that does not fit the rest of the buffer: part of it, coalesced
+            const uint32_t n_pc = __ldcg(cnt + cur_pc);
+            const uint32_t take = min(n_pc - cur_i, kChainRound - pos);
+            const uint32_t* list = base + piece_slot0(c, cur_pc) + cur_i;
+            for (uint32_t i = lane; i < take; i += 32) cp_async4(buf + pos + i, list + i);
+            pos += take;
+            cur_i += take;
+            if (cur_i == n_pc) {
+              ++cur_pc;
+              cur_i = 0;
+            }
           }
-          if (got[0] == 0 && got[1] == 0) break;
+          if (pos == 0) break;
+          nnz += pos;
           cp_async_wait_all();
           __syncwarp();
           const long long tc0 = clock64();
-          if (p.dbg && ea == 0 && lane == 0) p.dbg[8] = (unsigned long long)(tc0 - tg0);
-          if (lane < 4) {
-            const uint32_t* mybuf = buf + (lane >> 1) * kHalf;
-            const uint32_t n_my = (lane >> 1) ? got[1] : got[0];
-            // h = (h ^ byte) * P, P = 2^40 + 0x1b3, in 32-bit halves: lo' depends on lo alone and
-            // hi' = hi * 0x1b3 + t with t off the lo chain.  The class byte step is the same code on all
-            // four lanes: the Simple lanes multiply by 1.  Measured 53-64 cycles per entry: a lone warp
-            // owns its scheduler, but every IMAD occupies the 16-lane pipe for two cycles whether 4 or
-            // 32 lanes are active, so the ~20 instructions per entry are what bounds it (splitting the
-            // 64-bit product into IMAD + IMAD.HI to shorten the dependency made it slower: 72 cycles).
-            auto fnv32 = [&](uint32_t byte, uint32_t plo, uint32_t phi) {
-              const uint32_t x = lo ^ byte;
-              const uint64_t w = (uint64_t)x * plo;
-              const uint32_t t = (uint32_t)(w >> 32) + x * phi;
-              hi = hi * plo + t;
-              lo = (uint32_t)w;
-            };
-            auto step = [&](uint32_t en) {
-              fnv32(en & 0xffu, 0x1b3u, 0x100u);
-              fnv32((en >> 8) & 0xffu, 0x1b3u, 0x100u);
-              fnv32((1u << (en >> 24)) & cmask, p3lo, p3hi);
-            };
-            uint32_t i = 0;
-            if (n_my >= 4) {
-              uint4 cur = *reinterpret_cast<const uint4*>(mybuf);
-              for (; i + 8 <= n_my; i += 4) {
-                const uint4 nxt = *reinterpret_cast<const uint4*>(mybuf + i + 4);
-                step(cur.x); step(cur.y); step(cur.z); step(cur.w);
-                cur = nxt;
-              }
-              step(cur.x); step(cur.y); step(cur.z); step(cur.w);
-              i += 4;
-            }
-            for (; i < n_my; ++i) step(mybuf[i]);
-          }
-          if (p.dbg && ea == 0 && lane == 0) {
+          if (p.dbg && e == 0 && lane == 0) p.dbg[8] = (unsigned long long)(tc0 - tg0);
+          hf = pfnv::chain_entries<3>(hf, buf, pos, stream, lane);
+          hs = pfnv::chain_entries<2>(hs, buf, pos, stream, lane);
+          if (p.dbg && e == 0 && lane == 0) {
             p.dbg[9] = (unsigned long long)(clock64() - tc0);
-            p.dbg[10] = got[0];
+            p.dbg[10] = pos;
           }
           __syncwarp();
         }
-        if (lane < 4) {
-          const uint64_t e = ea + (lane >> 1);
-          if (e < c.n_exec) {
-            const uint64_t h = ((uint64_t)hi << 32) | lo;
-            if (full_lane) {
-              p.sig_full[e] = h;
-              if (p.nnz) p.nnz[e] = (lane >> 1) ? nnz[1] : nnz[0];
-            } else {
-              p.sig_simple[e] = h;
-            }
-          }
+        if (lane == 0) {
+          p.sig_full[e] = hf;
+          p.sig_simple[e] = hs;
+          if (p.nnz) p.nnz[e] = nnz;
         }
       }
     }
@@ -1910,8 +1863,9 @@ int launch_scan_two_stage(hfz_ctx* ctx, const ScanParams& sp) {
 int ensure_cand(hfz_ctx* ctx, uint64_t n_exec);
 bool small_step_ok(hfz_ctx* ctx, uint64_t n_exec) {
   if (!ctx->small_fused || n_exec == 0) return false;
-  // measured on B200 (65,536 slots, warm): 4,096 maps 0.27 ms fused vs 0.36 ms pipelined; 8,192 maps 0.51 vs 0.41 ms
-  const uint64_t limit = ctx->scan_two_stage >= 0 ? (uint64_t)ctx->scan_two_stage : 4096;
+  // measured on B200 (65,536 slots, warm / cold virgin): 4,096 maps 0.21 / 0.36 ms fused vs 0.36 / 0.70 pipelined;
+  // 8,192 maps 0.40 / 0.62 vs 0.40 / 1.47; 12,288 maps 0.58 / 0.90 vs 0.47 / 2.03 (pipelined wins warm from there on)
+  const uint64_t limit = ctx->scan_two_stage >= 0 ? (uint64_t)ctx->scan_two_stage : 8192;
   if (n_exec > limit || !two_stage_fits(ctx, n_exec)) return false;
   if (ctx->coop_grid < 0) {  // once: cooperative launch support and the co-resident grid size
     int coop = 0, per_sm = 0;
@@ -2409,4 +2363,46 @@ extern "C" int hfz_feedback_batch(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_
   if (rc) return rc;
   return hfz_feedback_resolve(ctx, raw_maps, n_exec, virgin_inout, edge_counts_inout, ctx->delta, 1,
                               0, admit_out);
+}
+
+// ---- dev / test entry: both signatures of an ordered entry list (slot | rung << 24) by the warp-parallel
+// FNV of hfz_fnv.cuh, one warp.  Not part of include/hfz.h; tests/test_feedback_gpu.py::test_warp_fnv.
+namespace {
+__global__ void __launch_bounds__(32) hfz_k_dbg_warp_fnv(const uint32_t* __restrict__ entries, uint64_t n,
+                                                         unsigned long long* __restrict__ out) {
+  __shared__ __align__(16) uint32_t buf[kChainRound];
+  __shared__ __align__(16) uint8_t stream[3072 + 16];
+  const int lane = threadIdx.x;
+  uint64_t hf = HFZ_FNV_OFFSET, hs = HFZ_FNV_OFFSET;
+  for (uint64_t i0 = 0; i0 < n; i0 += kChainRound) {
+    const uint32_t m = (uint32_t)(n - i0 < kChainRound ? n - i0 : kChainRound);
+    for (uint32_t i = lane; i < m; i += 32) buf[i] = entries[i0 + i];
+    __syncwarp();
+    hf = pfnv::chain_entries<3>(hf, buf, m, stream, lane);
+    hs = pfnv::chain_entries<2>(hs, buf, m, stream, lane);
+    __syncwarp();
+  }
+  if (lane == 0) {
+    out[0] = hf;
+    out[1] = hs;
+  }
+}
+}  // namespace
+
+extern "C" __attribute__((visibility("default"))) int hfz_dbg_warp_fnv(const uint32_t* entries_host, uint64_t n,
+                                                                       uint64_t* out2_host) {
+  uint32_t* d_e = nullptr;
+  unsigned long long* d_o = nullptr;
+  if (cudaMalloc(&d_e, (size_t)(n + 1) * 4) != cudaSuccess || cudaMalloc(&d_o, 16) != cudaSuccess) {
+    cudaFree(d_e);
+    return HFZ_ENOMEM;
+  }
+  cudaError_t e = cudaMemcpy(d_e, entries_host, (size_t)n * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    hfz_k_dbg_warp_fnv<<<1, 32>>>(d_e, n, d_o);
+    e = cudaMemcpy(out2_host, d_o, 16, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(d_e);
+  cudaFree(d_o);
+  return e == cudaSuccess ? HFZ_OK : hfz_cuda_fail(e, "hfz_dbg_warp_fnv");
 }

@@ -31,8 +31,12 @@ sel = {k: {"value": m[k][0], "unit": m[k][1]} for k in keys if k in m}
 stalls = {h: m[h][0] for h in hdr if "issue_stalled" in h and h.endswith("_per_warp_active.pct")}
 dur = scaled("gpu__time_duration.sum")
 rd, wr = scaled("dram__bytes_read.sum"), scaled("dram__bytes_write.sum")
+import hashlib, time
 summary = {
     "round": rnd, "kernel": m["Kernel Name"][0] if "Kernel Name" in m else "hfz_k_scan",
+    # bench.py attaches roofline.traffic only while this hash still matches the kernel source it runs
+    "kernel_source_sha256": hashlib.sha256(open(os.path.join(ROOT, "paper_2603_12485_b200", "csrc", "hfz_feedback.cu"), "rb").read()).hexdigest(),
+    "captured": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime(os.path.getmtime(rep))),
     "command": "ncu --set full --clock-control none --import-source on -k regex:hfz_k_scan -s 4 -c 1 "
                "python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu",
     "duration_s_under_ncu": dur, "dram_bytes_read": rd, "dram_bytes_write": wr,
@@ -67,7 +71,10 @@ print(json.dumps({k: summary[k] for k in ("duration_s_under_ncu", "dram_bytes_pe
 # ---- secondary kernels: one compact summary per extra report found in gpurun_out/
 EXTRA = {"scan_pipe": "scripts/probe_feedback.py --n 4096 --configs '' --reps 1 --sweep 4096 (-k regex:hfz_k_scan_pipe -s 2 -c 1)",
          "expand": "scripts/probe_sparse.py --execs 16384 --chunks 8192 (-k regex:hfz_k_expand -s 2 -c 2)",
-         "edge": "scripts/probe_k1k3.py edge (-k regex:hfz_k_edge_record -c 1)",
+         "edge": "EDGE_FLAT=0 scripts/probe_k1k3.py edge (-k regex:hfz_k_edge_record -c 1): the per-exec kernel (round 1's design; since round 2 only execs whose launches differ in geometry)",
+         "edge_flat": "EDGE_N=1024 scripts/probe_k1k3.py edge (-k regex:hfz_k_edge_(classify|divergent|count) -s 3 -c 3): the flat path's three kernels on 1,024 execs of the configs[2] trace recipe",
+         "edge_flat_large": "EDGE_N=1024 EDGE_S=262144 scripts/probe_k1k3.py edge (same three kernels, 262,144-slot map: the count kernel takes the device half in four ranges)",
+         "small_step": "scripts/probe_small.py (-k regex:hfz_k_small_step -s 8 -c 1): the fused small-batch step",
          "havoc": "scripts/probe_k1k3.py havoc (-k regex:hfz_k_havoc -s 2 -c 1)",
          "sparse": "scripts/probe_sparse.py --chunks 65536 (-k regex:hfz_k_sparse -s 6 -c 2: rank + chain of one 65,536-exec device call)"}
 for name, cmd in EXTRA.items():

@@ -21,11 +21,11 @@ def timeit(fn, pre, reps=30):
 
 
 dev = torch.device("cuda", 0)
-for S, ns in ((65536, (256, 1024, 2048, 3072, 4096, 8192)), (262144, (256, 1024, 2048, 4096))):
+for S, ns in ((65536, (256, 1024, 2048, 4096, 8192, 12288, 16384)), (262144, (256, 1024, 2048, 4096))):
     ctx = hfz.Context(0, S)
     nmax = max(ns)
     rec = ctx.rec
-    copies = 4 if nmax * rec * 4 < 8e9 else 2
+    copies = 4 if nmax * rec * 4 < 12e9 else 2
     raws = []
     for b in range(copies):
         raw = torch.empty(nmax * rec, dtype=torch.uint8, device=dev)

@@ -5,7 +5,7 @@ import numpy as np, torch
 import paper_2603_12485_b200 as hfz
 from paper_2603_12485_b200 import synth
 dev = torch.device("cuda", 0)
-for S, ns in ((65536, (256, 1024, 3072)), (262144, (256, 1024))):
+for S, ns in ((65536, (256, 1024, 4096)), (262144, (256, 1024))):
     ctx = hfz.Context(0, S)
     ctx.set_option("step_probe", 1)
     ctx.set_option("scan_two_stage", 1 << 40)

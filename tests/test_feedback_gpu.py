@@ -269,3 +269,32 @@ def test_pipelined_kernel_rows_and_teams(ctx, checker, row, n, scan_kernel):
         assert_same(run_gpu(ctx, raw, want_classed=False), run_cpu(checker, raw, n, want_classed=False))
     finally:
         ctx.set_option("scan_row", 0)
+
+
+def test_warp_fnv():
+    """The warp-parallel FNV-1a (csrc/hfz_fnv.cuh: bit-sliced low-byte chain + affine sum) equals the
+    byte-serial definition of trace_signature (src/coverage.cpp:89-97) on ordered entry lists of every
+    block-boundary length; the empty list gives the offset basis (tests/test_coverage.cpp:239-259)."""
+    import ctypes as C
+    from paper_2603_12485_b200 import _lib
+    lib = C.CDLL(_lib.LIB_PATH)
+    lib.hfz_dbg_warp_fnv.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p]
+    P, M = (1 << 40) + 0x1b3, (1 << 64) - 1
+
+    def serial(entries, full):
+        h = 0xcbf29ce484222325
+        for e in entries:
+            for b in ((e & 0xff, (e >> 8) & 0xff, 1 << (e >> 24)) if full else (e & 0xff, (e >> 8) & 0xff)):
+                h = ((h ^ b) * P) & M
+        return h
+
+    rng = np.random.default_rng(31)
+    for n in (0, 1, 2, 10, 11, 341, 342, 511, 512, 513, 682, 683, 1023, 1024, 1025, 1311, 2048, 2049, 5243):
+        slots = np.sort(rng.choice(1 << 18, n, replace=False)).astype(np.uint32) if n else np.zeros(0, np.uint32)
+        rung = rng.integers(0, 8, n).astype(np.uint32)
+        en = np.ascontiguousarray((slots & 0xFFFFFF) | (rung << 24), np.uint32)
+        out = np.zeros(2, np.uint64)
+        src = en if n else np.zeros(1, np.uint32)
+        assert lib.hfz_dbg_warp_fnv(src.ctypes.data, n, out.ctypes.data) == 0
+        assert int(out[0]) == serial(en.tolist(), True), n
+        assert int(out[1]) == serial(en.tolist(), False), n
