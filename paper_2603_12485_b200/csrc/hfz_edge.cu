@@ -1381,8 +1381,10 @@ __global__ void __launch_bounds__(kCountWarps * 32, 3) hfz_k_edge_count(const Fl
   __shared__ unsigned long long s_big_f[kBigCap];
   __shared__ uint32_t s_big_c[kBigCap];
   __shared__ uint32_t s_nbig;
-  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   __shared__ uint32_t s_wsum[kCountWarps];
+  __shared__ uint32_t s_used, s_full;  // dirty-slot table: rows taken / more distinct slots than it holds
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  static_assert(kHashCap * 8 == kCountSlots * 4, "the dirty-slot table and a pass's counters share the 64 KB");
   for (uint64_t e = p.e_lo + blockIdx.x; e < p.e_hi; e += gridDim.x) {
     if (!p.elig[e]) continue;  // the per-exec kernel writes this record
     const uint64_t q0 = p.exec_sw0[e] - p.q_lo, q1 = p.exec_sw0[e + 1] - p.q_lo;
@@ -1400,19 +1402,13 @@ __global__ void __launch_bounds__(kCountWarps * 32, 3) hfz_k_edge_count(const Fl
     for (int i = 0; i < kCountWarps; ++i) bound += s_wsum[i];
     const bool packed = bound < 65536u;
     const uint32_t R = packed ? (p.H < 2 * kCountSlots ? p.H : 2 * kCountSlots) : (p.H < kCountSlots ? p.H : kCountSlots);
-    auto add = [&](uint32_t rel) {
-      if (packed) atomicAdd(hist + (rel >> 1), 1u << ((rel & 1u) * 16u));
-      else bump(hist + rel);
-    };
-    for (uint32_t r0 = 0; r0 < p.H; r0 += R) {
-      const uint32_t n = p.H - r0 < R ? p.H - r0 : R;
-      uint4* z = reinterpret_cast<uint4*>(hist);
-      for (uint32_t i = threadIdx.x; i < (packed ? n / 8 : n / 4); i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
-      if (threadIdx.x == 0) s_nbig = 0;
-      __syncthreads();
-      // a warp takes 32 consecutive simulated warps: the coherent ones' lines are 32 independent coalesced
-      // loads (no load depends on another); the listed ones (divergent warps) are set aside and then dealt
-      // out over ALL warps of the CTA (they sit unevenly in the queue, and the CTA waits for its slowest warp)
+
+    // One walk over the exec's bump lists; add(slot relative to r0) for the slots of [r0, r0 + n).
+    // A warp takes 32 consecutive simulated warps: the coherent ones' lines are 4 KB contiguous -- eight
+    // 128-bit loads per lane, all in flight at once (lane L, load k: line 4k + L / 8, elements
+    // 4 (L % 8) .. + 3); the listed ones (divergent warps) are set aside and then dealt out over ALL
+    // warps of the CTA (they sit unevenly in the queue, and the CTA waits for its slowest warp).
+    auto walk = [&](uint32_t r0, uint32_t n, auto&& add) {
       for (uint64_t qb = q0 + (uint64_t)w * 32; qb < q1; qb += kCountWarps * 32) {
         const uint64_t q = qb + lane;
         const uint32_t cnt = q < q1 ? p.rec_cnt[q] : 0u;
@@ -1428,8 +1424,6 @@ __global__ void __launch_bounds__(kCountWarps * 32, 3) hfz_k_edge_count(const Fl
             seg = false;
           }
         }
-        // the group's 32 lines = 4 KB contiguous: eight 128-bit loads per lane, all in flight at once
-        // (lane L, load k: line 4k + L / 8, elements 4 (L % 8) .. + 3)
         uint4 v[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) v[k] = lines4[k * 32];
@@ -1458,19 +1452,76 @@ __global__ void __launch_bounds__(kCountWarps * 32, 3) hfz_k_edge_count(const Fl
         }
       }
       __syncthreads();
-      {
-        const uint32_t nb = s_nbig < kBigCap ? s_nbig : kBigCap;
-        for (uint32_t b = w; b < nb; b += kCountWarps) {
-          const uint32_t cc = s_big_c[b];
-          const uint32_t* list = p.scratch + s_big_f[b];
+      const uint32_t nb = s_nbig < kBigCap ? s_nbig : kBigCap;
+      for (uint32_t b = w; b < nb; b += kCountWarps) {
+        const uint32_t cc = s_big_c[b];
+        const uint32_t* list = p.scratch + s_big_f[b];
 #pragma unroll 12
-          for (uint32_t i = lane; i < cc; i += 32) {
-            const uint32_t rel = list[i] - r0;
-            if (rel < n) add(rel);
-          }
+        for (uint32_t i = lane; i < cc; i += 32) {
+          const uint32_t rel = list[i] - r0;
+          if (rel < n) add(rel);
         }
       }
       __syncthreads();
+    };
+
+    bool done = false;
+    if (p.H > R) {
+      // The device half needs more than one pass of counters (the 262,144-slot map: four), and every pass
+      // walks the lists again.  An exec touches a few thousand distinct slots, so first try ONE walk into
+      // a dirty-slot table (slot -> saturating u32 count, open addressing, the reference's own dirty list
+      // of src/hdvm.cpp:356-366): the record is zero-filled with fire-and-forget stores under the walk and
+      // the dirty slots are scattered over it afterwards.  More distinct slots than the table holds:
+      // the passes below redo the exec.
+      uint32_t* keys = hist;
+      uint32_t* counts = hist + kHashCap;
+      for (uint32_t i = threadIdx.x; i < kHashCap; i += blockDim.x) {
+        keys[i] = kHashEmpty;
+        counts[i] = 0;
+      }
+      if (threadIdx.x == 0) {
+        s_nbig = 0;
+        s_used = 0;
+        s_full = 0;
+      }
+      uint4* zg = reinterpret_cast<uint4*>(ghist);
+      for (uint32_t i = threadIdx.x; i < p.H / 4; i += blockDim.x) zg[i] = make_uint4(0, 0, 0, 0);
+      __syncthreads();
+      walk(0u, p.H, [&](uint32_t slot) {
+        if (*reinterpret_cast<volatile uint32_t*>(&s_full)) return;
+        uint32_t r = (slot * 0x9e3779b1u) >> (32 - kHashBits);
+        for (;;) {
+          const uint32_t cur = reinterpret_cast<volatile uint32_t*>(keys)[r];
+          if (cur == slot) break;
+          if (cur == kHashEmpty) {
+            const uint32_t old = atomicCAS(keys + r, kHashEmpty, slot);
+            if (old == kHashEmpty) {
+              if (atomicAdd(&s_used, 1u) >= kHashLimit) s_full = 1u;
+              break;
+            }
+            if (old == slot) break;
+          }
+          r = (r + 1) & (kHashCap - 1);
+        }
+        bump(counts + r);
+      });
+      if (!s_full) {  // (walk() ended on a barrier: the zero fill is ordered before the scatter)
+        for (uint32_t i = threadIdx.x; i < kHashCap; i += blockDim.x) {
+          const uint32_t k = keys[i];
+          if (k != kHashEmpty) ghist[k] = counts[i];
+        }
+        done = true;
+      }
+      __syncthreads();
+    }
+    for (uint32_t r0 = 0; r0 < p.H && !done; r0 += R) {
+      const uint32_t n = p.H - r0 < R ? p.H - r0 : R;
+      uint4* z = reinterpret_cast<uint4*>(hist);
+      for (uint32_t i = threadIdx.x; i < (packed ? n / 8 : n / 4); i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+      if (threadIdx.x == 0) s_nbig = 0;
+      __syncthreads();
+      if (packed) walk(r0, n, [&](uint32_t rel) { atomicAdd(hist + (rel >> 1), 1u << ((rel & 1u) * 16u)); });
+      else walk(r0, n, [&](uint32_t rel) { bump(hist + rel); });
       uint4* dst = reinterpret_cast<uint4*>(ghist + r0);
       if (packed) {
         const uint2* z2 = reinterpret_cast<const uint2*>(hist);

@@ -264,6 +264,28 @@ def test_large_map_262144_edges(port, edge_path):
         c2.close()
 
 
+def test_large_map_many_distinct_slots(port, edge_path):
+    """262,144-slot map, execs that touch more distinct slots than the count kernel's dirty-slot table
+    holds (6,144): the exec is redone in counter passes; next to execs that stay in the table."""
+    S2 = 262144
+    c2 = hfz.Context(0, S2)
+    c2.set_option("edge_flat", 1 if edge_path == "flat" else 0)
+    try:
+        rng = np.random.default_rng(29)
+        execs = []
+        for ex in range(4):
+            dims = np.array([[4, 1, 1, 64, 1, 1]], np.uint32)
+            ev, sites = [0], []
+            for t in range(256):
+                n = 60 if ex % 2 == 0 else 3
+                sites.extend(rng.integers(0, 2 ** 32, n, dtype=np.uint64).tolist())
+                ev.append(len(sites))
+            execs.append((dims, ev, sites))
+        check(c2, port, pack(execs), len(execs), S_=S2)
+    finally:
+        c2.close()
+
+
 def test_host_edge_record(ctx, port):
     rng = np.random.default_rng(13)
     seqs = [rng.integers(0, H, int(rng.integers(0, 4000)), dtype=np.uint64).astype(np.uint16) for _ in range(20)]
