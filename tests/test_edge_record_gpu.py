@@ -251,6 +251,30 @@ def test_flat_path_mixed_batch(ctx, port):
     check(ctx, port, pack(execs), len(execs))
 
 
+def test_flat_path_corner_batches(ctx, port):
+    """Batches the flat queue has nothing to do for: no launch at all; every exec left to the per-exec
+    kernel (differing geometries); threads without events only; an exec larger than the scratch cap."""
+    none = [(np.zeros((0, 6), np.uint32), [0], []) for _ in range(3)]
+    check(ctx, port, pack(none), 3)
+    mixed = []
+    for g in range(5):
+        d = np.array([[1, 1, 1, 8 + g, 1, 1], [2, 1, 1, 4, 2, 1]], np.uint32)
+        ev, sites = [0], []
+        for t in range(8 + g + 16):
+            sites.extend([3 + (t % 3), 9, 3 + (t % 3)])
+            ev.append(len(sites))
+        mixed.append((d, ev, sites))
+    check(ctx, port, pack(mixed), len(mixed))
+    idle = [(np.array([[2, 1, 1, 70, 1, 1]] * 3, np.uint32), np.zeros(421, np.uint64), [])]
+    check(ctx, port, pack(idle), 1)
+    ctx.set_option("edge_scratch_mb", 1)
+    try:
+        big = chain((256, 1, 1), [[5, 6, 7, 5] * 10] * 4, grid=(8, 1, 1))   # 327,680 events > 262,144
+        check(ctx, port, pack([big, chain((40, 1, 1), [[1, 2]]), big]), 3)
+    finally:
+        ctx.set_option("edge_scratch_mb", 2048)
+
+
 def test_large_map_262144_edges(port, edge_path):
     """262,144-slot map: the 131,072 device counters do not fit shared memory at once -> the count kernel
     takes them in ranges (flat path) / hashed dirty-slot table (per-exec kernel)."""
