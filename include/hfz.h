@@ -104,6 +104,13 @@ HFZ_API int hfz_ctx_get_stat(hfz_ctx* ctx, const char* key, double* out);
  *   admit_out         device, n_exec x u8 Admit codes, exactly the sequential ones
  *   sig_full_out / sig_simple_out   device, n_exec x u64
  *   nnz_out           device, n_exec x u32 (ClassedTrace::nonzero.size()) or NULL
+ *
+ * Context-owned scratch (grown geometrically, kept): 32 x S bytes of first-occurrence table (two of
+ * them once a small batch has been folded), 150 bytes per exec of the largest batch seen, and -- for
+ * batches of up to 8,192 execs, which are folded by one cooperative launch over ordered slot lists --
+ * n_exec x S x 4 bytes of list address space of which only the used prefix of each 4 KB piece's range
+ * is ever touched (2 GB at 8,192 execs of 65,536 slots; option "scan_two_stage" = 0 turns that path
+ * off, any other value is its batch-size limit).
  */
 HFZ_API int hfz_feedback_batch(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec,
                                uint8_t* virgin_inout, uint64_t* edge_counts_inout,
@@ -241,6 +248,14 @@ HFZ_API int hfz_feedback_resolve_allgather(hfz_ctx* ctx, void* nccl_comm, const 
  *   raw_maps    device, n_exec records; the DEVICE HALF of each is overwritten with the
  *               saturating warp counters (host half untouched)
  *   warp_events_out device, n_exec x u64 (ExecutionReport::warp_edge_events) or NULL
+ *
+ * The call reads a few batch sizes back once (it synchronises the stream before its main launches).
+ * Context-owned scratch, grown on demand and kept: 4 bytes per trace event of a chunk of execs (the
+ * bump lists; option "edge_scratch_mb", default 2048, bounds it by cutting the batch into chunks of
+ * whole execs -- one exec larger than the bound still gets what it needs) + 144 bytes per simulated
+ * warp of the chunk + 29 bytes per launch / exec of the batch.  Option "edge_flat" = 0 sends every
+ * exec through the per-exec kernel (which execs whose launches differ in geometry always take);
+ * its only scratch is 4 bytes per simulated thread of the largest launch per SM.
  */
 HFZ_API int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, const uint32_t* dims,
                                   const uint64_t* thread_off, const uint64_t* ev_off,
