@@ -1181,7 +1181,7 @@ __global__ void __launch_bounds__(kClassifyWarps * 32, 2) hfz_k_edge_classify(co
     // i + 1 are in flight, and once they have landed its events are pulled into L2
     bool have_next = false;
     uint64_t nx_e0 = 0, nx_e1 = 0, nx_pa = 0, nx_pb = 0;  // (nx_pa / nx_pb / nx_ps: lane 0 only)
-    uint32_t nx_ps = 0;
+    uint32_t nx_ps = 0, nx_bl = 0, nx_wi = 0;
     for (uint64_t qi = qb; qi < qe; ++qi) {
       const uint64_t q = p.q_lo + qi;
       if (q < c.sw0 || q >= c.sw1) {
@@ -1191,12 +1191,15 @@ __global__ void __launch_bounds__(kClassifyWarps * 32, 2) hfz_k_edge_classify(co
       const uint32_t tpb = c.tpb, wpb = c.wpb;
       const uint32_t sw = (uint32_t)(q - c.sw0);
       const uint32_t lq = (uint32_t)(c.l - c.l0);  // launch within its exec: every earlier one has this geometry
-      const uint32_t bl = sw / wpb, tl = (sw - bl * wpb) * 32 + lane;
+      const bool piped = have_next;
+      // block and warp within the block: carried over from the look-ahead of the item before (no division)
+      const uint32_t bl = piped ? nx_bl : sw / wpb;
+      const uint32_t wi = piped ? nx_wi : sw - bl * wpb;
+      const uint32_t tl = wi * 32 + lane;
       const bool active = tl < tpb;
       const uint64_t j = (uint64_t)bl * tpb + tl;  // thread within its launch
       uint64_t e0 = 0, e1 = 0, pa = 0, pb = 0;
       uint32_t ps = 0;  // the site that ends the lead lane's events one launch back
-      const bool piped = have_next;
       if (piped) {
         e0 = nx_e0;
         e1 = nx_e1;
@@ -1210,8 +1213,10 @@ __global__ void __launch_bounds__(kClassifyWarps * 32, 2) hfz_k_edge_classify(co
       have_next = qi + 1 < qe && q + 1 < c.sw1;
       bool nx_active = false;
       if (have_next) {
-        const uint32_t wi2 = sw + 1 - bl * wpb;  // warp within its block: the next warp, or the first one of the next block
-        const uint32_t bl2 = wi2 == wpb ? bl + 1 : bl, tl2 = (wi2 == wpb ? 0u : wi2) * 32 + lane;
+        const bool wrap = wi + 1 == wpb;  // the next warp of the block, or the first one of the next block
+        const uint32_t bl2 = wrap ? bl + 1 : bl, wi2 = wrap ? 0u : wi + 1, tl2 = wi2 * 32 + lane;
+        nx_bl = bl2;
+        nx_wi = wi2;
         nx_active = tl2 < tpb;
         nx_e0 = nx_e1 = 0;
         const uint64_t j2 = (uint64_t)bl2 * tpb + tl2;
