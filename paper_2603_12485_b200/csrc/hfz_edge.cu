@@ -1048,6 +1048,12 @@ constexpr uint32_t kSegFlag = 0x80000000u;  // rec_cnt: the bumps are a list in 
 __global__ void __launch_bounds__(256) hfz_k_edge_prep(const FlatParams p) {
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= p.n_exec; e += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t l0 = p.launch_off[e];
+    if (l0 > p.n_launch || (e < p.n_exec && (p.launch_off[e + 1] < l0 || p.launch_off[e + 1] > p.n_launch))) {
+      p.small[7] = 1;  // launch_off is not a CSR over n_launch launches: the host refuses the batch
+      p.exec_ev0[e] = 0;
+      if (e < p.n_exec) p.elig[e] = 1;
+      continue;
+    }
     p.exec_ev0[e] = p.n_launch ? p.ev_off[p.thread_off[l0]] : 0;
     if (e == p.n_exec) break;
     const uint64_t l1 = p.launch_off[e + 1];
@@ -1119,7 +1125,10 @@ __global__ void __launch_bounds__(1024, 1) hfz_k_edge_scan(const FlatParams p) {
     __syncthreads();
   }
   __syncthreads();  // (the CTA's own global writes are visible to it after the barrier)
-  for (uint64_t e = threadIdx.x; e <= p.n_exec; e += 1024) p.exec_sw0[e] = p.sw_off[p.launch_off[e]];
+  for (uint64_t e = threadIdx.x; e <= p.n_exec; e += 1024) {
+    const uint64_t l = p.launch_off[e];
+    p.exec_sw0[e] = p.sw_off[l <= p.n_launch ? l : p.n_launch];
+  }
 }
 
 // The launch a flat simulated-warp index belongs to, cached between consecutive items.
@@ -1731,7 +1740,7 @@ extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, c
   p.exec_sw0 = ctx->fl_exec_sw0;
   p.inelig = ctx->fl_inelig;
   p.small = ctx->d_small;
-  HFZ_CUDA(cudaMemsetAsync(ctx->d_small, 0, 5 * sizeof(unsigned long long), ctx->stream));
+  HFZ_CUDA(cudaMemsetAsync(ctx->d_small, 0, 8 * sizeof(unsigned long long), ctx->stream));
   {
     const uint64_t blocks = (n_exec + 1 + 255) / 256;
     hfz_k_edge_prep<<<(uint32_t)(blocks < 1024 ? blocks : 1024), 256, 0, ctx->stream>>>(p);
@@ -1739,12 +1748,23 @@ extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, c
     ctx->launches += 2;
     HFZ_CUDA(cudaGetLastError());
   }
-  unsigned long long h_small[5] = {0, 0, 0, 0, 0};
-  std::vector<uint64_t> h_ev0(n_exec + 1), h_sw0(n_exec + 1);
+  unsigned long long h_small[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  std::vector<uint64_t> h_ev0, h_sw0;
+  try {
+    h_ev0.resize(n_exec + 1);
+    h_sw0.resize(n_exec + 1);
+  } catch (...) {
+    hfz_set_error("hfz_edge_record_batch: host allocation failed");
+    return HFZ_ENOMEM;
+  }
   HFZ_CUDA(cudaMemcpyAsync(h_small, ctx->d_small, sizeof(h_small), cudaMemcpyDeviceToHost, ctx->stream));
   HFZ_CUDA(cudaMemcpyAsync(h_ev0.data(), ctx->fl_exec_ev0, (n_exec + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
   HFZ_CUDA(cudaMemcpyAsync(h_sw0.data(), ctx->fl_exec_sw0, (n_exec + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
   HFZ_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h_small[7]) {
+    hfz_set_error("hfz_edge_record_batch: launch_off is not a non-decreasing sequence within [0, n_launch]");
+    return HFZ_EINVAL;
+  }
   const uint64_t n_inelig = h_small[0];
   if (n_inelig) {  // execs whose launches differ in geometry (prev is launch-ordered there)
     const int rc = edge_record_per_exec(ctx, launch_off, dims, thread_off, ev_off, sites, n_inelig, ctx->fl_inelig,

@@ -275,6 +275,18 @@ def test_flat_path_corner_batches(ctx, port):
         ctx.set_option("edge_scratch_mb", 2048)
 
 
+def test_flat_path_refuses_bad_launch_offsets(ctx, edge_path):
+    """launch_off that is not a CSR over the launches given is refused (HFZ_EINVAL), not read past."""
+    if edge_path != "flat":
+        pytest.skip("flat path only")
+    tr = pack([chain((8, 1, 1), [[1, 2]]), chain((8, 1, 1), [[3]])])
+    tr["launch_off"] = np.array([0, 5, 2], np.uint64)
+    lo, dims, to, eo, sites = to_dev(ctx, tr)
+    with pytest.raises(Exception, match="launch_off"):
+        ctx.edge_record_batch(lo, dims, to, eo, sites, 2)
+    ctx.synchronize()
+
+
 def test_large_map_262144_edges(port, edge_path):
     """262,144-slot map: the 131,072 device counters do not fit shared memory at once -> the count kernel
     takes them in ranges (flat path) / hashed dirty-slot table (per-exec kernel)."""
