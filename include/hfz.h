@@ -144,7 +144,7 @@ HFZ_API int hfz_feedback_batch_host(hfz_ctx* ctx, const uint8_t* raw_maps_host, 
  *   entry_off  (n_exec+1) x u64, non-decreasing absolute indices into `entries` (entry_off[0] need
  *              not be 0: pass entry_off + k to fold execs k.. of a larger batch)
  * Outputs and in/out state exactly as hfz_feedback_batch: results are bit-identical to the
- * dense call on the maps the lists describe.  For S <= 65,536 the lists are folded directly
+ * dense call on the maps the lists describe.  For S <= 2^20 the lists are folded directly
  * (rank + chain kernels, option "sparse_native" = 1, the default; the device-buffer call reads
  * entry_off[n_exec] back once to size its scratch, i.e. it synchronises the stream before it
  * enqueues); otherwise, or with "sparse_native" = 0, they are expanded chunk by chunk into a
@@ -170,7 +170,7 @@ HFZ_API int hfz_feedback_batch_sparse_host(hfz_ctx* ctx, const uint32_t* entries
  * wide_off may be NULL when there are none).  Exec e owns compact[compact_off[e] ..
  * compact_off[e+1]) and wide[wide_off[e] .. wide_off[e+1]); a slot belongs in ONE of the two lists.
  * Everything else as hfz_feedback_batch_sparse_host; needs the list-native fold (HFZ_EINVAL when
- * map_slots > 65,536 or option "sparse_native" = 0). */
+ * map_slots > 2^20 or option "sparse_native" = 0). */
 HFZ_API int hfz_feedback_batch_compact_host(hfz_ctx* ctx, const uint32_t* compact_host,
                                             const uint64_t* compact_off_host, const uint32_t* wide_host,
                                             const uint64_t* wide_off_host, uint64_t n_exec,

@@ -814,7 +814,12 @@ __global__ void hfz_k_admit(const uint32_t* __restrict__ cand_list,
 //   chain  one lane per exec runs both FNV chains over its ordered list -- dense iterations, no
 //          row-synchronous max over lanes as in the dense kernels.
 // 65,536 execs (76 M pairs) take ~0.3 ms instead of ~10 ms through the dense staging buffer.
-constexpr int kRankWarps = 12;  // 12 x (8 KB bitmap + 4 KB prefix) + 64 KB virgin = 208 KB for S = 65,536
+constexpr int kRankWarps = 18;  // 18 x (8 KB bitmap + 4 KB prefix + padding) = 225 KB for S = 65,536; V0 is read through L1 / L2
+
+// shared memory of one warp of the rank kernel: padded bitmap, padded 16-bit prefix, lane bases + counter
+__host__ __device__ constexpr size_t rank_warp_bytes(uint32_t words) {
+  return ((size_t)(words + 32) * 4 + (size_t)(words + 64) * 2 + 256 + 15) / 16 * 16;
+}
 
 struct SparseParams {
   const uint2* pairs;       // wide pairs {slot, count}; may be null
@@ -842,29 +847,21 @@ __global__ void __launch_bounds__(kRankWarps * 32, 1) hfz_k_sparse_rank(const Sp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t words = p.S / 32, per = words / 32;  // bitmap words, words per lane in the prefix pass
   const uint32_t per_shift = 31 - __clz(per);         // S is a power of two >= 1024
-  uint8_t* s_virgin = smem;
-  uint32_t* bm = reinterpret_cast<uint32_t*>(smem + p.S + (size_t)warp * (words * 4 + words * 2 + 256));
-  uint16_t* pre = reinterpret_cast<uint16_t*>(bm + words);
-  uint32_t* lane_base = reinterpret_cast<uint32_t*>(pre + words);  // [32] + [1] novel counter
+  // (Round 1 staged V0 in shared memory by TMA: 64 KB that held the CTA at 12 warps, and the kernel's
+  // stalls are shared-memory round trips of the bitmap -- more warps hide them; V0's 64 KB stay hot in L2.)
+  // In the prefix pass lane l walks ITS words [l * per, (l + 1) * per): a lane stride of `per` words puts all 32
+  // lanes on one bank (91 % of the kernel's shared-memory wavefronts were conflicts of that pass).  One pad
+  // word per lane segment (two for the 16-bit prefix array) makes the stride odd: word w lives at
+  // w + (w >> per_shift), its prefix at w + 2 (w >> per_shift).
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem + (size_t)warp * rank_warp_bytes(words));
+  uint16_t* pre = reinterpret_cast<uint16_t*>(bm + words + 32);
+  uint32_t* lane_base = reinterpret_cast<uint32_t*>(pre + words + 64);  // [32] + [1] novel counter
   uint32_t* nov_cnt = lane_base + 32;
-  uint64_t* bar_virgin = reinterpret_cast<uint64_t*>(smem + p.S + (size_t)kRankWarps * (words * 4 + words * 2 + 256));
-  if (threadIdx.x == 0) {
-    hfz_mbar_init(bar_virgin, 1);
-    hfz_fence_barrier_init();
-  }
-  for (uint32_t i = lane; i < words; i += 32) bm[i] = 0;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const uint64_t pol = hfz_policy_evict_last();
-    hfz_mbar_expect_tx(bar_virgin, p.S);
-    for (uint32_t o = 0; o < p.S; o += 16384u) {
-      const uint32_t n = p.S - o < 16384u ? p.S - o : 16384u;
-      hfz_bulk_g2s_stream(s_virgin + o, p.v0 + o, n, bar_virgin, pol);
-    }
-  }
-  hfz_mbar_wait(bar_virgin, 0);
+  for (uint32_t i = lane; i < words + 32; i += 32) bm[i] = 0;
+  __syncwarp();
   uint32_t nbad = 0;
-  for (uint64_t e64 = (uint64_t)blockIdx.x * kRankWarps + warp; e64 < p.n_exec; e64 += (uint64_t)gridDim.x * kRankWarps) {
+  const uint32_t n_warps = blockDim.x >> 5;  // as many as the bitmaps leave room for (18 at 65,536 slots, 4 at 262,144)
+  for (uint64_t e64 = (uint64_t)blockIdx.x * n_warps + warp; e64 < p.n_exec; e64 += (uint64_t)gridDim.x * n_warps) {
     const uint32_t e = (uint32_t)e64;
     // exec e owns wide pairs [b, t) and compact pairs [cb, ct); its ordered list starts at b + cb
     const uint64_t b = p.off ? p.off[e64] : 0, t = p.off ? p.off[e64 + 1] : 0;
@@ -899,7 +896,8 @@ __global__ void __launch_bounds__(kRankWarps * 32, 1) hfz_k_sparse_rank(const Sp
       if (slot >= p.S) {
         ++nbad;
       } else if (c) {
-        atomicOr(&bm[slot >> 5], 1u << (slot & 31));
+        const uint32_t w = slot >> 5;
+        atomicOr(&bm[w + (w >> per_shift)], 1u << (slot & 31));
       }
     });
     __syncwarp();
@@ -907,8 +905,8 @@ __global__ void __launch_bounds__(kRankWarps * 32, 1) hfz_k_sparse_rank(const Sp
     uint32_t sum = 0;
     for (uint32_t k = 0; k < per; ++k) {
       const uint32_t w = lane * per + k;
-      pre[w] = (uint16_t)sum;
-      sum += __popc(bm[w]);
+      pre[w + 2 * lane] = (uint16_t)sum;
+      sum += __popc(bm[w + lane]);
     }
     uint32_t inc = sum;
 #pragma unroll
@@ -927,13 +925,13 @@ __global__ void __launch_bounds__(kRankWarps * 32, 1) hfz_k_sparse_rank(const Sp
       if (slot >= p.S) return;
       const uint32_t c = slot < p.H ? (cnt_raw & 0xffu) : cnt_raw;
       if (!c) return;
-      const uint32_t w = slot >> 5;
-      const uint32_t rank = lane_base[w >> per_shift] + pre[w] + __popc(bm[w] & ((1u << (slot & 31)) - 1u));
+      const uint32_t w = slot >> 5, seg = w >> per_shift;
+      const uint32_t rank = lane_base[seg] + pre[w + 2 * seg] + __popc(bm[w + seg] & ((1u << (slot & 31)) - 1u));
       const uint32_t klass = slot < p.H ? hfz_class_host(c) : hfz_class_device(c);
       const uint32_t rung = 31 - __clz(klass);
       const uint32_t en = slot | (rung << 24);
       out[rank] = en;
-      if (klass & ~(uint32_t)s_virgin[slot]) {
+      if (klass & ~(uint32_t)__ldg(p.v0 + slot)) {
         const uint32_t k = atomicAdd(nov_cnt, 1u);
         if (k < kNovMax) nov_row[k] = en;
         atomicMin(p.first + (size_t)slot * 8 + rung, e);
@@ -952,7 +950,7 @@ __global__ void __launch_bounds__(kRankWarps * 32, 1) hfz_k_sparse_rank(const Sp
         if (novel > kNovMax) p.slow_list[atomicAdd(p.cand_count + 1, 1u)] = ci;
       }
     }
-    for (uint32_t i = lane; i < words / 4; i += 32) reinterpret_cast<uint4*>(bm)[i] = make_uint4(0, 0, 0, 0);
+    for (uint32_t i = lane; i < (words + 32) / 4; i += 32) reinterpret_cast<uint4*>(bm)[i] = make_uint4(0, 0, 0, 0);
     __syncwarp();
   }
   nbad = __reduce_add_sync(0xffffffffu, nbad);
@@ -2140,8 +2138,8 @@ extern "C" int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t
 }
 
 bool hfz_sparse_native_ok(const hfz_ctx* c) {
-  // bitmap + prefix per warp and the virgin copy must fit shared memory
-  return c->sparse_native && c->S <= 65536u && c->S >= 1024u;
+  // one warp's bitmap + prefix (6 bytes per 32 slots) must fit shared memory: maps of up to 2^20 slots
+  return c->sparse_native && c->S <= (1u << 20) && c->S >= 1024u;
 }
 
 int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t* entry_off,
@@ -2196,11 +2194,18 @@ int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t
     p.classed = classed_out;
     p.bad = bad_pairs;
     const uint32_t words = ctx->S / 32;
-    const size_t smem = (size_t)ctx->S + (size_t)kRankWarps * (words * 4 + words * 2 + 256) + 16;
+    const size_t per_warp = rank_warp_bytes(words);
+    uint64_t rank_warps = (uint64_t)ctx->max_smem_optin / per_warp;
+    if (rank_warps > (uint64_t)kRankWarps) rank_warps = kRankWarps;
+    if (rank_warps == 0) {
+      hfz_set_error("sparse fold: a %u-slot bitmap does not fit shared memory", ctx->S);
+      return HFZ_EINVAL;
+    }
+    const size_t smem = (size_t)rank_warps * per_warp;
     HFZ_CUDA(cudaFuncSetAttribute(hfz_k_sparse_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    uint64_t grid = (n_exec + kRankWarps - 1) / kRankWarps;
+    uint64_t grid = (n_exec + rank_warps - 1) / rank_warps;
     if (grid > (uint64_t)ctx->num_sms) grid = (uint64_t)ctx->num_sms;
-    hfz_k_sparse_rank<<<(uint32_t)grid, kRankWarps * 32, smem, ctx->stream>>>(p);
+    hfz_k_sparse_rank<<<(uint32_t)grid, (uint32_t)rank_warps * 32, smem, ctx->stream>>>(p);
     ++ctx->launches;
     HFZ_CUDA(cudaGetLastError());
     hfz_k_sparse_chain<<<(uint32_t)((n_exec + 127) / 128), 128, 0, ctx->stream>>>(

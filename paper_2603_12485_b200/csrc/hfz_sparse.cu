@@ -225,8 +225,8 @@ int sparse_host_impl(hfz_ctx* c, const uint32_t* entries, const uint64_t* entry_
   rc = hfz_ensure_host_common(c, n_exec);
   if (rc) return rc;
   const bool native = hfz_sparse_native_ok(c);
-  if (compact_off && !native) {
-    hfz_set_error("%s: compact lists need the list-native fold (map_slots <= 65536, sparse_native = 1)", who);
+  if (compact_off && (!native || c->S > 65536u)) {
+    hfz_set_error("%s: compact lists need the list-native fold and a 16-bit slot (map_slots <= 65536, sparse_native = 1)", who);
     return HFZ_EINVAL;
   }
   uint64_t C;

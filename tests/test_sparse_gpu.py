@@ -162,14 +162,16 @@ def test_sparse_subrange_folds_equal_one_fold(sctx, checker):
     assert np.array_equal(v, wv) and np.array_equal(c, wc)
 
 
-def test_sparse_large_map():
-    """262,144-slot map (BASELINE.json configs[2])."""
+@pytest.mark.parametrize("S2,native,n", [(262144, 1, 48), (262144, 0, 48), (1 << 20, 1, 5)])
+def test_sparse_large_map(S2, native, n):
+    """262,144-slot map (BASELINE.json configs[2]) through the list-native kernels (4 warps per CTA:
+    a 32 KB bitmap each) and through the dense-staging fallback; 2^20 slots, the largest map whose
+    bitmap fits one warp's shared memory."""
     from oracle import pyoracle
-    S2 = 262144
     checker_large = pyoracle.best_checker(S2)
     c2 = hfz.Context(0, S2)
+    c2.set_option("sparse_native", native)
     try:
-        n = 48
         raw = synth.maps_iid(n, S2, seed=31)
         entries, off = synth.to_sparse(raw, n, S2, shuffle_seed=4)
         v = np.zeros(S2, np.uint8)
