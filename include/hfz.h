@@ -262,6 +262,25 @@ HFZ_API int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, cons
                                   const uint32_t* sites, uint64_t n_exec, uint64_t n_launch,
                                   uint8_t* raw_maps, uint64_t* warp_events_out);
 
+/* Edge record straight into touched-slot lists: the device half never has to exist as a dense record
+ * between K1 and K2.  As hfz_edge_record_batch, plus per exec a list of (logical slot, count) pairs --
+ * the form hfz_feedback_batch_sparse folds (logical slot = map_slots / 2 + device slot: the device half is
+ * the upper half of the map, coverage.hpp:13-15,88-91) -- at a fixed stride:
+ *   entries_out   device, n_exec x entry_cap x 2 x u32; exec e's pairs are the first n_slots_out[e] of
+ *                 [e * entry_cap, (e + 1) * entry_cap), in no particular order, the rest {0, 0} (padding the
+ *                 fold ignores), so entry_off[e] = e * entry_cap describes the batch
+ *   entry_cap     pairs per exec; the counting kernel's dirty-slot table holds 6,144 distinct slots
+ *   n_slots_out   device, n_exec x u32: distinct device slots of the exec, or 0xffffffff when the exec is NOT
+ *                 listed (more distinct slots than entry_cap or than the table holds, or launches of differing
+ *                 geometry): its list is all padding and the caller takes the dense record for it
+ *   raw_maps      as above, or NULL: lists only (nothing dense is written; warp_events_out as above)
+ * Needs option "edge_flat" = 1 (the default). */
+HFZ_API int hfz_edge_record_batch_lists(hfz_ctx* ctx, const uint64_t* launch_off, const uint32_t* dims,
+                                        const uint64_t* thread_off, const uint64_t* ev_off,
+                                        const uint32_t* sites, uint64_t n_exec, uint64_t n_launch,
+                                        uint8_t* raw_maps, uint64_t* warp_events_out, uint32_t* entries_out,
+                                        uint32_t entry_cap, uint32_t* n_slots_out);
+
 /* Host edge record: host_edge_update + CoverageMap::host_increment
  * (coverage.hpp:24-32,79-84) for batched u16 host site traces.
  *   site_off device (n_exec+1) x u64; sites device u16; fills the HOST HALF. */

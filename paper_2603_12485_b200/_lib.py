@@ -45,6 +45,7 @@ PROTOTYPES = {
     "hfz_virgin_merge": (C.c_int, [_vp, _vp, _vp, _vp, _u32]),
     "hfz_feedback_resolve_allgather": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _u32, _u32, _vp]),
     "hfz_edge_record_batch": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _u64, _u64, _vp, _vp]),
+    "hfz_edge_record_batch_lists": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _u64, _u64, _vp, _vp, _vp, _u32, _vp]),
     "hfz_host_edge_record_batch": (C.c_int, [_vp, _vp, _vp, _u64, _vp]),
     "hfz_havoc_max_out": (_u64, [_u64]),
     "hfz_havoc_batch": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp]),

@@ -290,6 +290,30 @@ class Context:
                                         _ptr(ev)))
         return raw, ev
 
+    def edge_record_batch_lists(self, launch_off, dims, thread_off, ev_off, sites, n_exec, cap=6144, raw=None,
+                                want_events=True, out=None):
+        """Device basic-block traces -> per-exec touched-slot lists at a fixed stride of `cap` pairs (the
+        form feedback_batch_sparse folds; entry_off = arange(n_exec + 1) * cap), optionally the dense
+        records too (`raw`).  Returns (entries (n_exec * cap, 2) int32, n_slots int32 [-1 = not listed],
+        entry_off int64, warp_edge_events)."""
+        for t in (launch_off, thread_off, ev_off):
+            _dev(t, self.device, torch.int64)
+        _dev(dims, self.device, torch.int32)
+        _dev(sites, self.device, torch.int32)
+        o = out or {}
+        if "entries" not in o:
+            o["entries"] = torch.empty((n_exec * cap, 2), dtype=torch.int32, device=self.device)
+            o["n_slots"] = torch.empty(n_exec, dtype=torch.int32, device=self.device)
+            o["entry_off"] = torch.arange(n_exec + 1, dtype=torch.int64, device=self.device) * cap
+            o["events"] = torch.empty(n_exec, dtype=torch.int64, device=self.device) if want_events else None
+        n_launch = thread_off.numel() - 1
+        self._sync_stream()
+        check(lib.hfz_edge_record_batch_lists(self._h, _ptr(launch_off), _ptr(dims), _ptr(thread_off), _ptr(ev_off),
+                                              _ptr(sites), n_exec, n_launch, _ptr(raw) if raw is not None else None,
+                                              _ptr(o["events"]) if o["events"] is not None else None,
+                                              _ptr(o["entries"]), cap, _ptr(o["n_slots"])))
+        return o
+
     def host_edge_record_batch(self, site_off, sites, n_exec, raw=None):
         _dev(site_off, self.device, torch.int64)
         _dev(sites, self.device, torch.int16)

@@ -1041,6 +1041,11 @@ struct FlatParams {
   uint32_t* rec_cnt;    // [q_hi - q_lo] its bumps; | kSegFlag: listed in scratch, else in its line
   uint32_t* div_list;   // [q_hi - q_lo] simulated warps (chunk-relative) that need a site table; small[5] of them
   uint32_t* lines;      // [q_hi - q_lo][32] a coherent warp's bump slots: one 128-byte line per simulated warp
+  // list output (hfz_edge_record_batch_lists): per exec list_cap (logical slot, count) pairs, zero-filled by
+  // the host call before the kernels run; list_n[e] = the exec's distinct slots or ~0u (not listed)
+  uint2* list_out;
+  uint32_t list_cap;
+  uint32_t* list_n;
 };
 constexpr uint32_t kSegFlag = 0x80000000u;  // rec_cnt: the bumps are a list in scratch (rec_first), not a line
 
@@ -1397,12 +1402,13 @@ __global__ void __launch_bounds__(kCountWarps * 32, 3) hfz_k_edge_count(const Fl
   __shared__ uint32_t s_nbig;
   __shared__ uint32_t s_wsum[kCountWarps];
   __shared__ uint32_t s_used, s_full;  // dirty-slot table: rows taken / more distinct slots than it holds
+  __shared__ uint32_t s_cursor;        // list output: pairs written
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   static_assert(kHashCap * 8 == kCountSlots * 4, "the dirty-slot table and a pass's counters share the 64 KB");
   for (uint64_t e = p.e_lo + blockIdx.x; e < p.e_hi; e += gridDim.x) {
     if (!p.elig[e]) continue;  // the per-exec kernel writes this record
     const uint64_t q0 = p.exec_sw0[e] - p.q_lo, q1 = p.exec_sw0[e + 1] - p.q_lo;
-    uint32_t* ghist = reinterpret_cast<uint32_t*>(p.raw + e * p.rec_bytes + p.H);
+    uint32_t* ghist = p.raw ? reinterpret_cast<uint32_t*>(p.raw + e * p.rec_bytes + p.H) : nullptr;
     // the exec's bumps in all: fewer than 65,536 (the rule) cannot overflow a 16-bit counter, so two
     // counters share a word and a pass covers twice the slots (the whole device half of a 65,536-slot map)
     unsigned long long total = 0;
@@ -1480,7 +1486,7 @@ __global__ void __launch_bounds__(kCountWarps * 32, 3) hfz_k_edge_count(const Fl
     };
 
     bool done = false;
-    if (p.H > R) {
+    if (p.H > R || p.list_out) {
       // The device half needs more than one pass of counters (the 262,144-slot map: four), and every pass
       // walks the lists again.  An exec touches a few thousand distinct slots, so first try ONE walk into
       // a dirty-slot table (slot -> saturating u32 count, open addressing, the reference's own dirty list
@@ -1497,9 +1503,11 @@ __global__ void __launch_bounds__(kCountWarps * 32, 3) hfz_k_edge_count(const Fl
         s_nbig = 0;
         s_used = 0;
         s_full = 0;
+        s_cursor = 0;
       }
       uint4* zg = reinterpret_cast<uint4*>(ghist);
-      for (uint32_t i = threadIdx.x; i < p.H / 4; i += blockDim.x) zg[i] = make_uint4(0, 0, 0, 0);
+      if (ghist)
+        for (uint32_t i = threadIdx.x; i < p.H / 4; i += blockDim.x) zg[i] = make_uint4(0, 0, 0, 0);
       __syncthreads();
       walk(0u, p.H, [&](uint32_t slot) {
         if (*reinterpret_cast<volatile uint32_t*>(&s_full)) return;
@@ -1519,13 +1527,23 @@ __global__ void __launch_bounds__(kCountWarps * 32, 3) hfz_k_edge_count(const Fl
         }
         bump(counts + r);
       });
+      const bool listed = p.list_out && !s_full && s_used <= p.list_cap;
       if (!s_full) {  // (walk() ended on a barrier: the zero fill is ordered before the scatter)
+        uint2* lst = listed ? p.list_out + e * p.list_cap : nullptr;
         for (uint32_t i = threadIdx.x; i < kHashCap; i += blockDim.x) {
           const uint32_t k = keys[i];
-          if (k != kHashEmpty) ghist[k] = counts[i];
+          if (k != kHashEmpty) {
+            const uint32_t cnt = counts[i];
+            if (ghist) ghist[k] = cnt;
+            // the exec's touched-slot list, LOGICAL slot indices (device half = upper half of the map), any
+            // order: what hfz_feedback_batch_sparse folds without a dense record
+            if (lst) lst[atomicAdd(&s_cursor, 1u)] = make_uint2(p.H + k, cnt);
+          }
         }
         done = true;
       }
+      if (p.list_n && threadIdx.x == 0) p.list_n[e] = listed ? s_used : 0xffffffffu;
+      if (!ghist) done = true;  // lists only: an exec that does not fit its list is reported, not counted densely
       __syncthreads();
     }
     for (uint32_t r0 = 0; r0 < p.H && !done; r0 += R) {
@@ -1684,17 +1702,28 @@ static bool edge_grow(T** buf, uint64_t* cap, uint64_t want) {
   return true;
 }
 
-extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, const uint32_t* dims,
-                                     const uint64_t* thread_off, const uint64_t* ev_off,
-                                     const uint32_t* sites, uint64_t n_exec, uint64_t n_launch,
-                                     uint8_t* raw_maps, uint64_t* warp_events_out) {
-  if (!ctx || (n_exec && (!launch_off || !raw_maps)) ||
-      (n_launch && (!dims || !thread_off || !ev_off))) {
+// lists: entries_out != NULL -> also (or, with raw_maps == NULL, only) the touched-slot list of every exec
+static int edge_record_impl(hfz_ctx* ctx, const uint64_t* launch_off, const uint32_t* dims,
+                            const uint64_t* thread_off, const uint64_t* ev_off, const uint32_t* sites, uint64_t n_exec,
+                            uint64_t n_launch, uint8_t* raw_maps, uint64_t* warp_events_out, uint32_t* entries_out,
+                            uint32_t entry_cap, uint32_t* n_slots_out) {
+  const bool lists = entries_out != nullptr;
+  if (!ctx || (n_exec && (!launch_off || (!raw_maps && !lists))) ||
+      (n_launch && (!dims || !thread_off || !ev_off)) || (lists && (!n_slots_out || entry_cap == 0))) {
     hfz_set_error("hfz_edge_record_batch: null argument");
     return HFZ_EINVAL;
   }
   if (n_exec == 0) return HFZ_OK;
   HFZ_CUDA(cudaSetDevice(ctx->device));
+  if (lists) {
+    if (!ctx->edge_flat) {
+      hfz_set_error("hfz_edge_record_batch_lists: needs the flat path (option edge_flat = 1)");
+      return HFZ_EINVAL;
+    }
+    // every list starts all-zero ({0, 0} pairs are padding: count 0 = unvisited) and not listed
+    HFZ_CUDA(cudaMemsetAsync(entries_out, 0, (size_t)n_exec * entry_cap * 8, ctx->stream));
+    HFZ_CUDA(cudaMemsetAsync(n_slots_out, 0xff, (size_t)n_exec * 4, ctx->stream));
+  }
   if (n_exec >= (1ull << 32) || n_launch >= (1ull << 32)) {
     hfz_set_error("hfz_edge_record_batch: more than 2^32 - 1 execs or launches in one call");
     return HFZ_EINVAL;
@@ -1766,7 +1795,7 @@ extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, c
     return HFZ_EINVAL;
   }
   const uint64_t n_inelig = h_small[0];
-  if (n_inelig) {  // execs whose launches differ in geometry (prev is launch-ordered there)
+  if (n_inelig && raw_maps) {  // execs whose launches differ in geometry (prev is launch-ordered there)
     const int rc = edge_record_per_exec(ctx, launch_off, dims, thread_off, ev_off, sites, n_inelig, ctx->fl_inelig,
                                         h_small[1], raw_maps, warp_events_out);
     if (rc != HFZ_OK) return rc;
@@ -1801,6 +1830,9 @@ extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, c
     p.rec_cnt = ctx->fl_rec_cnt;
     p.div_list = ctx->fl_div;
     p.lines = ctx->fl_lines;
+    p.list_out = reinterpret_cast<uint2*>(entries_out);
+    p.list_cap = entry_cap;
+    p.list_n = n_slots_out;
     if (n_items) {
       HFZ_CUDA(cudaMemsetAsync(ctx->d_small + 2, 0, 5 * sizeof(unsigned long long), ctx->stream));  // pop counters, divergent count
       const uint64_t want = (n_items + kPop * kClassifyWarps - 1) / (kPop * kClassifyWarps);
@@ -1819,6 +1851,31 @@ extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, c
     e_lo = e_hi;
   }
   return HFZ_OK;
+}
+
+extern "C" int hfz_edge_record_batch(hfz_ctx* ctx, const uint64_t* launch_off, const uint32_t* dims,
+                                     const uint64_t* thread_off, const uint64_t* ev_off,
+                                     const uint32_t* sites, uint64_t n_exec, uint64_t n_launch,
+                                     uint8_t* raw_maps, uint64_t* warp_events_out) {
+  if (n_exec && !raw_maps) {
+    hfz_set_error("hfz_edge_record_batch: null argument");
+    return HFZ_EINVAL;
+  }
+  return edge_record_impl(ctx, launch_off, dims, thread_off, ev_off, sites, n_exec, n_launch, raw_maps, warp_events_out,
+                          nullptr, 0, nullptr);
+}
+
+extern "C" int hfz_edge_record_batch_lists(hfz_ctx* ctx, const uint64_t* launch_off, const uint32_t* dims,
+                                           const uint64_t* thread_off, const uint64_t* ev_off,
+                                           const uint32_t* sites, uint64_t n_exec, uint64_t n_launch,
+                                           uint8_t* raw_maps, uint64_t* warp_events_out, uint32_t* entries_out,
+                                           uint32_t entry_cap, uint32_t* n_slots_out) {
+  if (n_exec && (!entries_out || !n_slots_out || entry_cap == 0)) {
+    hfz_set_error("hfz_edge_record_batch_lists: null argument");
+    return HFZ_EINVAL;
+  }
+  return edge_record_impl(ctx, launch_off, dims, thread_off, ev_off, sites, n_exec, n_launch, raw_maps, warp_events_out,
+                          entries_out, entry_cap, n_slots_out);
 }
 
 extern "C" int hfz_host_edge_record_batch(hfz_ctx* ctx, const uint64_t* site_off,

@@ -322,6 +322,63 @@ def test_large_map_many_distinct_slots(port, edge_path):
         c2.close()
 
 
+@pytest.mark.parametrize("S_", [65536, 262144])
+def test_lists_output_chains_into_the_sparse_fold(port, edge_path, S_):
+    """hfz_edge_record_batch_lists: the lists describe exactly the device halves the dense call writes
+    (slot for slot, count for count; logical indices), an exec with more distinct slots than the list holds
+    is reported as not listed, and folding the lists (hfz_feedback_batch_sparse, entry_off = e * cap) gives
+    the Admit codes, signatures, virgin map and counters of folding the dense records."""
+    if edge_path != "flat":
+        pytest.skip("flat path only")
+    c = hfz.Context(0, S_)
+    H_ = S_ // 2
+    try:
+        rng = np.random.default_rng(37)
+        tr = synth.bb_traces(24, seed=33, grid=(4, 1, 1), block=(96, 1, 1), n_launch=3)
+        lo, dims, to, eo, sites = to_dev(c, tr)
+        raw, ev = c.edge_record_batch(lo, dims, to, eo, sites, 24)
+        raw2 = torch.zeros_like(raw)
+        o = c.edge_record_batch_lists(lo, dims, to, eo, sites, 24, cap=4096, raw=raw2)
+        c.synchronize()
+        assert torch.equal(raw, raw2) and torch.equal(ev, o["events"])
+        want_raw, want_ev = port.edge_record_batch(tr["launch_off"], tr["dims"], tr["thread_off"], tr["ev_off"], tr["sites"], 24, S_)
+        assert np.array_equal(raw.cpu().numpy(), want_raw)
+        ent = o["entries"].cpu().numpy().view(np.uint32).reshape(24, 4096, 2)
+        ns = o["n_slots"].cpu().numpy()
+        dev = raw.cpu().numpy().reshape(24, synth.record_bytes(S_))[:, H_:].view(np.uint32)
+        for e in range(24):
+            assert ns[e] == np.count_nonzero(dev[e]), e
+            got = {int(s): int(k) for s, k in ent[e, :ns[e]]}
+            assert len(got) == ns[e] and not ent[e, ns[e]:].any()
+            nz = np.nonzero(dev[e])[0]
+            assert got == {int(H_ + s): int(dev[e][s]) for s in nz}
+        # lists only (no dense record), then the list fold against the dense fold
+        o2 = c.edge_record_batch_lists(lo, dims, to, eo, sites, 24, cap=4096)
+        v1, c1 = c.new_virgin(), c.new_edge_counts()
+        v2, c2 = c.new_virgin(), c.new_edge_counts()
+        a = c.feedback_batch(raw, v1, c1)
+        b = c.feedback_batch_sparse(o2["entries"], o2["entry_off"], v2, c2)
+        c.synchronize()
+        for k in ("admit", "sig_full", "sig_simple", "nnz"):
+            assert torch.equal(a[k], b[k]), k
+        assert torch.equal(v1, v2) and torch.equal(c1, c2)
+        # an exec with more distinct slots than the list holds: reported, its list stays padding
+        dims1 = np.array([[4, 1, 1, 64, 1, 1]], np.uint32)
+        evs, ss = [0], []
+        for t in range(256):
+            ss.extend(rng.integers(0, 2 ** 32, 30, dtype=np.uint64).tolist())
+            evs.append(len(ss))
+        tr2 = pack([(dims1, evs, ss), chain((16, 1, 1), [[1, 2, 3]])])
+        lo, dims, to, eo, sites = to_dev(c, tr2)
+        o3 = c.edge_record_batch_lists(lo, dims, to, eo, sites, 2, cap=4096)
+        c.synchronize()
+        ns3 = o3["n_slots"].cpu().numpy()
+        assert ns3[0] == -1 and ns3[1] > 0
+        assert not o3["entries"].cpu().numpy().reshape(2, 4096, 2)[0].any()
+    finally:
+        c.close()
+
+
 def test_host_edge_record(ctx, port):
     rng = np.random.default_rng(13)
     seqs = [rng.integers(0, H, int(rng.integers(0, 4000)), dtype=np.uint64).astype(np.uint16) for _ in range(20)]
