@@ -678,6 +678,44 @@ def bench_edge_and_large_map(hfz, dev, timer, peak, peak_src, args, threads):
                              f"warp_edge_events from K1, then Admit codes, both signatures, nnz, final virgin and edge counters from K2 on those maps",
            "l2_policy": f"{n2 * REC_LARGE / 1e6:.0f} MB of maps and {events * 4 / 1e6 * n2 / n1:.0f} MB of traces per step exceed L2"}
     big["frac"] = big["fold"]["roofline"]["frac"]
+    # ---- the same chain WITHOUT dense records in between: K1 writes per-exec touched-slot lists
+    # (hfz_edge_record_batch_lists, raw_maps = NULL), K2 folds the lists (hfz_feedback_batch_sparse).
+    # Checked against the dense chain above on every exec (which the reference pins on the first n_par).
+    cap = 4096  # pairs per exec (the recipe touches ~2,100 distinct device slots per exec; an exec that did not fit would be reported)
+    res["L"] = None
+
+    def run_k1_lists():
+        res["L"] = c2.edge_record_batch_lists(d2["launch_off"], d2["dims"], d2["thread_off"], d2["ev_off"], d2["sites"], n2,
+                                              cap=cap, out=res["L"])
+
+    run_k1_lists()
+    res["g"] = None
+
+    def run_fold_lists():
+        res["g"] = c2.feedback_batch_sparse(res["L"]["entries"], res["L"]["entry_off"], v2, cc2, out=res["g"])
+
+    pre_cold()
+    run_fold()
+    v_dense, c_dense = v2.clone(), cc2.clone()
+    pre_cold()
+    run_fold_lists()
+    torch.cuda.synchronize()
+    listed = int((res["L"]["n_slots"] >= 0).sum().item())
+    same = (listed == n2 and torch.equal(res["L"]["events"], res["l"][1])
+            and all(torch.equal(res["f"][k], res["g"][k]) for k in ("admit", "sig_full", "sig_simple", "nnz"))
+            and torch.equal(v2, v_dense) and torch.equal(cc2, c_dense))
+    if not same:
+        fail("configs[2] list chain (K1 lists -> sparse fold) differs from the dense chain")
+    t_k1s = timer.run(run_k1_lists, 10)
+    t_k2s = timer.run(run_fold_lists, 10, pre=pre_cold)
+    ms_lists = t_k1s["mean"] + t_k2s["mean"]
+    big["lists_chain"] = {
+        "what": "the same K1 -> K2 chain with per-exec touched-slot lists between the stages instead of dense 655,360-byte "
+                "records: hfz_edge_record_batch_lists (raw_maps = NULL) -> hfz_feedback_batch_sparse",
+        "value": n2 / (ms_lists / 1e3), "unit": "execs/s", "ms_per_step": ms_lists,
+        "edge_record_ms": t_k1s["mean"], "fold_ms": t_k2s["mean"], "list_stride_pairs": cap,
+        "mean_slots_per_exec": float(res["L"]["n_slots"].float().mean().item()),
+        "parity_checked": f"all {n2} execs: warp_edge_events, Admit codes, both signatures, nnz, final virgin and edge counters equal the dense chain's"}
     c2.close()
     return k1, big
 

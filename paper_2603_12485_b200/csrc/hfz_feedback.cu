@@ -1004,6 +1004,42 @@ __global__ void __launch_bounds__(128) hfz_k_sparse_chain(const uint32_t* __rest
   if (nnz_out) nnz_out[e] = n;
 }
 
+// The same for SMALL batches (at most one exec per resident warp): one WARP per exec, both chains by the
+// warp-parallel FNV of hfz_fnv.cuh over rounds of 1,024 entries staged in shared memory.  A lane
+// running an exec's chains alone needs ~100 cycles per entry (2,110 entries of a 262,144-slot map:
+// 0.24 ms however few execs there are); the warp needs ~850 instructions per 1,024 steps.
+constexpr uint32_t kChainRoundSp = 1024;
+constexpr int kChainWarps = 4;
+__global__ void __launch_bounds__(kChainWarps * 32) hfz_k_sparse_chain_warp(const uint32_t* __restrict__ sorted,
+                                                                            const uint64_t* __restrict__ off,
+                                                                            const uint64_t* __restrict__ coff,
+                                                                            const uint32_t* __restrict__ cnt, uint64_t n_exec,
+                                                                            uint64_t* __restrict__ sig_full,
+                                                                            uint64_t* __restrict__ sig_simple,
+                                                                            uint32_t* __restrict__ nnz_out) {
+  __shared__ __align__(16) uint32_t s_buf[kChainWarps][kChainRoundSp];
+  __shared__ __align__(16) uint8_t s_stream[kChainWarps][3072 + 16];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t e = (uint64_t)blockIdx.x * kChainWarps + warp;
+  if (e >= n_exec) return;
+  const uint32_t* list = sorted + (off ? off[e] : 0) + (coff ? coff[e] : 0);
+  const uint32_t n = cnt[e];
+  uint64_t hf = HFZ_FNV_OFFSET, hs = HFZ_FNV_OFFSET;
+  for (uint32_t i0 = 0; i0 < n; i0 += kChainRoundSp) {
+    const uint32_t m = n - i0 < kChainRoundSp ? n - i0 : kChainRoundSp;
+    for (uint32_t i = lane; i < m; i += 32) s_buf[warp][i] = __ldg(list + i0 + i);
+    __syncwarp();
+    hf = pfnv::chain_entries<3>(hf, s_buf[warp], m, s_stream[warp], lane);
+    hs = pfnv::chain_entries<2>(hs, s_buf[warp], m, s_stream[warp], lane);
+    __syncwarp();
+  }
+  if (lane == 0) {
+    sig_full[e] = hf;
+    sig_simple[e] = hs;
+    if (nnz_out) nnz_out[e] = n;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Two-stage scan of DENSE records for small and medium batches ("compact + chain").
 //   compact  work item = (map, 16 KB piece of its record), one warp each: the piece is streamed
@@ -2208,8 +2244,12 @@ int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t
     hfz_k_sparse_rank<<<(uint32_t)grid, (uint32_t)rank_warps * 32, smem, ctx->stream>>>(p);
     ++ctx->launches;
     HFZ_CUDA(cudaGetLastError());
-    hfz_k_sparse_chain<<<(uint32_t)((n_exec + 127) / 128), 128, 0, ctx->stream>>>(
-        ctx->sp_sorted, entry_off, compact_off, ctx->sp_cnt, n_exec, sig_full_out, sig_simple_out, nnz_out);
+    if (n_exec <= (uint64_t)ctx->num_sms * 32)  // latency regime: a warp per exec (one wave)
+      hfz_k_sparse_chain_warp<<<(uint32_t)((n_exec + kChainWarps - 1) / kChainWarps), kChainWarps * 32, 0, ctx->stream>>>(
+          ctx->sp_sorted, entry_off, compact_off, ctx->sp_cnt, n_exec, sig_full_out, sig_simple_out, nnz_out);
+    else
+      hfz_k_sparse_chain<<<(uint32_t)((n_exec + 127) / 128), 128, 0, ctx->stream>>>(
+          ctx->sp_sorted, entry_off, compact_off, ctx->sp_cnt, n_exec, sig_full_out, sig_simple_out, nnz_out);
     ++ctx->launches;
     HFZ_CUDA(cudaGetLastError());
   }
