@@ -99,7 +99,30 @@ def soak_edge(seeds, port):
                                                    tr["sites"], len(execs), S)
         assert np.array_equal(ev.cpu().numpy().view(np.uint64), want_ev), seed
         assert np.array_equal(raw.cpu().numpy(), want_raw), seed
+        # the list output of the same batch: every listed exec's pairs are its device half, the others
+        # (launches of differing geometry, too many distinct slots) are reported as not listed
+        cap = int(rng.choice([64, 700, 4096]))
+        o = ctx.edge_record_batch_lists(i64(tr["launch_off"]),
+                                        torch.from_numpy(np.ascontiguousarray(tr["dims"], np.uint32).view(np.int32)).to(ctx.device),
+                                        i64(tr["thread_off"]), i64(tr["ev_off"]),
+                                        torch.from_numpy(sites.view(np.int32)).to(ctx.device), len(execs), cap=cap)
+        ctx.synchronize()
+        ent = o["entries"].cpu().numpy().view(np.uint32).reshape(len(execs), cap, 2)
+        ns = o["n_slots"].cpu().numpy()
+        dev = want_raw.reshape(len(execs), synth.record_bytes(S))[:, S // 2:].view(np.uint32)
+        listed = 0
+        for e in range(len(execs)):
+            nz = np.nonzero(dev[e])[0]
+            if ns[e] < 0:
+                assert not ent[e].any(), (seed, e)
+                continue
+            listed += 1
+            assert ns[e] == nz.size and nz.size <= cap, (seed, e)
+            got = {int(a): int(b) for a, b in ent[e, :ns[e]]}
+            assert got == {int(S // 2 + k): int(dev[e][k]) for k in nz} and not ent[e, ns[e]:].any(), (seed, e)
+        n_listed_total = listed if seed == 0 else n_listed_total + listed
     ctx.close()
+    print(f"edge record lists: {n_listed_total} of {seeds * 24} execs listed, all equal to their dense halves", flush=True)
     print(f"edge record: {seeds} random batches of 24 execs ok in {time.time() - t:.0f} s", flush=True)
 
 
