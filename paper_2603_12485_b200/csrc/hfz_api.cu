@@ -82,6 +82,7 @@ extern "C" int hfz_ctx_destroy(hfz_ctx* c) {
   cudaFree(c->first);
   cudaFree(c->cand_list);
   cudaFree(c->cand_count);
+  cudaFree(c->admit_flags);
   cudaFree(c->prior);
   cudaFree(c->delta);
   cudaFree(c->v0);

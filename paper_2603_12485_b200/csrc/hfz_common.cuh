@@ -31,6 +31,8 @@ struct hfz_ctx {
   uint32_t* cand_list = nullptr;  // candidate exec indices (unordered)
   uint64_t cand_cap = 0;
   uint32_t* cand_count = nullptr;  // [1]
+  uint32_t* admit_flags = nullptr; // [admit_cap] per-exec novelty flags of the table resolve (1 = NewCounts, 2 = NewEdges); zero between calls
+  uint64_t admit_cap = 0;
   uint8_t* prior = nullptr;        // [S] P_r = V0 | OR_{q<r} D_q
   uint8_t* delta = nullptr;        // [S] this rank's delta (hfz_feedback_batch)
   uint8_t* v0 = nullptr;           // [S] batch-start snapshot

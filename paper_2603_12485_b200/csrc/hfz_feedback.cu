@@ -730,6 +730,51 @@ __device__ __forceinline__ uint32_t resolve_entry(const ResolveParams& p, uint32
   return 1;
 }
 
+// K2b, table form: the Admit codes of ALL execs straight from the first-occurrence table -- no candidate is
+// walked, no map or list is read again.  Entry (slot, bit) = e names the first exec of the batch that shows
+// class bit `bit` on `slot`, recorded only when the bit is not in V0.  With P = the virgin map before this
+// rank's first exec (V0 | the deltas of the ranks before it):
+//   bit in P[slot]                       -> an earlier rank had it: nothing;
+//   P[slot] == 0 and e == min over bits  -> exec e is the first ever on the slot: NewEdges (2);
+//   otherwise                            -> exec e adds a class to a known slot: NewCounts (1);
+// and Admit[e] is the maximum over the entries that name e (has_new_bits, src/coverage.cpp:74-87: the result is
+// the max over the map's slots).  One thread per slot: 32 bytes of table + 1 byte of P each (2 MB for the
+// 64 KB map, L2-resident: the scan has just written it), whatever the number of candidate execs -- a batch
+// folded into an empty virgin map costs what a warm one does.
+// Flags are ORed into a per-exec u32 (context scratch, zero between calls); hfz_k_admit_codes turns them into
+// the Admit bytes and re-zeroes them.
+__device__ __forceinline__ void resolve_slot(const uint4 a, const uint4 b, uint32_t pr, uint32_t* __restrict__ flags) {
+  if ((a.x & a.y & a.z & a.w & b.x & b.y & b.z & b.w) == kNone) return;  // no exec showed anything new here
+  const uint32_t lo = min(min(min(a.x, a.y), min(a.z, a.w)), min(min(b.x, b.y), min(b.z, b.w)));
+  const uint32_t ent[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int bit = 0; bit < 8; ++bit) {
+    const uint32_t e = ent[bit];
+    if (e == kNone || ((pr >> bit) & 1u)) continue;
+    const uint32_t code = (pr == 0 && e == lo) ? 2u : 1u;
+    const uint32_t cur = __ldcg(flags + e);  // an exec that opens many slots: one atomic, then reads
+    if (!(cur & (2u | code))) atomicOr(flags + e, code);
+  }
+}
+
+__global__ void __launch_bounds__(256) hfz_k_resolve_table(const uint32_t* __restrict__ first,
+                                                           const uint8_t* __restrict__ prior, uint32_t S,
+                                                           uint32_t* __restrict__ flags) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  const uint4* f = reinterpret_cast<const uint4*>(first + (size_t)s * 8);
+  resolve_slot(__ldcg(f), __ldcg(f + 1), __ldg(prior + s), flags);
+}
+
+__global__ void __launch_bounds__(256) hfz_k_admit_codes(uint32_t* __restrict__ flags, uint8_t* __restrict__ admit,
+                                                         uint64_t n_exec) {
+  const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_exec) return;
+  const uint32_t f = flags[e];
+  admit[e] = (f & 2u) ? 2 : (uint8_t)(f & 1u);
+  if (f) flags[e] = 0;
+}
+
 constexpr uint32_t kPiece = 16384;  // bytes per work item (divides H and 4H for S >= 32768... checked on host)
 
 __global__ void __launch_bounds__(256) hfz_k_resolve(const ResolveParams p, uint32_t piece) {
@@ -1264,6 +1309,7 @@ struct StepParams {
   const uint8_t* deltas;     // n_ranks x S (== delta_out when fused)
   uint32_t n_ranks, rank;
   uint8_t* admit;
+  uint32_t* flags;           // per-exec novelty flags of the table resolve (zero on entry, zero again on exit)
   int do_scan, do_resolve;
   unsigned long long* dbg;   // optional: [8] latest %globaltimer at each phase boundary (dev probe)
 };
@@ -1559,17 +1605,20 @@ __global__ void __launch_bounds__(kStepWarps * 32, 1) hfz_k_small_step(const Ste
         const uint64_t t = role * 32 + lane;  // word index, < S / 4
         const uint4* f = reinterpret_cast<const uint4*>(c.first + t * 32);
         uint32_t d = 0;
+        uint32_t* vw = reinterpret_cast<uint32_t*>(p.virgin) + t;
+        const uint32_t old = fused ? *vw : 0u;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const uint4 a = __ldcg(f + 2 * q), b = __ldcg(f + 2 * q + 1);
           const uint32_t byte = (a.x != kNone) | ((a.y != kNone) << 1) | ((a.z != kNone) << 2) | ((a.w != kNone) << 3) |
                                 ((b.x != kNone) << 4) | ((b.y != kNone) << 5) | ((b.z != kNone) << 6) | ((b.w != kNone) << 7);
           d |= byte << (8 * q);
+          // fused (single rank): P = the virgin map as it stood -- the Admit flags of the slot right here
+          if (fused) resolve_slot(a, b, (old >> (8 * q)) & 0xffu, p.flags);
         }
         reinterpret_cast<uint32_t*>(p.delta_out)[t] = d;
         if (fused) {
-          uint32_t* vw = reinterpret_cast<uint32_t*>(p.virgin) + t;
-          const uint32_t old = *vw, nw = old | d;
+          const uint32_t nw = old | d;
           reinterpret_cast<uint32_t*>(p.prior)[t] = old;
           if (nw != old) *vw = nw;
           const uint32_t turned = __popc(nz_bytes(nw) & ~nz_bytes(old));
@@ -1591,7 +1640,6 @@ __global__ void __launch_bounds__(kStepWarps * 32, 1) hfz_k_small_step(const Ste
             c.nov_cnt[e] = 0;
           }
         }
-        if (fused && e < c.n_exec && !novel) p.admit[e] = 0;
       } else {
         // signatures: ONE map per warp, the whole warp on its two chains (hfz_fnv.cuh).  The warp gathers the
         // map's ordered piece lists into shared memory (cp.async; one piece per lane, every copy in flight
@@ -1705,38 +1753,22 @@ __global__ void __launch_bounds__(kStepWarps * 32, 1) hfz_k_small_step(const Ste
       if (newh) atomicAdd(p.edge_counts + 0, (unsigned long long)newh);
       if (newd) atomicAdd(p.edge_counts + 1, (unsigned long long)newd);
     }
-    for (uint64_t e = gthread; e < c.n_exec; e += nthreads) p.admit[e] = 0;
+    __threadfence();
+    grid.sync();
+    // the table against P_r (just written above), one thread per slot
+    for (uint64_t s = gthread; s < c.S; s += nthreads) {
+      const uint4* f = reinterpret_cast<const uint4*>(c.first + s * 8);
+      resolve_slot(__ldcg(f), __ldcg(f + 1), __ldcg(p.prior + s), p.flags);
+    }
     __threadfence();
     grid.sync();
   }
 
-  // ---- phase 3: one warp per candidate
-  ResolveParams r;
-  r.S = c.S;
-  r.H = c.H;
-  r.prior = p.prior;
-  r.first = c.first;
-  const uint32_t n_cand = __ldcg(p.cand_count);
-  for (uint64_t ci = gw; ci < n_cand; ci += W) {
-    const uint32_t e = __ldcg(p.cand_list + ci), nov = __ldcg(p.cand_nov + ci);
-    uint32_t flags = 0;
-    if (nov <= kNovMax) {
-      if (lane < nov) {
-        const uint32_t en = __ldcg(c.novel_ent + (size_t)e * kNovMax + lane);
-        flags = resolve_entry(r, en & 0xffffffu, 1u << (en >> 24), e);
-      }
-    } else {  // more novel slots than were recorded: walk the map's ordered piece lists
-      for (uint32_t pc = 0; pc < c.pieces; ++pc) {
-        const uint32_t* list = c.sorted + (uint64_t)e * c.S + piece_slot0(c, pc);
-        const uint32_t n = __ldcg(c.cnt + (uint64_t)e * c.pieces + pc);
-        for (uint32_t i = lane; i < n; i += 32) {
-          const uint32_t en = __ldcg(list + i);
-          flags |= resolve_entry(r, en & 0xffffffu, 1u << (en >> 24), e);
-        }
-      }
-    }
-    flags = __reduce_or_sync(0xffffffffu, flags);
-    if (lane == 0) p.admit[e] = (flags & 2u) ? 2 : ((flags & 1u) ? 1 : 0);
+  // ---- phase 3: flags -> Admit codes (and the flags back to zero for the next call)
+  for (uint64_t e = gthread; e < c.n_exec; e += nthreads) {
+    const uint32_t f = __ldcg(p.flags + e);
+    p.admit[e] = (f & 2u) ? 2 : (uint8_t)(f & 1u);
+    if (f) p.flags[e] = 0;
   }
   dbg_mark(p, 6);
 }
@@ -1991,6 +2023,7 @@ int small_step_scan(hfz_ctx* ctx, const uint8_t* raw, uint64_t n_exec, const uin
   p.n_ranks = 1;
   p.rank = 0;
   p.admit = admit;
+  p.flags = ctx->admit_flags;
   p.do_scan = 1;
   p.do_resolve = virgin_inout != nullptr;
   p.dbg = ctx->ss_dbg ? ctx->d_small + 8 : nullptr;
@@ -2039,6 +2072,7 @@ int small_step_resolve(hfz_ctx* ctx, uint64_t n_exec, uint8_t* virgin_inout, uin
   p.n_ranks = n_ranks;
   p.rank = rank;
   p.admit = admit;
+  p.flags = ctx->admit_flags;
   p.do_scan = 0;
   p.do_resolve = 1;
   return launch_small_step(ctx, p);
@@ -2088,8 +2122,24 @@ int launch_scan(hfz_ctx* ctx, const ScanParams& p) {
   return vsmem ? launch_scan_r<0, true>(ctx, p, row) : launch_scan_r<0, false>(ctx, p, row);
 }
 
+// per-exec flags of the table resolve: zero between calls (hfz_k_admit_codes / the fused step re-zero what they read)
+int ensure_admit_flags(hfz_ctx* ctx, uint64_t n_exec) {
+  if (ctx->admit_cap >= n_exec) return HFZ_OK;
+  if (ctx->admit_flags) cudaFree(ctx->admit_flags);
+  ctx->admit_flags = nullptr;
+  ctx->admit_cap = 0;
+  const uint64_t cap = n_exec < 1024 ? 1024 : n_exec + n_exec / 4;
+  if (cudaMalloc(&ctx->admit_flags, cap * sizeof(uint32_t)) != cudaSuccess) {
+    hfz_set_error("cudaMalloc(admit flags, %llu) failed", (unsigned long long)cap * 4);
+    return HFZ_ENOMEM;
+  }
+  HFZ_CUDA(cudaMemsetAsync(ctx->admit_flags, 0, cap * sizeof(uint32_t), ctx->stream));
+  ctx->admit_cap = cap;
+  return HFZ_OK;
+}
+
 int ensure_cand(hfz_ctx* ctx, uint64_t n_exec) {
-  if (ctx->cand_cap >= n_exec) return HFZ_OK;
+  if (ctx->cand_cap >= n_exec) return ensure_admit_flags(ctx, n_exec);
   if (ctx->cand_list) cudaFree(ctx->cand_list);
   ctx->cand_list = nullptr;
   ctx->cand_cap = 0;
@@ -2099,7 +2149,7 @@ int ensure_cand(hfz_ctx* ctx, uint64_t n_exec) {
     return HFZ_ENOMEM;
   }
   ctx->cand_cap = cap;
-  return HFZ_OK;
+  return ensure_admit_flags(ctx, n_exec);
 }
 
 }  // namespace
@@ -2311,39 +2361,10 @@ int resolve_impl(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec, uint8_t
   ++ctx->launches;
   HFZ_CUDA(cudaGetLastError());
   if (n_exec) {
-    HFZ_CUDA(cudaMemsetAsync(admit_out, 0, n_exec, ctx->stream));
-    ResolveParams p;
-    p.raw = raw_maps;
-    p.rec_bytes = ctx->rec_bytes;
-    p.S = ctx->S;
-    p.H = ctx->H;
-    p.prior = ctx->prior;
-    p.first = ctx->first;
-    p.cand_list = ctx->cand_list;
-    p.cand_count = ctx->cand_count;
-    p.cand_flags = ctx->cand_list + ctx->cand_cap;
-    p.cand_nov = ctx->cand_list + 2 * ctx->cand_cap;
-    p.slow_list = ctx->cand_list + 3 * ctx->cand_cap;
-    p.novel_ent = ctx->cand_list + 4 * ctx->cand_cap;
-    p.admit = admit_out;
-    hfz_k_resolve_fast<<<(uint32_t)ctx->num_sms * 2, 256, 0, ctx->stream>>>(p);
+    hfz_k_resolve_table<<<(ctx->S + 255) / 256, 256, 0, ctx->stream>>>(ctx->first, ctx->prior, ctx->S, ctx->admit_flags);
     ++ctx->launches;
     HFZ_CUDA(cudaGetLastError());
-    if (ctx->sc_sparse) {
-      hfz_k_resolve_sparse<<<(uint32_t)ctx->num_sms * 4, 256, 0, ctx->stream>>>(p, ctx->sc_sorted, ctx->sc_off,
-                                                                                  ctx->sc_coff, ctx->sc_cnt);
-    } else if (ctx->sc_pieces) {
-      hfz_k_resolve_pieces<<<(uint32_t)ctx->num_sms * 4, 256, 0, ctx->stream>>>(
-          p, ctx->ts_sorted, ctx->ts_cnt, ctx->sc_piece, ctx->sc_host_pieces, ctx->sc_npieces);
-    } else {
-      uint32_t piece = kPiece;
-      while (ctx->H % piece) piece >>= 1;  // H is a power of two >= 512
-      hfz_k_resolve<<<(uint32_t)ctx->num_sms * 4, 256, 0, ctx->stream>>>(p, piece);
-    }
-    ++ctx->launches;
-    HFZ_CUDA(cudaGetLastError());
-    hfz_k_admit<<<(uint32_t)ctx->num_sms, 256, 0, ctx->stream>>>(ctx->cand_list, ctx->cand_count,
-                                                                  p.cand_flags, admit_out);
+    hfz_k_admit_codes<<<(uint32_t)((n_exec + 255) / 256), 256, 0, ctx->stream>>>(ctx->admit_flags, admit_out, n_exec);
     ++ctx->launches;
     HFZ_CUDA(cudaGetLastError());
   }
