@@ -13,6 +13,11 @@
 // oracle/_ref/libhetfuzz_ref.so (dlopen).  Every output of the two is compared: Admit codes in order,
 // both signatures, nnz, the final virgin map and both edge counters.
 //
+// A third leg, "streaming", is how a fuzzing loop actually meets the call: every worker thread owns ONE
+// CoverageMap, and after each execution (here: fill_map, untimed in every leg) it appends the still
+// cache-hot map to its batch and reset()s it for the next execution.  Timed: the append + reset calls
+// (summed per worker, maximum over workers) + the fold + the results back in host vectors.
+//
 // Prints one JSON object.  Test/bench infrastructure: the oracle is used as the checker and as the
 // timed CPU leg, never by the product path.
 #include <dlfcn.h>
@@ -225,6 +230,59 @@ int main(int argc, char** argv) {
   run_gpu(1, tot1, pack1, r1, v1);
   run_gpu(threads, totT, packT, rT, vT);
 
+  // ---- streaming leg: one reused map per worker, appended right after the execution that filled it
+  std::vector<double> totS, packS;
+  FeedbackResult rS;
+  VirginMap vS;
+  {
+    const unsigned T = threads;
+    std::vector<CompactBatch> batches(T);
+    for (std::uint64_t s = 0; s <= steps; ++s) {
+      VirginMap v = v0;
+      FeedbackResult all;
+      all.admit.resize(n);
+      all.sig_full.resize(n);
+      all.sig_simple.resize(n);
+      all.nnz.resize(n);
+      std::vector<double> worker_s(T, 0.0);
+      std::vector<std::thread> th;
+      for (unsigned t = 0; t < T; ++t)
+        th.emplace_back([&, t] {
+          CoverageMap m;  // this worker's map, as a fuzzing loop would hold it
+          batches[t].clear();
+          double acc = 0;
+          for (std::uint64_t e = n * t / T; e < n * (t + 1) / T; ++e) {
+            fill_map(prog, seed, e, m);  // the execution (untimed, as in the other legs)
+            const double a0 = now();
+            batches[t].append(m);
+            m.reset();
+            acc += now() - a0;
+          }
+          worker_s[t] = acc;
+        });
+      for (auto& x : th) x.join();
+      const double pack_s = *std::max_element(worker_s.begin(), worker_s.end());
+      const double t1 = now();
+      for (unsigned t = 0; t < T; ++t) {
+        const std::uint64_t first = n * t / T, cnt = n * (t + 1) / T - first;
+        if (!cnt) continue;
+        b200::check(hfz_feedback_batch_compact_host(ctx.get(), batches[t].compact(), batches[t].compact_offsets(),
+                                                    batches[t].wide(), batches[t].wide_offsets(), cnt, v.data(),
+                                                    v.edge_counts(), nullptr, all.admit.data() + first,
+                                                    all.sig_full.data() + first, all.sig_simple.data() + first,
+                                                    all.nnz.data() + first),
+                    "hfz_feedback_batch_compact_host");
+      }
+      const double fold_s = now() - t1;
+      if (s) {
+        totS.push_back(pack_s + fold_s);
+        packS.push_back(pack_s);
+      }
+      rS = std::move(all);
+      vS = v;
+    }
+  }
+
   // ---- reference leg: engine.cpp:471-478 over the same maps, one thread, in chunks of 2,048 maps
   RefLib ref;
   double ref_s = -1;
@@ -255,9 +313,9 @@ int main(int argc, char** argv) {
       ref_s += now() - t0;
       ref.maps_free(h);
     }
-    for (const FeedbackResult* r : {&r1, &rT})
+    for (const FeedbackResult* r : {&r1, &rT, &rS})
       equal = equal && r->admit == adm && r->sig_full == sf && r->sig_simple == ss && r->nnz == nz;
-    for (VirginMap* v : {&v1, &vT})
+    for (VirginMap* v : {&v1, &vT, &vS})
       equal = equal && std::memcmp(ref_v.data(), v->data(), kMapSize) == 0 && ref_c[0] == v->host_edges() &&
               ref_c[1] == v->device_edges();
   }
@@ -270,11 +328,13 @@ int main(int argc, char** argv) {
     for (double x : v) mean += x;
     mean /= v.size();
   };
-  double mn1, med1, mean1, pmn1, pmed1, pmean1, mnT, medT, meanT, pmnT, pmedT, pmeanT;
+  double mn1, med1, mean1, pmn1, pmed1, pmean1, mnT, medT, meanT, pmnT, pmedT, pmeanT, mnS, medS, meanS, pmnS, pmedS, pmeanS;
   stats(tot1, mn1, med1, mean1);
   stats(pack1, pmn1, pmed1, pmean1);
   stats(totT, mnT, medT, meanT);
   stats(packT, pmnT, pmedT, pmeanT);
+  stats(totS, mnS, medS, meanS);
+  stats(packS, pmnS, pmedS, pmeanS);
   std::uint64_t pairs = 0;
   for (const CoverageMap& m : maps) pairs += m.touched().size();
   std::printf(
@@ -284,12 +344,16 @@ int main(int argc, char** argv) {
       "\"seconds\": {\"mean\": %.6f, \"median\": %.6f, \"min\": %.6f, \"pack_mean\": %.6f, \"fold_and_readback_mean\": %.6f}, "
       "\"one_pack_thread\": {\"value\": %.1f, \"unit\": \"evals/s\", \"seconds\": {\"mean\": %.6f, \"median\": %.6f, \"min\": %.6f, "
       "\"pack_mean\": %.6f, \"fold_and_readback_mean\": %.6f}}, "
+      "\"streaming\": {\"value\": %.1f, \"unit\": \"evals/s\", \"pack_threads\": %u, \"seconds\": {\"mean\": %.6f, \"median\": %.6f, "
+      "\"min\": %.6f, \"pack_mean\": %.6f, \"fold_and_readback_mean\": %.6f}, \"what\": \"one reused CoverageMap per worker: append + reset() right "
+      "after the execution that filled it (cache-hot map); timed = append + reset summed per worker, max over workers, + fold + results\"}, "
       "\"reference_same_maps\": {\"available\": %s, \"threads\": 1, \"seconds\": %.4f, \"value\": %.1f, \"unit\": \"evals/s\", "
       "\"what\": \"classify_trace + 2 x trace_signature + has_new_bits per map (src/engine.cpp:471-478), unmodified reference build, same process\"}, "
       "\"equals_reference\": %s, \"compared\": \"all execs: Admit codes in order, both signatures, nnz; final virgin map; both edge counters; "
-      "for the 1-thread and the T-thread packing\"}\n",
+      "for the 1-thread, the T-thread and the streaming packing\"}\n",
       (unsigned long long)n, (unsigned long long)steps, double(pairs) / double(n), gen_s, double(n) / meanT, threads, meanT, medT, mnT,
-      pmeanT, meanT - pmeanT, double(n) / mean1, mean1, med1, mn1, pmean1, mean1 - pmean1, have_ref ? "true" : "false", ref_s,
+      pmeanT, meanT - pmeanT, double(n) / mean1, mean1, med1, mn1, pmean1, mean1 - pmean1, double(n) / meanS, threads, meanS, medS,
+      mnS, pmeanS, meanS - pmeanS, have_ref ? "true" : "false", ref_s,
       ref_s > 0 ? double(n) / ref_s : 0.0, have_ref ? (equal ? "true" : "false") : "null");
   return have_ref && !equal ? 1 : 0;
 }

@@ -15,7 +15,7 @@
  *     gives a thread-local message.  Nothing throws across the ABI.
  *   - all *device* pointers are caller-owned CUDA device memory on the
  *     context's device; the library never frees or reallocates them.  Scratch
- *     (first-occurrence table, candidate list, novelty delta) is owned by the
+ *     (first-occurrence table, per-exec Admit flags, novelty delta) is owned by the
  *     context.
  *   - work is enqueued on the context's stream and is asynchronous unless the
  *     function name ends in _host (those take HOST buffers and synchronise).
@@ -197,6 +197,9 @@ HFZ_API int hfz_host_free(void* p);
  *          P_r = V0 | OR_{q<r} D_q, then folds virgin_inout = V0 | OR_q D_q in
  *          fixed rank order and bumps the edge counters.  Identical on every
  *          rank and identical to the single-rank sequential oracle.
+ *          The codes come from the scan's first-occurrence table alone (one
+ *          thread per slot): raw_maps is not read again and may be NULL; the
+ *          parameter is kept for ABI stability.
  * With n_ranks == 1 and deltas == delta_out the pair equals hfz_feedback_batch.
  */
 HFZ_API int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec,

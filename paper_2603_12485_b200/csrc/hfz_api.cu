@@ -62,7 +62,6 @@ extern "C" int hfz_ctx_create(hfz_ctx** out, int device, uint32_t map_slots, voi
   c->num_sms = prop.multiProcessorCount;
   c->max_smem_optin = (int)prop.sharedMemPerBlockOptin;
   cudaError_t a = cudaMalloc(&c->first, (size_t)map_slots * 8 * sizeof(uint32_t));
-  if (a == cudaSuccess) a = cudaMalloc(&c->cand_count, 2 * sizeof(uint32_t));
   if (a == cudaSuccess) a = cudaMalloc(&c->prior, map_slots);
   if (a == cudaSuccess) a = cudaMalloc(&c->delta, map_slots);
   if (a == cudaSuccess) a = cudaMalloc(&c->v0, map_slots);
@@ -80,8 +79,6 @@ extern "C" int hfz_ctx_destroy(hfz_ctx* c) {
   if (!c) return HFZ_OK;
   cudaSetDevice(c->device);
   cudaFree(c->first);
-  cudaFree(c->cand_list);
-  cudaFree(c->cand_count);
   cudaFree(c->admit_flags);
   cudaFree(c->prior);
   cudaFree(c->delta);
@@ -130,8 +127,6 @@ extern "C" int hfz_ctx_destroy(hfz_ctx* c) {
   cudaFree(c->sp_cnt);
   cudaFree(c->ss_first[0]);
   cudaFree(c->ss_first[1]);
-  cudaFree(c->ss_counts);
-  cudaFree(c->ss_nov);
   cudaFree(c->ss_deltas);
   for (cudaEvent_t ev : c->sp_events) cudaEventDestroy(ev);
   delete c;

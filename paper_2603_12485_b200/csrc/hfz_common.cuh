@@ -28,9 +28,6 @@ struct hfz_ctx {
 
   // K2 scratch (owned)
   uint32_t* first = nullptr;      // [S * 8] first local exec index showing (slot, class bit); ~0u = none
-  uint32_t* cand_list = nullptr;  // candidate exec indices (unordered)
-  uint64_t cand_cap = 0;
-  uint32_t* cand_count = nullptr;  // [1]
   uint32_t* admit_flags = nullptr; // [admit_cap] per-exec novelty flags of the table resolve (1 = NewCounts, 2 = NewEdges); zero between calls
   uint64_t admit_cap = 0;
   uint8_t* prior = nullptr;        // [S] P_r = V0 | OR_{q<r} D_q
@@ -97,15 +94,6 @@ struct hfz_ctx {
   uint64_t sp_sorted_cap = 0;
   uint32_t* sp_cnt = nullptr;      // per exec: distinct non-zero slots
   uint64_t sp_cnt_cap = 0;
-  // set by the last scan: the resolve step re-reads a candidate either from its dense record or
-  // from its ordered list
-  bool sc_sparse = false;
-  bool sc_pieces = false;         // last scan was the two-stage dense path: resolve from its piece lists
-  uint32_t sc_piece = 0, sc_host_pieces = 0, sc_npieces = 0;
-  const uint32_t* sc_sorted = nullptr;
-  const uint64_t* sc_off = nullptr;
-  const uint64_t* sc_coff = nullptr;
-  const uint32_t* sc_cnt = nullptr;
 
   // tuning
   int scan_warps = 0;     // 0 = as many as fit
@@ -118,7 +106,7 @@ struct hfz_ctx {
   int64_t scan_two_stage = -1;  // batches of up to this many execs use compact + chain (-1 = auto, 0 = off)
   uint32_t* ts_sorted = nullptr;  // two-stage scratch: [n_exec][S] entries (only the used prefix of each piece is touched)
   uint64_t ts_sorted_cap = 0;     // entries
-  uint32_t* ts_cnt = nullptr;     // [n_exec][pieces] entries per piece, then [n_exec] novel-slot counters
+  uint32_t* ts_cnt = nullptr;     // [n_exec][pieces] entries per piece
   uint64_t ts_cnt_cap = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> scan_events;
 
@@ -126,10 +114,7 @@ struct hfz_ctx {
   int small_fused = 1;            // small dense batches: the whole fold as one cooperative launch
   int coop_grid = -1;             // co-resident grid of the fused step (-1 = not probed, 0 = unsupported)
   uint32_t* ss_first[2] = {nullptr, nullptr};  // double-buffered first-occurrence tables, all-ones between calls
-  int ss_pp = 0;                  // table / candidate counter the last call used
-  uint32_t* ss_counts = nullptr;  // [2] candidate counters, zero between calls
-  uint32_t* ss_nov = nullptr;     // [n_exec] novel-slot counters, zero between calls
-  uint64_t ss_nov_cap = 0;
+  int ss_pp = 0;                  // table the last call used
   uint8_t* ss_deltas = nullptr;   // staging for peer deltas (resolve_peers after a fused scan)
   int ss_dbg = 0;                 // dev probe: phase timestamps of the fused step in d_small[8..16)
   bool sc_small = false;          // last scan was the scan half of the fused step
@@ -141,7 +126,7 @@ int hfz_cuda_fail(cudaError_t e, const char* what);
 int hfz_ensure_host_common(hfz_ctx* c, uint64_t n_exec);   // hfz_api.cu
 int hfz_ensure_classed_stage(hfz_ctx* c, uint64_t execs);  // hfz_api.cu
 // hfz_feedback.cu: the scan half of the fold on touched-slot lists (device buffers); total_pairs =
-// entry_off[n_exec] (absolute).  Pair it with hfz_feedback_resolve(raw_maps = NULL).
+// entry_off[n_exec] (absolute).  Pair it with hfz_feedback_resolve, or (delta_out = NULL) hfz_feedback_fold_single.
 bool hfz_sparse_native_ok(const hfz_ctx* c);
 // pairs / entry_off = wide {slot, count} pairs, compact / compact_off = slot | count << 16 words;
 // either list may be absent (null); total_pairs = the sum of both lists' end offsets (absolute).
@@ -150,6 +135,9 @@ int hfz_feedback_scan_sparse(hfz_ctx* c, const uint32_t* pairs, const uint64_t* 
                              uint64_t total_pairs, const uint8_t* virgin_v0, uint8_t* classed_out,
                              uint64_t* sig_full_out, uint64_t* sig_simple_out, uint32_t* nnz_out,
                              uint8_t* delta_out, unsigned long long* bad_pairs);
+// single-rank second half after a scan with delta_out = NULL: delta + merge + Admit flags in one pass over the table
+int hfz_feedback_fold_single(hfz_ctx* ctx, uint64_t n_exec, uint8_t* virgin_inout, uint64_t* edge_counts_inout,
+                             uint8_t* admit_out);
 
 #define HFZ_CUDA(call)                                   \
   do {                                                   \

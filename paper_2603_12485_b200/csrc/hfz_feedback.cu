@@ -10,8 +10,8 @@
 //    back except 21 bytes per map.
 //  * exact sequential has_new_bits without a sequential pass: for every (slot, class bit) not
 //    in V0 the scan records the FIRST exec that shows it (atomicMin into `first`).  An exec's
-//    Admit code then only depends on whether it is that first exec (resolve kernel, runs on
-//    the few candidate maps only).  Final virgin = V0 | OR of the novelty deltas (merge).
+//    Admit code then only depends on which table entries name it (resolve: one pass over the
+//    table, whatever the number of novel maps).  Final virgin = V0 | OR of the novelty deltas (merge).
 #include <stdio.h>
 #include <string.h>
 
@@ -27,7 +27,6 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr uint32_t kNone = 0xffffffffu;
-constexpr uint32_t kNovMax = 32;  // novel entries kept per map (128 B of scratch each); more -> resolve re-reads the map
 constexpr int kPad = 16;  // per-lane slot padding: makes 128-bit shared loads conflict-free
 
 struct ScanParams {
@@ -37,12 +36,6 @@ struct ScanParams {
   uint64_t rec_bytes;
   const uint8_t* v0;
   uint32_t* first;
-  uint32_t* cand_list;
-  uint32_t* cand_count;  // [0] candidates, [1] candidates that need the map re-read
-  uint32_t* cand_flags;
-  uint32_t* cand_nov;    // novel entries recorded for candidate ci (kNovMax + 1 = re-read the map)
-  uint32_t* slow_list;   // candidate indices whose map must be re-read
-  uint32_t* novel_ent;   // [n_exec][kNovMax] idx | rung << 24 of the slots novel versus V0
   uint64_t* sig_full;
   uint64_t* sig_simple;
   uint32_t* nnz;
@@ -50,6 +43,14 @@ struct ScanParams {
   uint32_t n_groups;
   int prefetch;
 };
+
+// first-occurrence update: entry = min(entry, e).  Entries only ever decrease, so an L2 read
+// that already shows an exec <= e proves the atomic redundant -- on a batch folded into an empty virgin map
+// every non-zero slot of every map comes here (86 M updates of ~2.6 k entries for 65,536 maps), and a load is
+// cheaper in L2 than a reduction on a contended address.
+__device__ __forceinline__ void note_first(uint32_t* entry, uint32_t e) {
+  if (__ldcg(entry) > e) atomicMin(entry, e);
+}
 
 // non-zero-byte bitmask (4 bits) of a 32-bit word
 __device__ __forceinline__ uint32_t nz_bytes(uint32_t w) {
@@ -60,20 +61,18 @@ __device__ __forceinline__ uint32_t nz_bytes(uint32_t w) {
 template <bool VSMEM, bool CLASSED>
 struct Lane {
   uint64_t hf, hs;
-  uint32_t nnz, novel;
+  uint32_t nnz;
   // one non-zero slot: both FNV chains, novelty versus V0 (`known` = V0[idx]), optional class store
   __device__ __forceinline__ void visit(uint32_t idx, uint32_t klass, uint32_t known, uint32_t* first,
-                                        uint32_t e, uint8_t* classed_row, uint32_t* nov_row) {
+                                        uint32_t e, uint8_t* classed_row) {
     const uint32_t b0 = idx & 0xffu, b1 = (idx >> 8) & 0xffu;
     hf = hfz_fnv(hfz_fnv(hfz_fnv(hf, b0), b1), klass);
     hs = hfz_fnv(hfz_fnv(hs, b0), b1);
     ++nnz;
-    if (klass & ~known) {
-      const uint32_t rung = 31 - __clz(klass);
-      if (novel < kNovMax) nov_row[novel] = idx | (rung << 24);
-      ++novel;
-      atomicMin(first + (size_t)idx * 8 + rung, e);
-    }
+    // (rare once the virgin map is warm; hinted so: the block stays out of the chain loop's schedule -- measured
+    // 1.62 vs 1.68 ms per 65,536 maps.  A read-before-update as in note_first costs the serial loop more than it
+    // saves except on a batch folded into an EMPTY map: 1.86 vs 2.5 ms there, 1.06 vs 0.95 on iid maps.)
+    if (__builtin_expect((klass & ~known) != 0u, 0)) atomicMin(first + (size_t)idx * 8 + (31 - __clz(klass)), e);
     if (CLASSED) classed_row[idx] = (uint8_t)klass;
   }
 };
@@ -103,8 +102,7 @@ struct RowCfg {
 template <bool HOST, int ROW, bool VSMEM, bool CLASSED>
 __device__ __forceinline__ void phase_b(const uint8_t* slot, uint32_t vm, uint32_t slot_base,
                                         Lane<VSMEM, CLASSED>& st, const uint8_t* virgin,
-                                        uint32_t* first, uint32_t e, uint8_t* classed_row,
-                                        uint32_t* nov_row) {
+                                        uint32_t* first, uint32_t e, uint8_t* classed_row) {
   // Warp-uniform loop (exit by vote) so the warp is provably converged around it; lanes that
   // have run out of entries are predicated off inside.  Software-pipelined: the shared-memory
   // loads of the NEXT non-zero slot (vector, element, virgin byte) are issued before the FNV
@@ -141,7 +139,7 @@ __device__ __forceinline__ void phase_b(const uint8_t* slot, uint32_t vm, uint32
     const bool valid = n_valid;
     const uint32_t idx = n_idx, c = n_c, known = n_known;
     fetch();
-    if (valid) st.visit(idx, HOST ? hfz_class_host(c) : hfz_class_device(c), known, first, e, classed_row, nov_row);
+    if (valid) st.visit(idx, HOST ? hfz_class_host(c) : hfz_class_device(c), known, first, e, classed_row);
   }
 }
 
@@ -203,7 +201,6 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
     const uint64_t e64 = base + lane;
     const uint32_t e = (uint32_t)e64;
     uint8_t* classed_row = CLASSED ? p.classed + e64 * p.S : nullptr;
-    uint32_t* nov_row = p.novel_ent + (valid ? e64 : base) * kNovMax;
     // lane's source for load i: map (i*kMapsPerLoad + sub), unit `unit`
     const uint8_t* gsrc = p.raw + (base + sub) * rec + unit * 16;
 
@@ -211,7 +208,6 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
     st.hf = HFZ_FNV_OFFSET;
     st.hs = HFZ_FNV_OFFSET;
     st.nnz = 0;
-    st.novel = 0;
 
     // maps >= nm of a partial group alias the group's last map: always in bounds, their
     // votes are masked off below and their lanes never run phase B.
@@ -280,10 +276,10 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
         uint32_t vm = s_mask[lane];
         if (!FULL && !valid) vm = 0;  // no branch on `valid`: idle lanes just see an empty mask
         if (r < rows_host)
-          phase_b<true, ROW, VSMEM, CLASSED>(my_slot, vm, r * ROW, st, virgin, p.first, e, classed_row, nov_row);
+          phase_b<true, ROW, VSMEM, CLASSED>(my_slot, vm, r * ROW, st, virgin, p.first, e, classed_row);
         else
           phase_b<false, ROW, VSMEM, CLASSED>(my_slot, vm, p.H + (r - rows_host) * (ROW / 4), st,
-                                              virgin, p.first, e, classed_row, nov_row);
+                                              virgin, p.first, e, classed_row);
         __syncwarp();
       }
     };
@@ -296,19 +292,6 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
       p.sig_full[e64] = st.hf;
       p.sig_simple[e64] = st.hs;
       if (p.nnz) p.nnz[e64] = st.nnz;
-    }
-    const uint32_t cm = __ballot_sync(0xffffffffu, valid && st.novel);
-    if (cm) {
-      uint32_t basei = 0;
-      if (lane == 0) basei = atomicAdd(p.cand_count, __popc(cm));
-      basei = __shfl_sync(0xffffffffu, basei, 0);
-      if (valid && st.novel) {
-        const uint32_t ci = basei + __popc(cm & ((1u << lane) - 1u));
-        p.cand_list[ci] = e;
-        p.cand_flags[ci] = 0;
-        p.cand_nov[ci] = st.novel <= kNovMax ? st.novel : kNovMax + 1;
-        if (st.novel > kNovMax) p.slow_list[atomicAdd(p.cand_count + 1, 1u)] = ci;
-      }
     }
   }
   if (!virgin_ready) hfz_mbar_wait(bar_virgin, 0);  // never leave the bulk copy in flight
@@ -422,12 +405,10 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan_pipe(con
   const uint64_t e64 = base + lane;
   const uint32_t e = (uint32_t)e64;
   uint8_t* classed_row = CLASSED ? p.classed + e64 * p.S : nullptr;
-  uint32_t* nov_row = p.novel_ent + (valid ? e64 : base) * kNovMax;
   Lane<VSMEM, CLASSED> st;
   st.hf = HFZ_FNV_OFFSET;
   st.hs = HFZ_FNV_OFFSET;
   st.nnz = 0;
-  st.novel = 0;
   if (VSMEM) hfz_mbar_wait(bar_virgin, 0);
   const uint8_t* virgin = VSMEM ? s_virgin : p.v0;
   for (uint32_t r = 0; r < rows; ++r) {
@@ -438,29 +419,16 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan_pipe(con
     if (!valid) vm = 0;
     const uint8_t* my_slot = slot + lane * C::kSlot;
     if (r < rows_host)
-      phase_b<true, ROW, VSMEM, CLASSED>(my_slot, vm, r * ROW, st, virgin, p.first, e, classed_row, nov_row);
+      phase_b<true, ROW, VSMEM, CLASSED>(my_slot, vm, r * ROW, st, virgin, p.first, e, classed_row);
     else
       phase_b<false, ROW, VSMEM, CLASSED>(my_slot, vm, p.H + (r - rows_host) * (ROW / 4), st, virgin,
-                                          p.first, e, classed_row, nov_row);
+                                          p.first, e, classed_row);
     hfz_mbar_arrive(&empty[s]);
   }
   if (valid) {
     p.sig_full[e64] = st.hf;
     p.sig_simple[e64] = st.hs;
     if (p.nnz) p.nnz[e64] = st.nnz;
-  }
-  const uint32_t cm = __ballot_sync(0xffffffffu, valid && st.novel);
-  if (cm) {
-    uint32_t basei = 0;
-    if (lane == 0) basei = atomicAdd(p.cand_count, __popc(cm));
-    basei = __shfl_sync(0xffffffffu, basei, 0);
-    if (valid && st.novel) {
-      const uint32_t ci = basei + __popc(cm & ((1u << lane) - 1u));
-      p.cand_list[ci] = e;
-      p.cand_flags[ci] = 0;
-      p.cand_nov[ci] = st.novel <= kNovMax ? st.novel : kNovMax + 1;
-      if (st.novel > kNovMax) p.slow_list[atomicAdd(p.cand_count + 1, 1u)] = ci;
-    }
   }
 }
 
@@ -507,7 +475,7 @@ __global__ void __launch_bounds__(512, 1) hfz_k_scan_wpm(const ScanParams p) {
     const uint4* src = reinterpret_cast<const uint4*>(p.raw + e64 * p.rec_bytes);
     uint8_t* classed_row = CLASSED ? p.classed + e64 * p.S : nullptr;
     uint64_t h = HFZ_FNV_OFFSET;  // lane 0: Full chain, lane 1: Simple chain
-    uint32_t fill = 0, nnz = 0, novel = 0;
+    uint32_t fill = 0, nnz = 0;
 
     auto drain = [&]() {
       __syncwarp();
@@ -527,10 +495,7 @@ __global__ void __launch_bounds__(512, 1) hfz_k_scan_wpm(const ScanParams p) {
     auto element = [&](uint32_t idx, uint32_t klass, uint32_t pos) {
       list[pos] = idx | ((31 - __clz(klass)) << 24);
       const uint32_t known = VSMEM ? (uint32_t)virgin[idx] : (uint32_t)__ldg(virgin + idx);
-      if (klass & ~known) {
-        novel = 1;
-        atomicMin(p.first + (size_t)idx * 8 + (31 - __clz(klass)), e);
-      }
+      if (klass & ~known) note_first(p.first + (size_t)idx * 8 + (31 - __clz(klass)), e);
       if (CLASSED) classed_row[idx] = (uint8_t)klass;
     };
 
@@ -599,18 +564,10 @@ __global__ void __launch_bounds__(512, 1) hfz_k_scan_wpm(const ScanParams p) {
     }
     drain();
     const uint64_t h_simple = __shfl_sync(0xffffffffu, h, 1);
-    const uint32_t any_novel = __any_sync(0xffffffffu, novel != 0u);
     if (lane == 0) {
       p.sig_full[e64] = h;
       p.sig_simple[e64] = h_simple;
       if (p.nnz) p.nnz[e64] = nnz;
-      if (any_novel) {  // this kernel does not record the novel slots: resolve re-reads the map
-        const uint32_t ci = atomicAdd(p.cand_count, 1u);
-        p.cand_list[ci] = e;
-        p.cand_flags[ci] = 0;
-        p.cand_nov[ci] = kNovMax + 1;
-        p.slow_list[atomicAdd(p.cand_count + 1, 1u)] = ci;
-      }
     }
   }
 }
@@ -696,41 +653,7 @@ __global__ void hfz_k_merge_peers(uint8_t* __restrict__ virgin, const PeerPtrs p
 }
 
 // ---------------------------------------------------------------------------
-// K2b: exact Admit codes of the candidate execs.  Work item = (candidate, 16 KB piece of its
-// raw record), dealt round-robin to all warps; a piece ORs {1: new class bit on a known slot,
-// 2: new slot} into cand_flags[i]; hfz_k_admit turns the flags into Admit codes.
-struct ResolveParams {
-  const uint8_t* raw;
-  uint64_t rec_bytes;
-  uint32_t S, H;
-  const uint8_t* prior;     // P_r
-  const uint32_t* first;
-  const uint32_t* cand_list;
-  const uint32_t* cand_count;
-  uint32_t* cand_flags;
-  const uint32_t* cand_nov;
-  const uint32_t* slow_list;
-  const uint32_t* novel_ent;
-  uint8_t* admit;
-};
-
-__device__ __forceinline__ uint32_t first_any(const uint32_t* first, uint32_t idx) {
-  const uint4* f = reinterpret_cast<const uint4*>(first + (size_t)idx * 8);
-  const uint4 a = __ldcg(f), b = __ldcg(f + 1);
-  return min(min(min(a.x, a.y), min(a.z, a.w)), min(min(b.x, b.y), min(b.z, b.w)));
-}
-
-__device__ __forceinline__ uint32_t resolve_entry(const ResolveParams& p, uint32_t idx,
-                                                  uint32_t klass, uint32_t e) {
-  // (L2 loads: in the fused step these tables were written earlier in the SAME launch by other SMs)
-  const uint32_t pr = __ldcg(p.prior + idx);
-  if (!(klass & ~pr)) return 0;
-  if (__ldcg(p.first + (size_t)idx * 8 + (31 - __clz(klass))) != e) return 0;  // an earlier exec had it
-  if (pr == 0 && first_any(p.first, idx) == e) return 2;              // slot never seen before e
-  return 1;
-}
-
-// K2b, table form: the Admit codes of ALL execs straight from the first-occurrence table -- no candidate is
+// K2b: the Admit codes of ALL execs straight from the first-occurrence table -- no candidate is
 // walked, no map or list is read again.  Entry (slot, bit) = e names the first exec of the batch that shows
 // class bit `bit` on `slot`, recorded only when the bit is not in V0.  With P = the virgin map before this
 // rank's first exec (V0 | the deltas of the ranks before it):
@@ -766,6 +689,50 @@ __global__ void __launch_bounds__(256) hfz_k_resolve_table(const uint32_t* __res
   resolve_slot(__ldcg(f), __ldcg(f + 1), __ldg(prior + s), flags);
 }
 
+// One word (4 slots) of the single-rank fold, everything the table says about them in one read: delta word,
+// virgin |= delta, the slots that turned non-zero, and -- the virgin word as it stood being P -- the Admit
+// flags of the execs the slots' entries name.  `fold` = false: the delta word only (multi-rank scan half).
+__device__ __forceinline__ void fold_word(const uint32_t* __restrict__ first, uint64_t t, bool fold, uint8_t* virgin,
+                                          uint8_t* __restrict__ delta_out, uint32_t* __restrict__ flags, uint32_t H,
+                                          uint32_t& newh, uint32_t& newd) {
+  const uint4* f = reinterpret_cast<const uint4*>(first + t * 32);
+  uint32_t* vw = reinterpret_cast<uint32_t*>(virgin) + t;
+  const uint32_t old = fold ? *vw : 0u;
+  uint32_t d = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 a = __ldcg(f + 2 * q), b = __ldcg(f + 2 * q + 1);
+    const uint32_t byte = (a.x != kNone) | ((a.y != kNone) << 1) | ((a.z != kNone) << 2) | ((a.w != kNone) << 3) |
+                          ((b.x != kNone) << 4) | ((b.y != kNone) << 5) | ((b.z != kNone) << 6) | ((b.w != kNone) << 7);
+    d |= byte << (8 * q);
+    if (fold) resolve_slot(a, b, (old >> (8 * q)) & 0xffu, flags);
+  }
+  if (delta_out) reinterpret_cast<uint32_t*>(delta_out)[t] = d;
+  if (fold) {
+    const uint32_t nw = old | d;
+    if (nw != old) *vw = nw;
+    const uint32_t turned = __popc(nz_bytes(nw) & ~nz_bytes(old));
+    if (t * 4 < H) newh += turned; else newd += turned;
+  }
+}
+
+// delta + merge + resolve of a single-rank fold in one pass over the table (hfz_feedback_batch and the list
+// folds; the multi-rank path keeps hfz_k_delta / hfz_k_merge / hfz_k_resolve_table around its exchange step)
+__global__ void __launch_bounds__(256) hfz_k_fold_single(const uint32_t* __restrict__ first, uint8_t* virgin,
+                                                         uint32_t* __restrict__ flags,
+                                                         unsigned long long* __restrict__ edge_counts, uint32_t S,
+                                                         uint32_t H) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;  // word index
+  uint32_t newh = 0, newd = 0;
+  if (t < S / 4) fold_word(first, t, true, virgin, nullptr, flags, H, newh, newd);
+  newh = __reduce_add_sync(0xffffffffu, newh);
+  newd = __reduce_add_sync(0xffffffffu, newd);
+  if ((threadIdx.x & 31) == 0) {
+    if (newh) atomicAdd(edge_counts + 0, (unsigned long long)newh);
+    if (newd) atomicAdd(edge_counts + 1, (unsigned long long)newd);
+  }
+}
+
 __global__ void __launch_bounds__(256) hfz_k_admit_codes(uint32_t* __restrict__ flags, uint8_t* __restrict__ admit,
                                                          uint64_t n_exec) {
   const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -773,80 +740,6 @@ __global__ void __launch_bounds__(256) hfz_k_admit_codes(uint32_t* __restrict__ 
   const uint32_t f = flags[e];
   admit[e] = (f & 2u) ? 2 : (uint8_t)(f & 1u);
   if (f) flags[e] = 0;
-}
-
-constexpr uint32_t kPiece = 16384;  // bytes per work item (divides H and 4H for S >= 32768... checked on host)
-
-__global__ void __launch_bounds__(256) hfz_k_resolve(const ResolveParams p, uint32_t piece) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t total_warps = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t pieces = (uint32_t)(p.rec_bytes / piece);
-  const uint32_t host_pieces = p.H / piece;
-  const uint64_t items = (uint64_t)p.cand_count[1] * pieces;
-  for (uint64_t it = warp; it < items; it += total_warps) {
-    const uint32_t ci = p.slow_list[it / pieces], pc = (uint32_t)(it % pieces);
-    const uint32_t e = p.cand_list[ci];
-    const uint4* src = reinterpret_cast<const uint4*>(p.raw + (uint64_t)e * p.rec_bytes + (uint64_t)pc * piece);
-    uint32_t flags = 0;
-    const bool host = pc < host_pieces;
-    const uint32_t slot0 = host ? pc * piece : p.H + (pc - host_pieces) * (piece / 4);
-    for (uint32_t v0 = 0; v0 < piece / 16; v0 += 32 * 8) {
-      uint4 x[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const uint32_t v = v0 + j * 32 + lane;
-        x[j] = v < piece / 16 ? hfz_ldg_stream(src + v) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if ((x[j].x | x[j].y | x[j].z | x[j].w) == 0u) continue;
-        const uint32_t v = v0 + j * 32 + lane;
-        const uint32_t w[4] = {x[j].x, x[j].y, x[j].z, x[j].w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (host) {
-            uint32_t bm = nz_bytes(w[k]);
-            while (bm) {
-              const uint32_t b = __ffs(bm) - 1;
-              bm &= bm - 1;
-              flags |= resolve_entry(p, slot0 + v * 16 + k * 4 + b,
-                                     hfz_class_host((w[k] >> (8 * b)) & 0xffu), e);
-            }
-          } else if (w[k]) {
-            flags |= resolve_entry(p, slot0 + v * 4 + k, hfz_class_device(w[k]), e);
-          }
-        }
-      }
-    }
-    flags = __reduce_or_sync(0xffffffffu, flags);
-    if (lane == 0 && flags) atomicOr(p.cand_flags + ci, flags);
-  }
-}
-
-// candidates with at most kNovMax novel slots: the scan recorded them, no need to read the map again
-__global__ void __launch_bounds__(256) hfz_k_resolve_fast(const ResolveParams p) {
-  const uint64_t n = (uint64_t)p.cand_count[0] * kNovMax;
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
-       t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t ci = (uint32_t)(t / kNovMax), k = (uint32_t)(t % kNovMax);
-    const uint32_t cnt = p.cand_nov[ci];
-    if (cnt > kNovMax || k >= cnt) continue;
-    const uint32_t e = p.cand_list[ci];
-    const uint32_t en = p.novel_ent[(size_t)e * kNovMax + k];
-    const uint32_t f = resolve_entry(p, en & 0xffffffu, 1u << (en >> 24), e);
-    if (f) atomicOr(p.cand_flags + ci, f);
-  }
-}
-
-__global__ void hfz_k_admit(const uint32_t* __restrict__ cand_list,
-                            const uint32_t* __restrict__ cand_count,
-                            const uint32_t* __restrict__ cand_flags, uint8_t* __restrict__ admit) {
-  const uint32_t n = *cand_count;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const uint32_t f = cand_flags[i];
-    admit[cand_list[i]] = (f & 2u) ? 2 : ((f & 1u) ? 1 : 0);
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -875,12 +768,6 @@ struct SparseParams {
   uint32_t S, H;
   const uint8_t* v0;
   uint32_t* first;
-  uint32_t* cand_list;
-  uint32_t* cand_count;
-  uint32_t* cand_flags;
-  uint32_t* cand_nov;
-  uint32_t* slow_list;
-  uint32_t* novel_ent;
   uint32_t* sorted;
   uint32_t* cnt;
   uint8_t* classed;
@@ -900,8 +787,7 @@ __global__ void __launch_bounds__(kRankWarps * 32, 1) hfz_k_sparse_rank(const Sp
   // w + (w >> per_shift), its prefix at w + 2 (w >> per_shift).
   uint32_t* bm = reinterpret_cast<uint32_t*>(smem + (size_t)warp * rank_warp_bytes(words));
   uint16_t* pre = reinterpret_cast<uint16_t*>(bm + words + 32);
-  uint32_t* lane_base = reinterpret_cast<uint32_t*>(pre + words + 64);  // [32] + [1] novel counter
-  uint32_t* nov_cnt = lane_base + 32;
+  uint32_t* lane_base = reinterpret_cast<uint32_t*>(pre + words + 64);  // [32]
   for (uint32_t i = lane; i < words + 32; i += 32) bm[i] = 0;
   __syncwarp();
   uint32_t nbad = 0;
@@ -911,7 +797,6 @@ __global__ void __launch_bounds__(kRankWarps * 32, 1) hfz_k_sparse_rank(const Sp
     // exec e owns wide pairs [b, t) and compact pairs [cb, ct); its ordered list starts at b + cb
     const uint64_t b = p.off ? p.off[e64] : 0, t = p.off ? p.off[e64 + 1] : 0;
     const uint64_t cb = p.coff ? p.coff[e64] : 0, ct = p.coff ? p.coff[e64 + 1] : 0;
-    if (lane == 0) *nov_cnt = 0;
     // calls f(slot, count) for every pair of the exec, four loads in flight per lane
     auto for_pairs = [&](auto&& f) {
       for (uint64_t i0 = b; i0 < t; i0 += 128) {
@@ -964,7 +849,6 @@ __global__ void __launch_bounds__(kRankWarps * 32, 1) hfz_k_sparse_rank(const Sp
     __syncwarp();
     // pass 2: rank, classify, novelty, ordered write
     uint8_t* classed_row = p.classed ? p.classed + e64 * p.S : nullptr;
-    uint32_t* nov_row = p.novel_ent + e64 * kNovMax;
     uint32_t* out = p.sorted + b + cb;
     for_pairs([&](uint32_t slot, uint32_t cnt_raw) {
       if (slot >= p.S) return;
@@ -976,25 +860,11 @@ __global__ void __launch_bounds__(kRankWarps * 32, 1) hfz_k_sparse_rank(const Sp
       const uint32_t rung = 31 - __clz(klass);
       const uint32_t en = slot | (rung << 24);
       out[rank] = en;
-      if (klass & ~(uint32_t)__ldg(p.v0 + slot)) {
-        const uint32_t k = atomicAdd(nov_cnt, 1u);
-        if (k < kNovMax) nov_row[k] = en;
-        atomicMin(p.first + (size_t)slot * 8 + rung, e);
-      }
+      if (klass & ~(uint32_t)__ldg(p.v0 + slot)) note_first(p.first + (size_t)slot * 8 + rung, e);
       if (classed_row) classed_row[slot] = (uint8_t)klass;
     });
     __syncwarp();
-    const uint32_t novel = *nov_cnt;
-    if (lane == 0) {
-      p.cnt[e64] = total;
-      if (novel) {
-        const uint32_t ci = atomicAdd(p.cand_count, 1u);
-        p.cand_list[ci] = e;
-        p.cand_flags[ci] = 0;
-        p.cand_nov[ci] = novel <= kNovMax ? novel : kNovMax + 1;
-        if (novel > kNovMax) p.slow_list[atomicAdd(p.cand_count + 1, 1u)] = ci;
-      }
-    }
+    if (lane == 0) p.cnt[e64] = total;
     for (uint32_t i = lane; i < (words + 32) / 4; i += 32) reinterpret_cast<uint4*>(bm)[i] = make_uint4(0, 0, 0, 0);
     __syncwarp();
   }
@@ -1104,10 +974,8 @@ struct CompactParams {
   uint32_t S, H, piece, host_pieces, pieces;
   const uint8_t* v0;
   uint32_t* first;
-  uint32_t* novel_ent;
   uint32_t* sorted;   // [n_exec][S]
   uint32_t* cnt;      // [n_exec][pieces]
-  uint32_t* nov_cnt;  // [n_exec]
   uint8_t* classed;
 };
 
@@ -1169,11 +1037,7 @@ __device__ __forceinline__ void compact_item(const CompactParams& p, uint64_t it
           const uint32_t rung = 31 - __clz(klass);
           const uint32_t en = idx | (rung << 24);
           out[pos++] = en;
-          if (klass & ~(uint32_t)__ldg(p.v0 + idx)) {
-            const uint32_t k = atomicAdd(p.nov_cnt + e64, 1u);
-            if (k < kNovMax) p.novel_ent[e64 * kNovMax + k] = en;
-            atomicMin(p.first + (size_t)idx * 8 + rung, e);
-          }
+          if (klass & ~(uint32_t)__ldg(p.v0 + idx)) note_first(p.first + (size_t)idx * 8 + rung, e);
           if (classed_row) classed_row[idx] = (uint8_t)klass;
         }
       }
@@ -1190,13 +1054,8 @@ __global__ void __launch_bounds__(256) hfz_k_compact(const CompactParams p) {
   for (uint64_t it = warp; it < items; it += nwarps) compact_item(p, it, lane);
 }
 
-// one lane per map: chains over the map's piece lists, nnz, candidate bookkeeping
-__global__ void __launch_bounds__(128) hfz_k_chain_pieces(const CompactParams p, uint32_t* __restrict__ cand_list,
-                                                          uint32_t* __restrict__ cand_count,
-                                                          uint32_t* __restrict__ cand_flags,
-                                                          uint32_t* __restrict__ cand_nov,
-                                                          uint32_t* __restrict__ slow_list,
-                                                          uint64_t* __restrict__ sig_full,
+// one lane per map: chains over the map's piece lists, nnz
+__global__ void __launch_bounds__(128) hfz_k_chain_pieces(const CompactParams p, uint64_t* __restrict__ sig_full,
                                                           uint64_t* __restrict__ sig_simple,
                                                           uint32_t* __restrict__ nnz_out) {
   const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1213,83 +1072,25 @@ __global__ void __launch_bounds__(128) hfz_k_chain_pieces(const CompactParams p,
   sig_full[e] = hf;
   sig_simple[e] = hs;
   if (nnz_out) nnz_out[e] = nnz;
-  const uint32_t novel = p.nov_cnt[e];
-  if (novel) {
-    const uint32_t ci = atomicAdd(cand_count, 1u);
-    cand_list[ci] = (uint32_t)e;
-    cand_flags[ci] = 0;
-    cand_nov[ci] = novel <= kNovMax ? novel : kNovMax + 1;
-    if (novel > kNovMax) slow_list[atomicAdd(cand_count + 1, 1u)] = ci;
-  }
-}
-
-// resolve of the candidates with more than kNovMax novel slots, from their ordered lists
-__global__ void __launch_bounds__(256) hfz_k_resolve_sparse(const ResolveParams p, const uint32_t* __restrict__ sorted,
-                                                            const uint64_t* __restrict__ off,
-                                                            const uint64_t* __restrict__ coff,
-                                                            const uint32_t* __restrict__ cnt) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t total_warps = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t n_slow = p.cand_count[1];
-  for (uint32_t it = warp; it < n_slow; it += total_warps) {
-    const uint32_t ci = p.slow_list[it];
-    const uint32_t e = p.cand_list[ci];
-    const uint32_t* list = sorted + (off ? off[e] : 0) + (coff ? coff[e] : 0);
-    const uint32_t n = cnt[e];
-    uint32_t flags = 0;
-    for (uint32_t i = lane; i < n; i += 32) {
-      const uint32_t en = __ldg(list + i);
-      flags |= resolve_entry(p, en & 0xffffffu, 1u << (en >> 24), e);
-    }
-    flags = __reduce_or_sync(0xffffffffu, flags);
-    if (lane == 0 && flags) atomicOr(p.cand_flags + ci, flags);
-  }
-}
-
-// resolve of the slow candidates after a two-stage scan: from the piece lists, not the records
-__global__ void __launch_bounds__(256) hfz_k_resolve_pieces(const ResolveParams p, const uint32_t* __restrict__ sorted,
-                                                            const uint32_t* __restrict__ cnt, uint32_t piece,
-                                                            uint32_t host_pieces, uint32_t pieces) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t total_warps = (gridDim.x * blockDim.x) >> 5;
-  const uint64_t items = (uint64_t)p.cand_count[1] * pieces;
-  for (uint64_t it = warp; it < items; it += total_warps) {
-    const uint32_t ci = p.slow_list[it / pieces], pc = (uint32_t)(it % pieces);
-    const uint32_t e = p.cand_list[ci];
-    const uint32_t slot0 = pc < host_pieces ? pc * piece : p.H + (pc - host_pieces) * (piece / 4);
-    const uint32_t* list = sorted + (uint64_t)e * p.S + slot0;
-    const uint32_t n = cnt[(uint64_t)e * pieces + pc];
-    uint32_t flags = 0;
-    for (uint32_t i = lane; i < n; i += 32) {
-      const uint32_t en = __ldg(list + i);
-      flags |= resolve_entry(p, en & 0xffffffu, 1u << (en >> 24), e);
-    }
-    flags = __reduce_or_sync(0xffffffffu, flags);
-    if (lane == 0 && flags) atomicOr(p.cand_flags + ci, flags);
-  }
 }
 
 // ---------------------------------------------------------------------------
 // Small batches as ONE cooperative launch ("fused step").  The two-stage path above is latency-
 // bound by its launches: 7 kernels + 4 memsets for 26 us of HBM time at 1,024 maps.  Here the
-// whole fold -- compact, chains, candidate list, delta, ordered merge, resolve, Admit codes -- is
-// one persistent kernel (one 1,024-thread CTA per SM, cooperative launch) with two grid-wide
-// barriers, and nothing is memset between calls:
+// whole fold -- compact, chains, delta, ordered merge, resolve, Admit codes -- is one persistent
+// kernel (one 768-thread CTA per SM, cooperative launch) with two grid-wide barriers, and nothing
+// is memset between calls:
 //   * the first-occurrence table is double-buffered: a call uses one table (all-ones on entry)
 //     and scrubs the OTHER one, which the previous call left dirty, while it streams the maps;
-//   * the per-map novel counters are zeroed again by the warp that reads them; the candidate
-//     counter alternates between two words, each call zeroing the one the next call will use;
-//   * Admit codes of non-candidates are written (0) by the candidate pass, those of candidates by
-//     the resolve pass: one warp per candidate, no flag array, no separate admit kernel.
+//   * the per-exec Admit flags are zeroed again by the thread that turns them into codes.
 //   phase 1   all warps: (map, piece) items -> ordered piece lists + first-occurrence updates
 //   --- grid barrier ---
-//   phase 2   by role: one lane per map runs both FNV chains over its piece lists (32 maps per
-//             warp, the warps spread one per SM) | candidate list | delta + merge (4 slots per
-//             thread: delta word from the table, virgin |= delta, prior, edge counters)
+//   phase 2   by role: delta + merge + resolve (4 slots per thread: delta word from the table,
+//             virgin |= delta, edge counters, and -- the virgin word as it stood being P -- the
+//             Admit flags of the execs the slots' entries name, resolve_slot) | one warp per map:
+//             both FNV chains over its piece lists (hfz_fnv.cuh)
 //   --- grid barrier ---
-//   phase 3   one warp per candidate: exact Admit code from the first-occurrence table
+//   phase 3   Admit flags -> codes, one thread per exec
 // The scan and resolve halves can also be launched separately (multi-rank: the deltas of all ranks
 // are exchanged in between); the resolve half then starts with the rank-ordered merge.
 struct StepParams {
@@ -1299,10 +1100,6 @@ struct StepParams {
   uint64_t* sig_simple;
   uint32_t* nnz;
   uint8_t* delta_out;        // this rank's novelty delta (S bytes)
-  uint32_t* cand_list;
-  uint32_t* cand_nov;
-  uint32_t* cand_count;      // [1] candidates of this call (zero on entry)
-  uint32_t* cand_count_next; // [1] zeroed for the next call
   uint8_t* virgin;           // resolve half: virgin_inout
   uint8_t* prior;            // P_r
   unsigned long long* edge_counts;
@@ -1363,11 +1160,7 @@ __device__ __noinline__ void compact_staged_rows(const CompactParams& p, uint64_
     const uint32_t rung = 31 - __clz(klass);
     const uint32_t en = idx | (rung << 24);
     out[pos] = en;
-    if (klass & ~(uint32_t)__ldg(p.v0 + idx)) {
-      const uint32_t k = atomicAdd(p.nov_cnt + e64, 1u);
-      if (k < kNovMax) p.novel_ent[e64 * kNovMax + k] = en;
-      atomicMin(p.first + (size_t)idx * 8 + rung, e);
-    }
+    if (klass & ~(uint32_t)__ldg(p.v0 + idx)) note_first(p.first + (size_t)idx * 8 + rung, e);
     if (classed_row) classed_row[idx] = (uint8_t)klass;
   };
   auto flush = [&]() {
@@ -1503,21 +1296,7 @@ __device__ __forceinline__ void compact_staged(const CompactParams& p, uint32_t 
     const uint32_t rung = 31 - __clz(klass);
     const uint32_t en = idx | (rung << 24);
     out[t] = en;
-    const bool novel = (klass & ~(uint32_t)__ldg(p.v0 + idx)) != 0u;
-    // one counter update per warp and pass, not per element (cold start: every element is novel)
-    const uint32_t act = __activemask();
-    const uint32_t nm = __ballot_sync(act, novel);
-    if (nm) {
-      uint32_t k0 = 0;
-      const uint32_t leader = __ffs(nm) - 1;
-      if (lane == leader) k0 = atomicAdd(p.nov_cnt + e, __popc(nm));
-      k0 = __shfl_sync(act, k0, leader);
-      if (novel) {
-        const uint32_t k = k0 + __popc(nm & ((1u << lane) - 1u));
-        if (k < kNovMax) p.novel_ent[(uint64_t)e * kNovMax + k] = en;
-        atomicMin(p.first + (size_t)idx * 8 + rung, e);
-      }
-    }
+    if (klass & ~(uint32_t)__ldg(p.v0 + idx)) note_first(p.first + (size_t)idx * 8 + rung, e);
     if (classed_row) classed_row[idx] = (uint8_t)klass;
   }
   if (lane == 0) p.cnt[it] = total;
@@ -1540,7 +1319,6 @@ __global__ void __launch_bounds__(kStepWarps * 32, 1) hfz_k_small_step(const Ste
 
   dbg_mark(p, 0);
   if (p.do_scan) {
-    if (gthread == 0) *p.cand_count_next = 0;
     // ---- phase 1: compact.  (map, piece) items dealt round-robin over all warps of the grid; the
     // piece is staged in shared memory by ONE TMA bulk copy per item (SASS: UBLKCP), double-buffered:
     // item k + 1 is in flight while item k is compacted.
@@ -1595,51 +1373,14 @@ __global__ void __launch_bounds__(kStepWarps * 32, 1) hfz_k_small_step(const Ste
     grid.sync();
     dbg_mark(p, 3);
 
-    // ---- phase 2, by role: [0, D) delta (+ merge), [D, D + G) candidate list, then one warp per two maps: chains
+    // ---- phase 2, by role: [0, D) delta (+ merge + resolve), then one warp per map: chains
     const uint64_t D = c.S / 128;  // warps: 4 slots per thread
-    const uint64_t G = (c.n_exec + 31) / 32;
     uint32_t newh = 0, newd = 0;
-    for (uint64_t role = gw; role < D + G + c.n_exec; role += W) {
+    for (uint64_t role = gw; role < D + c.n_exec; role += W) {
       if (role < D) {
-        // delta word of 4 slots from the table; fused: the single-rank merge right here
+        // delta word of 4 slots from the table; fused: the single-rank merge and the Admit flags right here
         const uint64_t t = role * 32 + lane;  // word index, < S / 4
-        const uint4* f = reinterpret_cast<const uint4*>(c.first + t * 32);
-        uint32_t d = 0;
-        uint32_t* vw = reinterpret_cast<uint32_t*>(p.virgin) + t;
-        const uint32_t old = fused ? *vw : 0u;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint4 a = __ldcg(f + 2 * q), b = __ldcg(f + 2 * q + 1);
-          const uint32_t byte = (a.x != kNone) | ((a.y != kNone) << 1) | ((a.z != kNone) << 2) | ((a.w != kNone) << 3) |
-                                ((b.x != kNone) << 4) | ((b.y != kNone) << 5) | ((b.z != kNone) << 6) | ((b.w != kNone) << 7);
-          d |= byte << (8 * q);
-          // fused (single rank): P = the virgin map as it stood -- the Admit flags of the slot right here
-          if (fused) resolve_slot(a, b, (old >> (8 * q)) & 0xffu, p.flags);
-        }
-        reinterpret_cast<uint32_t*>(p.delta_out)[t] = d;
-        if (fused) {
-          const uint32_t nw = old | d;
-          reinterpret_cast<uint32_t*>(p.prior)[t] = old;
-          if (nw != old) *vw = nw;
-          const uint32_t turned = __popc(nz_bytes(nw) & ~nz_bytes(old));
-          if (t * 4 < c.H) newh += turned; else newd += turned;
-        }
-      } else if (role < D + G) {
-        // candidate list: maps with any novelty versus V0; the counters are left zeroed
-        const uint64_t e = (role - D) * 32 + lane;
-        const uint32_t novel = e < c.n_exec ? __ldcg(c.nov_cnt + e) : 0u;
-        const uint32_t cm = __ballot_sync(0xffffffffu, novel != 0u);
-        if (cm) {
-          uint32_t basei = 0;
-          if (lane == 0) basei = atomicAdd(p.cand_count, __popc(cm));
-          basei = __shfl_sync(0xffffffffu, basei, 0);
-          if (novel) {
-            const uint32_t ci = basei + __popc(cm & ((1u << lane) - 1u));
-            p.cand_list[ci] = (uint32_t)e;
-            p.cand_nov[ci] = novel <= kNovMax ? novel : kNovMax + 1;
-            c.nov_cnt[e] = 0;
-          }
-        }
+        fold_word(c.first, t, fused, p.virgin, p.delta_out, p.flags, c.H, newh, newd);
       } else {
         // signatures: ONE map per warp, the whole warp on its two chains (hfz_fnv.cuh).  The warp gathers the
         // map's ordered piece lists into shared memory (cp.async; one piece per lane, every copy in flight
@@ -1647,7 +1388,7 @@ __global__ void __launch_bounds__(kStepWarps * 32, 1) hfz_k_small_step(const Ste
         // bit-sliced, 32 steps per lane.  (Until round 2 of the build, lanes 0..3 ran the four chains of two
         // maps serially: 53-64 cycles per entry, ~78 k cycles for two maps at 2 % density; a scheduler had
         // one such warp to issue for and nothing could shorten the dependency.)
-        const uint64_t e = role - D - G;
+        const uint64_t e = role - D;
         uint32_t* buf = reinterpret_cast<uint32_t*>(wbuf);
         uint8_t* stream = wbuf + kChainRound * 4;  // 3,072 bytes of byte stream + slack (the buffer is 8 KB)
         static_assert(kChainRound * 4 + 3072 + 16 <= kStepBuf, "entry buffer + byte stream must fit the warp's staging buffer");
@@ -1897,16 +1638,13 @@ int launch_scan_two_stage(hfz_ctx* ctx, const ScanParams& sp) {
   p.pieces = (uint32_t)(sp.rec_bytes / piece);
   p.v0 = sp.v0;
   p.first = sp.first;
-  p.novel_ent = sp.novel_ent;
   p.classed = sp.classed;
   // grow-only scratch with geometric slack (hfz.h documents the footprint: 4 x S bytes per exec)
   int rc = grow(ctx->ts_sorted, ctx->ts_sorted_cap, sp.n_exec * (uint64_t)sp.S, "two-stage scan: piece lists");
   if (rc) return rc;
-  if ((rc = grow(ctx->ts_cnt, ctx->ts_cnt_cap, sp.n_exec * (uint64_t)(p.pieces + 1), "two-stage scan: piece counts"))) return rc;
+  if ((rc = grow(ctx->ts_cnt, ctx->ts_cnt_cap, sp.n_exec * (uint64_t)p.pieces, "two-stage scan: piece counts"))) return rc;
   p.sorted = ctx->ts_sorted;
   p.cnt = ctx->ts_cnt;
-  p.nov_cnt = ctx->ts_cnt + sp.n_exec * (uint64_t)p.pieces;
-  HFZ_CUDA(cudaMemsetAsync(p.nov_cnt, 0, sp.n_exec * 4, ctx->stream));
   const uint64_t items = sp.n_exec * p.pieces;
   uint64_t blocks = (items + 7) / 8;
   const uint64_t cap = (uint64_t)ctx->num_sms * 8;  // 64 warps per SM
@@ -1915,18 +1653,14 @@ int launch_scan_two_stage(hfz_ctx* ctx, const ScanParams& sp) {
   ++ctx->launches;
   HFZ_CUDA(cudaGetLastError());
   hfz_k_chain_pieces<<<(uint32_t)((sp.n_exec + 127) / 128), 128, 0, ctx->stream>>>(
-      p, sp.cand_list, sp.cand_count, sp.cand_flags, sp.cand_nov, sp.slow_list, sp.sig_full, sp.sig_simple, sp.nnz);
+      p, sp.sig_full, sp.sig_simple, sp.nnz);
   ++ctx->launches;
   HFZ_CUDA(cudaGetLastError());
-  ctx->sc_pieces = true;
-  ctx->sc_piece = p.piece;
-  ctx->sc_host_pieces = p.host_pieces;
-  ctx->sc_npieces = p.pieces;
   return HFZ_OK;
 }
 
 // ---- fused small step: host side
-int ensure_cand(hfz_ctx* ctx, uint64_t n_exec);
+int ensure_admit_flags(hfz_ctx* ctx, uint64_t n_exec);
 bool small_step_ok(hfz_ctx* ctx, uint64_t n_exec) {
   if (!ctx->small_fused || n_exec == 0) return false;
   // measured on B200 (65,536 slots, warm / cold virgin): 4,096 maps 0.21 / 0.36 ms fused vs 0.36 / 0.70 pipelined;
@@ -1948,24 +1682,16 @@ bool small_step_ok(hfz_ctx* ctx, uint64_t n_exec) {
 }
 
 int small_step_scratch(hfz_ctx* ctx, uint64_t n_exec, uint32_t pieces) {
-  int rc = ensure_cand(ctx, n_exec);
+  int rc = ensure_admit_flags(ctx, n_exec);
   if (rc) return rc;
   if ((rc = grow(ctx->ts_sorted, ctx->ts_sorted_cap, n_exec * (uint64_t)ctx->S, "small step: piece lists"))) return rc;
   if ((rc = grow(ctx->ts_cnt, ctx->ts_cnt_cap, n_exec * (uint64_t)pieces, "small step: piece counts"))) return rc;
-  if (ctx->ss_nov_cap < n_exec) {  // per-map novel counters: zero between calls (the kernel re-zeroes what it reads)
-    const uint64_t old = ctx->ss_nov_cap;
-    if ((rc = grow(ctx->ss_nov, ctx->ss_nov_cap, n_exec, "small step: novel counters"))) return rc;
-    (void)old;
-    HFZ_CUDA(cudaMemsetAsync(ctx->ss_nov, 0, ctx->ss_nov_cap * 4, ctx->stream));
-  }
-  if (!ctx->ss_first[0]) {  // two first-occurrence tables (all-ones between calls) + the two candidate counters
+  if (!ctx->ss_first[0]) {  // two first-occurrence tables (all-ones between calls)
     const size_t bytes = (size_t)ctx->S * 8 * sizeof(uint32_t);
     for (int i = 0; i < 2; ++i) {
       HFZ_CUDA(cudaMalloc(&ctx->ss_first[i], bytes));
       HFZ_CUDA(cudaMemsetAsync(ctx->ss_first[i], 0xff, bytes, ctx->stream));
     }
-    HFZ_CUDA(cudaMalloc(&ctx->ss_counts, 2 * sizeof(uint32_t)));
-    HFZ_CUDA(cudaMemsetAsync(ctx->ss_counts, 0, 2 * sizeof(uint32_t), ctx->stream));
   }
   return HFZ_OK;
 }
@@ -2002,20 +1728,14 @@ int small_step_scan(hfz_ctx* ctx, const uint8_t* raw, uint64_t n_exec, const uin
   ctx->ss_pp ^= 1;
   c.v0 = v0;
   c.first = ctx->ss_first[ctx->ss_pp];
-  c.novel_ent = ctx->cand_list + 4 * ctx->cand_cap;
   c.sorted = ctx->ts_sorted;
   c.cnt = ctx->ts_cnt;
-  c.nov_cnt = ctx->ss_nov;
   c.classed = classed;
   p.first_prev = ctx->ss_first[ctx->ss_pp ^ 1];
   p.sig_full = sig_full;
   p.sig_simple = sig_simple;
   p.nnz = nnz;
   p.delta_out = delta_out;
-  p.cand_list = ctx->cand_list;
-  p.cand_nov = ctx->cand_list + 2 * ctx->cand_cap;
-  p.cand_count = ctx->ss_counts + ctx->ss_pp;
-  p.cand_count_next = ctx->ss_counts + (ctx->ss_pp ^ 1);
   p.virgin = virgin_inout;
   p.prior = ctx->prior;
   p.edge_counts = reinterpret_cast<unsigned long long*>(edge_counts);
@@ -2031,8 +1751,6 @@ int small_step_scan(hfz_ctx* ctx, const uint8_t* raw, uint64_t n_exec, const uin
     HFZ_CUDA(cudaMemsetAsync(p.dbg, 0, 16 * 8, ctx->stream));
     HFZ_CUDA(cudaMemsetAsync(p.dbg, 0xff, 8, ctx->stream));
   }
-  ctx->sc_sparse = false;
-  ctx->sc_pieces = false;
   ctx->sc_small = !p.do_resolve;  // a resolve-only launch follows (hfz_feedback_resolve)
   if (ctx->sc_small) {
     ctx->sc_step.resize(sizeof(StepParams));
@@ -2138,27 +1856,28 @@ int ensure_admit_flags(hfz_ctx* ctx, uint64_t n_exec) {
   return HFZ_OK;
 }
 
-int ensure_cand(hfz_ctx* ctx, uint64_t n_exec) {
-  if (ctx->cand_cap >= n_exec) return ensure_admit_flags(ctx, n_exec);
-  if (ctx->cand_list) cudaFree(ctx->cand_list);
-  ctx->cand_list = nullptr;
-  ctx->cand_cap = 0;
-  const uint64_t cap = n_exec < 1024 ? 1024 : n_exec;
-  if (cudaMalloc(&ctx->cand_list, (4 + kNovMax) * cap * sizeof(uint32_t)) != cudaSuccess) {
-    hfz_set_error("cudaMalloc(cand_list, %llu) failed", (unsigned long long)cap * 4);
-    return HFZ_ENOMEM;
-  }
-  ctx->cand_cap = cap;
-  return ensure_admit_flags(ctx, n_exec);
-}
-
 }  // namespace
+
+// delta_out = NULL: no delta kernel (hfz_feedback_fold_single follows and reads the table itself)
+static int scan_dense(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec, const uint8_t* virgin_v0,
+                      uint8_t* classed_out, uint64_t* sig_full_out, uint64_t* sig_simple_out, uint32_t* nnz_out,
+                      uint8_t* delta_out);
 
 extern "C" int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec,
                                  const uint8_t* virgin_v0, uint8_t* classed_out,
                                  uint64_t* sig_full_out, uint64_t* sig_simple_out,
                                  uint32_t* nnz_out, uint8_t* delta_out) {
-  if (!ctx || !virgin_v0 || !delta_out || (n_exec && (!raw_maps || !sig_full_out || !sig_simple_out))) {
+  if (!delta_out) {
+    hfz_set_error("hfz_feedback_scan: null argument");
+    return HFZ_EINVAL;
+  }
+  return scan_dense(ctx, raw_maps, n_exec, virgin_v0, classed_out, sig_full_out, sig_simple_out, nnz_out, delta_out);
+}
+
+static int scan_dense(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec, const uint8_t* virgin_v0,
+                      uint8_t* classed_out, uint64_t* sig_full_out, uint64_t* sig_simple_out, uint32_t* nnz_out,
+                      uint8_t* delta_out) {
+  if (!ctx || !virgin_v0 || (n_exec && (!raw_maps || !sig_full_out || !sig_simple_out))) {
     hfz_set_error("hfz_feedback_scan: null argument");
     return HFZ_EINVAL;
   }
@@ -2171,16 +1890,13 @@ extern "C" int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t
     return HFZ_EINVAL;
   }
   HFZ_CUDA(cudaSetDevice(ctx->device));
-  if (small_step_ok(ctx, n_exec))  // small batch: the scan half of the fused step, one launch
+  if (delta_out && small_step_ok(ctx, n_exec))  // small batch: the scan half of the fused step, one launch
     return small_step_scan(ctx, raw_maps, n_exec, virgin_v0, classed_out, sig_full_out, sig_simple_out, nnz_out,
                            delta_out, nullptr, nullptr, nullptr);
   ctx->sc_small = false;
-  int rc = ensure_cand(ctx, n_exec);
+  int rc = ensure_admit_flags(ctx, n_exec);
   if (rc) return rc;
-  ctx->sc_sparse = false;  // the resolve step re-reads candidates from their dense records ...
-  ctx->sc_pieces = false;  // ... unless the two-stage path below leaves its piece lists behind
   HFZ_CUDA(cudaMemsetAsync(ctx->first, 0xff, (size_t)ctx->S * 8 * sizeof(uint32_t), ctx->stream));
-  HFZ_CUDA(cudaMemsetAsync(ctx->cand_count, 0, 2 * sizeof(uint32_t), ctx->stream));
   if (classed_out && n_exec)
     HFZ_CUDA(cudaMemsetAsync(classed_out, 0, n_exec * (size_t)ctx->S, ctx->stream));
   if (n_exec) {
@@ -2192,12 +1908,6 @@ extern "C" int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t
     p.rec_bytes = ctx->rec_bytes;
     p.v0 = virgin_v0;
     p.first = ctx->first;
-    p.cand_list = ctx->cand_list;
-    p.cand_count = ctx->cand_count;
-    p.cand_flags = ctx->cand_list + ctx->cand_cap;
-    p.cand_nov = ctx->cand_list + 2 * ctx->cand_cap;
-    p.slow_list = ctx->cand_list + 3 * ctx->cand_cap;
-    p.novel_ent = ctx->cand_list + 4 * ctx->cand_cap;
     p.sig_full = sig_full_out;
     p.sig_simple = sig_simple_out;
     p.nnz = nnz_out;
@@ -2217,9 +1927,32 @@ extern "C" int hfz_feedback_scan(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t
     }
     if (rc) return rc;
   }
-  hfz_k_delta<<<(ctx->S + 255) / 256, 256, 0, ctx->stream>>>(ctx->first, delta_out, ctx->S);
+  if (delta_out) {
+    hfz_k_delta<<<(ctx->S + 255) / 256, 256, 0, ctx->stream>>>(ctx->first, delta_out, ctx->S);
+    ++ctx->launches;
+    HFZ_CUDA(cudaGetLastError());
+  }
+  return HFZ_OK;
+}
+
+// Second half of a single-rank fold after a scan with delta_out = NULL: delta, merge, edge counters and Admit
+// flags in one pass over the table, then the codes.
+int hfz_feedback_fold_single(hfz_ctx* ctx, uint64_t n_exec, uint8_t* virgin_inout, uint64_t* edge_counts_inout,
+                             uint8_t* admit_out) {
+  if (!ctx || !virgin_inout || !edge_counts_inout || (n_exec && !admit_out)) {
+    hfz_set_error("hfz_feedback_batch: null argument");
+    return HFZ_EINVAL;
+  }
+  hfz_k_fold_single<<<(ctx->S / 4 + 255) / 256, 256, 0, ctx->stream>>>(
+      ctx->first, virgin_inout, ctx->admit_flags, reinterpret_cast<unsigned long long*>(edge_counts_inout), ctx->S,
+      ctx->H);
   ++ctx->launches;
   HFZ_CUDA(cudaGetLastError());
+  if (n_exec) {
+    hfz_k_admit_codes<<<(uint32_t)((n_exec + 255) / 256), 256, 0, ctx->stream>>>(ctx->admit_flags, admit_out, n_exec);
+    ++ctx->launches;
+    HFZ_CUDA(cudaGetLastError());
+  }
   return HFZ_OK;
 }
 
@@ -2238,7 +1971,7 @@ int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t
     return HFZ_ECAP;
   }
   HFZ_CUDA(cudaSetDevice(ctx->device));
-  int rc = ensure_cand(ctx, n_exec);
+  int rc = ensure_admit_flags(ctx, n_exec);
   if (rc) return rc;
   if (ctx->sp_sorted_cap < total_pairs) {
     cudaFree(ctx->sp_sorted);
@@ -2256,7 +1989,6 @@ int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t
     ctx->sp_cnt_cap = n_exec + 1024;
   }
   HFZ_CUDA(cudaMemsetAsync(ctx->first, 0xff, (size_t)ctx->S * 8 * sizeof(uint32_t), ctx->stream));
-  HFZ_CUDA(cudaMemsetAsync(ctx->cand_count, 0, 2 * sizeof(uint32_t), ctx->stream));
   if (classed_out && n_exec) HFZ_CUDA(cudaMemsetAsync(classed_out, 0, n_exec * (size_t)ctx->S, ctx->stream));
   if (n_exec) {
     SparseParams p;
@@ -2269,12 +2001,6 @@ int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t
     p.H = ctx->H;
     p.v0 = virgin_v0;
     p.first = ctx->first;
-    p.cand_list = ctx->cand_list;
-    p.cand_count = ctx->cand_count;
-    p.cand_flags = ctx->cand_list + ctx->cand_cap;
-    p.cand_nov = ctx->cand_list + 2 * ctx->cand_cap;
-    p.slow_list = ctx->cand_list + 3 * ctx->cand_cap;
-    p.novel_ent = ctx->cand_list + 4 * ctx->cand_cap;
     p.sorted = ctx->sp_sorted;
     p.cnt = ctx->sp_cnt;
     p.classed = classed_out;
@@ -2303,15 +2029,11 @@ int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t
     ++ctx->launches;
     HFZ_CUDA(cudaGetLastError());
   }
-  hfz_k_delta<<<(ctx->S + 255) / 256, 256, 0, ctx->stream>>>(ctx->first, delta_out, ctx->S);
-  ++ctx->launches;
-  HFZ_CUDA(cudaGetLastError());
-  ctx->sc_sparse = true;
-  ctx->sc_pieces = false;
-  ctx->sc_sorted = ctx->sp_sorted;
-  ctx->sc_off = entry_off;
-  ctx->sc_coff = compact_off;
-  ctx->sc_cnt = ctx->sp_cnt;
+  if (delta_out) {
+    hfz_k_delta<<<(ctx->S + 255) / 256, 256, 0, ctx->stream>>>(ctx->first, delta_out, ctx->S);
+    ++ctx->launches;
+    HFZ_CUDA(cudaGetLastError());
+  }
   return HFZ_OK;
 }
 
@@ -2335,7 +2057,7 @@ int resolve_impl(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_t n_exec, uint8_t
                  uint64_t* edge_counts_inout, const uint8_t* deltas, const PeerPtrs* peers, uint32_t n_ranks,
                  uint32_t rank, uint8_t* admit_out) {
   if (!ctx || !virgin_inout || !edge_counts_inout || (!deltas && !peers) || n_ranks == 0 || rank >= n_ranks ||
-      (n_exec && ((!raw_maps && !ctx->sc_sparse) || !admit_out))) {
+      (n_exec && !admit_out)) {
     hfz_set_error("hfz_feedback_resolve: bad argument");
     return HFZ_EINVAL;
   }
@@ -2424,11 +2146,13 @@ extern "C" int hfz_feedback_batch(hfz_ctx* ctx, const uint8_t* raw_maps, uint64_
     return small_step_scan(ctx, raw_maps, n_exec, virgin_inout, classed_out, sig_full_out, sig_simple_out, nnz_out,
                            ctx->delta, virgin_inout, edge_counts_inout, admit_out);
   }
-  int rc = hfz_feedback_scan(ctx, raw_maps, n_exec, virgin_inout, classed_out, sig_full_out,
-                             sig_simple_out, nnz_out, ctx->delta);
+  if (!edge_counts_inout || (n_exec && !admit_out)) {
+    hfz_set_error("hfz_feedback_batch: null argument");
+    return HFZ_EINVAL;
+  }
+  int rc = scan_dense(ctx, raw_maps, n_exec, virgin_inout, classed_out, sig_full_out, sig_simple_out, nnz_out, nullptr);
   if (rc) return rc;
-  return hfz_feedback_resolve(ctx, raw_maps, n_exec, virgin_inout, edge_counts_inout, ctx->delta, 1,
-                              0, admit_out);
+  return hfz_feedback_fold_single(ctx, n_exec, virgin_inout, edge_counts_inout, admit_out);
 }
 
 // ---- dev / test entry: both signatures of an ordered entry list (slot | rung << 24) by the warp-parallel

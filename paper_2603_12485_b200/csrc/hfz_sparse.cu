@@ -119,9 +119,9 @@ int fold_chunks(hfz_ctx* c, const uint32_t* entries, const uint64_t* off, const 
     if (native) {
       rc = hfz_feedback_scan_sparse(c, entries, off ? off + done : nullptr, compact, coff ? coff + done : nullptr, n,
                                     total_pairs, virgin, cls, sigf + done, sigs + done,
-                                    nnz ? nnz + done : nullptr, c->delta, c->d_small + kBadSlot);
+                                    nnz ? nnz + done : nullptr, nullptr, c->d_small + kBadSlot);
       if (rc) return rc;
-      rc = hfz_feedback_resolve(c, nullptr, n, virgin, counts, c->delta, 1, 0, admit + done);
+      rc = hfz_feedback_fold_single(c, n, virgin, counts, admit + done);
       if (rc) return rc;
     } else {
       rc = launch_expand<false>(c, entries, off + done, n);

@@ -67,16 +67,14 @@ class ShardedFeedback:
                                                             self.rank, admit=o.get("admit"))
             self._symm.barrier()                        # nobody overwrites a delta that is still being read
             return o
+        if self.world == 1:  # nothing to exchange: the single-rank fold (scan, then one pass over the table)
+            return self.engine.feedback_batch(raw_local, virgin, edge_counts, out=out)
         o = self.engine.feedback_scan(raw_local, virgin, out=out)
         delta = o["delta"]
-        if self.world == 1:
-            deltas = delta
-        else:
-            if self._deltas is None or self._deltas.numel() != self.world * delta.numel():
-                self._deltas = torch.empty(self.world * delta.numel(), dtype=delta.dtype,
-                                           device=delta.device)
-            deltas = self._deltas
-            dist.all_gather_into_tensor(deltas, delta, group=self.group)
+        if self._deltas is None or self._deltas.numel() != self.world * delta.numel():
+            self._deltas = torch.empty(self.world * delta.numel(), dtype=delta.dtype, device=delta.device)
+        deltas = self._deltas
+        dist.all_gather_into_tensor(deltas, delta, group=self.group)
         o["admit"] = self.engine.feedback_resolve(raw_local, virgin, edge_counts, deltas, self.world,
                                                   self.rank, admit=o.get("admit"))
         return o
