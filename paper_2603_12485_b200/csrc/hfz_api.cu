@@ -162,7 +162,7 @@ extern "C" int hfz_ctx_set_option(hfz_ctx* c, const char* key, int64_t value) {
     if (value < 0 || value > 32) return HFZ_EINVAL;
     c->scan_warps = (int)value;
   } else if (!strcmp(key, "scan_row")) {
-    if (value != 0 && value != 256 && value != 512) return HFZ_EINVAL;
+    if (value != 0 && value != 256 && value != 512 && value != 1024) return HFZ_EINVAL;
     c->scan_row = (int)value;
   } else if (!strcmp(key, "scan_prefetch")) {
     c->scan_prefetch = value != 0;

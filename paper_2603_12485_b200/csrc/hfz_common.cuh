@@ -97,7 +97,7 @@ struct hfz_ctx {
 
   // tuning
   int scan_warps = 0;     // 0 = as many as fit
-  int scan_row = 0;       // bytes per map per row: 0 = auto, 256 (18 warps/SM) or 512 (9 warps/SM)
+  int scan_row = 0;       // bytes per map per row: 0 = auto, 256 (18 warps/SM), 512 (9 warps/SM) or 1024 (16 maps per warp)
   int scan_prefetch = 1;  // L2 prefetch of the row after next
   int virgin_smem = 1;    // stage V0 in shared memory when it fits
   int time_scan = 0;      // bracket scan launches with events (bench roofline)

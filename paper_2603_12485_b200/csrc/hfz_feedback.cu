@@ -94,9 +94,11 @@ struct Lane {
 template <int ROW>
 struct RowCfg {
   static constexpr int kSlot = ROW + kPad;      // per-lane shared slot
-  static constexpr int kMapsPerLoad = 512 / ROW;  // maps covered by one warp-wide 128-bit load
-  static constexpr int kLanesPerMap = ROW / 16;
-  static constexpr int kLoads = 32 / kMapsPerLoad;  // loads per row
+  static constexpr int kMapsPerLoad = ROW >= 512 ? 1 : 512 / ROW;  // maps covered by one warp-wide 128-bit load
+  static constexpr int kLoadsPerMap = ROW >= 512 ? ROW / 512 : 1;  // warp-wide loads per map and row
+  static constexpr int kLanesPerMap = (ROW >= 512 ? 512 : ROW) / 16;
+  static constexpr int kLoads = 32 / kMapsPerLoad;  // loads per row (32 for 512- and 1,024-byte rows)
+  static constexpr int kGroup = 32 / kLoadsPerMap;  // maps per warp: 1,024-byte rows = 16 maps, lanes 16..31 idle in phase B
 };
 
 template <bool HOST, int ROW, bool VSMEM, bool CLASSED>
@@ -144,18 +146,19 @@ __device__ __forceinline__ void phase_b(const uint8_t* slot, uint32_t vm, uint32
 }
 
 template <int REC_CT, int ROW, bool VSMEM, bool CLASSED>
-__global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const ScanParams p) {
+__global__ void __launch_bounds__(ROW >= 512 ? 320 : 640, 1) hfz_k_scan(const ScanParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   using C = RowCfg<ROW>;
   constexpr int LB = C::kLoads / 2;  // loads per register buffer
-  constexpr int WARP_SMEM = 32 * C::kSlot + 128;
+  constexpr int G = C::kGroup;  // maps per warp and group
+  constexpr int WARP_SMEM = G * C::kSlot + 128;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const uint64_t rec = REC_CT ? (uint64_t)REC_CT : p.rec_bytes;
   uint8_t* s_virgin = smem;
   uint8_t* s_buf = smem + (VSMEM ? p.S : 0) + (size_t)warp * WARP_SMEM;
   uint64_t* bar_virgin =
       reinterpret_cast<uint64_t*>(smem + (VSMEM ? p.S : 0) + (size_t)nwarps * WARP_SMEM);
-  uint32_t* s_mask = reinterpret_cast<uint32_t*>(s_buf + 32 * C::kSlot);  // [32] u32 per warp
+  uint32_t* s_mask = reinterpret_cast<uint32_t*>(s_buf + G * C::kSlot);  // [32] u32 per warp
 
   if (VSMEM) {
     if (threadIdx.x == 0) {
@@ -182,11 +185,11 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
   // last one), so warps are left idle rather than given a few maps each.  Only the last active
   // warp sees a partial group.
   const uint64_t Wall = (uint64_t)gridDim.x * nwarps;
-  const uint64_t groups = (p.n_exec + 31) / 32;
+  const uint64_t groups = (p.n_exec + G - 1) / G;
   const uint64_t g = (groups + Wall - 1) / Wall;
   const uint64_t wg = (uint64_t)warp * gridDim.x + blockIdx.x;
-  const uint64_t start = wg * g * 32 < p.n_exec ? wg * g * 32 : p.n_exec;
-  const uint64_t stop = (wg + 1) * g * 32 < p.n_exec ? (wg + 1) * g * 32 : p.n_exec;
+  const uint64_t start = wg * g * G < p.n_exec ? wg * g * G : p.n_exec;
+  const uint64_t stop = (wg + 1) * g * G < p.n_exec ? (wg + 1) * g * G : p.n_exec;
   const uint64_t cnt = stop - start;
   const uint32_t rows_host = p.H / ROW;
   const uint32_t rows = (uint32_t)(rec / ROW);
@@ -195,8 +198,8 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
   const uint32_t sub = lane / C::kLanesPerMap, unit = lane % C::kLanesPerMap;
   uint8_t* scat = s_buf + sub * C::kSlot + unit * 16;
 
-  for (uint64_t base = start; base < start + cnt; base += 32) {
-    const uint32_t nm = (uint32_t)min((uint64_t)32, start + cnt - base);
+  for (uint64_t base = start; base < start + cnt; base += G) {
+    const uint32_t nm = (uint32_t)min((uint64_t)G, start + cnt - base);
     const bool valid = (uint32_t)lane < nm;
     const uint64_t e64 = base + lane;
     const uint32_t e = (uint32_t)e64;
@@ -219,34 +222,40 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
         const uint8_t* src = gsrc + (size_t)row * ROW;
 #pragma unroll
         for (int i = 0; i < LB; ++i) {
-          const uint32_t m0 = (half * LB + i) * C::kMapsPerLoad;  // first map of this load
+          const uint32_t li = half * LB + i;                                    // load index within the row
+          const uint32_t m0 = li * C::kMapsPerLoad / C::kLoadsPerMap;           // first map of this load
+          constexpr uint32_t kPartMask = C::kLoadsPerMap - 1;
+          const uint32_t part = (li & kPartMask) * 512;                         // 512-byte part of the map's row
           if (FULL) {
-            X[i] = hfz_ldg_stream(reinterpret_cast<const uint4*>(src + (size_t)m0 * rec));
+            X[i] = hfz_ldg_stream(reinterpret_cast<const uint4*>(src + (size_t)m0 * rec + part));
           } else {
             const uint32_t m = min(m0 + sub, last) - sub;  // clamp to the last map of the group
-            X[i] = hfz_ldg_stream(reinterpret_cast<const uint4*>(src + (int64_t)(int32_t)m * (int64_t)rec));
+            X[i] = hfz_ldg_stream(reinterpret_cast<const uint4*>(src + (int64_t)(int32_t)m * (int64_t)rec + part));
           }
         }
       };
       auto scatter = [&](const uint4* X, int half) {
 #pragma unroll
         for (int i = 0; i < LB; ++i) {
-          const uint32_t m0 = (half * LB + i) * C::kMapsPerLoad;
+          const uint32_t li = half * LB + i;
+          const uint32_t m0 = li * C::kMapsPerLoad / C::kLoadsPerMap;
+          constexpr uint32_t kPartMask = C::kLoadsPerMap - 1;
+          const uint32_t part = (li & kPartMask) * 512;
           bool nz = (X[i].x | X[i].y | X[i].z | X[i].w) != 0u;
           if (!FULL) nz = nz && (m0 + sub < nm);
           const uint32_t b = __ballot_sync(0xffffffffu, nz);
           if (lane == 0) {
             if (C::kMapsPerLoad == 1) {
-              s_mask[m0] = b;
+              s_mask[li] = b;  // mask of (map m0, part): lane m0 reads s_mask[m0 * kLoadsPerMap + part]
             } else {
               *reinterpret_cast<uint2*>(s_mask + m0) = make_uint2(b & 0xffffu, b >> 16);
             }
           }
-          if (nz) *reinterpret_cast<uint4*>(scat + m0 * C::kSlot) = X[i];
+          if (nz) *reinterpret_cast<uint4*>(scat + m0 * C::kSlot + part) = X[i];
         }
       };
       // L2 prefetch of the row after next (32 maps x ROW bytes, one 128-byte line per lane-step)
-      constexpr int PF_LINES = 32 * ROW / 128;  // lines per row
+      constexpr int PF_LINES = G * ROW / 128;  // lines per row
       const uint32_t pf_map = (uint32_t)lane / (ROW / 128), pf_off = ((uint32_t)lane % (ROW / 128)) * 128;
       auto prefetch = [&](uint32_t row) {
         if (p.prefetch && row < rows) {
@@ -273,17 +282,32 @@ __global__ void __launch_bounds__(ROW == 512 ? 320 : 640, 1) hfz_k_scan(const Sc
         load(A, r + 1 < rows ? r + 1 : r, 0);  // unconditional (last one reloads row r, unused)
         scatter(B, 1);
         __syncwarp();
-        uint32_t vm = s_mask[lane];
-        if (!FULL && !valid) vm = 0;  // no branch on `valid`: idle lanes just see an empty mask
-        if (r < rows_host)
-          phase_b<true, ROW, VSMEM, CLASSED>(my_slot, vm, r * ROW, st, virgin, p.first, e, classed_row);
-        else
-          phase_b<false, ROW, VSMEM, CLASSED>(my_slot, vm, p.H + (r - rows_host) * (ROW / 4), st,
-                                              virgin, p.first, e, classed_row);
+        if (C::kLoadsPerMap == 1) {
+          uint32_t vm = s_mask[lane];
+          if (!FULL && !valid) vm = 0;  // no branch on `valid`: idle lanes just see an empty mask
+          if (r < rows_host)
+            phase_b<true, ROW, VSMEM, CLASSED>(my_slot, vm, r * ROW, st, virgin, p.first, e, classed_row);
+          else
+            phase_b<false, ROW, VSMEM, CLASSED>(my_slot, vm, p.H + (r - rows_host) * (ROW / 4), st,
+                                                virgin, p.first, e, classed_row);
+        } else {
+          // 1,024-byte rows: lane m < 16 walks the two 512-byte parts of ITS map's row one after the other
+#pragma unroll
+          for (int part = 0; part < C::kLoadsPerMap; ++part) {
+            uint32_t vm = s_mask[(lane & (G - 1)) * C::kLoadsPerMap + part];
+            if (!valid) vm = 0;
+            if (r < rows_host)
+              phase_b<true, ROW, VSMEM, CLASSED>(my_slot + part * 512, vm, r * ROW + part * 512, st, virgin, p.first, e,
+                                                 classed_row);
+            else
+              phase_b<false, ROW, VSMEM, CLASSED>(my_slot + part * 512, vm, p.H + (r - rows_host) * (ROW / 4) + part * 128,
+                                                  st, virgin, p.first, e, classed_row);
+          }
+        }
         __syncwarp();
       }
     };
-    if (nm == 32)
+    if (nm == G)
       run(std::true_type{});
     else
       run(std::false_type{});
@@ -1519,19 +1543,19 @@ __global__ void __launch_bounds__(kStepWarps * 32, 1) hfz_k_small_step(const Ste
 
 template <int ROW>
 size_t scan_smem_bytes(uint32_t S, bool vsmem, int warps) {
-  return (vsmem ? S : 0) + (size_t)warps * (32 * RowCfg<ROW>::kSlot + 128) + 16;
+  return (vsmem ? S : 0) + (size_t)warps * (RowCfg<ROW>::kGroup * RowCfg<ROW>::kSlot + 128) + 16;
 }
 
 template <int REC_CT, int ROW, bool VSMEM, bool CLASSED>
 int launch_scan_t(hfz_ctx* ctx, const ScanParams& p) {
   auto kern = hfz_k_scan<REC_CT, ROW, VSMEM, CLASSED>;
-  int warps = ROW == 512 ? 10 : 20;  // __launch_bounds__ of the kernel
+  int warps = ROW >= 512 ? 10 : 20;  // __launch_bounds__ of the kernel
   while (warps > 1 && scan_smem_bytes<ROW>(p.S, VSMEM, warps) > (size_t)ctx->max_smem_optin) --warps;
   if (ctx->scan_warps > 0 && ctx->scan_warps < warps) warps = ctx->scan_warps;
   const size_t smem = scan_smem_bytes<ROW>(p.S, VSMEM, warps);
   HFZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   uint64_t grid = (uint64_t)ctx->num_sms;
-  const uint64_t groups = (p.n_exec + 31) / 32;
+  const uint64_t groups = (p.n_exec + RowCfg<ROW>::kGroup - 1) / RowCfg<ROW>::kGroup;
   if (grid > groups) grid = groups;  // warp w of CTA b owns work slice w * grid + b
   kern<<<(uint32_t)grid, warps * 32, smem, ctx->stream>>>(p);
   ++ctx->launches;
@@ -1545,6 +1569,9 @@ int launch_scan_r(hfz_ctx* ctx, const ScanParams& p, int row) {
   if (row == 256)
     return classed ? launch_scan_t<REC_CT, 256, VSMEM, true>(ctx, p)
                    : launch_scan_t<REC_CT, 256, VSMEM, false>(ctx, p);
+  if (row == 1024)
+    return classed ? launch_scan_t<REC_CT, 1024, VSMEM, true>(ctx, p)
+                   : launch_scan_t<REC_CT, 1024, VSMEM, false>(ctx, p);
   return classed ? launch_scan_t<REC_CT, 512, VSMEM, true>(ctx, p)
                  : launch_scan_t<REC_CT, 512, VSMEM, false>(ctx, p);
 }
@@ -1833,8 +1860,15 @@ int launch_scan(hfz_ctx* ctx, const ScanParams& p) {
   // 256-byte rows let 18 warps/SM hide the shared-memory latency of phase B (best when every SM
   // has more than 9 groups to run); 512-byte rows halve the number of rows a warp walks, which
   // wins while a batch gives each SM at most 9 groups anyway (latency-bound regime).
+  // 1,024-byte rows = 16 maps per warp (lanes 16..31 idle in the chain phase): twice the warps for a batch that
+  // leaves most of the grid without a 32-map group.  Measured (65,536 slots, ms per fold, 512- vs 1,024-byte rows):
+  // 14,336 maps 0.617 / 0.577, 16,384: 0.627 / 0.581, 20,480: 0.705 / 0.672, 24,576: 0.765 / 1.070.
   int row = ctx->scan_row;
-  if (row != 256 && row != 512) row = ((p.n_exec + 31) / 32 <= (uint64_t)ctx->num_sms * 9) ? 512 : 256;
+  if (row == 1024 && (p.H % 1024u)) row = 0;  // needs rows of 1,024 bytes in both halves
+  if (row != 256 && row != 512 && row != 1024) {
+    const uint64_t g32 = (p.n_exec + 31) / 32;
+    row = (g32 * 2 <= (uint64_t)ctx->num_sms * 9 && p.H % 1024u == 0) ? 1024 : (g32 <= (uint64_t)ctx->num_sms * 9 ? 512 : 256);
+  }
   if (p.S == 65536u && vsmem) return launch_scan_r<163840, true>(ctx, p, row);
   if (p.S == 262144u && !vsmem) return launch_scan_r<655360, false>(ctx, p, row);
   return vsmem ? launch_scan_r<0, true>(ctx, p, row) : launch_scan_r<0, false>(ctx, p, row);

@@ -214,7 +214,8 @@ def test_sharded_scan_resolve_equals_sequential(ctx, checker, scan_kernel):
 
 
 @pytest.mark.parametrize("opts", [dict(scan_row=512), dict(scan_row=256, scan_prefetch=0), dict(scan_row=512, scan_prefetch=0),
-                                  dict(scan_row=512, virgin_smem=0), dict(scan_row=256, virgin_smem=0), dict(scan_row=256, scan_warps=3)])
+                                  dict(scan_row=512, virgin_smem=0), dict(scan_row=256, virgin_smem=0), dict(scan_row=256, scan_warps=3),
+                                  dict(scan_row=1024), dict(scan_row=1024, virgin_smem=0), dict(scan_row=1024, scan_prefetch=0, scan_warps=2)])
 def test_scan_tunings_agree(ctx, checker, opts):
     """Every tuning of the scan kernel (row size, warps, L2 prefetch, virgin in smem or not)
     is the same function."""
@@ -228,6 +229,20 @@ def test_scan_tunings_agree(ctx, checker, opts):
             ctx.set_option(k, v)
 
 
+@pytest.mark.parametrize("n", [1, 15, 16, 17, 33, 16 * 148 * 2 + 5, 16 * 148 * 9 * 2 + 21])
+def test_sixteen_maps_per_warp(ctx, checker, n, scan_kernel):
+    """scan_row = 1024: a warp takes 16 maps (lanes 16..31 idle in the chain phase), for batches that leave most
+    warps of the grid without a 32-map group.  Full and partial groups, one and several groups per warp."""
+    if scan_kernel != "lane_per_map":
+        pytest.skip("lane-per-map kernel only")
+    raw = synth.maps_campaign(n, S, seed=59)
+    ctx.set_option("scan_row", 1024)
+    try:
+        assert_same(run_gpu(ctx, raw, want_classed=n < 64), run_cpu(checker, raw, n, want_classed=n < 64))
+    finally:
+        ctx.set_option("scan_row", 0)
+
+
 def test_many_maps_per_warp(ctx, checker):
     """More maps than one group per warp: 3 warps x 148 CTAs must walk 32+ maps each."""
     n = 148 * 3 * 32 + 148 * 3 * 5 + 7
@@ -237,6 +252,25 @@ def test_many_maps_per_warp(ctx, checker):
         assert_same(run_gpu(ctx, raw, want_classed=False), run_cpu(checker, raw, n, want_classed=False))
     finally:
         ctx.set_option("scan_warps", 0)
+
+
+@pytest.mark.parametrize("n,mode", [(9000, "iid"), (13000, "campaign"), (20000, "iid")])
+def test_every_map_novel_at_throughput_sizes(ctx, checker, n, mode, scan_kernel):
+    """An empty virgin map under a batch large enough for the automatic dispatch to take the pipelined and the
+    lane-per-map kernels: every map shows something new versus V0, thousands of them own an entry of the
+    first-occurrence table, and the Admit codes come from the table pass alone (no candidate is walked).
+    All three codes occur; iid maps keep ~a quarter of the batch admitted to the end."""
+    if scan_kernel != "lane_per_map":
+        pytest.skip("one pass: the dispatch is left automatic")
+    for k in ("scan_small", "scan_pipe", "scan_two_stage"):
+        ctx.set_option(k, -1)
+    ctx.set_option("small_fused", 1)
+    raw = (synth.maps_iid if mode == "iid" else synth.maps_campaign)(n, S, seed=77)
+    g = run_gpu(ctx, raw, want_classed=False)
+    c = run_cpu(checker, raw, n, want_classed=False)
+    assert_same(g, c)
+    codes = np.bincount(g[0]["admit"], minlength=3)
+    assert codes[2] > 0 and codes[0] > 0 and (mode == "campaign" or codes[1] > 0)
 
 
 def test_large_map_262144(checker, scan_kernel):
