@@ -15,7 +15,7 @@
 //
 // A third leg, "streaming", is how a fuzzing loop actually meets the call: every worker thread owns ONE
 // CoverageMap, and after each execution (here: fill_map, untimed in every leg) it appends the still
-// cache-hot map to its batch and reset()s it for the next execution.  Timed: the append + reset calls
+// cache-hot map to its batch and resets it for the next execution (CompactBatch::take).  Timed: the take calls
 // (summed per worker, maximum over workers) + the fold + the results back in host vectors.
 //
 // Prints one JSON object.  Test/bench infrastructure: the oracle is used as the checker and as the
@@ -254,8 +254,7 @@ int main(int argc, char** argv) {
           for (std::uint64_t e = n * t / T; e < n * (t + 1) / T; ++e) {
             fill_map(prog, seed, e, m);  // the execution (untimed, as in the other legs)
             const double a0 = now();
-            batches[t].append(m);
-            m.reset();
+            batches[t].take(m);  // append + reset in one walk
             acc += now() - a0;
           }
           worker_s[t] = acc;
@@ -345,8 +344,8 @@ int main(int argc, char** argv) {
       "\"one_pack_thread\": {\"value\": %.1f, \"unit\": \"evals/s\", \"seconds\": {\"mean\": %.6f, \"median\": %.6f, \"min\": %.6f, "
       "\"pack_mean\": %.6f, \"fold_and_readback_mean\": %.6f}}, "
       "\"streaming\": {\"value\": %.1f, \"unit\": \"evals/s\", \"pack_threads\": %u, \"seconds\": {\"mean\": %.6f, \"median\": %.6f, "
-      "\"min\": %.6f, \"pack_mean\": %.6f, \"fold_and_readback_mean\": %.6f}, \"what\": \"one reused CoverageMap per worker: append + reset() right "
-      "after the execution that filled it (cache-hot map); timed = append + reset summed per worker, max over workers, + fold + results\"}, "
+      "\"min\": %.6f, \"pack_mean\": %.6f, \"fold_and_readback_mean\": %.6f}, \"what\": \"one reused CoverageMap per worker: CompactBatch::take (append + reset in one walk) right "
+      "after the execution that filled it (cache-hot map); timed = take summed per worker, max over workers, + fold + results\"}, "
       "\"reference_same_maps\": {\"available\": %s, \"threads\": 1, \"seconds\": %.4f, \"value\": %.1f, \"unit\": \"evals/s\", "
       "\"what\": \"classify_trace + 2 x trace_signature + has_new_bits per map (src/engine.cpp:471-478), unmodified reference build, same process\"}, "
       "\"equals_reference\": %s, \"compared\": \"all execs: Admit codes in order, both signatures, nnz; final virgin map; both edge counters; "

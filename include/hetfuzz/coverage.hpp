@@ -66,6 +66,22 @@ class CoverageMap {
     touched_.clear();
     host_violations_ = device_violations_ = 0;
   }
+  // reset() that hands every touched slot's count to f(slot, count) on the way: one visit of each counter's
+  // cache line instead of two (b200::CompactBatch::take).
+  template <class F>
+  void drain(F&& f) {
+    for (std::uint32_t s : touched_) {
+      if (s < kHostSlots) {
+        f(s, static_cast<std::uint32_t>(host_[s]));
+        host_[s] = 0;
+      } else {
+        f(s, device_[s - kDeviceIndexBase]);
+        device_[s - kDeviceIndexBase] = 0;
+      }
+    }
+    touched_.clear();
+    host_violations_ = device_violations_ = 0;
+  }
   // Sets a host counter to a final value (importing a map recorded elsewhere).
   void host_assign(std::uint32_t idx, std::uint8_t value) {
     if (host_[idx] == 0 && value != 0) touched_.push_back(idx);
@@ -175,6 +191,19 @@ class CompactBatch {
         wide_.push_back(c);
       }
     }
+    coff_.push_back(compact_.size());
+    woff_.push_back(wide_.size() / 2);
+  }
+  // append(m) + m.reset() in one walk: what a fuzzing loop does with its one map after every execution
+  void take(CoverageMap& m) {
+    m.drain([this](std::uint32_t slot, std::uint32_t c) {
+      if (c < 65536u) {
+        compact_.push_back(slot | (c << 16));
+      } else {
+        wide_.push_back(slot);
+        wide_.push_back(c);
+      }
+    });
     coff_.push_back(compact_.size());
     woff_.push_back(wide_.size() / 2);
   }

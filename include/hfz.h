@@ -106,7 +106,7 @@ HFZ_API int hfz_ctx_get_stat(hfz_ctx* ctx, const char* key, double* out);
  *   nnz_out           device, n_exec x u32 (ClassedTrace::nonzero.size()) or NULL
  *
  * Context-owned scratch (grown geometrically, kept): 32 x S bytes of first-occurrence table (two of
- * them once a small batch has been folded), 150 bytes per exec of the largest batch seen, and -- for
+ * them once a small batch has been folded), 5 bytes per exec of the largest batch seen (Admit flags), and -- for
  * batches of up to 8,192 execs, which are folded by one cooperative launch over ordered slot lists --
  * n_exec x S x 4 bytes of list address space of which only the used prefix of each 4 KB piece's range
  * is ever touched (2 GB at 8,192 execs of 65,536 slots; option "scan_two_stage" = 0 turns that path

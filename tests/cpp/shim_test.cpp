@@ -142,6 +142,19 @@ int main() {
     for (std::uint32_t i = 0; i < kMapSize; ++i) same = same && va.at(i) == vb.at(i);
     REQUIRE(same);
     REQUIRE(va.host_edges() > 0 && va.device_edges() > 0);
+    // take() = append() + reset() in one walk: the same batch, and the maps end up all-zero and reusable
+    b200::CompactBatch tbatch;
+    for (int e = 0; e < n; ++e) tbatch.take(maps[e]);
+    VirginMap vd;
+    b200::FeedbackResult dd = b200::feedback_batch(b200::default_context(), tbatch, vd.data(), vd.edge_counts(), true);
+    REQUIRE(a.admit == dd.admit && a.sig_full == dd.sig_full && a.sig_simple == dd.sig_simple && a.nnz == dd.nnz);
+    REQUIRE(va.host_edges() == vd.host_edges() && va.device_edges() == vd.device_edges());
+    bool zero = true;
+    for (int e = 0; e < n; ++e) {
+      zero = zero && maps[e].touched().empty();
+      for (std::uint32_t i = 0; i < kHostSlots && zero; ++i) zero = maps[e].host_at(i) == 0 && maps[e].device_at(kDeviceIndexBase + i) == 0;
+    }
+    REQUIRE(zero);
   }
   if (g_fail) {
     std::printf("%d check(s) failed\n", g_fail);
