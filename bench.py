@@ -1084,6 +1084,7 @@ def run_ours(args):
         line.update(extra_cfg)
         print(json.dumps(line), flush=True)
     if world > 1:
+        eng.close()  # peers exchange: unmap / free the shared delta buffers (barrier inside)
         dist.barrier()
         dist.destroy_process_group()
     ctx.close()
@@ -1131,8 +1132,8 @@ def main():
     ap.add_argument("--no-check", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the configs[0]/[2]/[3] sub-benchmarks")
     ap.add_argument("--exchange", default="allgather", choices=["allgather", "peers"],
-                    help="N > 1: NCCL allgather of the deltas (default) or peer-memory loads through torch "
-                         "symmetric memory (hfz_feedback_resolve_peers)")
+                    help="N > 1: NCCL allgather of the deltas (default) or peer-memory loads from CUDA IPC "
+                         "buffers (hfz_peer_alloc / hfz_peer_open + hfz_feedback_resolve_peers)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

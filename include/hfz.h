@@ -223,6 +223,18 @@ HFZ_API int hfz_feedback_resolve_peers(hfz_ctx* ctx, const uint8_t* raw_maps, ui
                                        const uint8_t* const* delta_ptrs, uint32_t n_ranks, uint32_t rank,
                                        uint8_t* admit_out);
 
+/* Buffers for that table when the ranks are separate processes (one per GPU): hfz_peer_alloc makes a
+ * device buffer of its own (zero-filled) and exports its CUDA IPC handle; every other rank passes the
+ * handle -- exchanged once at start-up by whatever the host uses (torch.distributed, MPI, a socket) -- to
+ * hfz_peer_open and gets a pointer valid on ITS device: same device or any device with peer access
+ * (NVLink / NVSwitch).  The scan writes its delta into the rank's own buffer (delta_out), the ranks
+ * meet at a barrier, and hfz_feedback_resolve_peers reads all of them in place.  Close before the owner frees. */
+#define HFZ_PEER_HANDLE_BYTES 64
+HFZ_API int hfz_peer_alloc(hfz_ctx* ctx, uint64_t bytes, void** dev_ptr_out, uint8_t* handle_out /* [64] */);
+HFZ_API int hfz_peer_open(hfz_ctx* ctx, const uint8_t* handle /* [64] */, void** dev_ptr_out);
+HFZ_API int hfz_peer_close(hfz_ctx* ctx, void* dev_ptr);  /* a pointer from hfz_peer_open */
+HFZ_API int hfz_peer_free(hfz_ctx* ctx, void* dev_ptr);   /* a pointer from hfz_peer_alloc */
+
 /* K4 alone: virgin_inout |= OR_q deltas[q] in rank order, edge counters updated
  * (bitwise OR in reference polarity == AFL's virgin AND-merge). */
 HFZ_API int hfz_virgin_merge(hfz_ctx* ctx, uint8_t* virgin_inout, uint64_t* edge_counts_inout,

@@ -42,6 +42,10 @@ PROTOTYPES = {
     "hfz_feedback_scan": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hfz_feedback_resolve": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _u32, _u32, _vp]),
     "hfz_feedback_resolve_peers": (C.c_int, [_vp, _vp, _u64, _vp, _vp, _vp, _u32, _u32, _vp]),
+    "hfz_peer_alloc": (C.c_int, [_vp, _u64, C.POINTER(_vp), _vp]),
+    "hfz_peer_open": (C.c_int, [_vp, _vp, C.POINTER(_vp)]),
+    "hfz_peer_close": (C.c_int, [_vp, _vp]),
+    "hfz_peer_free": (C.c_int, [_vp, _vp]),
     "hfz_virgin_merge": (C.c_int, [_vp, _vp, _vp, _vp, _u32]),
     "hfz_feedback_resolve_allgather": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _u32, _u32, _vp]),
     "hfz_edge_record_batch": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _u64, _u64, _vp, _vp]),

@@ -151,15 +151,41 @@ class Context:
 
     def feedback_resolve_peers(self, raw, virgin, edge_counts, delta_tensors, rank, admit=None):
         """feedback_resolve reading every rank's delta in place: delta_tensors[q] is rank q's delta
-        tensor (own or peer-mapped memory visible from this device)."""
+        (a tensor, or the device address as an int: own or peer-mapped memory visible from this device)."""
         n = raw.numel() // self.rec
         if admit is None:
             admit = torch.empty(n, dtype=torch.uint8, device=self.device)
-        ptrs = (C.c_void_p * len(delta_tensors))(*[t.data_ptr() for t in delta_tensors])
+        ptrs = (C.c_void_p * len(delta_tensors))(*[t if isinstance(t, int) else t.data_ptr() for t in delta_tensors])
         self._sync_stream()
         check(lib.hfz_feedback_resolve_peers(self._h, _ptr(raw), n, _ptr(virgin), _ptr(edge_counts), ptrs,
                                              len(delta_tensors), rank, _ptr(admit)))
         return admit
+
+    # ---- peer-visible buffers (CUDA IPC) for the collective-free exchange ----
+    def peer_alloc(self, nbytes: int):
+        """(device address, 64-byte handle) of a zero-filled device buffer other PROCESSES can map (peer_open)."""
+        p = C.c_void_p()
+        h = (C.c_uint8 * 64)()
+        check(lib.hfz_peer_alloc(self._h, int(nbytes), C.byref(p), h))
+        return int(p.value), bytes(h)
+
+    def peer_open(self, handle: bytes) -> int:
+        p = C.c_void_p()
+        buf = (C.c_uint8 * 64).from_buffer_copy(handle)
+        check(lib.hfz_peer_open(self._h, buf, C.byref(p)))
+        return int(p.value)
+
+    def peer_close(self, ptr: int):
+        check(lib.hfz_peer_close(self._h, C.c_void_p(ptr)))
+
+    def peer_free(self, ptr: int):
+        check(lib.hfz_peer_free(self._h, C.c_void_p(ptr)))
+
+    def device_view(self, ptr: int, nbytes: int) -> torch.Tensor:
+        """uint8 tensor over device memory the library owns (no copy, no ownership)."""
+        class _Raw:
+            __cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1", "data": (int(ptr), False), "version": 2}
+        return torch.as_tensor(_Raw(), device=self.device)
 
     def virgin_merge(self, virgin, edge_counts, deltas, n_ranks):
         self._sync_stream()

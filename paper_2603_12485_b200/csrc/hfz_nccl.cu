@@ -2,6 +2,7 @@
 // per-rank novelty deltas, followed by the rank-ordered resolve/merge.  libnccl is dlopen()ed
 // so single-GPU users do not need it at load time.
 #include <dlfcn.h>
+#include <string.h>
 
 #include "hfz_common.cuh"
 
@@ -54,4 +55,65 @@ extern "C" int hfz_feedback_resolve_allgather(hfz_ctx* ctx, void* nccl_comm, con
   }
   return hfz_feedback_resolve(ctx, raw_maps, n_exec, virgin_inout, edge_counts_inout, deltas_scratch,
                               n_ranks, rank, admit_out);
+}
+
+// ---------------------------------------------------------------------------
+// Peer-visible buffers for the collective-free exchange (hfz_feedback_resolve_peers): the library
+// allocates the buffer itself -- its own cudaMalloc, so the CUDA IPC handle names exactly this
+// buffer at offset 0 -- and exports the 64-byte handle; the other ranks (other PROCESSES, on this or
+// on a peer-accessible device) open it and pass the mapped pointer in their delta_ptrs table.
+static_assert(sizeof(cudaIpcMemHandle_t) == HFZ_PEER_HANDLE_BYTES, "CUDA IPC handle size");
+
+extern "C" int hfz_peer_alloc(hfz_ctx* ctx, uint64_t bytes, void** dev_ptr_out, uint8_t* handle_out) {
+  if (!ctx || !dev_ptr_out || !handle_out || bytes == 0) {
+    hfz_set_error("hfz_peer_alloc: bad argument");
+    return HFZ_EINVAL;
+  }
+  HFZ_CUDA(cudaSetDevice(ctx->device));
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    hfz_set_error("hfz_peer_alloc: cudaMalloc(%llu) failed", (unsigned long long)bytes);
+    return HFZ_ENOMEM;
+  }
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return hfz_cuda_fail(e, "cudaIpcGetMemHandle");
+  }
+  HFZ_CUDA(cudaMemsetAsync(p, 0, bytes, ctx->stream));
+  memcpy(handle_out, &h, sizeof(h));
+  *dev_ptr_out = p;
+  return HFZ_OK;
+}
+
+extern "C" int hfz_peer_open(hfz_ctx* ctx, const uint8_t* handle, void** dev_ptr_out) {
+  if (!ctx || !handle || !dev_ptr_out) {
+    hfz_set_error("hfz_peer_open: bad argument");
+    return HFZ_EINVAL;
+  }
+  HFZ_CUDA(cudaSetDevice(ctx->device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  HFZ_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return HFZ_OK;
+}
+
+extern "C" int hfz_peer_close(hfz_ctx* ctx, void* dev_ptr) {
+  if (!ctx) return HFZ_EINVAL;
+  if (!dev_ptr) return HFZ_OK;
+  HFZ_CUDA(cudaSetDevice(ctx->device));
+  HFZ_CUDA(cudaStreamSynchronize(ctx->stream));
+  HFZ_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return HFZ_OK;
+}
+
+extern "C" int hfz_peer_free(hfz_ctx* ctx, void* dev_ptr) {
+  if (!ctx) return HFZ_EINVAL;
+  if (!dev_ptr) return HFZ_OK;
+  HFZ_CUDA(cudaSetDevice(ctx->device));
+  HFZ_CUDA(cudaStreamSynchronize(ctx->stream));
+  HFZ_CUDA(cudaFree(dev_ptr));
+  return HFZ_OK;
 }

@@ -35,9 +35,11 @@ def shard_range(n_total: int, world: int, rank: int):
 
 class ShardedFeedback:
     """exchange = "allgather" (default): one all_gather_into_tensor of the deltas per step (NCCL).
-    exchange = "peers": every rank's delta lives in torch symmetric memory; the merge kernel of
-    each rank loads the R deltas straight from their owners over NVLink (hfz_feedback_resolve_peers),
-    bracketed by the symmetric-memory barrier -- no collective, no staging copy."""
+    exchange = "peers": every rank's delta lives in a buffer the library exports over CUDA IPC
+    (hfz_peer_alloc / hfz_peer_open, handles exchanged once through the process group); the merge kernel
+    of each rank loads the R deltas straight from their owners -- same device, or NVLink / NVSwitch peers --
+    (hfz_feedback_resolve_peers), bracketed by two barriers of the group: no collective on the data path,
+    no staging copy."""
 
     def __init__(self, engine, group=None, exchange: str = "allgather"):
         self.engine = engine
@@ -46,26 +48,43 @@ class ShardedFeedback:
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self._deltas = None
         self.exchange = exchange
-        self._symm = None
+        self._peer_ptrs = None
         if exchange == "peers" and self.world > 1:
-            import torch.distributed._symmetric_memory as symm_mem
             S = engine.S
-            self._delta_buf = symm_mem.empty(S, dtype=torch.uint8, device=engine.device)
-            self._symm = symm_mem.rendezvous(self._delta_buf, group if group is not None else dist.group.WORLD)
-            self._peer_deltas = [self._symm.get_buffer(q, (S,), torch.uint8) for q in range(self.world)]
+            self._own_ptr, handle = engine.peer_alloc(S)
+            handles = [None] * self.world
+            dist.all_gather_object(handles, handle, group=group)
+            self._peer_ptrs = [self._own_ptr if q == self.rank else engine.peer_open(handles[q]) for q in range(self.world)]
+            self._delta_buf = engine.device_view(self._own_ptr, S)
+            dist.barrier(group=group)  # every rank has mapped every buffer before anyone writes or frees
+
+    def close(self):
+        """Unmap the peers' buffers and free this rank's (after a barrier: nobody still reads it)."""
+        if self._peer_ptrs is not None:
+            torch.cuda.synchronize()
+            for q, p in enumerate(self._peer_ptrs):
+                if q != self.rank:
+                    self.engine.peer_close(p)
+            dist.barrier(group=self.group)
+            self.engine.peer_free(self._own_ptr)
+            self._peer_ptrs = None
+
+    def _meet(self):
+        torch.cuda.current_stream().synchronize()  # this rank's kernels are done ...
+        dist.barrier(group=self.group)             # ... and so are everybody else's
 
     def step(self, raw_local: torch.Tensor, virgin: torch.Tensor, edge_counts: torch.Tensor,
              out: dict | None = None):
         """One campaign iteration on this rank's shard.  `virgin`/`edge_counts` are the
         replicated campaign state (identical on all ranks before and after)."""
-        if self._symm is not None:
+        if self._peer_ptrs is not None:
             out = dict(out or {})
             out["delta"] = self._delta_buf              # the scan writes this rank's delta in place
             o = self.engine.feedback_scan(raw_local, virgin, out=out)
-            self._symm.barrier()                        # every rank's delta is complete
-            o["admit"] = self.engine.feedback_resolve_peers(raw_local, virgin, edge_counts, self._peer_deltas,
+            self._meet()                                # every rank's delta is complete
+            o["admit"] = self.engine.feedback_resolve_peers(raw_local, virgin, edge_counts, self._peer_ptrs,
                                                             self.rank, admit=o.get("admit"))
-            self._symm.barrier()                        # nobody overwrites a delta that is still being read
+            self._meet()                                # nobody overwrites a delta that is still being read
             return o
         if self.world == 1:  # nothing to exchange: the single-rank fold (scan, then one pass over the table)
             return self.engine.feedback_batch(raw_local, virgin, edge_counts, out=out)

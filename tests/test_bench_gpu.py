@@ -38,11 +38,15 @@ def test_small_bench_line_has_every_key():
     assert d["roofline"]["bound"] == "hbm" and d["cpu_baseline"]["cores"] >= 1
 
 
-def test_two_rank_bench_path_over_gloo():
+@pytest.mark.parametrize("exchange,port", [("allgather", "29533"), ("peers", "29534")])
+def test_two_rank_bench_path_over_gloo(exchange, port):
+    """exchange = peers: the two PROCESSES map each other's delta buffer over CUDA IPC (hfz_peer_alloc /
+    hfz_peer_open) and the merge kernel of each reads both in place -- the collective-free exchange end to
+    end, on one device here (IPC between processes works on the same GPU as it does across NVLink peers)."""
     env = dict(os.environ, HFZ_BENCH_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
-           "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3",
-           "--warmup", "3", "--execs", "1024", "--no-cpu", "--e2e-steps", "1", "--no-e2e-dense"]
+           "127.0.0.1", "--master-port", port, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3",
+           "--warmup", "3", "--execs", "1024", "--no-cpu", "--e2e-steps", "1", "--no-e2e-dense", "--exchange", exchange]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     d = last_json(r.stdout)
