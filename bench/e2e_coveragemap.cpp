@@ -4,7 +4,7 @@
 // (Campaign::run_one, src/engine.cpp:464-471).  This harness builds N of them from the synthetic
 // campaign recipe (the same one bench.py uses, paper_2603_12485_b200/synth.py::maps_campaign) and times,
 // as ONE region per step:
-//     CompactBatch::append(map) x N   (touched-slot lists into pinned memory; 1 or T host threads)
+//     PackedBatch::append(map) x N   (touched-slot lists into pinned memory, 3 / 4 bytes per slot; 1 or T host threads)
 //   + feedback_batch(ctx, batch, virgin, counts)   (H2D, rank + chain + resolve kernels, D2H)
 //   + the results back in host vectors
 // and, in the same process, the reference's own loop over the SAME maps -- classify_trace, both
@@ -15,7 +15,7 @@
 //
 // A third leg, "streaming", is how a fuzzing loop actually meets the call: every worker thread owns ONE
 // CoverageMap, and after each execution (here: fill_map, untimed in every leg) it appends the still
-// cache-hot map to its batch and resets it for the next execution (CompactBatch::take).  Timed: the take calls
+// cache-hot map to its batch and resets it for the next execution (PackedBatch::take).  Timed: the take calls
 // (summed per worker, maximum over workers) + the fold + the results back in host vectors.
 //
 // Prints one JSON object.  Test/bench infrastructure: the oracle is used as the checker and as the
@@ -34,7 +34,7 @@
 #include "hetfuzz/coverage.hpp"
 
 using namespace hetfuzz;
-using b200::CompactBatch;
+using Batch = b200::PackedBatch;  // the densest host form (3 / 4 bytes per touched slot)
 using b200::Context;
 using b200::FeedbackResult;
 
@@ -174,7 +174,7 @@ int main(int argc, char** argv) {
   Context ctx(0, kMapSize);
   VirginMap v0;
   {
-    CompactBatch wb;
+    Batch wb;
     for (const CoverageMap& m : warm_maps) wb.append(m);
     b200::feedback_batch(ctx, wb, v0.data(), v0.edge_counts());
   }
@@ -183,7 +183,7 @@ int main(int argc, char** argv) {
   auto run_gpu = [&](unsigned pack_threads, std::vector<double>& total, std::vector<double>& pack, FeedbackResult& last,
                      VirginMap& v_out) {
     const unsigned T = std::max(1u, pack_threads);
-    std::vector<CompactBatch> batches(T);
+    std::vector<Batch> batches(T);
     for (std::uint64_t s = 0; s <= steps; ++s) {  // step 0 is the warm-up (pinned buffers grow once)
       VirginMap v = v0;
       FeedbackResult all;
@@ -208,12 +208,12 @@ int main(int argc, char** argv) {
       for (unsigned t = 0; t < T; ++t) {
         const std::uint64_t first = n * t / T, cnt = n * (t + 1) / T - first;
         if (!cnt) continue;
-        b200::check(hfz_feedback_batch_compact_host(ctx.get(), batches[t].compact(), batches[t].compact_offsets(),
-                                                    batches[t].wide(), batches[t].wide_offsets(), cnt, v.data(),
+        b200::check(hfz_feedback_batch_packed_host(ctx.get(), batches[t].host3(), batches[t].host3_offsets(),
+                                                   batches[t].dev17(), batches[t].dev17_offsets(), cnt, v.data(),
                                                     v.edge_counts(), nullptr, all.admit.data() + first,
                                                     all.sig_full.data() + first, all.sig_simple.data() + first,
                                                     all.nnz.data() + first),
-                    "hfz_feedback_batch_compact_host");
+                    "hfz_feedback_batch_packed_host");
       }
       const double t2 = now();
       if (s) {
@@ -236,7 +236,7 @@ int main(int argc, char** argv) {
   VirginMap vS;
   {
     const unsigned T = threads;
-    std::vector<CompactBatch> batches(T);
+    std::vector<Batch> batches(T);
     for (std::uint64_t s = 0; s <= steps; ++s) {
       VirginMap v = v0;
       FeedbackResult all;
@@ -265,12 +265,12 @@ int main(int argc, char** argv) {
       for (unsigned t = 0; t < T; ++t) {
         const std::uint64_t first = n * t / T, cnt = n * (t + 1) / T - first;
         if (!cnt) continue;
-        b200::check(hfz_feedback_batch_compact_host(ctx.get(), batches[t].compact(), batches[t].compact_offsets(),
-                                                    batches[t].wide(), batches[t].wide_offsets(), cnt, v.data(),
+        b200::check(hfz_feedback_batch_packed_host(ctx.get(), batches[t].host3(), batches[t].host3_offsets(),
+                                                   batches[t].dev17(), batches[t].dev17_offsets(), cnt, v.data(),
                                                     v.edge_counts(), nullptr, all.admit.data() + first,
                                                     all.sig_full.data() + first, all.sig_simple.data() + first,
                                                     all.nnz.data() + first),
-                    "hfz_feedback_batch_compact_host");
+                    "hfz_feedback_batch_packed_host");
       }
       const double fold_s = now() - t1;
       if (s) {
@@ -337,14 +337,14 @@ int main(int argc, char** argv) {
   std::uint64_t pairs = 0;
   for (const CoverageMap& m : maps) pairs += m.touched().size();
   std::printf(
-      "{\"api\": \"hetfuzz::CoverageMap -> b200::CompactBatch::append x N -> hfz_feedback_batch_compact_host -> host vectors\", "
+      "{\"api\": \"hetfuzz::CoverageMap -> b200::PackedBatch::append x N -> hfz_feedback_batch_packed_host -> host vectors\", "
       "\"execs\": %llu, \"steps\": %llu, \"touched_slots_per_exec\": %.1f, \"gen_seconds\": %.2f, "
       "\"value\": %.1f, \"unit\": \"evals/s\", \"pack_threads\": %u, "
       "\"seconds\": {\"mean\": %.6f, \"median\": %.6f, \"min\": %.6f, \"pack_mean\": %.6f, \"fold_and_readback_mean\": %.6f}, "
       "\"one_pack_thread\": {\"value\": %.1f, \"unit\": \"evals/s\", \"seconds\": {\"mean\": %.6f, \"median\": %.6f, \"min\": %.6f, "
       "\"pack_mean\": %.6f, \"fold_and_readback_mean\": %.6f}}, "
       "\"streaming\": {\"value\": %.1f, \"unit\": \"evals/s\", \"pack_threads\": %u, \"seconds\": {\"mean\": %.6f, \"median\": %.6f, "
-      "\"min\": %.6f, \"pack_mean\": %.6f, \"fold_and_readback_mean\": %.6f}, \"what\": \"one reused CoverageMap per worker: CompactBatch::take (append + reset in one walk) right "
+      "\"min\": %.6f, \"pack_mean\": %.6f, \"fold_and_readback_mean\": %.6f}, \"what\": \"one reused CoverageMap per worker: PackedBatch::take (append + reset in one walk) right "
       "after the execution that filled it (cache-hot map); timed = take summed per worker, max over workers, + fold + results\"}, "
       "\"reference_same_maps\": {\"available\": %s, \"threads\": 1, \"seconds\": %.4f, \"value\": %.1f, \"unit\": \"evals/s\", "
       "\"what\": \"classify_trace + 2 x trace_signature + has_new_bits per map (src/engine.cpp:471-478), unmodified reference build, same process\"}, "

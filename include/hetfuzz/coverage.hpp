@@ -134,6 +134,9 @@ class PinnedVec {
   std::uint64_t size() const { return n_; }
   const T* data() const { return buf_; }
   T* data() { return buf_; }
+  // unchecked tail writes after a reserve(): tail()[0 .. k) then advance(k)
+  T* tail() { return buf_ + n_; }
+  void advance(std::uint64_t k) { n_ += k; }
 
  private:
   T* buf_ = nullptr;
@@ -226,6 +229,75 @@ class CompactBatch {
   detail::PinnedVec<std::uint64_t> coff_, woff_;
 };
 
+// The densest host form (include/hfz.h, hfz_feedback_batch_packed_host): three bytes per host-half slot -- slot lo,
+// slot hi, count; every exec padded with zero entries to a multiple of four -- and four per device-half slot,
+// (slot - kHostSlots) | min(count, 65536) << 15 (the device ladder's last rung starts at 65,536: the clip keeps
+// every class).  ~4.1 KB per exec at 2 % density against ~5.0 KB of CompactBatch; the call is PCIe-bound.
+class PackedBatch {
+  static_assert(kMapSize == 65536, "packed lists carry 15-bit slots per half");
+
+ public:
+  PackedBatch() {
+    hoff_.push_back(0);
+    doff_.push_back(0);
+  }
+  void append(const CoverageMap& m) {
+    begin(m.touched().size());
+    for (std::uint32_t slot : m.touched()) put(slot, static_cast<std::uint32_t>(m.count_at(slot)));
+    finish();
+  }
+  // append(m) + m.reset() in one walk (see CompactBatch::take)
+  void take(CoverageMap& m) {
+    begin(m.touched().size());
+    m.drain([this](std::uint32_t slot, std::uint32_t c) { put(slot, c); });
+    finish();
+  }
+  void clear() {
+    host_.clear();
+    dev_.clear();
+    hoff_.clear();
+    doff_.clear();
+    hoff_.push_back(0);
+    doff_.push_back(0);
+  }
+  std::uint64_t size() const { return hoff_.size() - 1; }
+  const std::uint8_t* host3() const { return host_.data(); }
+  const std::uint64_t* host3_offsets() const { return hoff_.data(); }
+  const std::uint32_t* dev17() const { return dev_.data(); }
+  const std::uint64_t* dev17_offsets() const { return doff_.data(); }
+
+ private:
+  // room for one map's entries (all of them could land in either list) + the padding: put() writes unchecked
+  void begin(std::uint64_t touched) {
+    host_.reserve(host_.size() + 3 * touched + 12);
+    dev_.reserve(dev_.size() + touched);
+    h_ = host_.tail();
+    d_ = dev_.tail();
+  }
+  void put(std::uint32_t slot, std::uint32_t c) {
+    if (slot < kHostSlots) {
+      h_[0] = static_cast<std::uint8_t>(slot);
+      h_[1] = static_cast<std::uint8_t>(slot >> 8);
+      h_[2] = static_cast<std::uint8_t>(c);
+      h_ += 3;
+    } else {
+      *d_++ = (slot - kHostSlots) | ((c < 65536u ? c : 65536u) << 15);
+    }
+  }
+  void finish() {
+    host_.advance(static_cast<std::uint64_t>(h_ - host_.tail()));
+    dev_.advance(static_cast<std::uint64_t>(d_ - dev_.tail()));
+    while (host_.size() % 12) host_.push_back(0);  // whole groups of four 3-byte entries
+    hoff_.push_back(host_.size() / 3);
+    doff_.push_back(dev_.size());
+  }
+  std::uint8_t* h_ = nullptr;
+  std::uint32_t* d_ = nullptr;
+  detail::PinnedVec<std::uint8_t> host_;
+  detail::PinnedVec<std::uint32_t> dev_;
+  detail::PinnedVec<std::uint64_t> hoff_, doff_;
+};
+
 // Folds the batch into virgin / edge_counts in exec order (engine.cpp:471-478 per exec).
 inline FeedbackResult feedback_batch(Context& ctx, const SparseBatch& batch, std::uint8_t* virgin,
                                      std::uint64_t* edge_counts, bool want_classed = false) {
@@ -257,6 +329,23 @@ inline FeedbackResult feedback_batch(Context& ctx, const CompactBatch& batch, st
                                         want_classed ? r.classed.data() : nullptr, r.admit.data(),
                                         r.sig_full.data(), r.sig_simple.data(), r.nnz.data()),
         "hfz_feedback_batch_compact_host");
+  return r;
+}
+
+inline FeedbackResult feedback_batch(Context& ctx, const PackedBatch& batch, std::uint8_t* virgin,
+                                     std::uint64_t* edge_counts, bool want_classed = false) {
+  const std::uint64_t n = batch.size();
+  FeedbackResult r;
+  r.admit.resize(n);
+  r.sig_full.resize(n);
+  r.sig_simple.resize(n);
+  r.nnz.resize(n);
+  if (want_classed) r.classed.resize(n * std::uint64_t(ctx.map_slots()));
+  check(hfz_feedback_batch_packed_host(ctx.get(), batch.host3(), batch.host3_offsets(), batch.dev17(),
+                                       batch.dev17_offsets(), n, virgin, edge_counts,
+                                       want_classed ? r.classed.data() : nullptr, r.admit.data(),
+                                       r.sig_full.data(), r.sig_simple.data(), r.nnz.data()),
+        "hfz_feedback_batch_packed_host");
   return r;
 }
 

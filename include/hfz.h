@@ -46,7 +46,7 @@ extern "C" {
 #define HFZ_API __attribute__((visibility("default")))
 #endif
 
-#define HFZ_VERSION 110 /* 0.1.1: + sparse / compact list ingest, peer-memory resolve, serial-stream havoc with host buffers */
+#define HFZ_VERSION 120 /* 0.1.2: + packed list ingest, peer buffers over CUDA IPC (0.1.1: sparse / compact lists, peer-memory resolve, serial-stream havoc with host buffers) */
 
 enum {
   HFZ_OK = 0,
@@ -178,6 +178,23 @@ HFZ_API int hfz_feedback_batch_compact_host(hfz_ctx* ctx, const uint32_t* compac
                                             uint8_t* classed_out_host, uint8_t* admit_out_host,
                                             uint64_t* sig_full_out_host, uint64_t* sig_simple_out_host,
                                             uint32_t* nnz_out_host);
+/* Packed lists, for the reference's map of exactly 65,536 slots (H = 32,768): the same touched-slot lists
+ * at THREE bytes per host-half slot and FOUR per device-half slot, no second list for large counters.
+ *   host3  bytes; entry i = {slot & 0xff, slot >> 8, count u8} at bytes [3i, 3i + 3), slot < 32,768, count 0 =
+ *          ignored.  Exec e owns entries [host3_off[e], host3_off[e+1]); every exec's entry count is padded
+ *          with zero entries to a MULTIPLE OF FOUR (offsets are multiples of four; the base is 4-byte
+ *          aligned), so four entries are three aligned words on the device.
+ *   dev17  u32 words (slot - 32768) | min(count, 65536) << 15: the device ladder's last rung starts at
+ *          65,536 (src/coverage.cpp:21-32), so the clip keeps every class; count 0 = ignored.
+ *          Exec e owns words [dev17_off[e], dev17_off[e+1]).
+ * ~4.1 KB per exec of the bench batch against ~5.0 KB of the compact form: the host call is PCIe-bound, so
+ * that is what it gains.  Everything else as hfz_feedback_batch_compact_host. */
+HFZ_API int hfz_feedback_batch_packed_host(hfz_ctx* ctx, const uint8_t* host3_host, const uint64_t* host3_off_host,
+                                           const uint32_t* dev17_host, const uint64_t* dev17_off_host,
+                                           uint64_t n_exec, uint8_t* virgin_inout_host,
+                                           uint64_t* edge_counts_inout_host, uint8_t* classed_out_host,
+                                           uint8_t* admit_out_host, uint64_t* sig_full_out_host,
+                                           uint64_t* sig_simple_out_host, uint32_t* nnz_out_host);
 /* lists -> dense records (device buffers; raw_maps_out is overwritten, n_exec records) */
 HFZ_API int hfz_expand_sparse(hfz_ctx* ctx, const uint32_t* entries, const uint64_t* entry_off,
                               uint64_t n_exec, uint8_t* raw_maps_out);

@@ -289,6 +289,34 @@ class Context:
             o["classed"] = classed
         return o
 
+    def feedback_batch_packed_host(self, host3: np.ndarray, host3_off: np.ndarray, dev17: np.ndarray,
+                                   dev17_off: np.ndarray, virgin: np.ndarray, edge_counts: np.ndarray,
+                                   want_classed: bool = False):
+        """Touched-slot lists of 65,536-slot maps at 3 bytes per host-half slot (uint8 triples slot lo, slot hi,
+        count; every exec padded to a multiple of four entries) and 4 bytes per device-half slot (uint32 words
+        (slot - 32768) | min(count, 65536) << 15); one uint64 offsets array (in entries) per list."""
+        n = host3_off.size - 1
+        assert host3.dtype == np.uint8 and host3.flags.c_contiguous and host3.ctypes.data % 4 == 0
+        assert dev17.dtype == np.uint32 and dev17.flags.c_contiguous
+        for off in (host3_off, dev17_off):
+            assert off.dtype == np.uint64 and off.size == n + 1 and off.flags.c_contiguous
+        assert virgin.dtype == np.uint8 and virgin.size == self.S
+        assert edge_counts.dtype == np.uint64 and edge_counts.size == 2
+        admit = np.empty(n, np.uint8)
+        sf = np.empty(n, np.uint64)
+        ss = np.empty(n, np.uint64)
+        nnz = np.empty(n, np.uint32)
+        classed = np.empty((n, self.S), np.uint8) if want_classed else None
+        vp = lambda a: None if a is None else C.c_void_p(a.ctypes.data)
+        self._sync_stream()
+        check(lib.hfz_feedback_batch_packed_host(self._h, vp(host3), vp(host3_off), vp(dev17), vp(dev17_off), n,
+                                                 vp(virgin), vp(edge_counts), vp(classed), vp(admit), vp(sf), vp(ss),
+                                                 vp(nnz)))
+        o = dict(admit=admit, sig_full=sf, sig_simple=ss, nnz=nnz)
+        if want_classed:
+            o["classed"] = classed
+        return o
+
     def expand_sparse(self, entries: torch.Tensor, entry_off: torch.Tensor, raw: torch.Tensor | None = None):
         """Touched-slot lists -> dense raw records on the device."""
         n = entry_off.numel() - 1

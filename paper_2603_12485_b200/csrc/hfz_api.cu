@@ -121,6 +121,7 @@ extern "C" int hfz_ctx_destroy(hfz_ctx* c) {
   cudaFree(c->sp_off);
   cudaFree(c->sp_compact);
   cudaFree(c->sp_coff);
+  cudaFree(c->sp_h3);
   cudaFree(c->sp_sorted);
   cudaFree(c->ts_sorted);
   cudaFree(c->ts_cnt);

@@ -88,6 +88,8 @@ struct hfz_ctx {
   uint64_t sp_compact_cap = 0;
   uint64_t* sp_coff = nullptr;
   uint64_t sp_coff_cap = 0;
+  uint32_t* sp_h3 = nullptr;       // device copy of a packed host-half list (3 bytes per entry), in words
+  uint64_t sp_h3_cap = 0;
   std::vector<cudaEvent_t> sp_events;  // one "entries of chunk k copied" event per chunk
   int sparse_native = 1;           // 1 = rank + chain kernels on the lists (S <= 65,536), 0 = expand to dense records
   uint32_t* sp_sorted = nullptr;   // per pair: slot | rung << 24, ascending slots inside an exec
@@ -134,7 +136,9 @@ int hfz_feedback_scan_sparse(hfz_ctx* c, const uint32_t* pairs, const uint64_t* 
                              const uint32_t* compact, const uint64_t* compact_off, uint64_t n_exec,
                              uint64_t total_pairs, const uint8_t* virgin_v0, uint8_t* classed_out,
                              uint64_t* sig_full_out, uint64_t* sig_simple_out, uint32_t* nnz_out,
-                             uint8_t* delta_out, unsigned long long* bad_pairs);
+                             uint8_t* delta_out, unsigned long long* bad_pairs, int packed = 0);
+// packed = 1: `pairs` / `entry_off` are the 3-byte host-half list (entries, every exec a multiple of four) and
+// `compact` / `compact_off` the 17-bit-count device-half list of hfz_feedback_batch_packed_host (include/hfz.h)
 // single-rank second half after a scan with delta_out = NULL: delta + merge + Admit flags in one pass over the table
 int hfz_feedback_fold_single(hfz_ctx* ctx, uint64_t n_exec, uint8_t* virgin_inout, uint64_t* edge_counts_inout,
                              uint8_t* admit_out);

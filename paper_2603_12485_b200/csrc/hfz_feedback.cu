@@ -788,6 +788,9 @@ struct SparseParams {
   const uint64_t* off;
   const uint32_t* cpairs;   // compact pairs slot | count << 16; may be null
   const uint64_t* coff;
+  int packed;               // packed lists: `pairs` / `off` are the host-half list -- 3-byte entries {slot lo, slot hi,
+                            // count u8}, four per three words, every exec padded to a multiple of four (off in entries) --
+                            // and `cpairs` the device-half list (slot - H) | min(count, 65536) << 15
   uint64_t n_exec;
   uint32_t S, H;
   const uint8_t* v0;
@@ -823,6 +826,33 @@ __global__ void __launch_bounds__(kRankWarps * 32, 1) hfz_k_sparse_rank(const Sp
     const uint64_t cb = p.coff ? p.coff[e64] : 0, ct = p.coff ? p.coff[e64 + 1] : 0;
     // calls f(slot, count) for every pair of the exec, four loads in flight per lane
     auto for_pairs = [&](auto&& f) {
+      if (p.packed) {
+        // host half: one group of four 3-byte entries (three aligned words) per lane and step
+        const uint32_t* h3 = reinterpret_cast<const uint32_t*>(p.pairs);
+        for (uint64_t g0 = b / 4; g0 < t / 4; g0 += 32) {
+          const uint64_t g = g0 + lane;
+          uint32_t w0 = 0, w1 = 0, w2 = 0;
+          if (g < t / 4) {
+            w0 = __ldg(h3 + 3 * g);
+            w1 = __ldg(h3 + 3 * g + 1);
+            w2 = __ldg(h3 + 3 * g + 2);
+          }
+          const uint32_t en[4] = {w0 & 0xffffffu, (w0 >> 24) | ((w1 & 0xffffu) << 8), (w1 >> 16) | ((w2 & 0xffu) << 16), w2 >> 8};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) f(en[j] & 0xffffu, en[j] >> 16);
+        }
+        for (uint64_t i0 = cb; i0 < ct; i0 += 128) {
+          uint32_t x[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint64_t i = i0 + j * 32 + lane;
+            x[j] = i < ct ? __ldg(p.cpairs + i) : 0u;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) f(p.H + (x[j] & 0x7fffu), x[j] >> 15);
+        }
+        return;
+      }
       for (uint64_t i0 = b; i0 < t; i0 += 128) {
         uint2 x[4];
 #pragma unroll
@@ -1999,7 +2029,7 @@ int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t
                              const uint32_t* compact, const uint64_t* compact_off, uint64_t n_exec,
                              uint64_t total_pairs, const uint8_t* virgin_v0, uint8_t* classed_out,
                              uint64_t* sig_full_out, uint64_t* sig_simple_out, uint32_t* nnz_out,
-                             uint8_t* delta_out, unsigned long long* bad_pairs) {
+                             uint8_t* delta_out, unsigned long long* bad_pairs, int packed) {
   if (n_exec >= 0xfffffffeull) {
     hfz_set_error("hfz_feedback_scan_sparse: n_exec too large");
     return HFZ_ECAP;
@@ -2030,6 +2060,7 @@ int hfz_feedback_scan_sparse(hfz_ctx* ctx, const uint32_t* pairs, const uint64_t
     p.off = entry_off;
     p.cpairs = compact;
     p.coff = compact_off;
+    p.packed = packed;
     p.n_exec = n_exec;
     p.S = ctx->S;
     p.H = ctx->H;

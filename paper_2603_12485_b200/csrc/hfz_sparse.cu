@@ -108,7 +108,7 @@ int fold_chunks(hfz_ctx* c, const uint32_t* entries, const uint64_t* off, const 
                 const uint64_t* coff, uint64_t n_exec, uint64_t C,
                 bool native, uint64_t total_pairs, uint8_t* virgin, uint64_t* counts, uint8_t* classed_dev,
                 uint8_t* classed_host, uint8_t* admit, uint64_t* sigf, uint64_t* sigs, uint32_t* nnz,
-                const cudaEvent_t* events) {
+                const cudaEvent_t* events, int packed = 0) {
   if (!native) c->sp_dirty = true;  // until the last cleanup pass has been enqueued
   uint64_t k = 0;
   for (uint64_t done = 0; done < n_exec; done += C, ++k) {
@@ -119,7 +119,7 @@ int fold_chunks(hfz_ctx* c, const uint32_t* entries, const uint64_t* off, const 
     if (native) {
       rc = hfz_feedback_scan_sparse(c, entries, off ? off + done : nullptr, compact, coff ? coff + done : nullptr, n,
                                     total_pairs, virgin, cls, sigf + done, sigs + done,
-                                    nnz ? nnz + done : nullptr, nullptr, c->d_small + kBadSlot);
+                                    nnz ? nnz + done : nullptr, nullptr, c->d_small + kBadSlot, packed);
       if (rc) return rc;
       rc = hfz_feedback_fold_single(c, n, virgin, counts, admit + done);
       if (rc) return rc;
@@ -297,6 +297,84 @@ int sparse_host_impl(hfz_ctx* c, const uint32_t* entries, const uint64_t* entry_
   return HFZ_OK;
 }
 
+// Packed lists (include/hfz.h, hfz_feedback_batch_packed_host): host half 3 bytes per entry, device half 4 bytes with a
+// 17-bit count -- ~4.1 KB per exec of the bench batch against ~5.0 KB of the compact form.  Same streaming as above.
+int packed_host_impl(hfz_ctx* c, const uint8_t* host3, const uint64_t* host3_off, const uint32_t* dev17,
+                     const uint64_t* dev17_off, uint64_t n_exec, uint8_t* virgin, uint64_t* counts, uint8_t* classed,
+                     uint8_t* admit, uint64_t* sigf, uint64_t* sigs, uint32_t* nnz) {
+  const char* who = "hfz_feedback_batch_packed_host";
+  if (!c || !virgin || !counts || (n_exec && (!host3_off || !dev17_off || !admit || !sigf || !sigs))) {
+    hfz_set_error("%s: null argument", who);
+    return HFZ_EINVAL;
+  }
+  if (n_exec == 0) return HFZ_OK;
+  const uint64_t htotal = host3_off[n_exec], dtotal = dev17_off[n_exec];
+  if ((htotal > host3_off[0] && !host3) || (dtotal > dev17_off[0] && !dev17) || ((uintptr_t)host3 & 3)) {
+    hfz_set_error("%s: a list has entries but its pointer is null, or host3 is not 4-byte aligned", who);
+    return HFZ_EINVAL;
+  }
+  int rc;
+  if ((rc = check_offsets(who, host3_off, n_exec))) return rc;
+  if ((rc = check_offsets(who, dev17_off, n_exec))) return rc;
+  for (uint64_t e = 0; e <= n_exec; ++e)
+    if (host3_off[e] & 3) {
+      hfz_set_error("%s: host3_off[%llu] is not a multiple of four entries (pad every exec with zero entries)", who,
+                    (unsigned long long)e);
+      return HFZ_EINVAL;
+    }
+  HFZ_CUDA(cudaSetDevice(c->device));
+  if ((rc = hfz_ensure_host_common(c, n_exec))) return rc;
+  if (!hfz_sparse_native_ok(c) || c->S != 65536u) {
+    hfz_set_error("%s: packed lists need the list-native fold and map_slots = 65536 (15-bit slots per half)", who);
+    return HFZ_EINVAL;
+  }
+  const uint64_t C = c->sparse_chunk ? c->sparse_chunk : 4096;
+  const uint64_t n_chunks = (n_exec + C - 1) / C;
+  if (classed && (rc = hfz_ensure_classed_stage(c, n_exec < C ? n_exec : C))) return rc;
+  // device copies keep the absolute indexing (entries below off[0] are never read); the host list in words: 3 per 4 entries
+  if ((rc = grow(reinterpret_cast<void**>(&c->sp_h3), &c->sp_h3_cap, htotal / 4 * 3 + 4, 4))) return rc;
+  if ((rc = grow(reinterpret_cast<void**>(&c->sp_off), &c->sp_off_cap, n_exec + 1, 8))) return rc;
+  if ((rc = grow(reinterpret_cast<void**>(&c->sp_compact), &c->sp_compact_cap, dtotal, 4))) return rc;
+  if ((rc = grow(reinterpret_cast<void**>(&c->sp_coff), &c->sp_coff_cap, n_exec + 1, 8))) return rc;
+  while (c->sp_events.size() < n_chunks) {
+    cudaEvent_t ev;
+    HFZ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    c->sp_events.push_back(ev);
+  }
+  cudaStream_t st = c->stream;
+  HFZ_CUDA(cudaMemcpyAsync(c->sp_off, host3_off, (n_exec + 1) * 8, cudaMemcpyHostToDevice, st));
+  HFZ_CUDA(cudaMemcpyAsync(c->sp_coff, dev17_off, (n_exec + 1) * 8, cudaMemcpyHostToDevice, st));
+  HFZ_CUDA(cudaMemcpyAsync(c->d_virgin, virgin, c->S, cudaMemcpyHostToDevice, st));
+  HFZ_CUDA(cudaMemcpyAsync(c->d_counts, counts, 16, cudaMemcpyHostToDevice, st));
+  HFZ_CUDA(cudaMemsetAsync(c->d_small + kBadSlot, 0, sizeof(unsigned long long), st));
+  uint8_t* d_h3 = reinterpret_cast<uint8_t*>(c->sp_h3);
+  for (uint64_t k = 0; k < n_chunks; ++k) {
+    const uint64_t e0 = k * C, e1 = e0 + C < n_exec ? e0 + C : n_exec;
+    if (host3_off[e1] > host3_off[e0])
+      HFZ_CUDA(cudaMemcpyAsync(d_h3 + 3 * host3_off[e0], host3 + 3 * host3_off[e0], (host3_off[e1] - host3_off[e0]) * 3,
+                               cudaMemcpyHostToDevice, c->copy_stream));
+    if (dev17_off[e1] > dev17_off[e0])
+      HFZ_CUDA(cudaMemcpyAsync(c->sp_compact + dev17_off[e0], dev17 + dev17_off[e0], (dev17_off[e1] - dev17_off[e0]) * 4,
+                               cudaMemcpyHostToDevice, c->copy_stream));
+    HFZ_CUDA(cudaEventRecord(c->sp_events[k], c->copy_stream));
+  }
+  rc = fold_chunks(c, c->sp_h3, c->sp_off, c->sp_compact, c->sp_coff, n_exec, C, true, htotal + dtotal, c->d_virgin,
+                   c->d_counts, nullptr, classed, c->d_admit, c->d_sigf, c->d_sigs, c->d_nnz, c->sp_events.data(), 1);
+  if (rc) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamSynchronize(st);
+    return rc;
+  }
+  HFZ_CUDA(cudaMemcpyAsync(admit, c->d_admit, n_exec, cudaMemcpyDeviceToHost, st));
+  HFZ_CUDA(cudaMemcpyAsync(sigf, c->d_sigf, n_exec * 8, cudaMemcpyDeviceToHost, st));
+  HFZ_CUDA(cudaMemcpyAsync(sigs, c->d_sigs, n_exec * 8, cudaMemcpyDeviceToHost, st));
+  if (nnz) HFZ_CUDA(cudaMemcpyAsync(nnz, c->d_nnz, n_exec * 4, cudaMemcpyDeviceToHost, st));
+  HFZ_CUDA(cudaMemcpyAsync(virgin, c->d_virgin, c->S, cudaMemcpyDeviceToHost, st));
+  HFZ_CUDA(cudaMemcpyAsync(counts, c->d_counts, 16, cudaMemcpyDeviceToHost, st));
+  HFZ_CUDA(cudaStreamSynchronize(st));
+  return HFZ_OK;
+}
+
 }  // namespace
 
 extern "C" int hfz_feedback_batch_sparse_host(hfz_ctx* c, const uint32_t* entries, const uint64_t* entry_off,
@@ -321,6 +399,13 @@ extern "C" int hfz_feedback_batch_compact_host(hfz_ctx* c, const uint32_t* compa
   }
   return sparse_host_impl(c, wide, wide_off, compact, compact_off, n_exec, virgin, counts, classed, admit, sigf, sigs,
                           nnz);
+}
+
+extern "C" int hfz_feedback_batch_packed_host(hfz_ctx* c, const uint8_t* host3, const uint64_t* host3_off,
+                                              const uint32_t* dev17, const uint64_t* dev17_off, uint64_t n_exec,
+                                              uint8_t* virgin, uint64_t* counts, uint8_t* classed, uint8_t* admit,
+                                              uint64_t* sigf, uint64_t* sigs, uint32_t* nnz) {
+  return packed_host_impl(c, host3, host3_off, dev17, dev17_off, n_exec, virgin, counts, classed, admit, sigf, sigs, nnz);
 }
 
 extern "C" int hfz_expand_sparse(hfz_ctx* c, const uint32_t* entries, const uint64_t* entry_off,

@@ -202,6 +202,34 @@ def to_compact(raw: np.ndarray, n_exec: int, S: int = 65536, shuffle_seed: int |
     return np.ascontiguousarray(compact), coff, wide, woff
 
 
+def to_packed(raw: np.ndarray, n_exec: int, S: int = 65536, shuffle_seed: int | None = 1):
+    """Dense records -> the packed list form of hfz_feedback_batch_packed_host (S = 65,536): (host3 uint8 bytes, three
+    per host-half slot -- slot lo, slot hi, count -- every exec padded with zero entries to a multiple of four,
+    host3_off in entries; dev17 uint32 words (slot - H) | min(count, 65536) << 15, dev17_off)."""
+    assert S == 65536
+    H = S // 2
+    entries, off = to_sparse(raw, n_exec, S, shuffle_seed)
+    rows = np.repeat(np.arange(n_exec), np.diff(off).astype(np.int64))
+    is_host = entries[:, 0] < H
+    nh = np.bincount(rows[is_host], minlength=n_exec).astype(np.int64)
+    nh_pad = (nh + 3) // 4 * 4
+    hoff = np.zeros(n_exec + 1, np.uint64)
+    np.cumsum(nh_pad, out=hoff[1:])
+    host3 = np.zeros((int(hoff[-1]), 3), np.uint8)
+    hrows = rows[is_host]
+    within = np.arange(hrows.size) - np.repeat(np.cumsum(nh) - nh, nh)  # index of each host entry inside its exec
+    dst = hoff[:-1].astype(np.int64)[hrows] + within
+    hs = entries[is_host]
+    host3[dst, 0] = hs[:, 0] & 0xFF
+    host3[dst, 1] = hs[:, 0] >> 8
+    host3[dst, 2] = hs[:, 1]
+    ds = entries[~is_host]
+    dev17 = ((ds[:, 0] - np.uint32(H)) | (np.minimum(ds[:, 1], np.uint32(65536)) << np.uint32(15))).astype(np.uint32)
+    doff = np.zeros(n_exec + 1, np.uint64)
+    np.cumsum(np.bincount(rows[~is_host], minlength=n_exec), out=doff[1:])
+    return np.ascontiguousarray(host3.reshape(-1)), hoff, np.ascontiguousarray(dev17), doff
+
+
 # ---- havoc seeds (config 4) ---------------------------------------------------
 
 def havoc_inputs(n: int, seed: int = 45, lo: int = 1024, hi: int = 4096):

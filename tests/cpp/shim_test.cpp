@@ -142,6 +142,14 @@ int main() {
     for (std::uint32_t i = 0; i < kMapSize; ++i) same = same && va.at(i) == vb.at(i);
     REQUIRE(same);
     REQUIRE(va.host_edges() > 0 && va.device_edges() > 0);
+    // the packed form (3-byte host entries, 17-bit device counts): the same results again
+    b200::PackedBatch pbatch;
+    for (int e = 0; e < n; ++e) pbatch.append(maps[e]);
+    VirginMap vp;
+    b200::FeedbackResult pp = b200::feedback_batch(b200::default_context(), pbatch, vp.data(), vp.edge_counts(), true);
+    REQUIRE(a.admit == pp.admit && a.sig_full == pp.sig_full && a.sig_simple == pp.sig_simple && a.nnz == pp.nnz);
+    REQUIRE(a.classed == pp.classed);
+    REQUIRE(va.host_edges() == vp.host_edges() && va.device_edges() == vp.device_edges());
     // take() = append() + reset() in one walk: the same batch, and the maps end up all-zero and reusable
     b200::CompactBatch tbatch;
     for (int e = 0; e < n; ++e) tbatch.take(maps[e]);

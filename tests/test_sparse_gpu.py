@@ -267,6 +267,81 @@ def test_compact_lists_equal_oracle(checker, mode):
         c.close()
 
 
+@pytest.mark.parametrize("mode", ["campaign", "iid", "edge"])
+def test_packed_lists_equal_oracle(checker, mode):
+    """The packed form: 3-byte host-half entries (every exec padded to a multiple of four), 4-byte device-half
+    entries with the count clipped at 65,536 (the last rung's lower bound: every class survives the clip)."""
+    c = hfz.Context(0)
+    try:
+        if mode == "edge":
+            raw, n = synth.maps_edge_cases(S)
+        else:
+            n = 5000 if mode == "campaign" else 500  # 5,000 execs: two chunks of the H2D stream
+            raw = synth.maps_iid(n, S, seed=81) if mode == "iid" else synth.maps_campaign(n, S, seed=82, p_extra=8, p_rare=8)
+        h3, hoff, d17, doff = synth.to_packed(raw, n, S, shuffle_seed=13)
+        assert int((d17 >> 15).max()) == 65536 and (hoff % 4 == 0).all()
+        v, cnt = np.zeros(S, np.uint8), np.zeros(2, np.uint64)
+        want_classed = n <= 1000
+        got = c.feedback_batch_packed_host(h3, hoff, d17, doff, v, cnt, want_classed=want_classed)
+        if want_classed:
+            check_host(c, got, v, cnt, cpu(checker, raw, n))
+        else:
+            wo, wv, wc = cpu(checker, raw, n, want_classed=False)
+            for key in wo:
+                assert np.array_equal(got[key], wo[key]), key
+            assert np.array_equal(v, wv) and np.array_equal(cnt, wc)
+        # sub-range folds through absolute offsets
+        v2, cnt2 = np.zeros(S, np.uint8), np.zeros(2, np.uint64)
+        k = n // 3
+        a = c.feedback_batch_packed_host(h3, hoff[:k + 1].copy(), d17, doff[:k + 1].copy(), v2, cnt2)
+        b = c.feedback_batch_packed_host(h3, hoff[k:].copy(), d17, doff[k:].copy(), v2, cnt2)
+        assert np.array_equal(np.concatenate([a["admit"], b["admit"]]), got["admit"])
+        assert np.array_equal(np.concatenate([a["sig_full"], b["sig_full"]]), got["sig_full"])
+        assert np.array_equal(v2, v) and np.array_equal(cnt2, cnt)
+    finally:
+        c.close()
+
+
+def test_packed_lists_corner_cases_and_rejections(checker):
+    c = hfz.Context(0)
+    try:
+        H = S // 2
+        v, cnt = np.zeros(S, np.uint8), np.zeros(2, np.uint64)
+        # exec 0: nothing; exec 1: host slots only (5 entries + 3 padding); exec 2: device slots only, one of
+        # them listed with count 0 (ignored); exec 3: the last slot of each half
+        h3 = np.zeros((12, 3), np.uint8)
+        for i, (slot, count) in enumerate([(7, 1), (300, 255), (32767, 9), (256, 4), (1, 128)]):
+            h3[i] = (slot & 0xFF, slot >> 8, count)
+        h3[8] = (0xFF, 0x7F, 3)  # exec 3: slot 32767
+        hoff = np.array([0, 0, 8, 8, 12], np.uint64)
+        d17 = np.array([5 | 65536 << 15, 9 | 0 << 15, 10 | 2 << 15, 32767 | 600 << 15], np.uint32)  # 70,000 clipped to 65,536
+        doff = np.array([0, 0, 0, 3, 4], np.uint64)
+        raw = np.zeros((4, 5 * H), np.uint8)
+        for slot, count in [(7, 1), (300, 255), (32767, 9), (256, 4), (1, 128)]:
+            raw[1, slot] = count
+        dev = raw[:, H:].view(np.uint32)
+        dev[2, 5] = 70000
+        dev[2, 10] = 2
+        raw[3, 32767] = 3
+        dev[3, 32767] = 600
+        got = c.feedback_batch_packed_host(np.ascontiguousarray(h3.reshape(-1)), hoff, d17, doff, v, cnt, want_classed=True)
+        check_host(c, got, v, cnt, cpu(checker, np.ascontiguousarray(raw.reshape(-1)), 4))
+        assert got["nnz"].tolist() == [0, 5, 2, 2]
+        with pytest.raises(HfzError):  # an exec's host list that is not padded to four entries
+            c.feedback_batch_packed_host(np.ascontiguousarray(h3.reshape(-1)), np.array([0, 5, 8, 8, 12], np.uint64), d17, doff, v, cnt)
+        with pytest.raises(HfzError):  # decreasing offsets
+            c.feedback_batch_packed_host(np.ascontiguousarray(h3.reshape(-1)), hoff, d17, np.array([0, 3, 0, 3, 4], np.uint64), v, cnt)
+        c2 = hfz.Context(0, 262144)
+        try:
+            with pytest.raises(HfzError):  # 15-bit slots per half: the 65,536-slot map only
+                c2.feedback_batch_packed_host(np.ascontiguousarray(h3.reshape(-1)), hoff, d17, doff,
+                                              np.zeros(262144, np.uint8), np.zeros(2, np.uint64))
+        finally:
+            c2.close()
+    finally:
+        c.close()
+
+
 def test_compact_without_wide_list_and_rejections(checker):
     c = hfz.Context(0)
     try:
