@@ -137,7 +137,7 @@ extern "C" int hfz_ctx_destroy(hfz_ctx* c) {
 extern "C" int hfz_ctx_set_stream(hfz_ctx* c, void* stream) {
   if (!c) return HFZ_EINVAL;
   if (c->stream == (cudaStream_t)stream) return HFZ_OK;
-  // The context's scratch (first-occurrence tables, candidate lists, prior, piece lists) is shared by
+  // The context's scratch (first-occurrence tables, Admit flags, prior, piece lists) is shared by
   // all calls: work already enqueued on the old stream must finish before the new stream touches it.
   HFZ_CUDA(cudaSetDevice(c->device));
   if (!c->ev_stream) HFZ_CUDA(cudaEventCreateWithFlags(&c->ev_stream, cudaEventDisableTiming));
