@@ -954,9 +954,10 @@ def run_ours(args):
         ctx.get_stat("scan_ms_total")
 
     # --- end-to-end through the C-ABI with HOST buffers (pinned), copies inside the timed region.
-    # Host forms of the same batch: (a) touched-slot lists -- what hetfuzz::b200::CompactBatch /
-    # SparseBatch keep per CoverageMap -- at 4 bytes per pair (hfz_feedback_batch_compact_host) and at
-    # 8 bytes per pair (hfz_feedback_batch_sparse_host); (b) dense 163,840-byte records through
+    # Host forms of the same batch: (a) touched-slot lists -- what hetfuzz::b200::PackedBatch / CompactBatch /
+    # SparseBatch keep per CoverageMap -- packed at 3 / 4 bytes per slot (hfz_feedback_batch_packed_host: the `e2e`
+    # key), at 4 bytes per pair + wide pairs (hfz_feedback_batch_compact_host) and at 8 bytes per pair
+    # (hfz_feedback_batch_sparse_host); (b) dense 163,840-byte records through
     # hfz_feedback_batch_host (PCIe-bound).
     e2e = None
     e2e_compact = None
@@ -1148,7 +1149,7 @@ def run_ours(args):
 
 def run_coveragemap_harness(args):
     """bench/e2e_coveragemap (C++): builds hetfuzz::CoverageMap objects from the synthetic recipe, then
-    times CompactBatch::append x N + the fold + result read-back as one region, and the reference's
+    times PackedBatch::append x N + the fold + result read-back as one region, and the reference's
     engine.cpp:471-478 loop on the same maps in the same binary.  Returns its JSON or a reason."""
     exe = os.path.join(ROOT, "bench", "e2e_coveragemap")
     if not os.path.exists(exe):
