@@ -205,15 +205,22 @@ int main(int argc, char** argv) {
         for (auto& x : th) x.join();
       }
       const double t1 = now();
-      for (unsigned t = 0; t < T; ++t) {
-        const std::uint64_t first = n * t / T, cnt = n * (t + 1) / T - first;
-        if (!cnt) continue;
-        b200::check(hfz_feedback_batch_packed_host(ctx.get(), batches[t].host3(), batches[t].host3_offsets(),
-                                                   batches[t].dev17(), batches[t].dev17_offsets(), cnt, v.data(),
-                                                    v.edge_counts(), nullptr, all.admit.data() + first,
-                                                    all.sig_full.data() + first, all.sig_simple.data() + first,
-                                                    all.nnz.data() + first),
-                    "hfz_feedback_batch_packed_host");
+      {  // the workers' batches in exec order, ONE device call (batch k + 1 crosses PCIe under the fold of batch k)
+        std::vector<const std::uint8_t*> h3;
+        std::vector<const std::uint64_t*> hoff, doff;
+        std::vector<const std::uint32_t*> d17;
+        std::vector<std::uint64_t> cnts;
+        for (unsigned t = 0; t < T; ++t) {
+          h3.push_back(batches[t].host3());
+          hoff.push_back(batches[t].host3_offsets());
+          d17.push_back(batches[t].dev17());
+          doff.push_back(batches[t].dev17_offsets());
+          cnts.push_back(batches[t].size());
+        }
+        b200::check(hfz_feedback_batch_packed_host_v(ctx.get(), T, h3.data(), hoff.data(), d17.data(), doff.data(), cnts.data(),
+                                                     v.data(), v.edge_counts(), all.admit.data(), all.sig_full.data(),
+                                                     all.sig_simple.data(), all.nnz.data()),
+                    "hfz_feedback_batch_packed_host_v");
       }
       const double t2 = now();
       if (s) {
@@ -262,15 +269,22 @@ int main(int argc, char** argv) {
       for (auto& x : th) x.join();
       const double pack_s = *std::max_element(worker_s.begin(), worker_s.end());
       const double t1 = now();
-      for (unsigned t = 0; t < T; ++t) {
-        const std::uint64_t first = n * t / T, cnt = n * (t + 1) / T - first;
-        if (!cnt) continue;
-        b200::check(hfz_feedback_batch_packed_host(ctx.get(), batches[t].host3(), batches[t].host3_offsets(),
-                                                   batches[t].dev17(), batches[t].dev17_offsets(), cnt, v.data(),
-                                                    v.edge_counts(), nullptr, all.admit.data() + first,
-                                                    all.sig_full.data() + first, all.sig_simple.data() + first,
-                                                    all.nnz.data() + first),
-                    "hfz_feedback_batch_packed_host");
+      {  // the workers' batches in exec order, ONE device call (batch k + 1 crosses PCIe under the fold of batch k)
+        std::vector<const std::uint8_t*> h3;
+        std::vector<const std::uint64_t*> hoff, doff;
+        std::vector<const std::uint32_t*> d17;
+        std::vector<std::uint64_t> cnts;
+        for (unsigned t = 0; t < T; ++t) {
+          h3.push_back(batches[t].host3());
+          hoff.push_back(batches[t].host3_offsets());
+          d17.push_back(batches[t].dev17());
+          doff.push_back(batches[t].dev17_offsets());
+          cnts.push_back(batches[t].size());
+        }
+        b200::check(hfz_feedback_batch_packed_host_v(ctx.get(), T, h3.data(), hoff.data(), d17.data(), doff.data(), cnts.data(),
+                                                     v.data(), v.edge_counts(), all.admit.data(), all.sig_full.data(),
+                                                     all.sig_simple.data(), all.nnz.data()),
+                    "hfz_feedback_batch_packed_host_v");
       }
       const double fold_s = now() - t1;
       if (s) {
@@ -337,7 +351,7 @@ int main(int argc, char** argv) {
   std::uint64_t pairs = 0;
   for (const CoverageMap& m : maps) pairs += m.touched().size();
   std::printf(
-      "{\"api\": \"hetfuzz::CoverageMap -> b200::PackedBatch::append x N -> hfz_feedback_batch_packed_host -> host vectors\", "
+      "{\"api\": \"hetfuzz::CoverageMap -> b200::PackedBatch::append x N (one batch per packing thread) -> hfz_feedback_batch_packed_host_v (one call) -> host vectors\", "
       "\"execs\": %llu, \"steps\": %llu, \"touched_slots_per_exec\": %.1f, \"gen_seconds\": %.2f, "
       "\"value\": %.1f, \"unit\": \"evals/s\", \"pack_threads\": %u, "
       "\"seconds\": {\"mean\": %.6f, \"median\": %.6f, \"min\": %.6f, \"pack_mean\": %.6f, \"fold_and_readback_mean\": %.6f}, "

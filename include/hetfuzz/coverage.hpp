@@ -349,6 +349,35 @@ inline FeedbackResult feedback_batch(Context& ctx, const PackedBatch& batch, std
   return r;
 }
 
+// Several packed batches (one per packing thread, say) folded in the order given by ONE device call: batch k + 1
+// crosses PCIe under the fold of batch k.  The results hold the execs of all batches, in batch order.
+inline FeedbackResult feedback_batch(Context& ctx, const std::vector<const PackedBatch*>& batches, std::uint8_t* virgin,
+                                     std::uint64_t* edge_counts) {
+  std::vector<const std::uint8_t*> h3;
+  std::vector<const std::uint64_t*> hoff, doff;
+  std::vector<const std::uint32_t*> d17;
+  std::vector<std::uint64_t> n;
+  std::uint64_t total = 0;
+  for (const PackedBatch* b : batches) {
+    h3.push_back(b->host3());
+    hoff.push_back(b->host3_offsets());
+    d17.push_back(b->dev17());
+    doff.push_back(b->dev17_offsets());
+    n.push_back(b->size());
+    total += b->size();
+  }
+  FeedbackResult r;
+  r.admit.resize(total);
+  r.sig_full.resize(total);
+  r.sig_simple.resize(total);
+  r.nnz.resize(total);
+  check(hfz_feedback_batch_packed_host_v(ctx.get(), static_cast<std::uint32_t>(batches.size()), h3.data(), hoff.data(),
+                                         d17.data(), doff.data(), n.data(), virgin, edge_counts, r.admit.data(),
+                                         r.sig_full.data(), r.sig_simple.data(), r.nnz.data()),
+        "hfz_feedback_batch_packed_host_v");
+  return r;
+}
+
 }  // namespace b200
 
 struct HostEdgeState {

@@ -195,6 +195,17 @@ HFZ_API int hfz_feedback_batch_packed_host(hfz_ctx* ctx, const uint8_t* host3_ho
                                            uint64_t* edge_counts_inout_host, uint8_t* classed_out_host,
                                            uint8_t* admit_out_host, uint64_t* sig_full_out_host,
                                            uint64_t* sig_simple_out_host, uint32_t* nnz_out_host);
+/* The same over SEVERAL packed batches -- one per packing thread of the host, say -- folded in the order given by
+ * ONE call: every list is queued on the copy stream up front, batch k + 1 streams in under the fold of batch k,
+ * and the call synchronises once.  host3[k] / host3_off[k] / dev17[k] / dev17_off[k] / n_exec[k] describe batch k
+ * as above (HOST arrays of n_batches pointers / counts); the outputs hold sum(n_exec) entries in batch order.
+ * Classed maps are not returned by this form. */
+HFZ_API int hfz_feedback_batch_packed_host_v(hfz_ctx* ctx, uint32_t n_batches, const uint8_t* const* host3_host,
+                                             const uint64_t* const* host3_off_host, const uint32_t* const* dev17_host,
+                                             const uint64_t* const* dev17_off_host, const uint64_t* n_exec,
+                                             uint8_t* virgin_inout_host, uint64_t* edge_counts_inout_host,
+                                             uint8_t* admit_out_host, uint64_t* sig_full_out_host,
+                                             uint64_t* sig_simple_out_host, uint32_t* nnz_out_host);
 /* lists -> dense records (device buffers; raw_maps_out is overwritten, n_exec records) */
 HFZ_API int hfz_expand_sparse(hfz_ctx* ctx, const uint32_t* entries, const uint64_t* entry_off,
                               uint64_t n_exec, uint8_t* raw_maps_out);

@@ -37,6 +37,7 @@ PROTOTYPES = {
     "hfz_feedback_batch_sparse_host": (C.c_int, [_vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hfz_feedback_batch_compact_host": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hfz_feedback_batch_packed_host": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hfz_feedback_batch_packed_host_v": (C.c_int, [_vp, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hfz_expand_sparse": (C.c_int, [_vp, _vp, _vp, _u64, _vp]),
     "hfz_host_alloc": (C.c_int, [C.POINTER(_vp), _u64]),
     "hfz_host_free": (C.c_int, [_vp]),

@@ -297,78 +297,134 @@ int sparse_host_impl(hfz_ctx* c, const uint32_t* entries, const uint64_t* entry_
   return HFZ_OK;
 }
 
-// Packed lists (include/hfz.h, hfz_feedback_batch_packed_host): host half 3 bytes per entry, device half 4 bytes with a
-// 17-bit count -- ~4.1 KB per exec of the bench batch against ~5.0 KB of the compact form.  Same streaming as above.
-int packed_host_impl(hfz_ctx* c, const uint8_t* host3, const uint64_t* host3_off, const uint32_t* dev17,
-                     const uint64_t* dev17_off, uint64_t n_exec, uint8_t* virgin, uint64_t* counts, uint8_t* classed,
-                     uint8_t* admit, uint64_t* sigf, uint64_t* sigs, uint32_t* nnz) {
-  const char* who = "hfz_feedback_batch_packed_host";
-  if (!c || !virgin || !counts || (n_exec && (!host3_off || !dev17_off || !admit || !sigf || !sigs))) {
+// Packed lists (include/hfz.h, hfz_feedback_batch_packed_host[_v]): host half 3 bytes per entry, device half 4 bytes
+// with a 17-bit count -- ~4.1 KB per exec of the bench batch against ~5.0 KB of the compact form.  Same streaming as
+// above, over one batch or over several (one per packing thread of the host, folded in the order given): every list
+// of every batch is queued on the copy stream up front, the folds follow chunk by chunk, ONE synchronisation at the end.
+int packed_host_impl(hfz_ctx* c, uint32_t n_batches, const uint8_t* const* host3, const uint64_t* const* host3_off,
+                     const uint32_t* const* dev17, const uint64_t* const* dev17_off, const uint64_t* n_exec,
+                     uint8_t* virgin, uint64_t* counts, uint8_t* classed, uint8_t* admit, uint64_t* sigf, uint64_t* sigs,
+                     uint32_t* nnz) {
+  const char* who = n_batches == 1 ? "hfz_feedback_batch_packed_host" : "hfz_feedback_batch_packed_host_v";
+  if (!c || !virgin || !counts || !host3 || !host3_off || !dev17 || !dev17_off || !n_exec) {
     hfz_set_error("%s: null argument", who);
     return HFZ_EINVAL;
   }
-  if (n_exec == 0) return HFZ_OK;
-  const uint64_t htotal = host3_off[n_exec], dtotal = dev17_off[n_exec];
-  if ((htotal > host3_off[0] && !host3) || (dtotal > dev17_off[0] && !dev17) || ((uintptr_t)host3 & 3)) {
-    hfz_set_error("%s: a list has entries but its pointer is null, or host3 is not 4-byte aligned", who);
-    return HFZ_EINVAL;
-  }
+  uint64_t n_total = 0, h_words = 0, d_words = 0, n_chunks = 0, max_pairs = 0;
+  const uint64_t C = c->sparse_chunk ? c->sparse_chunk : 4096;
   int rc;
-  if ((rc = check_offsets(who, host3_off, n_exec))) return rc;
-  if ((rc = check_offsets(who, dev17_off, n_exec))) return rc;
-  for (uint64_t e = 0; e <= n_exec; ++e)
-    if (host3_off[e] & 3) {
-      hfz_set_error("%s: host3_off[%llu] is not a multiple of four entries (pad every exec with zero entries)", who,
-                    (unsigned long long)e);
+  for (uint32_t k = 0; k < n_batches; ++k) {
+    const uint64_t n = n_exec[k];
+    if (n == 0) continue;
+    if (!host3_off[k] || !dev17_off[k]) {
+      hfz_set_error("%s: batch %u has execs but no offsets", who, k);
       return HFZ_EINVAL;
     }
+    const uint64_t htotal = host3_off[k][n], dtotal = dev17_off[k][n];
+    if ((htotal > host3_off[k][0] && !host3[k]) || (dtotal > dev17_off[k][0] && !dev17[k]) || ((uintptr_t)host3[k] & 3)) {
+      hfz_set_error("%s: a list has entries but its pointer is null, or host3 is not 4-byte aligned", who);
+      return HFZ_EINVAL;
+    }
+    if ((rc = check_offsets(who, host3_off[k], n))) return rc;
+    if ((rc = check_offsets(who, dev17_off[k], n))) return rc;
+    for (uint64_t e = 0; e <= n; ++e)
+      if (host3_off[k][e] & 3) {
+        hfz_set_error("%s: host3_off[%llu] is not a multiple of four entries (pad every exec with zero entries)", who,
+                      (unsigned long long)e);
+        return HFZ_EINVAL;
+      }
+    n_total += n;
+    h_words += htotal / 4 * 3;
+    d_words += dtotal;
+    n_chunks += (n + C - 1) / C;
+    if (htotal + dtotal > max_pairs) max_pairs = htotal + dtotal;
+  }
+  if (n_total == 0) return HFZ_OK;
+  if (!admit || !sigf || !sigs) {
+    hfz_set_error("%s: null argument", who);
+    return HFZ_EINVAL;
+  }
+  if (classed && n_batches != 1) {
+    hfz_set_error("%s: classed maps are returned by the single-batch call only", who);
+    return HFZ_EINVAL;
+  }
   HFZ_CUDA(cudaSetDevice(c->device));
-  if ((rc = hfz_ensure_host_common(c, n_exec))) return rc;
+  if ((rc = hfz_ensure_host_common(c, n_total))) return rc;
   if (!hfz_sparse_native_ok(c) || c->S != 65536u) {
     hfz_set_error("%s: packed lists need the list-native fold and map_slots = 65536 (15-bit slots per half)", who);
     return HFZ_EINVAL;
   }
-  const uint64_t C = c->sparse_chunk ? c->sparse_chunk : 4096;
-  const uint64_t n_chunks = (n_exec + C - 1) / C;
-  if (classed && (rc = hfz_ensure_classed_stage(c, n_exec < C ? n_exec : C))) return rc;
-  // device copies keep the absolute indexing (entries below off[0] are never read); the host list in words: 3 per 4 entries
-  if ((rc = grow(reinterpret_cast<void**>(&c->sp_h3), &c->sp_h3_cap, htotal / 4 * 3 + 4, 4))) return rc;
-  if ((rc = grow(reinterpret_cast<void**>(&c->sp_off), &c->sp_off_cap, n_exec + 1, 8))) return rc;
-  if ((rc = grow(reinterpret_cast<void**>(&c->sp_compact), &c->sp_compact_cap, dtotal, 4))) return rc;
-  if ((rc = grow(reinterpret_cast<void**>(&c->sp_coff), &c->sp_coff_cap, n_exec + 1, 8))) return rc;
+  if (classed && (rc = hfz_ensure_classed_stage(c, n_total < C ? n_total : C))) return rc;
+  // device copies, batch after batch; inside a batch the absolute indexing is kept (entries below off[0] are never read)
+  if ((rc = grow(reinterpret_cast<void**>(&c->sp_h3), &c->sp_h3_cap, h_words + 4, 4))) return rc;
+  if ((rc = grow(reinterpret_cast<void**>(&c->sp_off), &c->sp_off_cap, n_total + n_batches, 8))) return rc;
+  if ((rc = grow(reinterpret_cast<void**>(&c->sp_compact), &c->sp_compact_cap, d_words + 1, 4))) return rc;
+  if ((rc = grow(reinterpret_cast<void**>(&c->sp_coff), &c->sp_coff_cap, n_total + n_batches, 8))) return rc;
   while (c->sp_events.size() < n_chunks) {
     cudaEvent_t ev;
     HFZ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     c->sp_events.push_back(ev);
   }
   cudaStream_t st = c->stream;
-  HFZ_CUDA(cudaMemcpyAsync(c->sp_off, host3_off, (n_exec + 1) * 8, cudaMemcpyHostToDevice, st));
-  HFZ_CUDA(cudaMemcpyAsync(c->sp_coff, dev17_off, (n_exec + 1) * 8, cudaMemcpyHostToDevice, st));
+  // small inputs first (the copy engine serves copies in issue order)
+  {
+    uint64_t ob = 0;
+    for (uint32_t k = 0; k < n_batches; ++k) {
+      if (!n_exec[k]) continue;
+      HFZ_CUDA(cudaMemcpyAsync(c->sp_off + ob, host3_off[k], (n_exec[k] + 1) * 8, cudaMemcpyHostToDevice, st));
+      HFZ_CUDA(cudaMemcpyAsync(c->sp_coff + ob, dev17_off[k], (n_exec[k] + 1) * 8, cudaMemcpyHostToDevice, st));
+      ob += n_exec[k] + 1;
+    }
+  }
   HFZ_CUDA(cudaMemcpyAsync(c->d_virgin, virgin, c->S, cudaMemcpyHostToDevice, st));
   HFZ_CUDA(cudaMemcpyAsync(c->d_counts, counts, 16, cudaMemcpyHostToDevice, st));
   HFZ_CUDA(cudaMemsetAsync(c->d_small + kBadSlot, 0, sizeof(unsigned long long), st));
-  uint8_t* d_h3 = reinterpret_cast<uint8_t*>(c->sp_h3);
-  for (uint64_t k = 0; k < n_chunks; ++k) {
-    const uint64_t e0 = k * C, e1 = e0 + C < n_exec ? e0 + C : n_exec;
-    if (host3_off[e1] > host3_off[e0])
-      HFZ_CUDA(cudaMemcpyAsync(d_h3 + 3 * host3_off[e0], host3 + 3 * host3_off[e0], (host3_off[e1] - host3_off[e0]) * 3,
-                               cudaMemcpyHostToDevice, c->copy_stream));
-    if (dev17_off[e1] > dev17_off[e0])
-      HFZ_CUDA(cudaMemcpyAsync(c->sp_compact + dev17_off[e0], dev17 + dev17_off[e0], (dev17_off[e1] - dev17_off[e0]) * 4,
-                               cudaMemcpyHostToDevice, c->copy_stream));
-    HFZ_CUDA(cudaEventRecord(c->sp_events[k], c->copy_stream));
+  {
+    uint64_t hb = 0, db = 0, ev = 0;  // word offsets of batch k's lists in the device buffers
+    for (uint32_t k = 0; k < n_batches; ++k) {
+      const uint64_t n = n_exec[k];
+      if (!n) continue;
+      uint8_t* d_h3 = reinterpret_cast<uint8_t*>(c->sp_h3 + hb);
+      for (uint64_t e0 = 0; e0 < n; e0 += C, ++ev) {
+        const uint64_t e1 = e0 + C < n ? e0 + C : n;
+        const uint64_t* ho = host3_off[k];
+        const uint64_t* dof = dev17_off[k];
+        if (ho[e1] > ho[e0])
+          HFZ_CUDA(cudaMemcpyAsync(d_h3 + 3 * ho[e0], host3[k] + 3 * ho[e0], (ho[e1] - ho[e0]) * 3, cudaMemcpyHostToDevice,
+                                   c->copy_stream));
+        if (dof[e1] > dof[e0])
+          HFZ_CUDA(cudaMemcpyAsync(c->sp_compact + db + dof[e0], dev17[k] + dof[e0], (dof[e1] - dof[e0]) * 4,
+                                   cudaMemcpyHostToDevice, c->copy_stream));
+        HFZ_CUDA(cudaEventRecord(c->sp_events[ev], c->copy_stream));
+      }
+      hb += host3_off[k][n] / 4 * 3;
+      db += dev17_off[k][n];
+    }
   }
-  rc = fold_chunks(c, c->sp_h3, c->sp_off, c->sp_compact, c->sp_coff, n_exec, C, true, htotal + dtotal, c->d_virgin,
-                   c->d_counts, nullptr, classed, c->d_admit, c->d_sigf, c->d_sigs, c->d_nnz, c->sp_events.data(), 1);
-  if (rc) {
-    cudaStreamSynchronize(c->copy_stream);
-    cudaStreamSynchronize(st);
-    return rc;
+  {
+    uint64_t hb = 0, db = 0, ob = 0, eb = 0, ev = 0;
+    for (uint32_t k = 0; k < n_batches; ++k) {
+      const uint64_t n = n_exec[k];
+      if (!n) continue;
+      rc = fold_chunks(c, c->sp_h3 + hb, c->sp_off + ob, c->sp_compact + db, c->sp_coff + ob, n, C, true, max_pairs,
+                       c->d_virgin, c->d_counts, nullptr, classed, c->d_admit + eb, c->d_sigf + eb, c->d_sigs + eb,
+                       c->d_nnz + eb, c->sp_events.data() + ev, 1);
+      if (rc) {
+        cudaStreamSynchronize(c->copy_stream);
+        cudaStreamSynchronize(st);
+        return rc;
+      }
+      hb += host3_off[k][n] / 4 * 3;
+      db += dev17_off[k][n];
+      ob += n + 1;
+      eb += n;
+      ev += (n + C - 1) / C;
+    }
   }
-  HFZ_CUDA(cudaMemcpyAsync(admit, c->d_admit, n_exec, cudaMemcpyDeviceToHost, st));
-  HFZ_CUDA(cudaMemcpyAsync(sigf, c->d_sigf, n_exec * 8, cudaMemcpyDeviceToHost, st));
-  HFZ_CUDA(cudaMemcpyAsync(sigs, c->d_sigs, n_exec * 8, cudaMemcpyDeviceToHost, st));
-  if (nnz) HFZ_CUDA(cudaMemcpyAsync(nnz, c->d_nnz, n_exec * 4, cudaMemcpyDeviceToHost, st));
+  HFZ_CUDA(cudaMemcpyAsync(admit, c->d_admit, n_total, cudaMemcpyDeviceToHost, st));
+  HFZ_CUDA(cudaMemcpyAsync(sigf, c->d_sigf, n_total * 8, cudaMemcpyDeviceToHost, st));
+  HFZ_CUDA(cudaMemcpyAsync(sigs, c->d_sigs, n_total * 8, cudaMemcpyDeviceToHost, st));
+  if (nnz) HFZ_CUDA(cudaMemcpyAsync(nnz, c->d_nnz, n_total * 4, cudaMemcpyDeviceToHost, st));
   HFZ_CUDA(cudaMemcpyAsync(virgin, c->d_virgin, c->S, cudaMemcpyDeviceToHost, st));
   HFZ_CUDA(cudaMemcpyAsync(counts, c->d_counts, 16, cudaMemcpyDeviceToHost, st));
   HFZ_CUDA(cudaStreamSynchronize(st));
@@ -405,7 +461,21 @@ extern "C" int hfz_feedback_batch_packed_host(hfz_ctx* c, const uint8_t* host3, 
                                               const uint32_t* dev17, const uint64_t* dev17_off, uint64_t n_exec,
                                               uint8_t* virgin, uint64_t* counts, uint8_t* classed, uint8_t* admit,
                                               uint64_t* sigf, uint64_t* sigs, uint32_t* nnz) {
-  return packed_host_impl(c, host3, host3_off, dev17, dev17_off, n_exec, virgin, counts, classed, admit, sigf, sigs, nnz);
+  if (n_exec && (!host3_off || !dev17_off)) {
+    hfz_set_error("hfz_feedback_batch_packed_host: null argument");
+    return HFZ_EINVAL;
+  }
+  return packed_host_impl(c, 1, &host3, &host3_off, &dev17, &dev17_off, &n_exec, virgin, counts, classed, admit, sigf, sigs,
+                          nnz);
+}
+
+extern "C" int hfz_feedback_batch_packed_host_v(hfz_ctx* c, uint32_t n_batches, const uint8_t* const* host3,
+                                                const uint64_t* const* host3_off, const uint32_t* const* dev17,
+                                                const uint64_t* const* dev17_off, const uint64_t* n_exec, uint8_t* virgin,
+                                                uint64_t* counts, uint8_t* admit, uint64_t* sigf, uint64_t* sigs,
+                                                uint32_t* nnz) {
+  return packed_host_impl(c, n_batches, host3, host3_off, dev17, dev17_off, n_exec, virgin, counts, nullptr, admit, sigf,
+                          sigs, nnz);
 }
 
 extern "C" int hfz_expand_sparse(hfz_ctx* c, const uint32_t* entries, const uint64_t* entry_off,

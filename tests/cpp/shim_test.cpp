@@ -150,6 +150,17 @@ int main() {
     REQUIRE(a.admit == pp.admit && a.sig_full == pp.sig_full && a.sig_simple == pp.sig_simple && a.nnz == pp.nnz);
     REQUIRE(a.classed == pp.classed);
     REQUIRE(va.host_edges() == vp.host_edges() && va.device_edges() == vp.device_edges());
+    {  // the same execs as three packed batches (one of them empty) folded by ONE call
+      b200::PackedBatch p0, p1, p2, p3;
+      for (int e = 0; e < n; ++e) (e < 70 ? p0 : (e < 71 ? p2 : p3)).append(maps[e]);
+      VirginMap vq;
+      b200::FeedbackResult qq = b200::feedback_batch(b200::default_context(), {&p0, &p1, &p2, &p3}, vq.data(), vq.edge_counts());
+      REQUIRE(a.admit == qq.admit && a.sig_full == qq.sig_full && a.sig_simple == qq.sig_simple && a.nnz == qq.nnz);
+      REQUIRE(va.host_edges() == vq.host_edges() && va.device_edges() == vq.device_edges());
+      bool same_v = true;
+      for (std::uint32_t i = 0; i < kMapSize; ++i) same_v = same_v && va.at(i) == vq.at(i);
+      REQUIRE(same_v);
+    }
     // take() = append() + reset() in one walk: the same batch, and the maps end up all-zero and reusable
     b200::CompactBatch tbatch;
     for (int e = 0; e < n; ++e) tbatch.take(maps[e]);
