@@ -41,13 +41,19 @@ def soak_fold(seeds, port):
         ctx = hfz.Context(0)
         got = ctx.feedback_batch_compact_host(comp, coff, wide if wide.shape[0] else None,
                                               woff if wide.shape[0] else None, v, c, want_classed=True)
+        # and the packed form of the same batch (3-byte host entries, 17-bit device counts)
+        h3, hoff, d17, doff = synth.to_packed(raw, n, 65536, shuffle_seed=seed + 1)
+        v2, c2 = np.zeros(65536, np.uint8), np.zeros(2, np.uint64)
+        got2 = ctx.feedback_batch_packed_host(h3, hoff, d17, doff, v2, c2, want_classed=True)
         ctx.close()
         wv, wc = np.zeros(65536, np.uint8), np.zeros(2, np.uint64)
         want = port.feedback_batch(raw, n, 65536, wv, wc, want_classed=True)
         for k in want:
             assert np.array_equal(got[k], want[k]), (seed, k)
+            assert np.array_equal(got2[k], want[k]), (seed, k, "packed")
         assert np.array_equal(v, wv) and np.array_equal(c, wc)
-    print(f"fold: {seeds} random batches x (dense + sparse) + {seeds // 4} compact ok in {time.time() - t:.0f} s", flush=True)
+        assert np.array_equal(v2, wv) and np.array_equal(c2, wc)
+    print(f"fold: {seeds} random batches x (dense + sparse) + {seeds // 4} compact and packed ok in {time.time() - t:.0f} s", flush=True)
 
 
 def soak_edge(seeds, port):

@@ -26,7 +26,7 @@ def test_small_bench_line_has_every_key():
     assert r.returncode == 0, r.stderr[-3000:]
     d = last_json(r.stdout)
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
-              "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "e2e_pairs", "e2e_dense", "stress_mode",
+              "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "e2e_compact", "e2e_pairs", "e2e_dense", "stress_mode",
               "gpu_launches", "clocks", "parity", "config0_small_batch", "k1_edge_record", "config2_large_map", "k3_havoc",
               "e2e_from_coveragemap"):
         assert k in d, k
