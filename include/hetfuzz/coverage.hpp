@@ -464,6 +464,13 @@ enum class Admit : std::uint8_t { None = 0, NewCounts = 1, NewEdges = 2 };
 enum class SignatureMode : std::uint8_t { Full, Simple };
 
 namespace detail {
+// The single-item calls below are batch-of-one device calls; their pinned list buffer is kept per thread
+// (allocating and freeing page-locked memory per call cost more than the call: cudaHostAlloc + cudaFreeHost).
+inline b200::SparseBatch& scratch_batch() {
+  static thread_local b200::SparseBatch one;
+  one.clear();
+  return one;
+}
 // The touched-slot list of a map that classifies to exactly the given class bytes (lowest count of
 // each rung): has_new_bits / trace_signature take a ClassedTrace, the device path takes counts.
 // ~1,300 pairs (10 KB) cross PCIe per call instead of a dense 163,840-byte record.  A class byte
@@ -471,7 +478,8 @@ namespace detail {
 inline void pairs_from_classed(const ClassedTrace& t, b200::SparseBatch& out) {
   static const std::uint32_t host_lo[8] = {1, 2, 3, 4, 8, 16, 32, 128};
   static const std::uint32_t dev_lo[7] = {1, 2, 3, 512, 4096, 16384, 65536};
-  CoverageMap m;
+  static thread_local CoverageMap m;  // 160 KB: reused, back to all-zero in O(touched slots)
+  m.reset();
   for (std::uint32_t idx : t.nonzero) {
     if (idx >= kMapSize) throw b200::Error("ClassedTrace: slot index out of range");
     const std::uint8_t k = t.classed[idx];
@@ -500,7 +508,8 @@ struct FeedbackOne {
   std::uint32_t nonzero_slots;
 };
 inline FeedbackOne feedback_one(const CoverageMap& map, VirginMap& virgin) {
-  SparseBatch one;
+  static thread_local SparseBatch one;  // pinned: kept per thread, not allocated per call
+  one.clear();
   one.append(map);
   FeedbackResult r = feedback_batch(default_context(), one, virgin.data(), virgin.edge_counts());
   return FeedbackOne{static_cast<Admit>(r.admit[0]), r.sig_full[0], r.sig_simple[0], r.nnz[0]};
@@ -508,7 +517,7 @@ inline FeedbackOne feedback_one(const CoverageMap& map, VirginMap& virgin) {
 }  // namespace b200
 
 inline ClassedTrace classify_trace(const CoverageMap& map) {
-  b200::SparseBatch one;
+  b200::SparseBatch& one = detail::scratch_batch();
   one.append(map);
   std::vector<std::uint8_t> scratch_virgin(kMapSize, 0);
   std::uint64_t counts[2] = {0, 0};
@@ -526,7 +535,7 @@ inline ClassedTrace classify_trace(const CoverageMap& map) {
 }
 
 inline Admit has_new_bits(const ClassedTrace& trace, VirginMap& virgin) {
-  b200::SparseBatch one;
+  b200::SparseBatch& one = detail::scratch_batch();
   detail::pairs_from_classed(trace, one);
   b200::FeedbackResult r =
       b200::feedback_batch(b200::default_context(), one, virgin.data(), virgin.edge_counts());
@@ -534,7 +543,7 @@ inline Admit has_new_bits(const ClassedTrace& trace, VirginMap& virgin) {
 }
 
 inline std::uint64_t trace_signature(const ClassedTrace& trace, SignatureMode mode) {
-  b200::SparseBatch one;
+  b200::SparseBatch& one = detail::scratch_batch();
   detail::pairs_from_classed(trace, one);
   std::vector<std::uint8_t> scratch_virgin(kMapSize, 0);
   std::uint64_t counts[2] = {0, 0};
